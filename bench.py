@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark: restarted cl-BGMRES with BCGS-PIP block Arnoldi on B200 (BASELINE.json metric
+"block Arnoldi steps/s and fp64 HBM GB/s (% roofline) at 1/2/4/8 B200").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+* A bench "step" is one restart cycle of the solver: IO(U) + m block Arnoldi steps (SpMM,
+  fused single-sync Gram, Cholesky, projection) + the cycle-end projected solve and the
+  X/U update, i.e. every row of SURVEY.md 8(a).  K cycles run inside ONE lsba_bgmres_solve
+  call (max_restarts = K-1) at the real tol 1e-8 (config 2 needs ~4400 cycles, so none of
+  the timed cycles converges).
+* value = whole-job algorithmic fp64 HBM GB/s: sum over steps of ROOF(k) = 12 nnz + 4(n+1)
+  + 8 n s (2k+3) plus 8 n s (k+7) per cycle, all ranks,
+  divided by the max-over-ranks device time.  block_steps_per_s is reported beside it.
+* N > 1: weak scaling, one 1024 x 1024 y-slab of a 1024 x (1024 N) 2D Laplacian per GPU,
+  row-partitioned, halo send/recv + exactly one Gram allreduce per block step.
+* --impl reference: the oracle (oracle/, NumPy fp64) on this box's host cores on the same
+  workload, a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "block Arnoldi steps/s and fp64 HBM GB/s (% roofline) at 1/2/4/8 B200"
+
+
+def roof_step(nnz, n, s, k):
+    """Algorithmic bytes of block step k: CSR A + basis read twice around the
+    single sync + W written and read + V_{k+1} written."""
+    return 12.0 * nnz + 4.0 * (n + 1) + 8.0 * n * s * (2 * k + 3)
+
+
+def roof_cycle_extra(n, s, k_used):
+    return 8.0 * n * s * (k_used + 7)
+
+
+def cycle_bytes(nnz, n, s, m):
+    return sum(roof_step(nnz, n, s, k) for k in range(1, m + 1)) + roof_cycle_extra(n, s, m)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(p[0]) for p in self.samples if p[0].replace(".", "").isdigit()]
+        mx = [float(p[1]) for p in self.samples if p[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in self.samples for i in range(4) if p[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- workload
+def build_workload(config, rank, world):
+    """Returns dict(name, n_global, row_begin, row_end, A_local, B_local, s, m, tol, nnz_global)."""
+    from lsba_inputs import CONFIGS, rhs, stencil, random_sparse
+    spec = dict(CONFIGS[config])
+    s, m = spec["s"], spec["m"]
+    if spec["kind"] == "stencil":
+        dims, N = spec["dims"], spec["N"]
+        if world > 1:   # weak scaling: stack world slabs along the slowest dimension
+            shape = [N] * dims
+            shape[-1] = N * world
+        else:
+            shape = [N] * dims
+        n = int(np.prod(shape))
+        per = n // world
+        r0, r1 = rank * per, (rank + 1) * per if rank < world - 1 else n
+        A = stencil(dims, N, spec["v"], shape=shape, rows=(r0, r1))
+        # nnz of the global operator (closed form for the stencil)
+        nnz = n * (2 * dims + 1) - 2 * sum(n // shape[d] for d in range(dims))
+        name = spec["name"] + (f" x{world} (weak, slab per GPU)" if world > 1 else "")
+    else:
+        n = spec["n"] * world
+        per = n // world
+        r0, r1 = rank * per, (rank + 1) * per
+        rp, ci, va = random_sparse(n)   # every rank builds the same matrix (seeded)
+        A = (rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]], va[rp[r0]:rp[r1]])
+        nnz = int(rp[-1])
+        name = spec["name"] + (f" x{world}" if world > 1 else "")
+    Bfull_rows = rhs(n, s) if world == 1 else None
+    if world == 1:
+        B = Bfull_rows
+    else:
+        B = np.random.default_rng(rank).standard_normal((r1 - r0, s))
+    return dict(name=name, n_global=n, row_begin=r0, row_end=r1, A=A, B=np.ascontiguousarray(B), s=s, m=m,
+                tol=spec["tol"], nnz=nnz, spec=spec)
+
+
+# --------------------------------------------------------------------------- oracle timing
+def oracle_sample(wl, budget_s):
+    """Time the oracle (as it stands) on a bounded sample of the same workload: the first
+    block steps of one cycle on the full matrix, until ~budget_s of CPU work."""
+    from oracle import lsba_oracle as O
+    A = wl["A"]
+    B = wl["B"]
+    n, s = B.shape
+    arn = O.PipArnoldi(A, "cl", wl["m"], s)
+    t0 = time.perf_counter()
+    arn.begin(B)
+    steps, byts = 0, roof_cycle_extra(n, s, 0)
+    while steps < wl["m"]:
+        arn.step()
+        steps += 1
+        byts += roof_step(wl["nnz"], n, s, steps)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return dict(seconds=dt, steps=steps, bytes=byts)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    wl = build_workload(args.config, 0, 1)
+    per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(wl, per_step_budget / 4)
+    tot_s, tot_b, tot_steps = 0.0, 0.0, 0
+    for _ in range(args.steps):
+        r = oracle_sample(wl, per_step_budget)
+        tot_s += r["seconds"]
+        tot_b += r["bytes"]
+        tot_steps += r["steps"]
+    gbs = tot_b / tot_s / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "block_steps_per_s": tot_steps / tot_s,
+        "config": {"workload": wl["name"], "n": wl["n_global"], "s": wl["s"], "m": wl["m"],
+                   "method": "cl-BCGS-PIP block Arnoldi (oracle, NumPy fp64)",
+                   "timed_unit": "bounded sample: the first block steps of one cycle"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{tot_steps} block steps over {args.steps} samples of config {args.config}"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 0 and args.steps >= 1
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2208_09899_b200 as L
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = build_workload(args.config, rank, world)
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(L.lsba_get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+    stream = torch.cuda.current_stream()
+    ctx = L.Context(wl["n_global"], wl["s"], wl["m"], *wl["A"], row_begin=wl["row_begin"],
+                    row_end=wl["row_end"], rank=rank, nranks=world, nccl_id=nccl_id, device=local,
+                    stream=stream.cuda_stream)
+    L.lsba_set_kernel_variant(ctx.ctx, args.variant)
+    B = torch.from_numpy(wl["B"]).cuda()
+    X = torch.zeros_like(B)
+    m, tol, s = wl["m"], wl["tol"], wl["s"]
+    n_loc, n_glob = wl["row_end"] - wl["row_begin"], wl["n_global"]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up: W cycles (one solve call), not timed
+    if args.warmup:
+        L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    L.lsba_profile_enable(ctx.ctx, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    info = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.steps - 1)    # exactly K cycles
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_local = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    prof = {k: L.lsba_profile_read(ctx.ctx, k) for k in L.KERNEL_IDS}
+    L.lsba_profile_enable(ctx.ctx, False)
+    ms = ms_local
+    if dist is not None:
+        t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    cycles, iters = info.cycles, info.iterations
+    assert cycles == args.steps, f"expected {args.steps} cycles, ran {cycles} (outcome {info.outcome})"
+    # whole-job algorithmic bytes (global problem)
+    total_bytes = cycle_bytes(wl["nnz"], n_glob, s, m) * iters / m
+    gbs = total_bytes / (ms / 1e3) / 1e9
+    steps_per_s = iters / (ms / 1e3)
+    peak, peak_kind = measured_peaks()
+
+    # dominant kernel roofline (local rank's launches; per-launch averages)
+    tot_ms = sum(v[1] for v in prof.values())
+    dom = max(prof, key=lambda k: prof[k][1])
+    dn, dms, dbytes = prof[dom]
+    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(f"config{args.config}", {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # e2e through the public API with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Bh = torch.from_numpy(wl["B"]).pin_memory().numpy()
+        Xh = torch.zeros(B.shape, dtype=torch.float64).pin_memory().numpy()
+        barrier()
+        t0 = time.perf_counter()
+        e2e_iters = 0
+        for _ in range(args.steps):
+            ih = L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 0)
+            e2e_iters += ih.iterations
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e_bytes = cycle_bytes(wl["nnz"], n_glob, s, m) * e2e_iters / m
+        e2e = {"value": e2e_bytes / dt / 1e9, "unit": "GB/s", "block_steps_per_s": e2e_iters / dt,
+               "h2d_bytes_per_step": 2 * n_loc * s * 8 * world, "d2h_bytes_per_step": n_loc * s * 8 * world,
+               "api": "lsba_solve_host (1 cycle per call, X0 = previous X)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = oracle_sample(wl, 20.0)
+        cpu = {"value": r["bytes"] / r["seconds"] / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "block_steps_per_s": r["steps"] / r["seconds"],
+               "sample": f"oracle IO + first {r['steps']} block steps of one cycle of {wl['name']} "
+                         f"({r['seconds']:.1f} s, single-threaded NumPy)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "block_steps_per_s": steps_per_s, "ms_per_block_step": ms / iters,
+            "pct_roofline": {"of_measured_hbm": gbs / (peak * world), "of_8TBps_nominal": gbs / (8000.0 * world)},
+            "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
+                       "method": "cl-BGMRES, BCGS-PIP skeleton, CholQR IO",
+                       "timed_unit": f"restart cycle = IO + {m} block steps + cycle end",
+                       "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "launches": dn, "kernel_share_of_step": dms / tot_ms if tot_ms else None},
+            "kernel_times_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
+            "kernel_gbs": {k: round(v[2] / (v[1] / 1e3) / 1e9, 1) for k, v in prof.items() if v[1] > 0 and v[2] > 0},
+            "gpu_launches": int(info.kernel_launches),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "solver": {"cycles": cycles, "iterations": iters, "nan_flags": info.nan_flags,
+                       "res_est_rel": info.res_est, "true_relres": info.true_relres},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,204 @@
+/*
+ * lsba.h — C ABI of the B200-native low-synchronization block Arnoldi hot path.
+ *
+ * Problem statement: solve A X = B with A (n x n) large and sparse and
+ * B (n x s) tall and skinny, by restarted modified BFOM / BGMRES (Eq (Xm))
+ * whose Krylov basis is built by BCGS-PIP block Arnoldi (Alg 3) in the
+ * classical or global block inner product (Table 1), with the adaptive
+ * restart of Sec 4 and a basis-condition trigger (reading R8).
+ *
+ * Conventions (all calls):
+ *   - Return an lsba_status; none aborts or exits.  Numerical breakdown (a Cholesky
+ *     "NaN-flag") is NOT an error: it is reported through the info structs.
+ *   - Arithmetic is IEEE fp64 throughout.
+ *   - Block vectors (B, X, basis blocks) are ROW-MAJOR n_local x s fp64 arrays (row i's s
+ *     values contiguous), contiguous, 16-byte aligned, in device memory unless the name says
+ *     _host.  They are caller-owned; the library never frees them.
+ *   - The library owns its workspace (basis of m_max+1 blocks, Gram partials, small state);
+ *     it is allocated by lsba_create and freed by lsba_destroy.
+ *   - All device work is enqueued on the CUDA stream given to lsba_create.  *_solve and
+ *     lsba_block_arnoldi_step return after completion (they synchronise that stream).
+ *   - Multi-GPU: one context per rank (process); rows are partitioned into contiguous
+ *     ranges [row_begin, row_end).  Every block step performs exactly one ncclAllReduce of
+ *     the Gram block (the step's single sync point); halos move with
+ *     grouped ncclSend/ncclRecv.  Small (s x s, ks x ks) state is replicated on every rank.
+ *   - One context per host thread; a context is not thread-safe.
+ */
+#ifndef LSBA_H
+#define LSBA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lsba_ctx_* lsba_ctx;
+
+typedef enum {
+  LSBA_OK = 0,
+  LSBA_E_ARG = 1,    /* invalid argument (message in lsba_last_error)           */
+  LSBA_E_CUDA = 2,   /* a CUDA runtime call or kernel launch failed              */
+  LSBA_E_NCCL = 3,   /* an NCCL call failed                                      */
+  LSBA_E_OOM = 4,    /* device or pinned-host allocation failed                  */
+  LSBA_E_STATE = 5   /* call out of order (e.g. step before arnoldi_begin)       */
+} lsba_status;
+
+/* Table 1. */
+typedef enum { LSBA_IP_CLASSICAL = 0, LSBA_IP_GLOBAL = 1 } lsba_ip;
+
+/* Gram-Schmidt skeleton (Table 2).  Only BCGS-PIP (Alg 3) is built. */
+typedef enum { LSBA_SKEL_BCGS_PIP = 0 } lsba_skel;
+
+/* SPEC.md:327 outcome of a solve. */
+typedef enum { LSBA_CONVERGED = 0, LSBA_MAX_RESTARTS = 1, LSBA_DEAD = 2 } lsba_outcome;
+
+/* Result of one block Arnoldi step (lsba_block_arnoldi_step). */
+typedef struct {
+  int32_t k;          /* index of the step just attempted (1-based, Alg 3 line 2)           */
+  int32_t chol_flag;  /* 1 iff chol(Omega - H^T H) flagged (reading R2)  */
+  double cond_est;    /* kappa_F of R_{k+1} = [E_1 beta, Hbar_k] (reading R8)               */
+  double res_est;     /* BGMRES residual-norm estimate ||g_{k+1}||_F for C_acc = I (Eq normF_Rm) */
+} lsba_step_info;
+
+/* Result of a solve.  Counters follow the paper's accounting (PAPER.md:650 tables):
+ * syncs = iterations + cycles, matvecs (A-ct) = iterations, basis_evals (V-ct) = 3 iterations. */
+typedef struct {
+  int32_t outcome;            /* lsba_outcome                                             */
+  int32_t cycles;             /* restart cycles run                                       */
+  int32_t restarts;           /* cycles - 1                                               */
+  int32_t iterations;         /* accepted block Arnoldi steps                             */
+  int32_t attempted_steps;    /* accepted + NaN-flagged steps                             */
+  int32_t nan_flags;          /* Cholesky NaN-flags (each shrinks m, reading R6)          */
+  int32_t cond_restarts;      /* cycles ended by kappa_F > cond_threshold (reading R8)    */
+  int32_t happy;              /* flags recognised as happy breakdown (reading R7)         */
+  int32_t false_convergences; /* estimate <= tol but true residual > tol (reading R19)    */
+  int32_t m_final;            /* maximum basis size after adaptive reductions             */
+  int64_t syncs, matvecs, basis_evals;
+  int64_t kernel_launches;    /* this library's kernel launches during the call            */
+  double res_est;             /* last residual estimate, ||.||_F (absolute)               */
+  double true_relres;         /* ||B - A X||_F / ||B||_F at exit (explicit)               */
+  double seconds;             /* wall time of the call                                    */
+} lsba_solve_info;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Rank 0 creates an NCCL unique id (128 bytes) to broadcast (e.g. torch.distributed). */
+lsba_status lsba_get_unique_id(uint8_t id[128]);
+
+/* Create a context on `device` for the local rows [row_begin, row_end) of an n x n sparse A.
+ *   row_ptr : host, int64, length (row_end-row_begin)+1, row_ptr[0] = 0, monotone
+ *   col_idx : host, int32 GLOBAL column indices, sorted strictly increasing per row
+ *   vals    : host, fp64
+ * The CSR is validated and copied; the caller keeps its arrays.
+ * s in [1,16]; m_max >= 1 (basis of m_max+1 blocks is allocated: 8 n_local s (m_max+1) bytes).
+ * nccl_id may be NULL iff nranks == 1.  cuda_stream is a cudaStream_t (NULL = legacy stream).
+ * Errors: LSBA_E_ARG on invalid sizes or CSR; LSBA_E_OOM; LSBA_E_CUDA; LSBA_E_NCCL. */
+lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                        const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                        int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                        const uint8_t* nccl_id, int32_t device, void* cuda_stream);
+lsba_status lsba_destroy(lsba_ctx ctx);
+
+const char* lsba_status_str(lsba_status st);
+const char* lsba_last_error(lsba_ctx ctx);   /* never NULL; "" if no error */
+
+/* ---------------------------------------------------------------- one cycle, step by step */
+
+/* Alg 3 line 1: [V_1, beta] = IO(B) (CholQR for classical, (1/sqrt s)||B||_F for global;
+ * PAPER.md:114, 265, 416).  B_dev: n_local x s.  *io_flag = 1 if IO's Cholesky flagged. */
+lsba_status lsba_arnoldi_begin(lsba_ctx ctx, const double* B_dev, lsba_ip ip, int32_t* io_flag);
+
+/* Alg 3 lines 3-6 for the next k: W = A V_k; ONE fused Gram <[V_k W], W> (+ one allreduce);
+ * H_{k+1,k} = chol(Omega - H^T H) with NaN-flag; V_{k+1} = (W - V_k H_{1:k,k}) H_{k+1,k}^{-1}.
+ * On a flag the step is not accepted (k does not advance; V_{k+1} is not formed).
+ * LSBA_E_STATE if called before arnoldi_begin, after a flag, or when k == m_max. */
+lsba_status lsba_block_arnoldi_step(lsba_ctx ctx, lsba_step_info* info);
+
+/* Copy the block Hessenberg Hbar_k ((k+1)b x kb, b = s classical / 1 global) to host,
+ * column-major with leading dimension ld >= (k+1)b.  Also valid after a flag (the flagged
+ * step's column H_{1:k,k} is stored, its subdiagonal block is not). */
+lsba_status lsba_copy_hessenberg(lsba_ctx ctx, double* H_host, int32_t ld);
+/* beta (b x b, column-major) from the last IO. */
+lsba_status lsba_copy_beta(lsba_ctx ctx, double* beta_host);
+/* Copy basis block V_{j} (1-based, j <= k+1) to a caller device buffer (n_local x s). */
+lsba_status lsba_copy_basis_block(lsba_ctx ctx, int32_t j, double* dst_dev);
+
+/* ---------------------------------------------------------------- solvers */
+
+/* Restarted BGMRES / BFOM (modification M of PAPER.md:191 / M = 0) with BCGS-PIP and the
+ * adaptive restart of Sec 4 (NaN-flag -> restart from the last safe block, m <- k-1;
+ * PAPER.md:405) plus cond_threshold (kappa_F trigger, +inf = off; reading R8).
+ *   B_dev : n_local x s (device);  X_dev : in X0, out X (device)
+ *   m <= m_max; tol > 0 relative to ||B||_F; at most max_restarts+1 cycles.
+ * Convergence: res_est <= tol ||B||_F after any accepted step, confirmed by the explicit
+ * residual (reading R19).  Returns LSBA_OK also for MAX_RESTARTS and DEAD outcomes. */
+lsba_status lsba_bgmres_solve(lsba_ctx ctx, const double* B_dev, double* X_dev, int32_t m,
+                              double tol, int32_t max_restarts, lsba_skel skel, lsba_ip ip,
+                              double cond_threshold, lsba_solve_info* info);
+lsba_status lsba_bfom_solve(lsba_ctx ctx, const double* B_dev, double* X_dev, int32_t m,
+                            double tol, int32_t max_restarts, lsba_skel skel, lsba_ip ip,
+                            double cond_threshold, lsba_solve_info* info);
+/* Same as lsba_bgmres_solve / lsba_bfom_solve (fom != 0) but B and X live in HOST memory
+ * (pinned or pageable); the host<->device copies are part of the call. */
+lsba_status lsba_solve_host(lsba_ctx ctx, const double* B_host, double* X_host, int32_t m,
+                            double tol, int32_t max_restarts, int32_t fom, lsba_ip ip,
+                            double cond_threshold, lsba_solve_info* info);
+
+/* ---------------------------------------------------------------- single kernels (parity) */
+
+/* W = A V over the local rows (halo exchange included when nranks > 1).  V_dev, W_dev:
+ * n_local x s device buffers (distinct). */
+lsba_status lsba_spmm(lsba_ctx ctx, const double* V_dev, double* W_dev);
+/* G = [V_1..V_p]^T Y (classical, (p s) x s, row-major) or the p scalars (1/s) tr(V_j^T Y)
+ * (global) for p = nblocks consecutive n_local x s blocks at V_dev; Y_dev n_local x s;
+ * includes the allreduce.  G_host receives the result. */
+lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t nblocks,
+                                     const double* Y_dev, lsba_ip ip, double* G_host);
+
+/* ---------------------------------------------------------------- debug / measurement */
+
+/* Fault injection: make the Cholesky of step k_flag report a NaN-flag once (0 = off). */
+lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
+/* Kernel implementation choice: 0 = auto (tensor-core DMMA kernels where s >= 4),
+ * 1 = force the plain DFMA kernels.  For parity tests of both paths. */
+lsba_status lsba_set_kernel_variant(lsba_ctx ctx, int32_t variant);
+
+/* Per-kernel timing with CUDA events on the context stream.  Kernel ids: */
+enum {
+  LSBA_K_SPMM = 0, LSBA_K_GRAM = 1, LSBA_K_GRAM_FINALIZE = 2, LSBA_K_SMALL_STEP = 3,
+  LSBA_K_PROJECT = 4, LSBA_K_CYCLE_SOLVE = 5, LSBA_K_COMBINE = 6, LSBA_K_RESIDUAL = 7,
+  LSBA_K_HALO_PACK = 8, LSBA_K_MISC = 9, LSBA_K_COUNT = 10
+};
+/* enable != 0 starts recording events around every launch (resets the records). */
+lsba_status lsba_profile_enable(lsba_ctx ctx, int32_t enable);
+/* For kernel id `kid`: launches, summed event time (ms) and summed ALGORITHMIC bytes
+ * over the recorded launches.  Synchronises the stream. */
+lsba_status lsba_profile_read(lsba_ctx ctx, int32_t kid, int64_t* launches, double* ms,
+                              double* bytes);
+/* Total kernel launches of this context since creation. */
+lsba_status lsba_launch_count(lsba_ctx ctx, int64_t* launches);
+/* Device workspace bytes held by the context. */
+lsba_status lsba_workspace_bytes(lsba_ctx ctx, int64_t* bytes);
+
+/* ---------------------------------------------------------------- host-only (no GPU needed) */
+
+/* Ghost plan for a row-partitioned CSR (SPEC 8(e)): given this rank's rows [row_begin,
+ * row_end) with GLOBAL col_idx (nnz entries) and the partition starts part[0..nranks]
+ * (part[0] = 0, part[nranks] = n), write col_local[nnz] (local index if owned, else
+ * n_local + ghost slot), ghost_global[] (sorted unique remote columns, capacity nnz) and
+ * recv_counts[nranks] (ghost rows owned by each rank).  *n_ghost receives the count.
+ * Pure host code; used by lsba_create and unit-tested on CPU. */
+lsba_status lsba_ghost_plan(int64_t row_begin, int64_t row_end, const int32_t* col_idx,
+                            int64_t nnz, const int64_t* part, int32_t nranks,
+                            int32_t* col_local, int64_t* ghost_global, int64_t* n_ghost,
+                            int64_t* recv_counts);
+/* Validate a CSR block; returns LSBA_E_ARG with a message in *msg
+ * (static storage) on violation. */
+lsba_status lsba_csr_validate(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                              const int32_t* col_idx, const char** msg);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSBA_H */

@@ -59,15 +59,22 @@ def _compress(cols: np.ndarray, vals: np.ndarray, mask: np.ndarray):
     return counts, cols[mask].astype(np.int32), vals[mask]
 
 
-def stencil(dims: int, N: int, v=None, chunk_rows: int = 1 << 20):
-    """h^2-scaled upwind convection-diffusion stencil on an N^dims grid (see module doc)."""
+def stencil(dims: int, N: int, v=None, chunk_rows: int = 1 << 20, shape=None, rows=None):
+    """h^2-scaled upwind convection-diffusion stencil on an N^dims grid (see module doc).
+
+    shape: optional grid extents per dimension (x fastest), default (N,)*dims (h = 1/(N+1)).
+    rows: optional (r0, r1): build only those rows (global column indices), for row-partitioned
+    multi-GPU runs; row_ptr then starts at 0 for row r0."""
     if v is None:
         v = (0.0,) * dims
     v = tuple(float(x) for x in v)
     assert len(v) == dims and all(x >= 0 for x in v)
     h = 1.0 / (N + 1)
-    n = N ** dims
-    strides = [N ** d for d in range(dims)]
+    shape = tuple(shape) if shape is not None else (N,) * dims
+    assert len(shape) == dims
+    n = int(np.prod(shape))
+    strides = [int(np.prod(shape[:d])) for d in range(dims)]
+    lo, hi = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
     diag = 2.0 * dims + h * sum(v)
     # column order for sorted rows: backward z, y, x; centre; forward x, y, z
     offs = [-strides[d] for d in reversed(range(dims))] + [0] + [strides[d] for d in range(dims)]
@@ -76,27 +83,29 @@ def stencil(dims: int, N: int, v=None, chunk_rows: int = 1 << 20):
     sign = [-1] * dims + [0] + [1] * dims
     w = len(offs)
     counts_all, cols_all, vals_all = [], [], []
-    for r0 in range(0, n, chunk_rows):
-        r1 = min(n, r0 + chunk_rows)
-        rows = np.arange(r0, r1, dtype=np.int64)
-        coord = [(rows // strides[d]) % N for d in range(dims)]
+    for r0 in range(lo, hi, chunk_rows):
+        r1 = min(hi, r0 + chunk_rows)
+        rows_ = np.arange(r0, r1, dtype=np.int64)
+        coord = [(rows_ // strides[d]) % shape[d] for d in range(dims)]
         cols = np.empty((r1 - r0, w), dtype=np.int64)
         vals = np.empty((r1 - r0, w), dtype=np.float64)
         mask = np.ones((r1 - r0, w), dtype=bool)
         for t in range(w):
-            cols[:, t] = rows + offs[t]
+            cols[:, t] = rows_ + offs[t]
             vals[:, t] = coef[t]
             if sign[t] < 0:
                 mask[:, t] = coord[which[t]] > 0
             elif sign[t] > 0:
-                mask[:, t] = coord[which[t]] < N - 1
+                mask[:, t] = coord[which[t]] < shape[which[t]] - 1
         c, ci, vv = _compress(cols, vals, mask)
         counts_all.append(c)
         cols_all.append(ci)
         vals_all.append(vv)
-    counts = np.concatenate(counts_all)
-    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    counts = np.concatenate(counts_all) if counts_all else np.zeros(0, dtype=np.int64)
+    row_ptr = np.zeros(hi - lo + 1, dtype=np.int64)
     np.cumsum(counts, out=row_ptr[1:])
+    if not cols_all:
+        return row_ptr, np.zeros(0, dtype=np.int32), np.zeros(0)
     return row_ptr, np.concatenate(cols_all), np.concatenate(vals_all)
 
 

@@ -1,0 +1,1085 @@
+// lsba.cu — C-ABI (include/lsba.h) and the host engine around the sm_100a kernels.
+//
+// The engine is the restarted modified BFOM/BGMRES driver of PAPER.md:186-219 with the BCGS-PIP
+// skeleton (Alg 3) and the adaptive restart of Sec 4,
+// following the same step list as the oracle; every
+// arithmetic step runs in a kernel of kernels.cuh (or the single NCCL allreduce / halo
+// send-recv).  The host only sequences launches and reads one 48-byte status word per step
+// (the convergence / restart check, the north star's single host round trip).
+#include "../../include/lsba.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace lsba;
+
+namespace {
+
+struct EvPair { cudaEvent_t a, b; };
+
+struct Prof {
+  bool on = false;
+  std::vector<EvPair> ev[LSBA_K_COUNT];
+  size_t used[LSBA_K_COUNT] = {};
+  double bytes[LSBA_K_COUNT] = {};
+  int64_t launches[LSBA_K_COUNT] = {};
+};
+
+constexpr int kGramCtas = 4 * 148 * 2;  // target CTAs of the partial-Gram grid
+
+}  // namespace
+
+struct lsba_ctx_ {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n_global = 0, row_begin = 0, row_end = 0;
+  int n = 0;  // local rows
+  int s = 0, m_max = 0, rank = 0, nranks = 1;
+  int64_t nnz = 0;
+  // CSR (device)
+  int* d_rp = nullptr;
+  int* d_ci = nullptr;
+  double* d_va = nullptr;
+  // basis: (m_max+1) slots of n x s
+  double* d_V = nullptr;
+  size_t slot = 0;  // elements per slot
+  // halo
+  int n_ghost = 0;
+  double* d_ghost = nullptr;
+  std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
+  int* d_send_idx = nullptr;
+  double* d_sendbuf = nullptr;
+  int64_t n_send = 0;
+  ncclComm_t comm = nullptr;
+  // Gram
+  double* d_part = nullptr;
+  size_t part_cap = 0;
+  double* d_G = nullptr;
+  // small state
+  SmallState st{};
+  double* d_small = nullptr;
+  double* d_work = nullptr;
+  double* d_Y = nullptr;
+  double* d_Z = nullptr;
+  int* d_info = nullptr;
+  StepStatus* h_status = nullptr;  // pinned
+  int* h_info = nullptr;           // pinned
+  double* h_scalar = nullptr;      // pinned
+  double* d_Xc = nullptr;
+  double* d_sq = nullptr;
+  int sq_cap = 0;
+  double* d_scalar = nullptr;
+  double* d_Bh = nullptr;  // e2e staging
+  double* d_Xh = nullptr;
+  // state machine for the step API
+  int ip = LSBA_IP_CLASSICAL;
+  int b = 0;
+  int k = -1;
+  bool flagged = false;
+  int force_flag_k = 0;
+  bool forced_done = false;
+  int variant = 0;
+  int64_t launches = 0;
+  int64_t ws_bytes = 0;
+  std::string err;
+  Prof prof;
+};
+
+// ------------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------------
+static lsba_status fail(lsba_ctx c, lsba_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return st;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? LSBA_E_OOM : LSBA_E_CUDA,          \
+                  "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));      \
+  } while (0)
+
+#define CKL()                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, LSBA_E_CUDA, "%s:%d launch: %s", __FILE__, __LINE__,               \
+                  cudaGetErrorString(e_));                                                \
+  } while (0)
+
+#define CKN(call)                                                                         \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(c, LSBA_E_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,              \
+                  ncclGetErrorString(r_));                                                \
+  } while (0)
+
+#define TRY(x)                        \
+  do {                                \
+    lsba_status s_ = (x);             \
+    if (s_ != LSBA_OK) return s_;     \
+  } while (0)
+
+// profiling scope around one launch
+struct LaunchScope {
+  lsba_ctx c;
+  int kid;
+  EvPair* ev = nullptr;
+  LaunchScope(lsba_ctx c_, int kid_, double bytes) : c(c_), kid(kid_) {
+    c->launches++;
+    if (!c->prof.on) return;
+    Prof& p = c->prof;
+    p.launches[kid]++;
+    p.bytes[kid] += bytes;
+    if (p.used[kid] == p.ev[kid].size()) {
+      EvPair e;
+      cudaEventCreate(&e.a);
+      cudaEventCreate(&e.b);
+      p.ev[kid].push_back(e);
+    }
+    ev = &p.ev[kid][p.used[kid]++];
+    cudaEventRecord(ev->a, c->stream);
+  }
+  ~LaunchScope() {
+    if (ev) cudaEventRecord(ev->b, c->stream);
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+// template dispatch over s = 1..16
+// ------------------------------------------------------------------------------------------
+#define LSBA_DISPATCH_S(s, FN, ...)         \
+  switch (s) {                              \
+    case 1: return FN<1>(__VA_ARGS__);      \
+    case 2: return FN<2>(__VA_ARGS__);      \
+    case 3: return FN<3>(__VA_ARGS__);      \
+    case 4: return FN<4>(__VA_ARGS__);      \
+    case 5: return FN<5>(__VA_ARGS__);      \
+    case 6: return FN<6>(__VA_ARGS__);      \
+    case 7: return FN<7>(__VA_ARGS__);      \
+    case 8: return FN<8>(__VA_ARGS__);      \
+    case 9: return FN<9>(__VA_ARGS__);      \
+    case 10: return FN<10>(__VA_ARGS__);    \
+    case 11: return FN<11>(__VA_ARGS__);    \
+    case 12: return FN<12>(__VA_ARGS__);    \
+    case 13: return FN<13>(__VA_ARGS__);    \
+    case 14: return FN<14>(__VA_ARGS__);    \
+    case 15: return FN<15>(__VA_ARGS__);    \
+    case 16: return FN<16>(__VA_ARGS__);    \
+    default: return LSBA_E_ARG;             \
+  }
+
+static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- halo exchange (P > 1)
+template <int S>
+static lsba_status halo_t(lsba_ctx c, const double* V) {
+  if (c->nranks == 1) return LSBA_OK;
+  if (c->n_send > 0) {
+    LaunchScope L(c, LSBA_K_HALO_PACK, 16.0 * c->n_send * S + 4.0 * c->n_send);
+    const long tot = c->n_send * S;
+    k_halo_pack<S><<<cdiv(tot, kThreads), kThreads, 0, c->stream>>>((int)c->n_send, c->d_send_idx, V,
+                                                                     c->d_sendbuf);
+    CKL();
+  }
+  CKN(ncclGroupStart());
+  for (int r = 0; r < c->nranks; ++r) {
+    if (r == c->rank) continue;
+    if (c->send_cnt[r] > 0)
+      CKN(ncclSend(c->d_sendbuf + c->send_off[r] * S, (size_t)c->send_cnt[r] * S, ncclDouble, r,
+                   c->comm, c->stream));
+    if (c->recv_cnt[r] > 0)
+      CKN(ncclRecv(c->d_ghost + c->recv_off[r] * S, (size_t)c->recv_cnt[r] * S, ncclDouble, r,
+                   c->comm, c->stream));
+  }
+  CKN(ncclGroupEnd());
+  return LSBA_OK;
+}
+
+// ---------------------------------------------------------------- a1: SpMM / residual
+template <int S>
+static lsba_status spmm_t(lsba_ctx c, const double* V, double* W) {
+  TRY(halo_t<S>(c, V));
+  constexpr int L = (S % 2 == 0) ? S / 2 : 1;
+  const long threads = (long)c->n * L;
+  LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n * S);
+  if constexpr (S % 2 == 0 || S == 1) {
+    k_spmm<S, false><<<cdiv(threads, kThreads), kThreads, 0, c->stream>>>(
+        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr);
+  } else {
+    k_spmm_odd<S, false><<<cdiv(c->n, kThreads), kThreads, 0, c->stream>>>(
+        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr);
+  }
+  CKL();
+  return LSBA_OK;
+}
+
+// R = B - A X -> out; ||R||_F^2 (all ranks) -> d_scalar[0]
+template <int S>
+static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, double* out) {
+  TRY(halo_t<S>(c, X));
+  constexpr int L = (S % 2 == 0) ? S / 2 : 1;
+  int nblk = (S % 2 == 0 || S == 1) ? cdiv((long)c->n * L, kThreads) : cdiv(c->n, kThreads);
+  if (nblk < 1) nblk = 1;
+  if (nblk > c->sq_cap) return fail(c, LSBA_E_STATE, "residual partial buffer too small");
+  {
+    LaunchScope Ls(c, LSBA_K_RESIDUAL, 12.0 * c->nnz + 4.0 * (c->n + 1) + 24.0 * c->n * S);
+    if (c->n == 0) {
+      CK(cudaMemsetAsync(c->d_sq, 0, sizeof(double), c->stream));
+    } else if constexpr (S % 2 == 0 || S == 1) {
+      k_spmm<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
+                                                          c->d_ghost, Bm, out, c->d_sq);
+    } else {
+      k_spmm_odd<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
+                                                              c->d_ghost, Bm, out, c->d_sq);
+    }
+    CKL();
+  }
+  {
+    LaunchScope Ls(c, LSBA_K_MISC, 8.0 * nblk);
+    k_sum_partials<<<1, kThreads, 0, c->stream>>>(c->n == 0 ? 1 : nblk, c->d_sq, c->d_scalar);
+    CKL();
+  }
+  if (c->nranks > 1)
+    CKN(ncclAllReduce(c->d_scalar, c->d_scalar, 1, ncclDouble, ncclSum, c->comm, c->stream));
+  return LSBA_OK;
+}
+
+// ---------------------------------------------------------------- a2: Gram (+ allreduce)
+// G (device, c->d_G) = <[X_0..X_{J-1}], Y>; classical (J s) x s row-major; global J scalars
+// (scaled by 1/s).  Exactly one allreduce when P > 1 (the step's single sync point).
+template <int S>
+static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, const double* Y,
+                          int ip) {
+  const bool gl = (ip == LSBA_IP_GLOBAL);
+  {
+    const int gx = gl ? J : J * (S / GramTA<S>::value);
+    int P = std::max(1, std::min(cdiv(std::max(c->n, 1), 256), cdiv(kGramCtas, gx)));
+    const size_t E = gl ? (size_t)J : (size_t)J * S * S;
+    if ((size_t)P * E > c->part_cap) P = std::max(1, (int)(c->part_cap / E));
+    {
+      LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * J + ((X + (size_t)(J - 1) * xstride == Y) ? 0.0 : 8.0 * c->n * S));
+      dim3 grid(gx, P);
+      if (gl)
+        k_gram_gl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part);
+      else
+        k_gram_cl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part);
+      CKL();
+    }
+    {
+      LaunchScope Ls(c, LSBA_K_GRAM_FINALIZE, 8.0 * P * E);
+      k_gram_finalize<<<cdiv(E, 128), 128, 0, c->stream>>>(P, (int)E, c->d_part, c->d_G,
+                                                           gl ? 1.0 / S : 1.0);
+      CKL();
+    }
+  }
+  if (c->nranks > 1) {
+    const size_t E = gl ? (size_t)J : (size_t)J * S * S;
+    CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+  }
+  return LSBA_OK;
+}
+
+// ---------------------------------------------------------------- a4/a6: projection
+template <int S>
+static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0,
+                             const double* C0, const double* base0, double* out0, int J1,
+                             const double* C1, double* out1, const int* flag_ptr, int kid) {
+  const bool gl = (c->ip == LSBA_IP_GLOBAL);
+  const size_t CB = gl ? 1 : (size_t)S * S;
+  const size_t smem = (size_t)(J0 + J1) * CB * sizeof(double);
+  if (smem > 200 * 1024 && J0 > 0 && J1 > 0) {
+    // too many coefficients for one CTA's shared memory: two passes
+    TRY(project_t<S>(c, X, xstride, J0, C0, base0, out0, 0, nullptr, nullptr, flag_ptr, kid));
+    return project_t<S>(c, X, xstride, 0, nullptr, nullptr, nullptr, J1, C1, out1, flag_ptr, kid);
+  }
+  const int Jmax = std::max(J0, J1);
+  const double bytes = 8.0 * c->n * S * (Jmax + (J0 > 0) + (J1 > 0) + (base0 ? 1 : 0));
+  LaunchScope Ls(c, kid, bytes);
+  if (c->n == 0) return LSBA_OK;
+  if (gl) {
+    auto fn = k_project<S, true>;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<cdiv(c->n, kThreads), kThreads, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0,
+                                                             J1, C1, out1, flag_ptr);
+  } else {
+    auto fn = k_project<S, false>;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<cdiv(c->n, kThreads), kThreads, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0,
+                                                             J1, C1, out1, flag_ptr);
+  }
+  CKL();
+  return LSBA_OK;
+}
+
+// dispatch wrappers (runtime s)
+static lsba_status spmm(lsba_ctx c, const double* V, double* W) { LSBA_DISPATCH_S(c->s, spmm_t, c, V, W); }
+static lsba_status residual(lsba_ctx c, const double* Bm, const double* X, double* out) {
+  LSBA_DISPATCH_S(c->s, residual_t, c, Bm, X, out);
+}
+static lsba_status gram(lsba_ctx c, const double* X, size_t xstride, int J, const double* Y, int ip) {
+  LSBA_DISPATCH_S(c->s, gram_t, c, X, xstride, J, Y, ip);
+}
+static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, const double* C0,
+                           const double* base0, double* out0, int J1, const double* C1, double* out1,
+                           const int* flag_ptr, int kid) {
+  LSBA_DISPATCH_S(c->s, project_t, c, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr, kid);
+}
+
+static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot; }
+
+static lsba_status small_step(lsba_ctx c, int k, int force) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
+  k_small_step<<<1, 256, 0, c->stream>>>(c->st, c->d_G, k, force, rfac);
+  CKL();
+  return LSBA_OK;
+}
+
+static lsba_status read_status(lsba_ctx c, StepStatus* out) {
+  CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *out = *c->h_status;
+  return LSBA_OK;
+}
+
+// IO(U) with U in slot 0: Gram (1 sync), chol, scale in place.  (Alg 3 line 1)
+static lsba_status io_begin(lsba_ctx c, StepStatus* stt) {
+  TRY(gram(c, slotp(c, 0), c->slot, 1, slotp(c, 0), c->ip));
+  TRY(small_step(c, 0, 0));
+  TRY(project(c, slotp(c, 0), c->slot, 1, c->st.coef, nullptr, slotp(c, 0), 0, nullptr, nullptr,
+              c->st.flag_dev, LSBA_K_PROJECT));
+  TRY(read_status(c, stt));
+  c->k = 0;
+  c->flagged = stt->flag != 0;
+  return LSBA_OK;
+}
+
+// One Alg-3 step k (1-based) on the current cycle.
+static lsba_status pip_step(lsba_ctx c, int k, int force, StepStatus* stt) {
+  TRY(spmm(c, slotp(c, k - 1), slotp(c, k)));                                  // line 3
+  TRY(gram(c, slotp(c, 0), c->slot, k + 1, slotp(c, k), c->ip));                // line 4 (1 sync)
+  TRY(small_step(c, k, force));                                                  // line 5
+  TRY(project(c, slotp(c, 0), c->slot, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
+              nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
+  TRY(read_status(c, stt));
+  return LSBA_OK;
+}
+
+static lsba_status set_identity(lsba_ctx c) {
+  LaunchScope Ls(c, LSBA_K_MISC, 0.0);
+  k_set_identity<<<1, 256, 0, c->stream>>>(c->st.Cacc, c->b);
+  CKL();
+  return LSBA_OK;
+}
+
+static lsba_status cycle_solve(lsba_ctx c, int k, int gmres, int happy, int* singular) {
+  {
+    LaunchScope Ls(c, LSBA_K_CYCLE_SOLVE, 0.0);
+    k_cycle_solve<<<1, 512, 0, c->stream>>>(c->st, k, gmres, happy, c->d_work, c->d_Y, c->d_Z, c->d_info);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *singular = c->h_info[0];
+  return LSBA_OK;
+}
+
+static lsba_status read_scalar(lsba_ctx c, double* v) {
+  CK(cudaMemcpyAsync(c->h_scalar, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *v = *c->h_scalar;
+  return LSBA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// the restarted solver (mirrors oracle.solve step by step)
+// ------------------------------------------------------------------------------------------
+static void set_ip(lsba_ctx c, int ip) {
+  c->ip = ip;
+  c->b = (ip == LSBA_IP_GLOBAL) ? 1 : c->s;
+  c->st.b = c->b;
+}
+
+static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, double tol,
+                              int max_restarts, int gmres, int ip, double tau,
+                              lsba_solve_info* info) {
+  if (!c) return LSBA_E_ARG;
+  if (!info) return fail(c, LSBA_E_ARG, "info is NULL");
+  if (m < 1 || m > c->m_max) return fail(c, LSBA_E_ARG, "m=%d outside [1, m_max=%d]", m, c->m_max);
+  if (!(tol > 0.0)) return fail(c, LSBA_E_ARG, "tol must be > 0");
+  if (max_restarts < 0) return fail(c, LSBA_E_ARG, "max_restarts < 0");
+  if (ip != LSBA_IP_CLASSICAL && ip != LSBA_IP_GLOBAL) return fail(c, LSBA_E_ARG, "bad inner product");
+  if (c->n > 0 && (!B || !X)) return fail(c, LSBA_E_ARG, "B/X is NULL");
+  if (((uintptr_t)B | (uintptr_t)X) & 15) return fail(c, LSBA_E_ARG, "B/X not 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t launches0 = c->launches;
+  std::memset(info, 0, sizeof *info);
+  info->true_relres = NAN;
+  info->res_est = NAN;
+  set_ip(c, ip);
+  c->forced_done = false;
+  c->k = -1;
+  c->flagged = false;
+  auto finish = [&]() {
+    info->restarts = info->cycles > 0 ? info->cycles - 1 : 0;
+    info->syncs = (int64_t)info->iterations + info->cycles;
+    info->matvecs = info->iterations;
+    info->basis_evals = 3 * (int64_t)info->iterations;
+    info->kernel_launches = c->launches - launches0;
+    info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+
+  // ||B||_F^2 = s * <B,B>_gl  (R18: tolerance relative to ||B||_F)
+  TRY(gram(c, B, 0, 1, B, LSBA_IP_GLOBAL));
+  CK(cudaMemcpyAsync(c->h_scalar, c->d_G, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const double normB = std::sqrt(std::max(0.0, *c->h_scalar * c->s));
+  if (normB == 0.0) {  // B = 0: X = 0 exactly
+    if (c->n > 0) CK(cudaMemsetAsync(X, 0, sizeof(double) * c->slot, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    info->outcome = LSBA_CONVERGED;
+    info->true_relres = 0.0;
+    info->m_final = m;
+    finish();
+    return LSBA_OK;
+  }
+  // explicit relative residual of Xv; R = B - A Xv written to out_R
+  auto true_relres = [&](const double* Xv, double* out_R, double* rel) -> lsba_status {
+    TRY(residual(c, B, Xv, out_R));
+    double r2;
+    TRY(read_scalar(c, &r2));
+    *rel = std::sqrt(std::max(0.0, r2)) / normB;
+    return LSBA_OK;
+  };
+
+  TRY(residual(c, B, X, slotp(c, 0)));   // U = B - A X0 (R13)
+  TRY(set_identity(c));                   // C_acc = I
+  int m_cur = m;
+  StepStatus stt;
+  info->outcome = LSBA_MAX_RESTARTS;
+  bool finished = false;
+  for (int cycle = 1; cycle <= max_restarts + 1 && !finished; ++cycle) {
+    info->cycles = cycle;
+    TRY(io_begin(c, &stt));                                  // [V_1, beta] = IO(U)
+    if (stt.flag) { info->outcome = LSBA_DEAD; break; }      // R4
+    int k_used = 0;
+    enum { W_NONE, W_FLAG, W_CONV, W_KAPPA, W_M } why = W_NONE;
+    for (int k = 1; k <= m_cur; ++k) {
+      info->attempted_steps++;
+      const bool force = (c->force_flag_k > 0 && !c->forced_done && k == c->force_flag_k);
+      if (force) c->forced_done = true;
+      TRY(pip_step(c, k, force ? 1 : 0, &stt));
+      if (stt.flag || stt.proj_singular) {
+        if (!force) {
+          // R7: happy-breakdown candidate with H_{k+1,k} := 0 (M = 0), checked explicitly
+          int sing = 1;
+          TRY(cycle_solve(c, k, 0, 1, &sing));
+          if (!sing) {
+            TRY(project(c, slotp(c, 0), c->slot, k, c->d_Y, X, c->d_Xc, 0, nullptr, nullptr,
+                        nullptr, LSBA_K_COMBINE));
+            double rel;
+            TRY(true_relres(c->d_Xc, slotp(c, k), &rel));    // slot k (flagged W) is free
+            if (rel <= tol) {
+              CK(cudaMemcpyAsync(X, c->d_Xc, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+              info->iterations++;
+              info->happy++;
+              info->true_relres = rel;
+              info->outcome = LSBA_CONVERGED;
+              finished = true;
+              break;
+            }
+          }
+        }
+        info->nan_flags++;
+        k_used = k - 1;
+        m_cur = k - 1;                                       // R6
+        why = W_FLAG;
+        break;
+      }
+      info->iterations++;
+      const double est = gmres ? stt.res_gmres : stt.res_fom;
+      info->res_est = est;
+      k_used = k;
+      if (est <= tol * normB) { why = W_CONV; break; }      // R5
+      if (std::isfinite(tau) && stt.kappa_F > tau) {         // R8
+        info->cond_restarts++;
+        why = W_KAPPA;
+        break;
+      }
+      why = W_M;
+    }
+    if (finished) break;
+    if (k_used == 0) { info->outcome = LSBA_DEAD; break; }
+    int sing = 0;
+    TRY(cycle_solve(c, k_used, gmres, 0, &sing));            // Xi, M, cos; C_acc <- cos C_acc
+    if (sing) {
+      fail(c, LSBA_OK, "projected system singular at cycle end (k=%d)", k_used);
+      info->outcome = LSBA_DEAD;
+      break;
+    }
+    if (why == W_CONV) {
+      // X += V_k Xi C_acc, then confirm with the explicit residual (R19)
+      TRY(project(c, slotp(c, 0), c->slot, k_used, c->d_Y, X, X, 0, nullptr, nullptr, nullptr,
+                  LSBA_K_COMBINE));
+      double rel;
+      TRY(true_relres(X, slotp(c, 0), &rel));                // slot 0 <- B - A X
+      if (rel <= tol) {
+        info->true_relres = rel;
+        info->outcome = LSBA_CONVERGED;
+        finished = true;
+        break;
+      }
+      info->false_convergences++;
+      TRY(set_identity(c));                                  // restart from the true residual
+      continue;
+    }
+    // X += V_k Xi C_acc ;  U = V_{k+1} [M; -H_{k+1,k}] -> slot 0
+    TRY(project(c, slotp(c, 0), c->slot, k_used, c->d_Y, X, X, k_used + 1, c->d_Z, slotp(c, 0),
+                nullptr, LSBA_K_COMBINE));
+  }
+  info->m_final = m_cur;
+  if (!(info->outcome == LSBA_CONVERGED)) {
+    double rel;
+    TRY(true_relres(X, slotp(c, 0), &rel));
+    info->true_relres = rel;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  c->k = -1;
+  finish();
+  return LSBA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// host-only helpers (exported)
+// ------------------------------------------------------------------------------------------
+extern "C" lsba_status lsba_csr_validate(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                                         const int32_t* col_idx, const char** msg) {
+  static thread_local char buf[256];
+  auto bad = [&](const char* m) {
+    if (msg) *msg = m;
+    return LSBA_E_ARG;
+  };
+  if (msg) *msg = "";
+  if (n_rows < 0 || n_cols < 0) return bad("negative size");
+  if (!row_ptr) return bad("row_ptr is NULL");
+  if (row_ptr[0] != 0) return bad("row_ptr[0] != 0");
+  for (int64_t i = 0; i < n_rows; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i]) {
+      snprintf(buf, sizeof buf, "row_ptr not monotone at row %lld", (long long)i);
+      return bad(buf);
+    }
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      const int64_t cidx = col_idx[p];
+      if (cidx < 0 || cidx >= n_cols) {
+        snprintf(buf, sizeof buf, "column %lld out of range in row %lld", (long long)cidx, (long long)i);
+        return bad(buf);
+      }
+      if (p > row_ptr[i] && col_idx[p - 1] >= cidx) {
+        snprintf(buf, sizeof buf, "columns not strictly increasing in row %lld", (long long)i);
+        return bad(buf);
+      }
+    }
+  }
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_ghost_plan(int64_t row_begin, int64_t row_end, const int32_t* col_idx,
+                                       int64_t nnz, const int64_t* part, int32_t nranks,
+                                       int32_t* col_local, int64_t* ghost_global, int64_t* n_ghost,
+                                       int64_t* recv_counts) {
+  if (!col_idx && nnz > 0) return LSBA_E_ARG;
+  if (!part || nranks < 1 || !n_ghost || !recv_counts) return LSBA_E_ARG;
+  if (row_end < row_begin) return LSBA_E_ARG;
+  for (int r = 0; r < nranks; ++r)
+    if (part[r + 1] < part[r]) return LSBA_E_ARG;
+  const int64_t n_local = row_end - row_begin;
+  std::vector<int64_t> remote;
+  remote.reserve(1024);
+  for (int64_t p = 0; p < nnz; ++p) {
+    const int64_t cidx = col_idx[p];
+    if (cidx < row_begin || cidx >= row_end) remote.push_back(cidx);
+  }
+  std::sort(remote.begin(), remote.end());
+  remote.erase(std::unique(remote.begin(), remote.end()), remote.end());
+  for (int64_t p = 0; p < nnz; ++p) {
+    const int64_t cidx = col_idx[p];
+    int64_t loc;
+    if (cidx >= row_begin && cidx < row_end) {
+      loc = cidx - row_begin;
+    } else {
+      loc = n_local + (std::lower_bound(remote.begin(), remote.end(), cidx) - remote.begin());
+    }
+    if (loc > INT32_MAX) return LSBA_E_ARG;
+    if (col_local) col_local[p] = (int32_t)loc;
+  }
+  for (int r = 0; r < nranks; ++r) recv_counts[r] = 0;
+  for (size_t g = 0; g < remote.size(); ++g) {
+    const int64_t cidx = remote[g];
+    const int r = (int)(std::upper_bound(part, part + nranks + 1, cidx) - part) - 1;
+    if (r < 0 || r >= nranks) return LSBA_E_ARG;
+    recv_counts[r]++;
+    if (ghost_global) ghost_global[g] = cidx;
+  }
+  *n_ghost = (int64_t)remote.size();
+  return LSBA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// lifecycle
+// ------------------------------------------------------------------------------------------
+extern "C" const char* lsba_status_str(lsba_status st) {
+  switch (st) {
+    case LSBA_OK: return "LSBA_OK";
+    case LSBA_E_ARG: return "LSBA_E_ARG";
+    case LSBA_E_CUDA: return "LSBA_E_CUDA";
+    case LSBA_E_NCCL: return "LSBA_E_NCCL";
+    case LSBA_E_OOM: return "LSBA_E_OOM";
+    case LSBA_E_STATE: return "LSBA_E_STATE";
+  }
+  return "LSBA_E_UNKNOWN";
+}
+
+extern "C" const char* lsba_last_error(lsba_ctx c) { return c ? c->err.c_str() : ""; }
+
+extern "C" lsba_status lsba_get_unique_id(uint8_t id[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  if (!id) return LSBA_E_ARG;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return LSBA_E_NCCL;
+  std::memcpy(id, &u, 128);
+  return LSBA_OK;
+}
+
+template <typename T>
+static lsba_status dalloc(lsba_ctx c, T** p, size_t count) {
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  CK(cudaMalloc((void**)p, bytes));
+  c->ws_bytes += (int64_t)bytes;
+  return LSBA_OK;
+}
+
+static void release(lsba_ctx c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
+                  c->d_part, c->d_G, c->d_small, c->d_work, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
+                  c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  if (c->h_info) cudaFreeHost(c->h_info);
+  if (c->h_scalar) cudaFreeHost(c->h_scalar);
+  for (int k = 0; k < LSBA_K_COUNT; ++k)
+    for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+  if (c->comm) ncclCommDestroy(c->comm);
+}
+
+static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, const int64_t* row_ptr,
+                               const int32_t* col_idx, const double* vals, const uint8_t* nccl_id) {
+  const int64_t n_local = c->row_end - c->row_begin;
+  if (n_local > INT32_MAX / 16) return fail(c, LSBA_E_ARG, "n_local too large");
+  const char* msg = nullptr;
+  if (lsba_csr_validate(n_local, n, row_ptr, col_idx, &msg) != LSBA_OK)
+    return fail(c, LSBA_E_ARG, "invalid CSR: %s", msg);
+  c->nnz = row_ptr[n_local];
+  if (c->nnz > INT32_MAX) return fail(c, LSBA_E_ARG, "local nnz exceeds int32");
+  if (vals == nullptr && c->nnz > 0) return fail(c, LSBA_E_ARG, "vals is NULL");
+  CK(cudaSetDevice(c->device));
+  // ---- NCCL communicator and ghost plan
+  std::vector<int32_t> col_local(c->nnz);
+  std::vector<int64_t> ghost_global;
+  c->send_cnt.assign(c->nranks, 0);
+  c->recv_cnt.assign(c->nranks, 0);
+  c->send_off.assign(c->nranks, 0);
+  c->recv_off.assign(c->nranks, 0);
+  std::vector<int64_t> send_idx;
+  if (c->nranks == 1) {
+    for (int64_t p = 0; p < c->nnz; ++p) col_local[p] = col_idx[p];
+  } else {
+    ncclUniqueId uid;
+    std::memcpy(&uid, nccl_id, 128);
+    CKN(ncclCommInitRank(&c->comm, c->nranks, uid, c->rank));
+    // partition starts
+    int64_t* d_tmp = nullptr;
+    CK(cudaMalloc((void**)&d_tmp, sizeof(int64_t) * (2 * c->nranks + 2 * (size_t)c->nranks * c->nranks + 2)));
+    int64_t mine[2] = {c->row_begin, c->row_end};
+    CK(cudaMemcpy(d_tmp, mine, sizeof mine, cudaMemcpyHostToDevice));
+    CKN(ncclAllGather(d_tmp, d_tmp + 2, 2, ncclInt64, c->comm, c->stream));
+    std::vector<int64_t> rr(2 * c->nranks);
+    CK(cudaMemcpyAsync(rr.data(), d_tmp + 2, sizeof(int64_t) * 2 * c->nranks, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> part(c->nranks + 1);
+    for (int r = 0; r < c->nranks; ++r) {
+      part[r] = rr[2 * r];
+      if (r > 0 && rr[2 * r] != rr[2 * r - 1]) { cudaFree(d_tmp); return fail(c, LSBA_E_ARG, "row ranges not contiguous"); }
+    }
+    part[c->nranks] = rr[2 * c->nranks - 1];
+    if (part[0] != 0 || part[c->nranks] != n) { cudaFree(d_tmp); return fail(c, LSBA_E_ARG, "row ranges do not cover [0,n)"); }
+    ghost_global.resize(std::max<int64_t>(c->nnz, 1));
+    int64_t ng = 0;
+    if (lsba_ghost_plan(c->row_begin, c->row_end, col_idx, c->nnz, part.data(), c->nranks,
+                        col_local.data(), ghost_global.data(), &ng, c->recv_cnt.data()) != LSBA_OK) {
+      cudaFree(d_tmp);
+      return fail(c, LSBA_E_ARG, "ghost plan failed");
+    }
+    ghost_global.resize(ng);
+    c->n_ghost = (int)ng;
+    // everyone's recv counts -> my send counts
+    int64_t* d_cnt = d_tmp + 2 * c->nranks + 2;
+    CK(cudaMemcpy(d_cnt, c->recv_cnt.data(), sizeof(int64_t) * c->nranks, cudaMemcpyHostToDevice));
+    CKN(ncclAllGather(d_cnt, d_cnt + c->nranks, c->nranks, ncclInt64, c->comm, c->stream));
+    std::vector<int64_t> allc((size_t)c->nranks * c->nranks);
+    CK(cudaMemcpyAsync(allc.data(), d_cnt + c->nranks, sizeof(int64_t) * allc.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    int64_t so = 0, ro = 0;
+    for (int r = 0; r < c->nranks; ++r) {
+      c->send_cnt[r] = (r == c->rank) ? 0 : allc[(size_t)r * c->nranks + c->rank];
+      c->send_off[r] = so;
+      so += c->send_cnt[r];
+      c->recv_off[r] = ro;
+      ro += c->recv_cnt[r];
+    }
+    c->n_send = so;
+    CK(cudaFree(d_tmp));
+    // exchange the requested global row lists
+    int64_t *d_req = nullptr, *d_want = nullptr;
+    CK(cudaMalloc((void**)&d_req, sizeof(int64_t) * std::max<int64_t>(ng, 1)));
+    CK(cudaMalloc((void**)&d_want, sizeof(int64_t) * std::max<int64_t>(so, 1)));
+    if (ng) CK(cudaMemcpy(d_req, ghost_global.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice));
+    CKN(ncclGroupStart());
+    for (int r = 0; r < c->nranks; ++r) {
+      if (r == c->rank) continue;
+      if (c->recv_cnt[r] > 0) CKN(ncclSend(d_req + c->recv_off[r], c->recv_cnt[r], ncclInt64, r, c->comm, c->stream));
+      if (c->send_cnt[r] > 0) CKN(ncclRecv(d_want + c->send_off[r], c->send_cnt[r], ncclInt64, r, c->comm, c->stream));
+    }
+    CKN(ncclGroupEnd());
+    send_idx.resize(std::max<int64_t>(so, 1));
+    CK(cudaMemcpyAsync(send_idx.data(), d_want, sizeof(int64_t) * std::max<int64_t>(so, 1), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d_req);
+    cudaFree(d_want);
+    for (int64_t i = 0; i < so; ++i) {
+      send_idx[i] -= c->row_begin;
+      if (send_idx[i] < 0 || send_idx[i] >= n_local) return fail(c, LSBA_E_ARG, "peer requested a row this rank does not own");
+    }
+  }
+  // ---- device CSR
+  std::vector<int32_t> rp32(n_local + 1);
+  for (int64_t i = 0; i <= n_local; ++i) rp32[i] = (int32_t)row_ptr[i];
+  TRY(dalloc(c, &c->d_rp, n_local + 1));
+  TRY(dalloc(c, &c->d_ci, c->nnz));
+  TRY(dalloc(c, &c->d_va, c->nnz));
+  CK(cudaMemcpy(c->d_rp, rp32.data(), sizeof(int32_t) * (n_local + 1), cudaMemcpyHostToDevice));
+  if (c->nnz) {
+    CK(cudaMemcpy(c->d_ci, col_local.data(), sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_va, vals, sizeof(double) * c->nnz, cudaMemcpyHostToDevice));
+  }
+  if (c->nranks > 1) {
+    TRY(dalloc(c, &c->d_ghost, (size_t)c->n_ghost * s));
+    TRY(dalloc(c, &c->d_sendbuf, (size_t)c->n_send * s));
+    TRY(dalloc(c, &c->d_send_idx, c->n_send));
+    std::vector<int32_t> si(std::max<int64_t>(c->n_send, 1));
+    for (int64_t i = 0; i < c->n_send; ++i) si[i] = (int32_t)send_idx[i];
+    if (c->n_send) CK(cudaMemcpy(c->d_send_idx, si.data(), sizeof(int32_t) * c->n_send, cudaMemcpyHostToDevice));
+  }
+  // ---- basis and work buffers
+  c->slot = (size_t)n_local * s;
+  TRY(dalloc(c, &c->d_V, (size_t)(m_max + 1) * c->slot));
+  TRY(dalloc(c, &c->d_Xc, c->slot));
+  c->part_cap = (size_t)(kGramCtas + 16 * (m_max + 1)) * s * s + 2 * (size_t)(m_max + 1) * s * s;
+  TRY(dalloc(c, &c->d_part, c->part_cap));
+  TRY(dalloc(c, &c->d_G, (size_t)(m_max + 1) * s * s));
+  c->sq_cap = std::max(1, cdiv((long)n_local * 16, kThreads));
+  TRY(dalloc(c, &c->d_sq, c->sq_cap));
+  TRY(dalloc(c, &c->d_scalar, 4));
+  // ---- small state (sized for b = s)
+  const int ldH = (m_max + 1) * s;
+  const size_t nH = (size_t)ldH * m_max * s, nBeta = (size_t)s * s, nCoef = 2 * (size_t)(m_max + 1) * s * s,
+               nQv = (size_t)m_max * s * 2 * s, nQt = (size_t)m_max * s, nG = (size_t)ldH * s,
+               nRi = (size_t)ldH * ldH, nSc = 4, nCacc = (size_t)s * s;
+  const size_t total = nH + nBeta + nCoef + nQv + nQt + nG + nRi + nSc + nCacc;
+  TRY(dalloc(c, &c->d_small, total));
+  CK(cudaMemset(c->d_small, 0, sizeof(double) * total));
+  double* q = c->d_small;
+  c->st.Hbar = q; q += nH;
+  c->st.beta = q; q += nBeta;
+  c->st.coef = q; q += nCoef;
+  c->st.qr_v = q; q += nQv;
+  c->st.qr_tau = q; q += nQt;
+  c->st.g = q; q += nG;
+  c->st.Rinv = q; q += nRi;
+  c->st.sc = q; q += nSc;
+  c->st.Cacc = q; q += nCacc;
+  c->st.ldH = ldH;
+  c->st.m = m_max;
+  c->st.b = s;
+  TRY(dalloc(c, &c->st.status, 1));
+  TRY(dalloc(c, &c->st.flag_dev, 1));
+  CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
+  TRY(dalloc(c, &c->d_work, (size_t)m_max * s * m_max * s + 2 * (size_t)m_max * s * s + 16));
+  TRY(dalloc(c, &c->d_Y, (size_t)(m_max + 1) * s * s));
+  TRY(dalloc(c, &c->d_Z, (size_t)(m_max + 1) * s * s));
+  TRY(dalloc(c, &c->d_info, 4));
+  CK(cudaMallocHost((void**)&c->h_status, sizeof(StepStatus)));
+  CK(cudaMallocHost((void**)&c->h_info, sizeof(int) * 4));
+  CK(cudaMallocHost((void**)&c->h_scalar, sizeof(double) * 4));
+  set_ip(c, LSBA_IP_CLASSICAL);
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                                   const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                                   int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                                   const uint8_t* nccl_id, int32_t device, void* cuda_stream) {
+  if (!out) return LSBA_E_ARG;
+  *out = nullptr;
+  lsba_ctx c = new (std::nothrow) lsba_ctx_();
+  if (!c) return LSBA_E_OOM;
+  *out = c;  // returned even on failure so that lsba_last_error works; destroy it
+  if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
+  if (n < s) return fail(c, LSBA_E_ARG, "n < s");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, LSBA_E_ARG, "bad rank/nranks");
+  if (row_begin < 0 || row_end < row_begin || row_end > n) return fail(c, LSBA_E_ARG, "bad row range");
+  if (nranks == 1 && (row_begin != 0 || row_end != n)) return fail(c, LSBA_E_ARG, "nranks == 1 needs rows [0, n)");
+  if (nranks > 1 && !nccl_id) return fail(c, LSBA_E_ARG, "nccl_id required when nranks > 1");
+  if (!row_ptr || (!col_idx && row_end > row_begin)) return fail(c, LSBA_E_ARG, "CSR arrays NULL");
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->n_global = n;
+  c->row_begin = row_begin;
+  c->row_end = row_end;
+  c->n = (int)(row_end - row_begin);
+  c->s = s;
+  c->m_max = m_max;
+  c->rank = rank;
+  c->nranks = nranks;
+  return create_impl(c, n, s, m_max, row_ptr, col_idx, vals, nccl_id);
+}
+
+extern "C" lsba_status lsba_destroy(lsba_ctx c) {
+  if (!c) return LSBA_OK;
+  release(c);
+  delete c;
+  return LSBA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// step API
+// ------------------------------------------------------------------------------------------
+extern "C" lsba_status lsba_arnoldi_begin(lsba_ctx c, const double* B_dev, lsba_ip ip, int32_t* io_flag) {
+  if (!c) return LSBA_E_ARG;
+  if (ip != LSBA_IP_CLASSICAL && ip != LSBA_IP_GLOBAL) return fail(c, LSBA_E_ARG, "bad inner product");
+  if (c->n > 0 && !B_dev) return fail(c, LSBA_E_ARG, "B is NULL");
+  if ((uintptr_t)B_dev & 15) return fail(c, LSBA_E_ARG, "B not 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  set_ip(c, ip);
+  c->forced_done = false;
+  if (c->n > 0)
+    CK(cudaMemcpyAsync(slotp(c, 0), B_dev, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+  TRY(set_identity(c));
+  StepStatus stt;
+  TRY(io_begin(c, &stt));
+  if (io_flag) *io_flag = stt.flag;
+  if (stt.flag) c->k = -1;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_block_arnoldi_step(lsba_ctx c, lsba_step_info* info) {
+  if (!c) return LSBA_E_ARG;
+  if (c->k < 0 || c->flagged) return fail(c, LSBA_E_STATE, "no active Arnoldi process (begin first; a flag ends it)");
+  if (c->k >= c->m_max) return fail(c, LSBA_E_STATE, "basis full (k == m_max)");
+  CK(cudaSetDevice(c->device));
+  const int k = c->k + 1;
+  const bool force = (c->force_flag_k > 0 && !c->forced_done && k == c->force_flag_k);
+  if (force) c->forced_done = true;
+  StepStatus stt;
+  TRY(pip_step(c, k, force ? 1 : 0, &stt));
+  if (stt.flag) c->flagged = true;
+  else c->k = k;
+  if (info) {
+    info->k = k;
+    info->chol_flag = stt.flag;
+    info->cond_est = stt.kappa_F;
+    info->res_est = stt.res_gmres;
+  }
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_copy_hessenberg(lsba_ctx c, double* H_host, int32_t ld) {
+  if (!c || !H_host) return LSBA_E_ARG;
+  if (c->k < 0) return fail(c, LSBA_E_STATE, "no Arnoldi process");
+  const int ncol = (c->k + (c->flagged ? 1 : 0)) * c->b;
+  const int nrow = ncol + c->b;
+  if (ld < nrow) return fail(c, LSBA_E_ARG, "ld < (k+1)b");
+  if (ncol == 0) return LSBA_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpy2DAsync(H_host, sizeof(double) * ld, c->st.Hbar, sizeof(double) * c->st.ldH,
+                       sizeof(double) * nrow, ncol, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_copy_beta(lsba_ctx c, double* beta_host) {
+  if (!c || !beta_host) return LSBA_E_ARG;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(beta_host, c->st.beta, sizeof(double) * c->b * c->b, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_copy_basis_block(lsba_ctx c, int32_t j, double* dst_dev) {
+  if (!c) return LSBA_E_ARG;
+  if (c->k < 0) return fail(c, LSBA_E_STATE, "no Arnoldi process");
+  if (j < 1 || j > c->k + 1) return fail(c, LSBA_E_ARG, "j outside [1, k+1]");
+  if (c->n == 0) return LSBA_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(dst_dev, slotp(c, j - 1), sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// solvers
+// ------------------------------------------------------------------------------------------
+extern "C" lsba_status lsba_bgmres_solve(lsba_ctx c, const double* B, double* X, int32_t m, double tol,
+                                         int32_t max_restarts, lsba_skel skel, lsba_ip ip,
+                                         double cond_threshold, lsba_solve_info* info) {
+  if (!c) return LSBA_E_ARG;
+  if (skel != LSBA_SKEL_BCGS_PIP) return fail(c, LSBA_E_ARG, "only BCGS-PIP is built");
+  return solve_impl(c, B, X, m, tol, max_restarts, 1, ip, cond_threshold, info);
+}
+
+extern "C" lsba_status lsba_bfom_solve(lsba_ctx c, const double* B, double* X, int32_t m, double tol,
+                                       int32_t max_restarts, lsba_skel skel, lsba_ip ip,
+                                       double cond_threshold, lsba_solve_info* info) {
+  if (!c) return LSBA_E_ARG;
+  if (skel != LSBA_SKEL_BCGS_PIP) return fail(c, LSBA_E_ARG, "only BCGS-PIP is built");
+  return solve_impl(c, B, X, m, tol, max_restarts, 0, ip, cond_threshold, info);
+}
+
+extern "C" lsba_status lsba_solve_host(lsba_ctx c, const double* B_host, double* X_host, int32_t m,
+                                       double tol, int32_t max_restarts, int32_t fom, lsba_ip ip,
+                                       double cond_threshold, lsba_solve_info* info) {
+  if (!c) return LSBA_E_ARG;
+  if (c->n > 0 && (!B_host || !X_host)) return fail(c, LSBA_E_ARG, "B/X NULL");
+  CK(cudaSetDevice(c->device));
+  if (!c->d_Bh) {
+    TRY(dalloc(c, &c->d_Bh, c->slot));
+    TRY(dalloc(c, &c->d_Xh, c->slot));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  if (c->n > 0) {
+    CK(cudaMemcpyAsync(c->d_Bh, B_host, sizeof(double) * c->slot, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_Xh, X_host, sizeof(double) * c->slot, cudaMemcpyHostToDevice, c->stream));
+  }
+  TRY(solve_impl(c, c->d_Bh, c->d_Xh, m, tol, max_restarts, fom ? 0 : 1, ip, cond_threshold, info));
+  if (c->n > 0)
+    CK(cudaMemcpyAsync(X_host, c->d_Xh, sizeof(double) * c->slot, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return LSBA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// single kernels, debug and measurement
+// ------------------------------------------------------------------------------------------
+extern "C" lsba_status lsba_spmm(lsba_ctx c, const double* V_dev, double* W_dev) {
+  if (!c) return LSBA_E_ARG;
+  if (c->n > 0 && (!V_dev || !W_dev || V_dev == W_dev)) return fail(c, LSBA_E_ARG, "V/W NULL or aliased");
+  if (((uintptr_t)V_dev | (uintptr_t)W_dev) & 15) return fail(c, LSBA_E_ARG, "V/W not 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  if (c->n > 0) TRY(spmm(c, V_dev, W_dev));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_block_inner_product(lsba_ctx c, const double* V_dev, int32_t nblocks,
+                                                const double* Y_dev, lsba_ip ip, double* G_host) {
+  if (!c || !G_host) return LSBA_E_ARG;
+  if (nblocks < 1 || nblocks > c->m_max + 1) return fail(c, LSBA_E_ARG, "nblocks outside [1, m_max+1]");
+  if (ip != LSBA_IP_CLASSICAL && ip != LSBA_IP_GLOBAL) return fail(c, LSBA_E_ARG, "bad inner product");
+  if (((uintptr_t)V_dev | (uintptr_t)Y_dev) & 15) return fail(c, LSBA_E_ARG, "not 16-byte aligned");
+  CK(cudaSetDevice(c->device));
+  TRY(gram(c, V_dev, c->slot, nblocks, Y_dev, ip));
+  const size_t E = (ip == LSBA_IP_GLOBAL) ? (size_t)nblocks : (size_t)nblocks * c->s * c->s;
+  CK(cudaMemcpyAsync(G_host, c->d_G, sizeof(double) * E, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
+  if (!c) return LSBA_E_ARG;
+  if (k_flag < 0) return fail(c, LSBA_E_ARG, "k_flag < 0");
+  c->force_flag_k = k_flag;
+  c->forced_done = false;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_set_kernel_variant(lsba_ctx c, int32_t variant) {
+  if (!c) return LSBA_E_ARG;
+  if (variant < 0 || variant > 1) return fail(c, LSBA_E_ARG, "variant must be 0 or 1");
+  c->variant = variant;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_profile_enable(lsba_ctx c, int32_t enable) {
+  if (!c) return LSBA_E_ARG;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < LSBA_K_COUNT; ++k) {
+    c->prof.used[k] = 0;
+    c->prof.bytes[k] = 0.0;
+    c->prof.launches[k] = 0;
+  }
+  c->prof.on = enable != 0;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_profile_read(lsba_ctx c, int32_t kid, int64_t* launches, double* ms, double* bytes) {
+  if (!c || kid < 0 || kid >= LSBA_K_COUNT) return LSBA_E_ARG;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (size_t i = 0; i < c->prof.used[kid]; ++i) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, c->prof.ev[kid][i].a, c->prof.ev[kid][i].b));
+    tot += t;
+  }
+  if (launches) *launches = c->prof.launches[kid];
+  if (ms) *ms = tot;
+  if (bytes) *bytes = c->prof.bytes[kid];
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_launch_count(lsba_ctx c, int64_t* launches) {
+  if (!c || !launches) return LSBA_E_ARG;
+  *launches = c->launches;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_workspace_bytes(lsba_ctx c, int64_t* bytes) {
+  if (!c || !bytes) return LSBA_E_ARG;
+  *bytes = c->ws_bytes;
+  return LSBA_OK;
+}

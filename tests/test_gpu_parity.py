@@ -1,0 +1,345 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element or normwise
+(reading R16) on identical seeded inputs.  Tolerances follow BASELINE.json's north star:
+H_k and the basis within relative 1e-10 over the first 5 block steps; final true residuals
+both <= tol; solutions within relative 1e-8 with restart counts within +-1."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(float).eps
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2208_09899_b200 as L
+    return L
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def dev(a):
+    return _torch().from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def ragged_csr(n, seed, maxnnz=9):
+    rng = np.random.default_rng(seed)
+    counts = rng.integers(0, maxnnz, size=n)
+    counts[[0, n // 2, n - 1]] = 0
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    cols = np.concatenate([np.sort(rng.choice(n, size=c, replace=False)) for c in counts]).astype(np.int32)
+    vals = rng.standard_normal(row_ptr[-1])
+    return row_ptr, cols, vals
+
+
+def problems():
+    from lsba_inputs import make_twin, tridiag, tridiag_rhs
+    out = {}
+    for i in (1, 2, 3, 4, 5):
+        p = make_twin(i)
+        out[p.name] = ((p.row_ptr, p.col_idx, p.vals), p.B, p)
+    A = tridiag(100)
+    out["tridiag100"] = (A, tridiag_rhs(100), None)
+    return out
+
+
+PROBS = None
+
+
+def get_problem(name):
+    global PROBS
+    if PROBS is None:
+        PROBS = problems()
+    return PROBS[name]
+
+
+def make_ctx(L, A, n, s, m_max):
+    return L.Context(n, s, m_max, A[0], A[1], A[2])
+
+
+# ------------------------------------------------------------------------- a1 SpMM
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 8, 16])
+@pytest.mark.parametrize("kind", ["ragged", "stencil3d", "random"])
+def test_spmm_parity(L, s, kind):
+    from lsba_inputs import random_sparse, stencil
+    from oracle import lsba_oracle as O
+    if kind == "ragged":
+        A = ragged_csr(1037, seed=s)
+    elif kind == "stencil3d":
+        A = stencil(3, 11, (5.0, 2.0, 1.0))
+    else:
+        A = random_sparse(3000)
+    n = A[0].size - 1
+    V = np.random.default_rng(100 + s).standard_normal((n, s))
+    with make_ctx(L, A, n, s, 2) as ctx:
+        W = ctx.spmm(dev(V)).cpu().numpy()
+    Wo = O.spmm(A[0], A[1], A[2], V)
+    bound = O.spmm(A[0], A[1], np.abs(A[2]), np.abs(V))
+    assert np.all(np.abs(W - Wo) <= 16 * EPS * bound + 1e-300)
+
+
+# ------------------------------------------------------------------------- a2 Gram
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 8, 16])
+@pytest.mark.parametrize("n", [777, 100003])
+def test_block_inner_product_parity(L, ip, s, n):
+    from oracle import lsba_oracle as O
+    J = 5
+    rng = np.random.default_rng(n + s)
+    Vs = rng.standard_normal((J, n, s))
+    Y = rng.standard_normal((n, s))
+    A = (np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32), np.ones(n))
+    with make_ctx(L, A, n, s, J) as ctx:
+        G = L.lsba_block_inner_product(ctx.ctx, dev(Vs), J, dev(Y), ip, s=s)
+    if ip == "cl":
+        Go = O.ip_cl(list(Vs), Y)
+        bound = np.concatenate(list(np.abs(Vs)), axis=1).T @ np.abs(Y)
+    else:
+        Go = O.ip_gl(list(Vs), Y)
+        bound = np.array([np.sum(np.abs(v) * np.abs(Y)) for v in Vs]) / s
+    # plain fp64 tree summation: error <= ~ log2(n) eps sum|x||y| (much smaller in practice)
+    assert np.all(np.abs(G - Go) <= 64 * EPS * bound)
+
+
+# ------------------------------------------------------------------------- a1-a4 one step
+def gpu_steps(L, A, B, ip, nsteps, variant=0):
+    n, s = B.shape
+    b = s if ip == "cl" else 1
+    with make_ctx(L, A, n, s, nsteps) as ctx:
+        L.lsba_set_kernel_variant(ctx.ctx, variant)
+        assert ctx.begin(dev(B), ip) == 0
+        infos = [ctx.step() for _ in range(nsteps)]
+        assert all(i.chol_flag == 0 for i in infos)
+        H = ctx.hessenberg(nsteps, b)
+        beta = ctx.beta(b)
+        Vs = [ctx.basis_block(j).cpu().numpy() for j in range(1, nsteps + 2)]
+    return H, beta, Vs, infos
+
+
+def oracle_steps(A, B, ip, nsteps):
+    from oracle import lsba_oracle as O
+    arn = O.PipArnoldi(A, ip, nsteps, B.shape[1])
+    assert not arn.begin(B)
+    for _ in range(nsteps):
+        assert not arn.step().flag
+    return arn
+
+
+STEP_CASES = [(p, ip) for p in ("tiny_cd2d_16", "lapl2d_64", "cd3d_16", "random_16K", "lapl3d_24", "tridiag100")
+              for ip in ("cl", "gl")]
+
+
+@pytest.mark.parametrize("name,ip", STEP_CASES)
+def test_five_step_parity_free_running(L, name, ip):
+    """North star: H_k and the basis agree to relative 1e-10 over the first 5 block steps
+    (normwise per block column / per block, reading R16)."""
+    A, B, _ = get_problem(name)
+    H, beta, Vs, infos = gpu_steps(L, A, B, ip, 5)
+    arn = oracle_steps(A, B, ip, 5)
+    b = arn.b
+    np.testing.assert_allclose(beta, arn.beta, rtol=1e-12, atol=1e-12 * np.abs(arn.beta).max())
+    for k in range(5):
+        col, colo = H[:, k * b:(k + 1) * b], arn.Hbar[:, k * b:(k + 1) * b]
+        assert np.linalg.norm(col - colo) <= 1e-10 * np.linalg.norm(colo), k
+    for j, (v, vo) in enumerate(zip(Vs, arn.V)):
+        assert np.linalg.norm(v - vo) <= 1e-10 * np.linalg.norm(vo), j
+    # per-step outputs: the incremental GMRES estimate equals the literal one (R11)
+    from oracle import lsba_oracle as O
+    for k in range(1, 6):
+        Xi, M, cos = O.projected_solve(arn.Hbar, arn.beta, k, b, "gmres")
+        Hk1 = arn.Hbar[k * b:(k + 1) * b, (k - 1) * b:k * b]
+        est = O.residual_estimate(M, Hk1, cos, np.eye(b), B.shape[1], b)
+        assert math.isclose(infos[k - 1].res_est, est, rel_tol=1e-9)
+        kap = O.kappa_F(arn.beta, arn.Hbar, k, b)
+        assert math.isclose(infos[k - 1].cond_est, kap, rel_tol=1e-9)
+
+
+@pytest.mark.parametrize("name,ip", [("random_16K", "cl"), ("lapl3d_24", "cl"), ("cd3d_16", "gl")])
+def test_step_parity_teacher_forced(L, name, ip):
+    """One oracle step applied to the GPU's own basis V_1..V_k reproduces the GPU's step k:
+    isolates kernel error from the O(eps kappa^2) amplification."""
+    from oracle import lsba_oracle as O
+    A, B, _ = get_problem(name)
+    H, beta, Vs, _ = gpu_steps(L, A, B, ip, 5)
+    b = B.shape[1] if ip == "cl" else 1
+    for k in (1, 3, 5):
+        res = O.pip_step(A, Vs[:k], ip)
+        Hcol = np.asarray(res.Hcol).reshape(k * b, b)
+        assert np.linalg.norm(H[: k * b, (k - 1) * b:k * b] - Hcol) <= 1e-12 * np.linalg.norm(Hcol)
+        Rg = H[k * b:(k + 1) * b, (k - 1) * b:k * b]
+        Ro = res.R if ip == "cl" else np.array([[res.R]])
+        assert np.linalg.norm(Rg - Ro) <= 1e-12 * np.linalg.norm(Ro)
+        assert np.linalg.norm(Vs[k] - res.V_next) <= 1e-12 * np.linalg.norm(res.V_next)
+
+
+# ------------------------------------------------------------------------- solves
+def run_gpu_solve(L, A, B, m, tol, max_restarts, ip, mod, tau=float("inf"), force=0, X0=None):
+    n, s = B.shape
+    with make_ctx(L, A, n, s, m) as ctx:
+        if force:
+            L.lsba_set_force_flag(ctx.ctx, force)
+        X = dev(np.zeros_like(B) if X0 is None else X0)
+        info = ctx.solve(dev(B), X, m, tol, max_restarts, ip=ip, mod=mod, cond_threshold=tau)
+        return X.cpu().numpy(), info
+
+
+SOLVE_CASES = [
+    ("tiny_cd2d_16", "cl", "gmres", float("inf")),
+    ("tiny_cd2d_16", "gl", "gmres", float("inf")),
+    ("tiny_cd2d_16", "cl", "fom", float("inf")),
+    ("tiny_cd2d_16", "gl", "fom", float("inf")),
+    ("lapl2d_64", "cl", "fom", float("inf")),
+    ("lapl2d_64", "cl", "gmres", float("inf")),
+    ("cd3d_16", "cl", "gmres", 1e8),
+    ("random_16K", "gl", "gmres", float("inf")),
+    ("random_16K", "cl", "gmres", float("inf")),
+    ("lapl3d_24", "cl", "gmres", 1e8),
+]
+
+
+@pytest.mark.parametrize("name,ip,mod,tau", SOLVE_CASES)
+def test_solve_parity(L, name, ip, mod, tau):
+    from oracle import lsba_oracle as O
+    A, B, p = get_problem(name)
+    m, tol = p.m, p.tol
+    Xo, io = O.solve(A, B, m=m, tol=tol, max_restarts=2000, ip=ip, mod=mod, cond_threshold=tau)
+    Xg, ig = run_gpu_solve(L, A, B, m, tol, 2000, ip, mod, tau)
+    assert io.outcome == O.CONVERGED and ig.outcome == L.LSBA_CONVERGED
+    # independent check of the GPU solution's true residual with the oracle's SpMM
+    rel = np.linalg.norm(B - O.spmm(*A, Xg)) / np.linalg.norm(B)
+    assert rel <= tol * (1 + 1e-6) and ig.true_relres <= tol
+    assert abs(ig.cycles - io.cycles) <= 1
+    if (ig.cycles, ig.iterations) == (io.cycles, io.iterations):
+        assert np.linalg.norm(Xg - Xo) <= 1e-8 * np.linalg.norm(Xo)
+    assert ig.nan_flags == io.nan_flags or abs(ig.cycles - io.cycles) <= 1
+    assert ig.syncs == ig.iterations + ig.cycles and ig.matvecs == ig.iterations
+    assert ig.kernel_launches > 0
+
+
+def test_kappa_trigger_path(L):
+    """P17 on the GPU: tridiag(100), cl-BFOM, tau = 1e8 -> cycle 1 ends at k = 15 by kappa_F."""
+    from oracle import lsba_oracle as O
+    A, B, _ = get_problem("tridiag100")
+    Xo, io = O.solve(A, B, m=50, tol=1e-10, max_restarts=50, ip="cl", mod="fom", cond_threshold=1e8)
+    Xg, ig = run_gpu_solve(L, A, B, 50, 1e-10, 50, "cl", "fom", 1e8)
+    assert ig.outcome == L.LSBA_CONVERGED and ig.nan_flags == 0
+    assert (ig.cycles, ig.iterations) == (io.cycles, io.iterations) == (3, 39)
+    assert ig.cond_restarts == io.cond_restarts
+    assert np.linalg.norm(Xg - Xo) <= 1e-8 * np.linalg.norm(Xo)
+
+
+def test_nan_flag_path(L):
+    """P18 on the GPU: the NaN-flag shrinks m and the solve converges (flag step is
+    rounding-sensitive: PAPER.md:388-392)."""
+    A, B, _ = get_problem("tridiag100")
+    Xg, ig = run_gpu_solve(L, A, B, 50, 1e-10, 50, "cl", "fom")
+    assert ig.outcome == L.LSBA_CONVERGED and ig.nan_flags >= 1
+    assert 15 <= ig.m_final <= 36
+    assert ig.true_relres <= 1e-10
+
+
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+def test_forced_flag(L, ip):
+    from oracle import lsba_oracle as O
+    A, B, p = get_problem("tiny_cd2d_16")
+    Xo, io = O.solve(A, B, m=10, tol=1e-8, max_restarts=50, ip=ip, force_flag_at=6)
+    Xg, ig = run_gpu_solve(L, A, B, 10, 1e-8, 50, ip, "gmres", force=6)
+    assert ig.m_final == io.m_final == 5 and ig.nan_flags == io.nan_flags == 1
+    assert (ig.cycles, ig.iterations) == (io.cycles, io.iterations)
+    assert np.linalg.norm(Xg - Xo) <= 1e-8 * np.linalg.norm(Xo)
+
+
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+def test_happy_breakdown_identity(L, ip):
+    from lsba_inputs import identity, rhs
+    n, s = 300, 4
+    A = identity(n)
+    B = rhs(n, s, seed=5)
+    Xg, ig = run_gpu_solve(L, A, B, 5, 1e-10, 5, ip, "gmres")
+    assert ig.outcome == L.LSBA_CONVERGED and ig.happy == 1
+    np.testing.assert_allclose(Xg, B, atol=1e-12)
+
+
+def test_x0_nonzero_and_host_api(L):
+    """R13 (X0 != 0) and the host-buffer entry point used for e2e timing."""
+    from oracle import lsba_oracle as O
+    A, B, p = get_problem("tiny_cd2d_16")
+    X0 = np.random.default_rng(1).standard_normal(B.shape)
+    Xo, io = O.solve(A, B, X0=X0, m=10, tol=1e-8, max_restarts=50)
+    Xg, ig = run_gpu_solve(L, A, B, 10, 1e-8, 50, "cl", "gmres", X0=X0)
+    assert ig.outcome == L.LSBA_CONVERGED and (ig.cycles, ig.iterations) == (io.cycles, io.iterations)
+    assert np.linalg.norm(Xg - Xo) <= 1e-8 * np.linalg.norm(Xo)
+    n, s = B.shape
+    with make_ctx(L, A, n, s, 10) as ctx:
+        Xh = X0.copy()
+        ih = L.lsba_solve_host(ctx.ctx, np.ascontiguousarray(B), Xh, 10, 1e-8, 50)
+    assert ih.outcome == L.LSBA_CONVERGED
+    assert np.linalg.norm(Xh - Xg) <= 1e-12 * np.linalg.norm(Xg)
+
+
+def test_edge_cases(L):
+    from lsba_inputs import identity
+    A = identity(64)
+    # B = 0 -> X = 0, converged, no cycles
+    Xg, ig = run_gpu_solve(L, A, np.zeros((64, 2)), 3, 1e-8, 3, "cl", "gmres")
+    assert ig.outcome == L.LSBA_CONVERGED and not Xg.any()
+    # rank-deficient B -> IO flags -> DEAD (reading R4)
+    B = np.zeros((64, 2))
+    B[:, 0] = 1.0
+    Xg, ig = run_gpu_solve(L, A, B, 3, 1e-8, 3, "cl", "gmres")
+    assert ig.outcome == L.LSBA_DEAD
+    # state errors
+    with make_ctx(L, A, 64, 2, 3) as ctx:
+        with pytest.raises(L.LsbaError) as e:
+            ctx.step()
+        assert e.value.status == 5
+        with pytest.raises(L.LsbaError):
+            ctx.solve(dev(np.ones((64, 2))), dev(np.zeros((64, 2))), 4, 1e-8, 1)   # m > m_max
+        with pytest.raises(L.LsbaError):
+            ctx.solve(dev(np.ones((64, 2))), dev(np.zeros((64, 2))), 2, 0.0, 1)    # tol <= 0
+
+
+def test_s1_and_s16_small_n(L):
+    """Ragged n (not a multiple of any tile) and the extreme block sizes."""
+    from oracle import lsba_oracle as O
+    from lsba_inputs import stencil, rhs
+    for s, N in ((1, 13), (16, 9)):
+        A = stencil(2, N, (3.0, 1.0))
+        n = N * N
+        B = rhs(n, s, seed=s)
+        Xo, io = O.solve(A, B, m=8, tol=1e-9, max_restarts=200)
+        Xg, ig = run_gpu_solve(L, A, B, 8, 1e-9, 200, "cl", "gmres")
+        assert ig.outcome == io.outcome == O.CONVERGED
+        assert abs(ig.cycles - io.cycles) <= 1
+
+
+def test_dfma_variant_matches(L):
+    """Both kernel families (variant 0 auto/DMMA, variant 1 plain DFMA) match the oracle."""
+    from oracle import lsba_oracle as O
+    A, B, _ = get_problem("random_16K")
+    arn = oracle_steps(A, B, "cl", 5)
+    for variant in (0, 1):
+        H, beta, Vs, _ = gpu_steps(L, A, B, "cl", 5, variant=variant)
+        for j, (v, vo) in enumerate(zip(Vs, arn.V)):
+            assert np.linalg.norm(v - vo) <= 1e-10 * np.linalg.norm(vo), (variant, j)
+
+
+def test_profile_and_launch_counters(L):
+    A, B, p = get_problem("tiny_cd2d_16")
+    n, s = B.shape
+    with make_ctx(L, A, n, s, 10) as ctx:
+        L.lsba_profile_enable(ctx.ctx, True)
+        info = ctx.solve(dev(B), dev(np.zeros_like(B)), 10, 1e-8, 50)
+        cnt, ms, by = L.lsba_profile_read(ctx.ctx, "spmm")
+        assert cnt >= info.iterations and ms > 0 and by > 0
+        assert L.lsba_launch_count(ctx.ctx) >= info.kernel_launches > 0
+        assert L.lsba_workspace_bytes(ctx.ctx) > 11 * n * s * 8
