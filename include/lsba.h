@@ -59,6 +59,9 @@ typedef struct {
   int32_t chol_flag;  /* 1 iff chol(Omega - H^T H) flagged (reading R2)  */
   double cond_est;    /* kappa_F of R_{k+1} = [E_1 beta, Hbar_k] (reading R8)               */
   double res_est;     /* BGMRES residual-norm estimate ||g_{k+1}||_F for C_acc = I (Eq normF_Rm) */
+  double res_est_fom; /* BFOM residual-norm estimate ||H_{k+1,k} E_k^T Xi_FOM||_F (Eq normF_Rm, M = 0) */
+  int32_t proj_singular; /* 1 iff the BFOM projected matrix H_k is singular (reading R22)   */
+  int32_t pad_;
 } lsba_step_info;
 
 /* Result of a solve.  Counters follow the paper's accounting (PAPER.md:650 tables):
@@ -114,6 +117,12 @@ lsba_status lsba_arnoldi_begin(lsba_ctx ctx, const double* B_dev, lsba_ip ip, in
  * On a flag the step is not accepted (k does not advance; V_{k+1} is not formed).
  * LSBA_E_STATE if called before arnoldi_begin, after a flag, or when k == m_max. */
 lsba_status lsba_block_arnoldi_step(lsba_ctx ctx, lsba_step_info* info);
+
+/* The projected problem of the current Arnoldi state (after k >= 1 accepted steps, C_acc = I):
+ * Xi = (H_k + M E_k^T)^{-1} E_1 beta (Eq Xm) with M = 0 (fom != 0) or the BGMRES
+ * M of PAPER.md:191, written row-major (k b) x b to Xi_host, and Z = [M; -H_{k+1,k}]
+ * ((k+1) b x b, row-major; Thm 2.4's restart generator coefficients) to Z_host. */
+lsba_status lsba_projected_solve(lsba_ctx ctx, int32_t fom, double* Xi_host, double* Z_host);
 
 /* Copy the block Hessenberg Hbar_k ((k+1)b x kb, b = s classical / 1 global) to host,
  * column-major with leading dimension ld >= (k+1)b.  Also valid after a flag (the flagged

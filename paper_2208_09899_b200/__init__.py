@@ -26,6 +26,7 @@ from ._lib import (  # noqa: F401
     lsba_arnoldi_begin,
     lsba_block_arnoldi_step,
     lsba_copy_hessenberg,
+    lsba_projected_solve,
     lsba_copy_beta,
     lsba_copy_basis_block,
     lsba_bgmres_solve,

@@ -29,7 +29,8 @@ _IP = {"cl": LSBA_IP_CLASSICAL, "gl": LSBA_IP_GLOBAL, 0: 0, 1: 1}
 
 class StepInfo(C.Structure):
     _fields_ = [("k", C.c_int32), ("chol_flag", C.c_int32), ("cond_est", C.c_double),
-                ("res_est", C.c_double)]
+                ("res_est", C.c_double), ("res_est_fom", C.c_double), ("proj_singular", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class SolveInfo(C.Structure):
@@ -53,6 +54,7 @@ _sigs = {
     "lsba_arnoldi_begin": [_vp, _vp, C.c_int, C.POINTER(_i32)],
     "lsba_block_arnoldi_step": [_vp, C.POINTER(StepInfo)],
     "lsba_copy_hessenberg": [_vp, _vp, _i32],
+    "lsba_projected_solve": [_vp, _i32, _vp, _vp],
     "lsba_copy_beta": [_vp, _vp],
     "lsba_copy_basis_block": [_vp, _i32, _vp],
     "lsba_bgmres_solve": [_vp, _vp, _vp, _i32, _d, _i32, C.c_int, C.c_int, _d, C.POINTER(SolveInfo)],
@@ -160,6 +162,13 @@ def lsba_copy_hessenberg(ctx, nrows, ncols):
     H = np.zeros((ncols, nrows))        # column-major (ld = nrows) == C-order transpose
     _check(lib.lsba_copy_hessenberg(ctx, _hptr(H), int(nrows)), ctx)
     return H.T.copy()
+
+
+def lsba_projected_solve(ctx, k, b, fom=False):
+    Xi = np.zeros((k * b, b))
+    Z = np.zeros(((k + 1) * b, b))
+    _check(lib.lsba_projected_solve(ctx, 1 if fom else 0, _hptr(Xi), _hptr(Z)), ctx)
+    return Xi, Z
 
 
 def lsba_copy_beta(ctx, b):

@@ -283,7 +283,7 @@ k_gram_gl(int n, const double* __restrict__ X, size_t xstride, int J,
 }
 
 // G[e] = scale * sum_{p=0..P-1} part[p][e]   (fixed order: deterministic, rank-independent)
-__global__ void k_gram_finalize(int P, int E, const double* __restrict__ part,
+static __global__ void k_gram_finalize(int P, int E, const double* __restrict__ part,
                                 double* __restrict__ G, double scale) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
@@ -293,7 +293,7 @@ __global__ void k_gram_finalize(int P, int E, const double* __restrict__ part,
 }
 
 // sum of partials -> out[0] (single thread block, fixed order)
-__global__ void k_sum_partials(int P, const double* __restrict__ part, double* __restrict__ out) {
+static __global__ void k_sum_partials(int P, const double* __restrict__ part, double* __restrict__ out) {
   __shared__ double red[kThreads];
   double t = 0.0;
   const int chunk = (P + blockDim.x - 1) / blockDim.x;
@@ -377,15 +377,7 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
 }
 
 // ------------------------------------------------------------------------------------------
-// Small-state kernels (one CTA).  State layout (column-major small matrices, fp64):
-//   Hbar  : ((m+1)b) x (m b), ld = ldH = (m+1)b         block upper Hessenberg (D3)
-//   beta  : b x b                                        IO factor of the cycle's start block
-//   coef  : ((k+1)b) x b row-major [j][a][c]             projection coefficients
-//   qr_v  : m x b x 2b, qr_tau: m x b                    Householder reflectors of Hbar's QR
-//   g     : ((m+1)b) x b, ld = ldH                       Q^T (E_1 beta) (reading R11)
-//   Rinv  : ((m+1)b)^2, ld = ldH                         R_{k+1}^{-1}, R_{k+1} = [E_1 beta, Hbar_k] (R8)
-//   sc[]  : scalars: [0] ||R||_F^2, [1] ||R^{-1}||_F^2
-//   Cacc  : b x b                                        accumulated cospatial product (R10)
+// small-state helpers shared with small.cuh
 // ------------------------------------------------------------------------------------------
 struct StepStatus {
   int32_t k;
@@ -398,16 +390,10 @@ struct StepStatus {
   double normU2;         // IO only: ||U||_F^2 (k == 0)
 };
 
-struct SmallState {
-  double* Hbar; double* beta; double* coef; double* qr_v; double* qr_tau; double* g;
-  double* Rinv; double* sc; double* Cacc; StepStatus* status; int* flag_dev;
-  int ldH; int m; int b;
-};
-
 constexpr int kMaxB = 16;
 
 // block-wide sum (blockDim multiple of 32, <= 1024); all threads get the result
-__device__ double block_sum(double v, double* red) {
+__device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
@@ -419,472 +405,7 @@ __device__ double block_sum(double v, double* red) {
   return t;
 }
 
-// Upper Cholesky with NaN-flag (reading R2), sequential; S symmetric b x b, column-major.
-__device__ bool chol_upper(const double* S, double* R, int b) {
-  for (int x = 0; x < b * b; ++x) R[x] = 0.0;
-  for (int j = 0; j < b; ++j) {
-    double d = S[j + j * b];
-    for (int i = 0; i < j; ++i) d -= R[i + j * b] * R[i + j * b];
-    if (!(d > 0.0) || !isfinite(d)) return true;
-    const double r = sqrt(d);
-    R[j + j * b] = r;
-    for (int c = j + 1; c < b; ++c) {
-      double t = S[j + c * b];
-      for (int i = 0; i < j; ++i) t -= R[i + j * b] * R[i + c * b];
-      R[j + c * b] = t / r;
-    }
-  }
-  for (int x = 0; x < b * b; ++x)
-    if (!isfinite(R[x])) return true;
-  return false;
-}
-
-// Householder (LAPACK dlarfg convention): x (len) -> v (v[0]=1), tau, beta.
-__device__ void house(const double* x, int len, double* v, double* tau, double* beta_out) {
-  double alpha = x[0];
-  double xn2 = 0.0;
-  for (int i = 1; i < len; ++i) xn2 += x[i] * x[i];
-  v[0] = 1.0;
-  if (xn2 == 0.0) {
-    *tau = 0.0;
-    *beta_out = alpha;
-    for (int i = 1; i < len; ++i) v[i] = 0.0;
-    return;
-  }
-  double nrm = sqrt(alpha * alpha + xn2);
-  double beta = (alpha >= 0.0) ? -nrm : nrm;
-  *tau = (beta - alpha) / beta;
-  const double sc = 1.0 / (alpha - beta);
-  for (int i = 1; i < len; ++i) v[i] = x[i] * sc;
-  *beta_out = beta;
-}
-
-// Solve the b x b system Hm X = Gm (column-major, in place copies) by Gaussian elimination
-// with partial pivoting (sequential).  Returns true if singular.
-__device__ bool small_solve(double* Hm, double* Gm, int b) {
-  for (int p = 0; p < b; ++p) {
-    int piv = p;
-    double best = fabs(Hm[p + p * b]);
-    for (int r = p + 1; r < b; ++r)
-      if (fabs(Hm[r + p * b]) > best) { best = fabs(Hm[r + p * b]); piv = r; }
-    if (!(best > 0.0) || !isfinite(best)) return true;
-    if (piv != p) {
-      for (int c = 0; c < b; ++c) { double t = Hm[p + c * b]; Hm[p + c * b] = Hm[piv + c * b]; Hm[piv + c * b] = t; }
-      for (int c = 0; c < b; ++c) { double t = Gm[p + c * b]; Gm[p + c * b] = Gm[piv + c * b]; Gm[piv + c * b] = t; }
-    }
-    const double d = Hm[p + p * b];
-    for (int r = p + 1; r < b; ++r) {
-      const double f = Hm[r + p * b] / d;
-      for (int c = p; c < b; ++c) Hm[r + c * b] -= f * Hm[p + c * b];
-      for (int c = 0; c < b; ++c) Gm[r + c * b] -= f * Gm[p + c * b];
-    }
-  }
-  for (int c = 0; c < b; ++c)
-    for (int r = b - 1; r >= 0; --r) {
-      double t = Gm[r + c * b];
-      for (int q = r + 1; q < b; ++q) t -= Hm[r + q * b] * Gm[q + c * b];
-      Gm[r + c * b] = t / Hm[r + r * b];
-    }
-  for (int x = 0; x < b * b; ++x)
-    if (!isfinite(Gm[x])) return true;
-  return false;
-}
-
-// a3 + a5: one block, blockDim = 256.  k >= 1: step k; k == 0: IO of the cycle's start block.
-// G: ((k+1)b) x b row-major (classical) or k+1 scalars (global, already scaled by 1/s).
-// rfac: sqrt(s) for global (residual norms), 1 for classical.
-__global__ void __launch_bounds__(256)
-k_small_step(SmallState st, const double* __restrict__ G, int k, int force_flag, double rfac) {
-  const int b = st.b, ldH = st.ldH;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ double S_[kMaxB * kMaxB], R_[kMaxB * kMaxB], Ri_[kMaxB * kMaxB];
-  __shared__ double col_[2 * kMaxB * kMaxB], tmpA[kMaxB * kMaxB], tmpB[kMaxB * kMaxB];
-  __shared__ double red[32];
-  __shared__ int flag_s;
-  const int kb = k * b;
-  // Hcol -> Hbar column block k-1 (rows 0..kb-1); G is row-major [(row) * b + col]
-  if (k > 0)
-    for (int e = tid; e < kb * b; e += nt) {
-      const int r = e / b, c = e % b;
-      st.Hbar[r + (size_t)((k - 1) * b + c) * ldH] = G[e];
-    }
-  // S = Omega - Hcol^T Hcol, symmetrised (R2); column-major b x b
-  for (int e = tid; e < b * b; e += nt) {
-    const int x = e % b, y = e / b;
-    double t = G[(size_t)(kb + x) * b + y];
-    for (int r = 0; r < kb; ++r) t -= G[(size_t)r * b + x] * G[(size_t)r * b + y];
-    tmpA[x + y * b] = t;
-  }
-  __syncthreads();
-  for (int e = tid; e < b * b; e += nt) {
-    const int x = e % b, y = e / b;
-    S_[x + y * b] = 0.5 * (tmpA[x + y * b] + tmpA[y + x * b]);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    bool f = chol_upper(S_, R_, b);
-    if (force_flag) f = true;
-    flag_s = f ? 1 : 0;
-    *st.flag_dev = flag_s;
-    if (f && k > 0)  // flagged step: no H_{k+1,k}; keep Hbar's subdiagonal block clean
-      for (int x = 0; x < b; ++x)
-        for (int y = 0; y < b; ++y) st.Hbar[(kb + x) + (size_t)((k - 1) * b + y) * ldH] = 0.0;
-    st.status->k = k;
-    st.status->flag = flag_s;
-    st.status->proj_singular = 0;
-    st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
-    if (k == 0) {
-      double tr = 0.0;
-      for (int x = 0; x < b; ++x) tr += G[x * b + x];
-      st.status->normU2 = tr * (rfac * rfac);
-    }
-  }
-  __syncthreads();
-  if (flag_s) return;
-  // R^{-1} (upper triangular), column c by back substitution (threads over columns)
-  if (tid < b) {
-    const int c = tid;
-    for (int r = b - 1; r >= 0; --r) {
-      double t = (r == c) ? 1.0 : 0.0;
-      for (int q = r + 1; q <= c; ++q) t -= R_[r + q * b] * Ri_[q + c * b];
-      Ri_[r + c * b] = (r <= c) ? t / R_[r + r * b] : 0.0;
-    }
-    for (int r = c + 1; r < b; ++r) Ri_[r + c * b] = 0.0;
-  }
-  __syncthreads();
-  // projection coefficients, row-major [(row)*b + c]: rows < kb: -Hcol R^{-1}; then R^{-1}
-  for (int e = tid; e < (kb + b) * b; e += nt) {
-    const int r = e / b, c = e % b;
-    double t;
-    if (r < kb) {
-      t = 0.0;
-      for (int q = 0; q <= c; ++q) t -= G[(size_t)r * b + q] * Ri_[q + c * b];
-    } else {
-      t = Ri_[(r - kb) + c * b];
-    }
-    st.coef[e] = t;
-  }
-  if (k == 0) {
-    // IO: beta = R; QR / kappa state of the cycle start: g = E_1 beta, R_1^{-1} = beta^{-1}
-    for (int e = tid; e < b * b; e += nt) {
-      const int x = e % b, y = e / b;
-      st.beta[e] = R_[e];
-      st.Rinv[x + (size_t)y * ldH] = Ri_[e];
-    }
-    for (int e = tid; e < (st.m + 1) * b * b; e += nt) {
-      const int r = e % ((st.m + 1) * b), c = e / ((st.m + 1) * b);
-      st.g[r + (size_t)c * ldH] = (r < b) ? R_[r + c * b] : 0.0;
-    }
-    double nr = 0.0, ni = 0.0;
-    for (int e = tid; e < b * b; e += nt) { nr += R_[e] * R_[e]; ni += Ri_[e] * Ri_[e]; }
-    nr = block_sum(nr, red);
-    ni = block_sum(ni, red);
-    if (tid == 0) { st.sc[0] = nr; st.sc[1] = ni; st.status->kappa_F = sqrt(nr * ni); }
-    return;
-  }
-  // store H_{k+1,k} = R into Hbar
-  for (int e = tid; e < b * b; e += nt) {
-    const int x = e % b, y = e / b;
-    st.Hbar[(kb + x) + (size_t)((k - 1) * b + y) * ldH] = R_[e];
-  }
-  __syncthreads();
-  // ---- incremental Householder QR of Hbar (reading R11) ----
-  // new column c ((k+1)b x b) -> col_ local copy of the last two block rows after applying
-  // reflectors 1..k-1 (reflector j acts on block rows j-1, j).  Thread per column of c.
-  // We only need block rows k-1 and k of the transformed column at the end, but the
-  // transformation sweeps down the column, so carry a 2b window.
-  if (tid < b) {
-    const int c = tid;
-    // window holds rows [(j-1)b, (j+1)b) of the working column; start with j = 1
-    double win[2 * kMaxB];
-    for (int r = 0; r < 2 * b; ++r) {
-      const int gr = r;
-      win[r] = (gr < kb + b) ? st.Hbar[gr + (size_t)((k - 1) * b + c) * ldH] : 0.0;
-    }
-    for (int j = 1; j <= k - 1; ++j) {
-      const double* V = st.qr_v + (size_t)(j - 1) * b * 2 * b;
-      const double* T = st.qr_tau + (size_t)(j - 1) * b;
-      for (int q = 0; q < b; ++q) {
-        const double* v = V + (size_t)q * 2 * b;
-        double d = 0.0;
-        for (int r = q; r < 2 * b; ++r) d += v[r] * win[r];
-        d *= T[q];
-        for (int r = q; r < 2 * b; ++r) win[r] -= d * v[r];
-      }
-      // top block row of the window is final (an R entry, not needed): shift down by b
-      for (int r = 0; r < b; ++r) win[r] = win[b + r];
-      for (int r = 0; r < b; ++r) {
-        const int gr = (j + 1) * b + r;
-        win[b + r] = (gr < kb + b) ? st.Hbar[gr + (size_t)((k - 1) * b + c) * ldH] : 0.0;
-      }
-    }
-    for (int r = 0; r < 2 * b; ++r) col_[r + c * 2 * b] = win[r];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // FOM estimate: h~ = col_ rows 0..b-1, g^ = g rows (k-1)b..kb-1 (before reflector k)
-    for (int x = 0; x < b; ++x)
-      for (int y = 0; y < b; ++y) {
-        tmpA[x + y * b] = col_[x + y * 2 * b];
-        tmpB[x + y * b] = st.g[((k - 1) * b + x) + (size_t)y * ldH];
-      }
-    const bool sing = small_solve(tmpA, tmpB, b);   // tmpB <- h~^{-1} g^
-    st.status->proj_singular = sing ? 1 : 0;
-    double rf = nan("");
-    if (!sing) {
-      // ||R cos C_acc||_F with R = H_{k+1,k} (upper) ; tmpA <- cos C_acc
-      double acc2 = 0.0;
-      for (int x = 0; x < b; ++x)
-        for (int y = 0; y < b; ++y) {
-          double t = 0.0;
-          for (int q = 0; q < b; ++q) t += tmpB[x + q * b] * st.Cacc[q + y * b];
-          tmpA[x + y * b] = t;
-        }
-      for (int x = 0; x < b; ++x)
-        for (int y = 0; y < b; ++y) {
-          double t = 0.0;
-          for (int q = x; q < b; ++q) t += R_[x + q * b] * tmpA[q + y * b];
-          acc2 += t * t;
-        }
-      rf = sqrt(acc2) * rfac;
-    }
-    st.status->res_fom = rf;
-    // Householder QR of the 2b x b stack col_ -> reflectors for block column k
-    double* Vk = st.qr_v + (size_t)(k - 1) * b * 2 * b;
-    double* Tk = st.qr_tau + (size_t)(k - 1) * b;
-    for (int q = 0; q < b; ++q) {
-      double* v = Vk + (size_t)q * 2 * b;
-      for (int r = 0; r < q; ++r) v[r] = 0.0;
-      double tau, beta_;
-      house(col_ + q + q * 2 * b, 2 * b - q, v + q, &tau, &beta_);
-      Tk[q] = tau;
-      // apply to remaining columns of the stack
-      for (int c = q; c < b; ++c) {
-        double d = 0.0;
-        for (int r = q; r < 2 * b; ++r) d += v[r] * col_[r + c * 2 * b];
-        d *= tau;
-        for (int r = q; r < 2 * b; ++r) col_[r + c * 2 * b] -= d * v[r];
-      }
-      // apply to g rows (k-1)b .. (k+1)b-1
-      for (int c = 0; c < b; ++c) {
-        double* gc = st.g + (size_t)c * ldH + (k - 1) * b;
-        double d = 0.0;
-        for (int r = q; r < 2 * b; ++r) d += v[r] * gc[r];
-        d *= tau;
-        for (int r = q; r < 2 * b; ++r) gc[r] -= d * v[r];
-      }
-    }
-    // GMRES estimate: ||g_{k+1} C_acc||_F
-    double acc2 = 0.0;
-    for (int x = 0; x < b; ++x)
-      for (int y = 0; y < b; ++y) {
-        double t = 0.0;
-        for (int q = 0; q < b; ++q) t += st.g[(kb + x) + (size_t)q * ldH] * st.Cacc[q + y * b];
-        acc2 += t * t;
-      }
-    st.status->res_gmres = sqrt(acc2) * rfac;
-  }
-  // ---- kappa_F update (reading R8): new block column of R_{k+1}^{-1} ----
-  // T = R_k^{-1} Hcol (kb x b), X = -T R^{-1};  Rinv[:, kb..kb+b) = [X; R^{-1}]
-  double part_r = 0.0, part_i = 0.0;
-  for (int e = tid; e < kb * b; e += nt) {
-    const int r = e % kb, c = e / kb;
-    double t = 0.0;
-    // row r of R_k^{-1} is nonzero for columns q >= r (upper triangular)
-    for (int q = r; q < kb; ++q) t += st.Rinv[r + (size_t)q * ldH] * G[(size_t)q * b + c];
-    // store T temporarily in Rinv's new column block (column-major), finished below
-    st.Rinv[r + (size_t)(kb + c) * ldH] = t;
-    part_r += G[(size_t)r * b + c] * G[(size_t)r * b + c];
-  }
-  __syncthreads();
-  for (int e = tid; e < kb * b; e += nt) {
-    const int r = e % kb, c = e / kb;
-    // X[r][c] = - sum_q T[r][q] Ri[q][c], q <= c
-    double t = 0.0;
-    for (int q = 0; q <= c; ++q) t -= st.Rinv[r + (size_t)(kb + q) * ldH] * Ri_[q + c * b];
-    // write into a scratch column-major buffer (qr g column space is busy; use coef tail)
-    st.coef[(kb + b) * b + e] = t;
-  }
-  __syncthreads();
-  for (int e = tid; e < kb * b; e += nt) {
-    const int r = e % kb, c = e / kb;
-    const double x = st.coef[(kb + b) * b + e];
-    st.Rinv[r + (size_t)(kb + c) * ldH] = x;
-    part_i += x * x;
-  }
-  for (int e = tid; e < b * b; e += nt) {
-    const int x = e % b, y = e / b;
-    st.Rinv[(kb + x) + (size_t)(kb + y) * ldH] = Ri_[e];
-    part_i += Ri_[e] * Ri_[e];
-    part_r += R_[e] * R_[e];
-  }
-  const double dr = block_sum(part_r, red);
-  const double di = block_sum(part_i, red);
-  if (tid == 0) {
-    st.sc[0] += dr;
-    st.sc[1] += di;
-    st.status->kappa_F = sqrt(st.sc[0] * st.sc[1]);
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// a5/a6 at cycle end: projected solve by dense LU with partial pivoting (one CTA).
-//   mode 0: FOM      M = 0
-//   mode 1: GMRES    M = H_k^{-T} E_k H_{k+1,k}^T H_{k+1,k}
-//   happy != 0: H_{k+1,k} := 0 (reading R7) -> FOM solution, C_acc not updated
-// Outputs (row-major, [row][c]):  Y = Xi C_acc (kb x b);  Z = [M; -H_{k+1,k}] ((k+1)b x b);
-// then C_acc <- cos C_acc (unless happy).  work: >= (kb)^2 + 2 kb b doubles.
-// info[0] = 1 if singular.
-// ------------------------------------------------------------------------------------------
-__device__ void block_lu_solve(double* Am, int N, double* Bm, int nrhs, int* piv_s,
-                               double* red, int* ired, bool* sing) {
-  // Am column-major N x N (ld N), Bm column-major N x nrhs (ld N); solved in place.
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int p = 0; p < N; ++p) {
-    // pivot search (thread-parallel argmax, deterministic tie-break on index)
-    double best = -1.0;
-    int bi = p;
-    for (int r = p + tid; r < N; r += nt) {
-      const double v = fabs(Am[r + (size_t)p * N]);
-      if (v > best || (v == best && r < bi)) { best = v; bi = r; }
-    }
-    red[tid] = best;
-    ired[tid] = bi;
-    __syncthreads();
-    for (int o = nt / 2; o > 0; o >>= 1) {
-      if (tid < o) {
-        const double v2 = red[tid + o];
-        const int i2 = ired[tid + o];
-        if (v2 > red[tid] || (v2 == red[tid] && i2 < ired[tid])) { red[tid] = v2; ired[tid] = i2; }
-      }
-      __syncthreads();
-    }
-    const int pr = ired[0];
-    const double pv = red[0];
-    __syncthreads();
-    if (!(pv > 0.0) || !isfinite(pv)) { *sing = true; return; }
-    if (pr != p) {
-      for (int c = tid; c < N; c += nt) {
-        const double t = Am[p + (size_t)c * N];
-        Am[p + (size_t)c * N] = Am[pr + (size_t)c * N];
-        Am[pr + (size_t)c * N] = t;
-      }
-      for (int c = tid; c < nrhs; c += nt) {
-        const double t = Bm[p + (size_t)c * N];
-        Bm[p + (size_t)c * N] = Bm[pr + (size_t)c * N];
-        Bm[pr + (size_t)c * N] = t;
-      }
-    }
-    __syncthreads();
-    const double d = Am[p + (size_t)p * N];
-    for (int r = p + 1 + tid; r < N; r += nt) Am[r + (size_t)p * N] /= d;
-    __syncthreads();
-    const int rem = N - p - 1;
-    const int tot = rem * (rem + nrhs);
-    for (int e = tid; e < tot; e += nt) {
-      const int r = p + 1 + e % rem;
-      const int c = e / rem;  // 0..rem-1: matrix columns p+1+c; rem..: rhs columns
-      const double l = Am[r + (size_t)p * N];
-      if (c < rem) Am[r + (size_t)(p + 1 + c) * N] -= l * Am[p + (size_t)(p + 1 + c) * N];
-      else         Bm[r + (size_t)(c - rem) * N] -= l * Bm[p + (size_t)(c - rem) * N];
-    }
-    __syncthreads();
-  }
-  // back substitution, column-parallel over rhs, row-sequential
-  for (int r = N - 1; r >= 0; --r) {
-    for (int c = tid; c < nrhs; c += nt) Bm[r + (size_t)c * N] /= Am[r + (size_t)r * N];
-    __syncthreads();
-    const int tot = r * nrhs;
-    for (int e = tid; e < tot; e += nt) {
-      const int q = e % r, c = e / r;
-      Bm[q + (size_t)c * N] -= Am[q + (size_t)r * N] * Bm[r + (size_t)c * N];
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < N * nrhs; e += nt)
-    if (!isfinite(Bm[e])) *sing = true;
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(512)
-k_cycle_solve(SmallState st, int k, int gmres, int happy, double* __restrict__ work,
-              double* __restrict__ Y, double* __restrict__ Z, int* __restrict__ info) {
-  const int b = st.b, ldH = st.ldH, kb = k * b;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  __shared__ double red[512];
-  __shared__ int ired[512];
-  __shared__ bool sing;
-  __shared__ double HtH[kMaxB * kMaxB], cosC[kMaxB * kMaxB];
-  if (tid == 0) sing = false;
-  double* Am = work;                         // kb x kb
-  double* Mm = work + (size_t)kb * kb;       // kb x b  (column-major, ld kb)
-  double* Xi = Mm + (size_t)kb * b;          // kb x b
-  const double* Hk1 = st.Hbar + kb + (size_t)(k - 1) * b * ldH;  // (row kb, col (k-1)b)
-  // HtH = H_{k+1,k}^T H_{k+1,k}  (zero if happy)
-  for (int e = tid; e < b * b; e += nt) {
-    const int x = e % b, y = e / b;
-    double t = 0.0;
-    if (!happy)
-      for (int q = 0; q < b; ++q) t += Hk1[q + (size_t)x * ldH] * Hk1[q + (size_t)y * ldH];
-    HtH[e] = t;
-  }
-  for (int e = tid; e < kb * b; e += nt) Mm[e] = 0.0;
-  __syncthreads();
-  if (gmres && !happy) {
-    // A = H_k^T ; rhs = E_k HtH
-    for (int e = tid; e < kb * kb; e += nt) {
-      const int r = e % kb, c = e / kb;
-      Am[e] = st.Hbar[c + (size_t)r * ldH];
-    }
-    for (int e = tid; e < kb * b; e += nt) {
-      const int r = e % kb, c = e / kb;
-      Mm[e] = (r >= kb - b) ? HtH[(r - (kb - b)) + c * b] : 0.0;
-    }
-    __syncthreads();
-    block_lu_solve(Am, kb, Mm, b, nullptr, red, ired, &sing);
-    __syncthreads();
-  }
-  // A = H_k + M E_k^T ; rhs = E_1 beta
-  for (int e = tid; e < kb * kb; e += nt) {
-    const int r = e % kb, c = e / kb;
-    double t = st.Hbar[r + (size_t)c * ldH];
-    if (c >= kb - b) t += Mm[r + (size_t)(c - (kb - b)) * kb];
-    Am[e] = t;
-  }
-  for (int e = tid; e < kb * b; e += nt) {
-    const int r = e % kb, c = e / kb;
-    Xi[e] = (r < b) ? st.beta[r + c * b] : 0.0;
-  }
-  __syncthreads();
-  block_lu_solve(Am, kb, Xi, b, nullptr, red, ired, &sing);
-  __syncthreads();
-  // Y = Xi C_acc (row-major), Z = [M; -H_{k+1,k}] (row-major)
-  for (int e = tid; e < kb * b; e += nt) {
-    const int r = e / b, c = e % b;
-    double t = 0.0;
-    for (int q = 0; q < b; ++q) t += Xi[r + (size_t)q * kb] * st.Cacc[q + c * b];
-    Y[e] = t;
-  }
-  for (int e = tid; e < (kb + b) * b; e += nt) {
-    const int r = e / b, c = e % b;
-    Z[e] = (r < kb) ? Mm[r + (size_t)c * kb] : -Hk1[(r - kb) + (size_t)c * ldH];
-  }
-  __syncthreads();
-  if (!happy) {
-    // C_acc <- cos C_acc, cos = Xi rows kb-b..kb-1
-    for (int e = tid; e < b * b; e += nt) {
-      const int x = e % b, y = e / b;
-      double t = 0.0;
-      for (int q = 0; q < b; ++q) t += Xi[(kb - b + x) + (size_t)q * kb] * st.Cacc[q + y * b];
-      cosC[e] = t;
-    }
-    __syncthreads();
-    for (int e = tid; e < b * b; e += nt) st.Cacc[e] = cosC[e];
-  }
-  if (tid == 0) info[0] = sing ? 1 : 0;
-}
-
-__global__ void k_set_identity(double* Cm, int b) {
+static __global__ void k_set_identity(double* Cm, int b) {
   const int e = threadIdx.x;
   if (e < b * b) Cm[e] = (e % b == e / b) ? 1.0 : 0.0;
 }

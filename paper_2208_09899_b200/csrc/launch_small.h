@@ -1,0 +1,28 @@
+// launch_small.h — host launchers of the per-B small-state kernels (small.cuh).  Each B is
+// compiled in its own translation unit (small_inst.cu with -DLSBA_B=B) so the 16 fully
+// unrolled instantiations build in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace lsba {
+struct SmallState2;
+
+template <int B>
+cudaError_t launch_step_small(const SmallState2& st, const double* G, int k, int force, double rfac,
+                              cudaStream_t stream);
+template <int B>
+cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy, int upd, double* Y,
+                             double* Z, int* info, cudaStream_t stream);
+
+#define LSBA_DECL_SMALL(B)                                                                              \
+  template <>                                                                                           \
+  cudaError_t launch_step_small<B>(const SmallState2&, const double*, int, int, double, cudaStream_t); \
+  template <>                                                                                           \
+  cudaError_t launch_cycle_end<B>(const SmallState2&, int, int, int, int, double*, double*, int*,     \
+                                  cudaStream_t);
+LSBA_DECL_SMALL(1) LSBA_DECL_SMALL(2) LSBA_DECL_SMALL(3) LSBA_DECL_SMALL(4)
+LSBA_DECL_SMALL(5) LSBA_DECL_SMALL(6) LSBA_DECL_SMALL(7) LSBA_DECL_SMALL(8)
+LSBA_DECL_SMALL(9) LSBA_DECL_SMALL(10) LSBA_DECL_SMALL(11) LSBA_DECL_SMALL(12)
+LSBA_DECL_SMALL(13) LSBA_DECL_SMALL(14) LSBA_DECL_SMALL(15) LSBA_DECL_SMALL(16)
+#undef LSBA_DECL_SMALL
+}  // namespace lsba

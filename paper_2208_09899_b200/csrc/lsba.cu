@@ -21,6 +21,8 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "small.cuh"  // SmallState2 / StepStatus layouts (kernels are in small_inst.cu)
+#include "launch_small.h"
 
 using namespace lsba;
 
@@ -67,9 +69,8 @@ struct lsba_ctx_ {
   size_t part_cap = 0;
   double* d_G = nullptr;
   // small state
-  SmallState st{};
+  SmallState2 st{};
   double* d_small = nullptr;
-  double* d_work = nullptr;
   double* d_Y = nullptr;
   double* d_Z = nullptr;
   int* d_info = nullptr;
@@ -347,13 +348,14 @@ static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, 
 
 static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot; }
 
-static lsba_status small_step(lsba_ctx c, int k, int force) {
+template <int B>
+static lsba_status small_step_t(lsba_ctx c, int k, int force) {
   LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
   const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
-  k_small_step<<<1, 256, 0, c->stream>>>(c->st, c->d_G, k, force, rfac);
-  CKL();
+  CK(launch_step_small<B>(c->st, c->d_G, k, force, rfac, c->stream));
   return LSBA_OK;
 }
+static lsba_status small_step(lsba_ctx c, int k, int force) { LSBA_DISPATCH_S(c->b, small_step_t, c, k, force); }
 
 static lsba_status read_status(lsba_ctx c, StepStatus* out) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
@@ -392,12 +394,23 @@ static lsba_status set_identity(lsba_ctx c) {
   return LSBA_OK;
 }
 
-static lsba_status cycle_solve(lsba_ctx c, int k, int gmres, int happy, int* singular) {
-  {
-    LaunchScope Ls(c, LSBA_K_CYCLE_SOLVE, 0.0);
-    k_cycle_solve<<<1, 512, 0, c->stream>>>(c->st, k, gmres, happy, c->d_work, c->d_Y, c->d_Z, c->d_info);
-    CKL();
+template <int B>
+static lsba_status cycle_end_t(lsba_ctx c, int k, int gmres, int happy, int upd) {
+  LaunchScope Ls(c, LSBA_K_CYCLE_SOLVE, 0.0);
+  CK(launch_cycle_end<B>(c->st, k, gmres, happy, upd, c->d_Y, c->d_Z, c->d_info, c->stream));
+  return LSBA_OK;
+}
+
+static lsba_status cycle_solve(lsba_ctx c, int k, int gmres, int happy, int* singular, int upd = 1) {
+  lsba_status st;
+  switch (c->b) {
+#define CASE(B) case B: st = cycle_end_t<B>(c, k, gmres, happy, upd); break;
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return LSBA_E_ARG;
   }
+  TRY(st);
   CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   *singular = c->h_info[0];
@@ -417,7 +430,6 @@ static lsba_status read_scalar(lsba_ctx c, double* v) {
 static void set_ip(lsba_ctx c, int ip) {
   c->ip = ip;
   c->b = (ip == LSBA_IP_GLOBAL) ? 1 : c->s;
-  c->st.b = c->b;
 }
 
 static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, double tol,
@@ -683,7 +695,7 @@ static void release(lsba_ctx c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
-                  c->d_part, c->d_G, c->d_small, c->d_work, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
+                  c->d_part, c->d_G, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -817,8 +829,9 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   const int ldH = (m_max + 1) * s;
   const size_t nH = (size_t)ldH * m_max * s, nBeta = (size_t)s * s, nCoef = 2 * (size_t)(m_max + 1) * s * s,
                nQv = (size_t)m_max * s * 2 * s, nQt = (size_t)m_max * s, nG = (size_t)ldH * s,
+               nRf = (size_t)ldH * ldH, nHt = (size_t)m_max * s * s, nGh = (size_t)m_max * s * s,
                nRi = (size_t)ldH * ldH, nSc = 4, nCacc = (size_t)s * s;
-  const size_t total = nH + nBeta + nCoef + nQv + nQt + nG + nRi + nSc + nCacc;
+  const size_t total = nH + nBeta + nCoef + nQv + nQt + nG + nRf + nHt + nGh + nRi + nSc + nCacc;
   TRY(dalloc(c, &c->d_small, total));
   CK(cudaMemset(c->d_small, 0, sizeof(double) * total));
   double* q = c->d_small;
@@ -828,16 +841,18 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.qr_v = q; q += nQv;
   c->st.qr_tau = q; q += nQt;
   c->st.g = q; q += nG;
+  c->st.Rfac = q; q += nRf;
+  c->st.htil = q; q += nHt;
+  c->st.ghat = q; q += nGh;
   c->st.Rinv = q; q += nRi;
   c->st.sc = q; q += nSc;
   c->st.Cacc = q; q += nCacc;
   c->st.ldH = ldH;
   c->st.m = m_max;
-  c->st.b = s;
+  c->st.bmax = s;
   TRY(dalloc(c, &c->st.status, 1));
   TRY(dalloc(c, &c->st.flag_dev, 1));
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
-  TRY(dalloc(c, &c->d_work, (size_t)m_max * s * m_max * s + 2 * (size_t)m_max * s * s + 16));
   TRY(dalloc(c, &c->d_Y, (size_t)(m_max + 1) * s * s));
   TRY(dalloc(c, &c->d_Z, (size_t)(m_max + 1) * s * s));
   TRY(dalloc(c, &c->d_info, 4));
@@ -922,8 +937,23 @@ extern "C" lsba_status lsba_block_arnoldi_step(lsba_ctx c, lsba_step_info* info)
     info->chol_flag = stt.flag;
     info->cond_est = stt.kappa_F;
     info->res_est = stt.res_gmres;
+    info->res_est_fom = stt.res_fom;
+    info->proj_singular = stt.proj_singular;
   }
   return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_projected_solve(lsba_ctx c, int32_t fom, double* Xi_host, double* Z_host) {
+  if (!c || !Xi_host || !Z_host) return LSBA_E_ARG;
+  if (c->k < 1 || c->flagged) return fail(c, LSBA_E_STATE, "needs k >= 1 accepted steps and no flag");
+  CK(cudaSetDevice(c->device));
+  int sing = 0;
+  TRY(cycle_solve(c, c->k, fom ? 0 : 1, 0, &sing, 0));
+  const int kb = c->k * c->b;
+  CK(cudaMemcpyAsync(Xi_host, c->d_Y, sizeof(double) * kb * c->b, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(Z_host, c->d_Z, sizeof(double) * (kb + c->b) * c->b, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return sing ? fail(c, LSBA_OK, "singular projected system") : LSBA_OK;
 }
 
 extern "C" lsba_status lsba_copy_hessenberg(lsba_ctx c, double* H_host, int32_t ld) {

@@ -1,0 +1,559 @@
+// small.cuh — the s x s / ks x s work of a block step and of a cycle end, one CTA each,
+// templated on the block size B (b = s classical, 1 global).  Register- and warp-parallel.
+//
+// Per step k (k_step_small):
+//   S = sym(Omega - H^T H); R = chol(S) with NaN-flag (R2)      [warp 0]
+//   coefficients C = [-H R^{-1}; R^{-1}] for V_{k+1} = [V_k W] C  (Alg 3 l.6)        [all]
+//   incremental block-Householder QR of Hbar_k (reading R11):                       [warps 1..B]
+//     apply reflector sets 1..k-1 to the new column -> R-factor column, h~_k
+//   FOM estimate ||H_{k+1,k} h~_k^{-1} g^_k C_acc||_F; QR of [h~_k; H_{k+1,k}] ->
+//     GMRES estimate ||g_{k+1} C_acc||_F (Eq normF_Rm via Thm 2.4)                 [warps 0, 1]
+//   kappa_F of R_{k+1} = [E_1 beta, Hbar_k] (reading R8): new block column of R^{-1} [all]
+// Per cycle end (k_cycle_end):                                  (a5, a6: PAPER.md:189-219)
+//   Xi by block back-substitution with the stored R factor (GMRES: R Xi = g; FOM: last
+//   diagonal block h~_k, rhs g^_k); cos = E_k^T Xi;
+//   M = H_k^{-T} E_k H^T H = Q^ E_k h~_k^{-T} H^T H  (Q^ = reflector sets 1..k-1, since
+//   Q^T H_k = [R~] is block upper triangular with last diagonal block h~_k)
+//   Y = Xi C_acc, Z = [M; -H_{k+1,k}], C_acc <- cos C_acc.
+#pragma once
+#include "kernels.cuh"
+
+namespace lsba {
+
+struct SmallState2 {
+  double* Hbar;    // ((m+1)bmax) x (m bmax), ld ldH
+  double* beta;    // b x b col-major
+  double* coef;    // ((k+1)b) x b row-major
+  double* qr_v;    // [set j][q][2b]   (stride 2*bmax per reflector, bmax*2*bmax per set)
+  double* qr_tau;  // [set j][q]
+  double* g;       // ((m+1)bmax) x b, ld ldH
+  double* Rfac;    // (m bmax)^2 upper block triangular R of Hbar, ld ldH
+  double* htil;    // [step][b*b] col-major h~_k
+  double* ghat;    // [step][b*b] col-major g^_k
+  double* Rinv;    // ((m+1)bmax)^2, ld ldH
+  double* sc;      // [0] ||R||_F^2, [1] ||R^{-1}||_F^2
+  double* Cacc;    // b x b col-major
+  StepStatus* status;
+  int* flag_dev;
+  int ldH, m, bmax;
+};
+
+// ---------------------------------------------------------------------------- warp helpers
+template <int B>
+__device__ __forceinline__ double sel(const double (&a)[B], int i) {
+  double v = 0.0;
+#pragma unroll
+  for (int r = 0; r < B; ++r) v = (r == i) ? a[r] : v;
+  return v;
+}
+
+// Solve A X = R (B x B each) by Gaussian elimination with partial pivoting, one warp.
+// Lane c < B holds column c of A in colv; lane B + c holds column c of the right-hand side.
+// On return lanes B..2B-1 hold the solution columns.  Returns true (all lanes) if singular.
+template <int B>
+__device__ bool warp_gesv(double (&colv)[B]) {
+  const int lane = threadIdx.x & 31;
+  bool sing = false;
+#pragma unroll
+  for (int p = 0; p < B; ++p) {
+    // pivot search in lane p's column
+    int piv = p;
+    double best = -1.0;
+#pragma unroll
+    for (int r = p; r < B; ++r) {
+      const double a = fabs(colv[r]);
+      if (a > best) { best = a; piv = r; }
+    }
+    piv = __shfl_sync(0xffffffffu, piv, p);
+    best = __shfl_sync(0xffffffffu, best, p);
+    if (!(best > 0.0) || !isfinite(best)) sing = true;
+    // swap rows p <-> piv in every column
+    double vp = colv[p], vq = sel<B>(colv, piv);
+#pragma unroll
+    for (int r = p; r < B; ++r) if (r == piv) colv[r] = vp;
+    colv[p] = vq;
+    const double dpp = __shfl_sync(0xffffffffu, colv[p], p);
+#pragma unroll
+    for (int r = p + 1; r < B; ++r) {
+      const double f = __shfl_sync(0xffffffffu, colv[r], p) / dpp;
+      if (lane != p) colv[r] -= f * colv[p];
+    }
+    if (lane == p) {
+#pragma unroll
+      for (int r = p + 1; r < B; ++r) colv[r] = 0.0;
+    }
+  }
+  // back substitution on the right-hand-side lanes
+#pragma unroll
+  for (int q = B - 1; q >= 0; --q) {
+    const double dqq = __shfl_sync(0xffffffffu, colv[q], q);
+    const double xq = colv[q] / dqq;
+    if (lane >= B) colv[q] = xq;
+#pragma unroll
+    for (int r = 0; r < q; ++r) {
+      const double arq = __shfl_sync(0xffffffffu, colv[r], q);
+      if (lane >= B) colv[r] -= arq * xq;
+    }
+  }
+  if (lane >= B && lane < 2 * B) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) if (!isfinite(colv[r])) sing = true;
+  }
+  return __any_sync(0xffffffffu, sing);
+}
+
+// ||Rs X Cacc||_F for a B x B matrix X held column-wise in lanes B..2B-1 (as left by warp_gesv),
+// optionally premultiplied by the upper triangular Rs (smem, col-major).  One warp.
+template <int B>
+__device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, const double* Rs) {
+  const int lane = threadIdx.x & 31;
+  // column y of (X Cacc) = sum_q X[:,q] Cacc[q,y]; X[:,q] lives in lane B+q
+  double acc2 = 0.0;
+#pragma unroll
+  for (int y = 0; y < B; ++y) {
+    double col[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) col[r] = 0.0;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const double cq = Cacc[q + y * B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) col[r] += __shfl_sync(0xffffffffu, colv[r], B + q) * cq;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int x = 0; x < B; ++x) {
+        double t = col[x];
+        if (Rs) {
+          t = 0.0;
+#pragma unroll
+          for (int q = x; q < B; ++q) t += Rs[x + q * B] * col[q];
+        }
+        acc2 += t * t;
+      }
+    }
+  }
+  return sqrt(__shfl_sync(0xffffffffu, acc2, 0));
+}
+
+// ---------------------------------------------------------------------------- step kernel
+// blockDim = 32 * (B + 2).  dynamic smem: (k+1) B B doubles (copy of G).
+template <int B>
+__global__ void __launch_bounds__(32 * (B + 2))
+k_step_small(SmallState2 st, const double* __restrict__ G, int k, int force_flag, double rfac) {
+  extern __shared__ double Gs[];
+  __shared__ double Ss[B * B], Rs[B * B], Ris[B * B], Ht[B * B], Gh[B * B];
+  __shared__ double red[32];
+  __shared__ int flag_s;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int ldH = st.ldH, kb = k * B;
+  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
+  __syncthreads();
+  // Hcol -> Hbar column block k-1; S = Omega - Hcol^T Hcol
+  if (k > 0)
+    for (int e = tid; e < kb * B; e += nt) {
+      const int r = e / B, c = e % B;
+      st.Hbar[r + (size_t)((k - 1) * B + c) * ldH] = Gs[e];
+    }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = Gs[(kb + x) * B + y];
+    for (int r = 0; r < kb; ++r) t -= Gs[r * B + x] * Gs[r * B + y];
+    Ss[x + y * B] = t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // symmetrise (R2) then right-looking Cholesky with NaN-flag; R^{-1}
+    for (int e = lane; e < B * B; e += 32) {
+      const int x = e % B, y = e / B;
+      if (x <= y) {
+        const double v = 0.5 * (Ss[x + y * B] + Ss[y + x * B]);
+        Rs[x + y * B] = v;  // work copy (upper part used)
+      } else {
+        Rs[x + y * B] = 0.0;
+      }
+    }
+    __syncwarp();
+    bool f = false;
+    for (int j = 0; j < B; ++j) {
+      const double d = Rs[j + j * B];
+      if (!(d > 0.0) || !isfinite(d)) { f = true; break; }
+      const double r = sqrt(d);
+      __syncwarp();
+      for (int c = j + lane; c < B; c += 32) Rs[j + c * B] = (c == j) ? r : Rs[j + c * B] / r;
+      __syncwarp();
+      const int rem = B - j - 1;
+      for (int e = lane; e < rem * rem; e += 32) {
+        const int x = j + 1 + e % rem, y = j + 1 + e / rem;
+        if (x <= y) Rs[x + y * B] -= Rs[j + x * B] * Rs[j + y * B];
+      }
+      __syncwarp();
+    }
+    if (!f)
+      for (int e = 0; e < B * B; ++e)
+        if (!isfinite(Rs[e])) f = true;
+    if (force_flag) f = true;
+    if (lane == 0) {
+      flag_s = f ? 1 : 0;
+      *st.flag_dev = flag_s;
+      st.status->k = k;
+      st.status->flag = flag_s;
+      st.status->proj_singular = 0;
+      st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
+      if (k == 0) {
+        double tr = 0.0;
+        for (int x = 0; x < B; ++x) tr += Gs[x * B + x];
+        st.status->normU2 = tr * (rfac * rfac);
+      }
+    }
+    __syncwarp();
+    if (!f && lane < B) {   // R^{-1}, column `lane` by back substitution
+      const int c = lane;
+      double x[B];
+#pragma unroll
+      for (int r = B - 1; r >= 0; --r) {
+        double t = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = r + 1; q < B; ++q) t -= Rs[r + q * B] * x[q];
+        x[r] = (r <= c) ? t / Rs[r + r * B] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < B; ++r) Ris[r + c * B] = (r <= c) ? x[r] : 0.0;
+    }
+  } else if (k > 0 && warp - 1 < B) {
+    // QR window for column c: apply reflector sets 1..k-1 (set j acts on block rows j-1, j)
+    const int c = warp - 1;
+    const int colg = (k - 1) * B + c;   // global column index in Hbar / Rfac
+    double w = (lane < 2 * B && lane < kb) ? Gs[lane * B + c] : 0.0;
+    for (int j = 1; j <= k - 1; ++j) {
+      const double* V = st.qr_v + (size_t)(j - 1) * st.bmax * 2 * st.bmax;
+      const double* T = st.qr_tau + (size_t)(j - 1) * st.bmax;
+      double v[B], tau[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        v[q] = (lane < 2 * B) ? V[(size_t)q * 2 * st.bmax + lane] : 0.0;
+        tau[q] = T[q];
+      }
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        const double d = warp_sum(v[q] * w);
+        w -= tau[q] * d * v[q];
+      }
+      // rows (j-1)B.. of the window are final: R-factor entries
+      if (lane < B) st.Rfac[((j - 1) * B + lane) + (size_t)colg * ldH] = w;
+      // shift the window down by one block
+      const double up = __shfl_down_sync(0xffffffffu, w, B);
+      const int gr = (j + 1) * B + (lane - B);
+      w = (lane < B) ? up : ((lane < 2 * B && gr < kb) ? Gs[gr * B + c] : 0.0);
+    }
+    if (lane < B) {   // h~_k column c, and g^_k column c (g block k-1 before reflector k)
+      Ht[lane + c * B] = w;
+      st.htil[(size_t)(k - 1) * B * B + lane + c * B] = w;
+      const double gv = st.g[((k - 1) * B + lane) + (size_t)c * ldH];
+      Gh[lane + c * B] = gv;
+      st.ghat[(size_t)(k - 1) * B * B + lane + c * B] = gv;
+    }
+  }
+  __syncthreads();
+  if (flag_s) {
+    if (k > 0)
+      for (int e = tid; e < B * B; e += nt) {
+        const int x = e % B, y = e / B;
+        st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = 0.0;
+      }
+    return;
+  }
+  // projection coefficients (row-major): rows < kb: -Hcol R^{-1}; rows kb..: R^{-1}
+  for (int e = tid; e < (kb + B) * B; e += nt) {
+    const int r = e / B, c = e % B;
+    double t;
+    if (r < kb) {
+      t = 0.0;
+      for (int q = 0; q <= c; ++q) t -= Gs[r * B + q] * Ris[q + c * B];
+    } else {
+      t = Ris[(r - kb) + c * B];
+    }
+    st.coef[e] = t;
+  }
+  if (k == 0) {
+    // IO: beta = R; g = E_1 beta; R_1^{-1} = beta^{-1}; norms for kappa_F
+    for (int e = tid; e < B * B; e += nt) {
+      const int x = e % B, y = e / B;
+      st.beta[e] = Rs[e];
+      st.Rinv[x + (size_t)y * ldH] = Ris[e];
+    }
+    const int rows = (st.m + 1) * B;
+    for (int e = tid; e < rows * B; e += nt) {
+      const int r = e % rows, c = e / rows;
+      st.g[r + (size_t)c * ldH] = (r < B) ? Rs[r + c * B] : 0.0;
+    }
+    double nr = 0.0, ni = 0.0;
+    for (int e = tid; e < B * B; e += nt) { nr += Rs[e] * Rs[e]; ni += Ris[e] * Ris[e]; }
+    nr = block_sum(nr, red);
+    ni = block_sum(ni, red);
+    if (tid == 0) { st.sc[0] = nr; st.sc[1] = ni; st.status->kappa_F = sqrt(nr * ni); }
+    return;
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
+  }
+  if (warp == 0) {
+    // FOM estimate: cos_F = h~^{-1} g^ ; ||H_{k+1,k} cos_F C_acc||_F
+    double colv[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+      colv[r] = (lane < B) ? Ht[r + lane * B] : ((lane < 2 * B) ? Gh[r + (lane - B) * B] : 0.0);
+    const bool sing = warp_gesv<B>(colv);
+    double rf = nan("");
+    if (!sing) rf = warp_norm_prod<B>(colv, st.Cacc, Rs) * rfac;
+    if (lane == 0) {
+      st.status->proj_singular = sing ? 1 : 0;
+      st.status->res_fom = rf;
+    }
+  } else if (warp == 1) {
+    // Householder QR of the 2B x B stack [h~_k; H_{k+1,k}], applied to g rows (k-1)B..(k+1)B-1
+    double row[B], gr[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      row[c] = (lane < B) ? Ht[lane + c * B] : ((lane < 2 * B) ? Rs[(lane - B) + c * B] : 0.0);
+      gr[c] = (lane < 2 * B) ? st.g[((k - 1) * B + lane) + (size_t)c * ldH] : 0.0;
+    }
+    double* Vk = st.qr_v + (size_t)(k - 1) * st.bmax * 2 * st.bmax;
+    double* Tk = st.qr_tau + (size_t)(k - 1) * st.bmax;
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const double alpha = __shfl_sync(0xffffffffu, row[q], q);
+      const double xn2 = warp_sum((lane > q && lane < 2 * B) ? row[q] * row[q] : 0.0);
+      double tau = 0.0, v = (lane == q) ? 1.0 : 0.0, beta_ = alpha;
+      if (xn2 > 0.0) {
+        const double nrm = sqrt(alpha * alpha + xn2);
+        beta_ = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta_ - alpha) / beta_;
+        if (lane > q && lane < 2 * B) v = row[q] / (alpha - beta_);
+      }
+      if (lane < 2 * B) Vk[(size_t)q * 2 * st.bmax + lane] = v;
+      if (lane == 0) Tk[q] = tau;
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        if (c < q) continue;
+        if (c == q) {
+          row[c] = (lane == q) ? beta_ : ((lane > q) ? 0.0 : row[c]);
+        } else {
+          const double d = warp_sum(v * row[c]);
+          row[c] -= tau * d * v;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < B; ++c) {
+        const double d = warp_sum(v * gr[c]);
+        gr[c] -= tau * d * v;
+      }
+    }
+    const int colg0 = (k - 1) * B;
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      if (lane < B) st.Rfac[(colg0 + lane) + (size_t)(colg0 + c) * ldH] = row[c];
+      if (lane < 2 * B) st.g[((k - 1) * B + lane) + (size_t)c * ldH] = gr[c];
+    }
+    // GMRES estimate ||g_{k+1} C_acc||_F  (g_{k+1} = lanes B..2B-1)
+    double acc2 = 0.0;
+#pragma unroll
+    for (int y = 0; y < B; ++y) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < B; ++q) t += gr[q] * st.Cacc[q + y * B];
+      if (lane >= B && lane < 2 * B) acc2 += t * t;
+    }
+    acc2 = warp_sum(acc2);
+    if (lane == 0) st.status->res_gmres = sqrt(acc2) * rfac;
+  }
+  // kappa_F (reading R8): T = R_k^{-1} Hcol (kb x B); X = -T R^{-1} -> Rinv[:, kb..kb+B)
+  double part_r = 0.0, part_i = 0.0;
+  for (int r = tid; r < kb; r += nt) {
+    double acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
+    const double* Rr = st.Rinv + r;
+    int q = r;
+    for (; q + 3 < kb; q += 4) {
+      const double a0 = Rr[(size_t)q * ldH], a1 = Rr[(size_t)(q + 1) * ldH];
+      const double a2 = Rr[(size_t)(q + 2) * ldH], a3 = Rr[(size_t)(q + 3) * ldH];
+#pragma unroll
+      for (int c = 0; c < B; ++c)
+        acc[c] += a0 * Gs[q * B + c] + a1 * Gs[(q + 1) * B + c] + a2 * Gs[(q + 2) * B + c] + a3 * Gs[(q + 3) * B + c];
+    }
+    for (; q < kb; ++q) {
+      const double a0 = Rr[(size_t)q * ldH];
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] += a0 * Gs[q * B + c];
+    }
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+      double x = 0.0;
+#pragma unroll
+      for (int q2 = 0; q2 <= c; ++q2) x -= acc[q2] * Ris[q2 + c * B];
+      st.Rinv[r + (size_t)(kb + c) * ldH] = x;
+      part_i += x * x;
+      part_r += Gs[r * B + c] * Gs[r * B + c];
+    }
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    st.Rinv[(kb + x) + (size_t)(kb + y) * ldH] = Ris[e];
+    part_i += Ris[e] * Ris[e];
+    part_r += Rs[e] * Rs[e];
+  }
+  const double dr = block_sum(part_r, red);
+  const double di = block_sum(part_i, red);
+  if (tid == 0) {
+    st.sc[0] += dr;
+    st.sc[1] += di;
+    st.status->kappa_F = sqrt(st.sc[0] * st.sc[1]);
+  }
+}
+
+// ---------------------------------------------------------------------------- cycle end
+// blockDim = 32 * max(8, B).  dynamic smem: k B B (Xi) doubles.
+// gmres: 1 -> R Xi = g (least squares); 0 -> FOM (last diagonal block h~_k, rhs g^_k).
+// happy: FOM solution, Y only, C_acc untouched.   info[0] = 1 if singular.
+template <int B>
+__global__ void __launch_bounds__(512)
+k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double* __restrict__ Y,
+            double* __restrict__ Z, int* __restrict__ info) {
+  extern __shared__ double Xi[];             // kb x B, column-major (ld kb)
+  __shared__ double Db[B * B], Tb[B * B], HtH[B * B], cosC[B * B];
+  __shared__ int sing_s;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int ldH = st.ldH, kb = k * B;
+  const bool use_fom = happy || !gmres;
+  if (tid == 0) sing_s = 0;
+  // rhs -> Xi
+  for (int e = tid; e < kb * B; e += nt) {
+    const int r = e % kb, c = e / kb;
+    double v = st.g[r + (size_t)c * ldH];
+    if (use_fom && r >= kb - B) v = st.ghat[(size_t)(k - 1) * B * B + (r - (kb - B)) + c * B];
+    Xi[e] = v;
+  }
+  __syncthreads();
+  // block back substitution, column-oriented
+  for (int j = k - 1; j >= 0; --j) {
+    if (warp == 0) {
+      double colv[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        double a;
+        if (lane < B) {
+          a = (use_fom && j == k - 1) ? st.htil[(size_t)(k - 1) * B * B + r + lane * B]
+                                     : st.Rfac[(j * B + r) + (size_t)(j * B + lane) * ldH];
+        } else if (lane < 2 * B) {
+          a = Xi[(j * B + r) + (size_t)(lane - B) * kb];
+        } else {
+          a = 0.0;
+        }
+        colv[r] = a;
+      }
+      const bool sg = warp_gesv<B>(colv);
+      if (lane >= B && lane < 2 * B) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) Xi[(j * B + r) + (size_t)(lane - B) * kb] = colv[r];
+      }
+      if (sg && lane == 0) sing_s = 1;
+    }
+    __syncthreads();
+    // rhs_i -= U_{i,j} Xi_j for rows i < jB
+    const int rows = j * B;
+    for (int e = tid; e < rows * B; e += nt) {
+      const int r = e % rows, c = e / rows;
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < B; ++q) t += st.Rfac[r + (size_t)(j * B + q) * ldH] * Xi[(j * B + q) + (size_t)c * kb];
+      Xi[r + (size_t)c * kb] -= t;
+    }
+    __syncthreads();
+  }
+  // Y = Xi C_acc (row-major kb x B)
+  for (int e = tid; e < kb * B; e += nt) {
+    const int r = e / B, c = e % B;
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < B; ++q) t += Xi[r + (size_t)q * kb] * st.Cacc[q + c * B];
+    Y[e] = t;
+  }
+  if (happy) {
+    if (tid == 0) info[0] = sing_s;
+    return;
+  }
+  const double* Hk1 = st.Hbar + kb + (size_t)(k - 1) * B * ldH;   // H_{k+1,k}
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int q = 0; q < B; ++q) t += Hk1[q + (size_t)x * ldH] * Hk1[q + (size_t)y * ldH];
+    HtH[e] = t;
+  }
+  __syncthreads();
+  // Z = [M; -H_{k+1,k}]
+  if (gmres) {
+    // z = h~_k^{-T} H^T H  (warp 0), then M = Q^ E_k z by the stored reflector sets
+    if (warp == 0) {
+      double colv[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+        colv[r] = (lane < B) ? st.htil[(size_t)(k - 1) * B * B + lane + r * B]   // (h~^T)[r][lane]
+                             : ((lane < 2 * B) ? HtH[r + (lane - B) * B] : 0.0);
+      const bool sg = warp_gesv<B>(colv);
+      if (lane >= B && lane < 2 * B) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) Tb[r + (lane - B) * B] = colv[r];
+      }
+      if (sg && lane == 0) sing_s = 1;
+    }
+    __syncthreads();
+    if (warp < B) {
+      const int c = warp;
+      // window over block rows (j-1, j); start j = k-1 with [0; z]
+      double w = (lane >= B && lane < 2 * B) ? Tb[(lane - B) + c * B] : 0.0;
+      if (k == 1) {
+        if (lane >= B && lane < 2 * B) Z[(size_t)(lane - B) * B + c] = w;
+      }
+      for (int j = k - 1; j >= 1; --j) {
+        const double* V = st.qr_v + (size_t)(j - 1) * st.bmax * 2 * st.bmax;
+        const double* T = st.qr_tau + (size_t)(j - 1) * st.bmax;
+#pragma unroll
+        for (int q = B - 1; q >= 0; --q) {
+          const double v = (lane < 2 * B) ? V[(size_t)q * 2 * st.bmax + lane] : 0.0;
+          const double d = warp_sum(v * w);
+          w -= T[q] * d * v;
+        }
+        // bottom block (block j) final -> M rows jB..(j+1)B-1
+        if (lane >= B && lane < 2 * B) Z[(size_t)(j * B + lane - B) * B + c] = w;
+        if (j == 1) {
+          if (lane < B) Z[(size_t)lane * B + c] = w;
+        } else {
+          const double dn = __shfl_up_sync(0xffffffffu, w, B);
+          w = (lane >= B && lane < 2 * B) ? dn : 0.0;
+        }
+      }
+    }
+  } else {
+    for (int e = tid; e < kb * B; e += nt) Z[e] = 0.0;
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e / B, y = e % B;   // row-major Z row kb+x, col y
+    Z[(size_t)(kb + x) * B + y] = -Hk1[x + (size_t)y * ldH];
+  }
+  // C_acc <- cos C_acc, cos = Xi rows kb-B..kb-1
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < B; ++q) t += Xi[(kb - B + x) + (size_t)q * kb] * st.Cacc[q + y * B];
+    cosC[e] = t;
+  }
+  __syncthreads();
+  if (update_cacc)
+    for (int e = tid; e < B * B; e += nt) st.Cacc[e] = cosC[e];
+  if (tid == 0) info[0] = sing_s;
+}
+
+}  // namespace lsba

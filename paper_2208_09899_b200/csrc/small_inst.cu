@@ -1,0 +1,39 @@
+// small_inst.cu — compiled once per block size with -DLSBA_B=<1..16> (see build.sh).
+#include "small.cuh"
+#include "launch_small.h"
+
+#ifndef LSBA_B
+#error "compile with -DLSBA_B=<block size>"
+#endif
+
+namespace lsba {
+
+template <>
+cudaError_t launch_step_small<LSBA_B>(const SmallState2& st, const double* G, int k, int force,
+                                      double rfac, cudaStream_t stream) {
+  constexpr int B = LSBA_B;
+  const size_t smem = sizeof(double) * (size_t)(k + 1) * B * B;
+  auto fn = k_step_small<B>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<1, 32 * (B + 2), smem, stream>>>(st, G, k, force, rfac);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_cycle_end<LSBA_B>(const SmallState2& st, int k, int gmres, int happy, int upd,
+                                     double* Y, double* Z, int* info, cudaStream_t stream) {
+  constexpr int B = LSBA_B;
+  const size_t smem = sizeof(double) * (size_t)k * B * B;
+  auto fn = k_cycle_end<B>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<1, 32 * (B > 8 ? B : 8), smem, stream>>>(st, k, gmres, happy, upd, Y, Z, info);
+  return cudaGetLastError();
+}
+
+}  // namespace lsba
