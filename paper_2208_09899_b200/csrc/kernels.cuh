@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kThreads)
 k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ va, const double* __restrict__ V,
        const double* __restrict__ Vghost, const double* __restrict__ Bm,
-       double* __restrict__ W, double* __restrict__ sq_part) {
+       double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr) {
+  if (active && *active == 0) return;
   constexpr int L = (S >= 2) ? S / 2 : 1;
   constexpr int C = (S >= 2) ? 2 : 1;  // columns per lane
   const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -145,7 +146,8 @@ __global__ void __launch_bounds__(kThreads)
 k_spmm_odd(int n, const int* __restrict__ rp, const int* __restrict__ ci,
            const double* __restrict__ va, const double* __restrict__ V,
            const double* __restrict__ Vghost, const double* __restrict__ Bm,
-           double* __restrict__ W, double* __restrict__ sq_part) {
+           double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr) {
+  if (active && *active == 0) return;
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
   if (row < n) {
@@ -207,7 +209,8 @@ struct GramTA {
 template <int S>
 __global__ void __launch_bounds__(kThreads)
 k_gram_cl(int n, const double* __restrict__ X, size_t xstride, int J,
-          const double* __restrict__ Y, double* __restrict__ part) {
+          const double* __restrict__ Y, double* __restrict__ part, const int* __restrict__ active) {
+  if (active && *active == 0) return;
   constexpr int TA = GramTA<S>::value;
   constexpr int NA = S / TA;
   const int j = blockIdx.x / NA;
@@ -256,7 +259,8 @@ k_gram_cl(int n, const double* __restrict__ X, size_t xstride, int J,
 template <int S>
 __global__ void __launch_bounds__(kThreads)
 k_gram_gl(int n, const double* __restrict__ X, size_t xstride, int J,
-          const double* __restrict__ Y, double* __restrict__ part) {
+          const double* __restrict__ Y, double* __restrict__ part, const int* __restrict__ active) {
+  if (active && *active == 0) return;
   const int j = blockIdx.x;
   const int P = gridDim.y;
   const int chunk = (n + P - 1) / P;
@@ -284,7 +288,8 @@ k_gram_gl(int n, const double* __restrict__ X, size_t xstride, int J,
 
 // G[e] = scale * sum_{p=0..P-1} part[p][e]   (fixed order: deterministic, rank-independent)
 static __global__ void k_gram_finalize(int P, int E, const double* __restrict__ part,
-                                double* __restrict__ G, double scale) {
+                                double* __restrict__ G, double scale, const int* __restrict__ active) {
+  if (active && *active == 0) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   double t = 0.0;
@@ -388,6 +393,28 @@ struct StepStatus {
   double res_fom;        // ||H_{k+1,k} h~^{-1} g^_k C_acc||_F * rfac
   double kappa_F;        // ||R_{k+1}||_F ||R_{k+1}^{-1}||_F
   double normU2;         // IO only: ||U||_F^2 (k == 0)
+};
+
+// Device-side cycle control (one per context): the step kernel takes the continue /
+// restart decision of SURVEY 8(c) step 2.2 on the device, so the host can enqueue a whole
+// cycle and read this block once per cycle.
+struct CycleCtl {
+  int32_t active;        // 1 while the cycle continues (kernels of later steps no-op when 0)
+  int32_t why;           // 0 running, 1 NaN-flag / singular FOM matrix, 2 res_est <= tol,
+                         // 3 kappa_F > tau, 4 k == m_cur, 5 IO flagged
+  int32_t k_used;        // accepted steps of this cycle
+  int32_t k_flag;        // step index of the flag (why == 1)
+  int32_t forced_here;   // the flag was injected (lsba_set_force_flag)
+  int32_t force_k;       // fault-injection step (0 = off)
+  int32_t forced_done;   // the injected flag already happened in this solve
+  int32_t proj_singular; // why == 1 because h~_k was singular (reading R22)
+  int32_t m_cur;         // step budget of this cycle
+  int32_t gmres;         // 1: BGMRES estimate, 0: BFOM estimate
+  int32_t pad0, pad1;
+  double tol_abs;        // tol * ||B||_F (negative: never converge)
+  double tau;            // kappa_F threshold (inf: off)
+  double res_est;        // estimate of the last accepted step (times C_acc)
+  double kappa;          // kappa_F of the last accepted step
 };
 
 constexpr int kMaxB = 16;

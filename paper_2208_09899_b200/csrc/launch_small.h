@@ -6,17 +6,19 @@
 
 namespace lsba {
 struct SmallState2;
+struct CycleParams;
 
 template <int B>
-cudaError_t launch_step_small(const SmallState2& st, const double* G, int k, int force, double rfac,
-                              cudaStream_t stream);
+cudaError_t launch_step_small(const SmallState2& st, const double* G, int k, const CycleParams& prm,
+                              double rfac, cudaStream_t stream);
 template <int B>
 cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy, int upd, double* Y,
                              double* Z, int* info, cudaStream_t stream);
 
 #define LSBA_DECL_SMALL(B)                                                                              \
   template <>                                                                                           \
-  cudaError_t launch_step_small<B>(const SmallState2&, const double*, int, int, double, cudaStream_t); \
+  cudaError_t launch_step_small<B>(const SmallState2&, const double*, int, const CycleParams&, double,  \
+                                   cudaStream_t);                                                        \
   template <>                                                                                           \
   cudaError_t launch_cycle_end<B>(const SmallState2&, int, int, int, int, double*, double*, int*,     \
                                   cudaStream_t);

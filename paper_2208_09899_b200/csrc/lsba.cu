@@ -22,6 +22,7 @@
 
 #include "kernels.cuh"
 #include "small.cuh"  // SmallState2 / StepStatus layouts (kernels are in small_inst.cu)
+#include "dmma.cuh"
 #include "launch_small.h"
 
 using namespace lsba;
@@ -68,6 +69,12 @@ struct lsba_ctx_ {
   double* d_part = nullptr;
   size_t part_cap = 0;
   double* d_G = nullptr;
+  double* d_gpart = nullptr;     // DMMA Gram: first-level group partials
+  unsigned* d_tickets = nullptr;  // DMMA Gram: CTA arrival counters (self-resetting)
+  int gram_grid = 0;              // DMMA Gram: persistent grid size
+  CycleCtl* d_ctl = nullptr;      // device-side cycle control
+  CycleCtl* h_ctl = nullptr;      // pinned copy
+  int n_sms = 148;
   // small state
   SmallState2 st{};
   double* d_small = nullptr;
@@ -218,17 +225,18 @@ static lsba_status halo_t(lsba_ctx c, const double* V) {
 
 // ---------------------------------------------------------------- a1: SpMM / residual
 template <int S>
-static lsba_status spmm_t(lsba_ctx c, const double* V, double* W) {
+static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* active) {
   TRY(halo_t<S>(c, V));
   constexpr int L = (S % 2 == 0) ? S / 2 : 1;
   const long threads = (long)c->n * L;
   LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n * S);
+  if (c->n == 0) return LSBA_OK;
   if constexpr (S % 2 == 0 || S == 1) {
     k_spmm<S, false><<<cdiv(threads, kThreads), kThreads, 0, c->stream>>>(
-        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr);
+        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
   } else {
     k_spmm_odd<S, false><<<cdiv(c->n, kThreads), kThreads, 0, c->stream>>>(
-        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr);
+        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
   }
   CKL();
   return LSBA_OK;
@@ -248,10 +256,10 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
       CK(cudaMemsetAsync(c->d_sq, 0, sizeof(double), c->stream));
     } else if constexpr (S % 2 == 0 || S == 1) {
       k_spmm<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
-                                                          c->d_ghost, Bm, out, c->d_sq);
+                                                          c->d_ghost, Bm, out, c->d_sq, nullptr);
     } else {
       k_spmm_odd<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
-                                                              c->d_ghost, Bm, out, c->d_sq);
+                                                              c->d_ghost, Bm, out, c->d_sq, nullptr);
     }
     CKL();
   }
@@ -265,38 +273,76 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
   return LSBA_OK;
 }
 
-// ---------------------------------------------------------------- a2: Gram (+ allreduce)
-// G (device, c->d_G) = <[X_0..X_{J-1}], Y>; classical (J s) x s row-major; global J scalars
-// (scaled by 1/s).  Exactly one allreduce when P > 1 (the step's single sync point).
 template <int S>
-static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, const double* Y,
-                          int ip) {
+static bool dmma_gram_ok(lsba_ctx c, int J, int ip) {
+  if (ip == LSBA_IP_GLOBAL || c->variant != 0) return false;
+  if constexpr (!(S == 1 || S == 2 || S == 4 || S == 8 || S == 16)) {
+    return false;
+  } else {
+    using Cg = GramCfg<S>;
+    const int NG = (J + Cg::JP - 1) / Cg::JP;
+    return (NG + Cg::NW - 1) / Cg::NW + 1 <= Cg::JMAX && c->d_tickets != nullptr &&
+           (size_t)c->gram_grid * J * S * S <= c->part_cap;
+  }
+}
+
+// ---------------------------------------------------------------- a1+a2: (SpMM +) Gram (+ allreduce)
+// G (device, c->d_G) = <[X_0..X_{J-1}], Y>; classical (J s) x s row-major; global J scalars
+// (scaled by 1/s).  If Vk != nullptr, Y = W is first computed as A Vk (fused into the Gram
+// pass on the tensor-core path).  Exactly one allreduce when P > 1 (the step's single sync).
+template <int S>
+static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, double* Y, int ip,
+                          const double* Vk, const int* active) {
   const bool gl = (ip == LSBA_IP_GLOBAL);
-  {
+  const size_t E = gl ? (size_t)J : (size_t)J * S * S;
+  if (dmma_gram_ok<S>(c, J, ip)) {
+    if constexpr (S == 1 || S == 2 || S == 4 || S == 8 || S == 16) {
+      if (Vk) TRY(halo_t<S>(c, Vk));
+      const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+      const double bytes = (Vk ? 12.0 * c->nnz + 4.0 * (c->n + 1) : 0.0) +
+                           8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S;
+      LaunchScope Ls(c, LSBA_K_GRAM, bytes);
+      if (c->n > 0) {
+        GramArgs a;
+        a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+        a.Vk = Vk; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J; a.Y = Y;
+        a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+        a.active = active;
+        const size_t smem = sizeof(double) * ((size_t)GramCfg<S>::T * S + E);
+        auto fn = k_spmm_gram<S>;
+        if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 1;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+        const int grid = std::max(1, std::min(occ * c->n_sms, c->gram_grid));
+        fn<<<grid, 256, smem, c->stream>>>(a);
+        CKL();
+      } else {
+        CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+      }
+    }
+  } else {
+    if (Vk) TRY(spmm_t<S>(c, Vk, Y, active));
     const int gx = gl ? J : J * (S / GramTA<S>::value);
     int P = std::max(1, std::min(cdiv(std::max(c->n, 1), 256), cdiv(kGramCtas, gx)));
-    const size_t E = gl ? (size_t)J : (size_t)J * S * S;
     if ((size_t)P * E > c->part_cap) P = std::max(1, (int)(c->part_cap / E));
     {
       LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * J + ((X + (size_t)(J - 1) * xstride == Y) ? 0.0 : 8.0 * c->n * S));
       dim3 grid(gx, P);
       if (gl)
-        k_gram_gl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part);
+        k_gram_gl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part, active);
       else
-        k_gram_cl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part);
+        k_gram_cl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part, active);
       CKL();
     }
     {
       LaunchScope Ls(c, LSBA_K_GRAM_FINALIZE, 8.0 * P * E);
       k_gram_finalize<<<cdiv(E, 128), 128, 0, c->stream>>>(P, (int)E, c->d_part, c->d_G,
-                                                           gl ? 1.0 / S : 1.0);
+                                                           gl ? 1.0 / S : 1.0, active);
       CKL();
     }
   }
-  if (c->nranks > 1) {
-    const size_t E = gl ? (size_t)J : (size_t)J * S * S;
+  if (c->nranks > 1)
     CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
-  }
   return LSBA_OK;
 }
 
@@ -317,14 +363,27 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
   const double bytes = 8.0 * c->n * S * (Jmax + (J0 > 0) + (J1 > 0) + (base0 ? 1 : 0));
   LaunchScope Ls(c, kid, bytes);
   if (c->n == 0) return LSBA_OK;
+  if constexpr (S == 4 || S == 8 || S == 16) {
+    if (!gl && c->variant == 0) {
+      auto fn = k_project_dmma<S>;
+      if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+      const int rows_per_warp = (S >= 16 ? 16 : 32);
+      const int grid = std::max(1, std::min(cdiv(cdiv(c->n, rows_per_warp), 8), occ * c->n_sms));
+      fn<<<grid, 256, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr);
+      CKL();
+      return LSBA_OK;
+    }
+  }
   if (gl) {
     auto fn = k_project<S, true>;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<cdiv(c->n, kThreads), kThreads, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0,
                                                              J1, C1, out1, flag_ptr);
   } else {
     auto fn = k_project<S, false>;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<cdiv(c->n, kThreads), kThreads, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0,
                                                              J1, C1, out1, flag_ptr);
   }
@@ -333,12 +392,13 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
 }
 
 // dispatch wrappers (runtime s)
-static lsba_status spmm(lsba_ctx c, const double* V, double* W) { LSBA_DISPATCH_S(c->s, spmm_t, c, V, W); }
+static lsba_status spmm(lsba_ctx c, const double* V, double* W) { LSBA_DISPATCH_S(c->s, spmm_t, c, V, W, nullptr); }
 static lsba_status residual(lsba_ctx c, const double* Bm, const double* X, double* out) {
   LSBA_DISPATCH_S(c->s, residual_t, c, Bm, X, out);
 }
-static lsba_status gram(lsba_ctx c, const double* X, size_t xstride, int J, const double* Y, int ip) {
-  LSBA_DISPATCH_S(c->s, gram_t, c, X, xstride, J, Y, ip);
+static lsba_status gram(lsba_ctx c, const double* X, size_t xstride, int J, double* Y, int ip,
+                        const double* Vk = nullptr, const int* active = nullptr) {
+  LSBA_DISPATCH_S(c->s, gram_t, c, X, xstride, J, Y, ip, Vk, active);
 }
 static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, const double* C0,
                            const double* base0, double* out0, int J1, const double* C1, double* out1,
@@ -349,41 +409,44 @@ static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, 
 static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot; }
 
 template <int B>
-static lsba_status small_step_t(lsba_ctx c, int k, int force) {
+static lsba_status small_step_t(lsba_ctx c, int k, const CycleParams& prm) {
   LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
   const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
-  CK(launch_step_small<B>(c->st, c->d_G, k, force, rfac, c->stream));
+  CK(launch_step_small<B>(c->st, c->d_G, k, prm, rfac, c->stream));
   return LSBA_OK;
 }
-static lsba_status small_step(lsba_ctx c, int k, int force) { LSBA_DISPATCH_S(c->b, small_step_t, c, k, force); }
+static lsba_status small_step(lsba_ctx c, int k, const CycleParams& prm) {
+  LSBA_DISPATCH_S(c->b, small_step_t, c, k, prm);
+}
 
-static lsba_status read_status(lsba_ctx c, StepStatus* out) {
+static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  *out = *c->h_status;
+  if (out) *out = *c->h_status;
+  if (ctl) *ctl = *c->h_ctl;
   return LSBA_OK;
 }
 
-// IO(U) with U in slot 0: Gram (1 sync), chol, scale in place.  (Alg 3 line 1)
-static lsba_status io_begin(lsba_ctx c, StepStatus* stt) {
+// IO(U) with U in slot 0: Gram (1 sync), chol, scale in place (Alg 3 line 1).  Resets the
+// device cycle control with this cycle's parameters.  Asynchronous.
+static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
   TRY(gram(c, slotp(c, 0), c->slot, 1, slotp(c, 0), c->ip));
-  TRY(small_step(c, 0, 0));
+  TRY(small_step(c, 0, prm));
   TRY(project(c, slotp(c, 0), c->slot, 1, c->st.coef, nullptr, slotp(c, 0), 0, nullptr, nullptr,
               c->st.flag_dev, LSBA_K_PROJECT));
-  TRY(read_status(c, stt));
-  c->k = 0;
-  c->flagged = stt->flag != 0;
   return LSBA_OK;
 }
 
-// One Alg-3 step k (1-based) on the current cycle.
-static lsba_status pip_step(lsba_ctx c, int k, int force, StepStatus* stt) {
-  TRY(spmm(c, slotp(c, k - 1), slotp(c, k)));                                  // line 3
-  TRY(gram(c, slotp(c, 0), c->slot, k + 1, slotp(c, k), c->ip));                // line 4 (1 sync)
-  TRY(small_step(c, k, force));                                                  // line 5
+// One Alg-3 step k (1-based), asynchronous; every kernel no-ops once the device cycle
+// control says the cycle has ended (speculative enqueue of a whole cycle).
+static lsba_status pip_step_async(lsba_ctx c, int k) {
+  const CycleParams none{};
+  TRY(gram(c, slotp(c, 0), c->slot, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
+           &c->d_ctl->active));                                                  // lines 3-4
+  TRY(small_step(c, k, none));                                                   // line 5
   TRY(project(c, slotp(c, 0), c->slot, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
               nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
-  TRY(read_status(c, stt));
   return LSBA_OK;
 }
 
@@ -463,7 +526,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   };
 
   // ||B||_F^2 = s * <B,B>_gl  (R18: tolerance relative to ||B||_F)
-  TRY(gram(c, B, 0, 1, B, LSBA_IP_GLOBAL));
+  TRY(gram(c, B, 0, 1, const_cast<double*>(B), LSBA_IP_GLOBAL));
   CK(cudaMemcpyAsync(c->h_scalar, c->d_G, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const double normB = std::sqrt(std::max(0.0, *c->h_scalar * c->s));
@@ -488,60 +551,55 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   TRY(residual(c, B, X, slotp(c, 0)));   // U = B - A X0 (R13)
   TRY(set_identity(c));                   // C_acc = I
   int m_cur = m;
-  StepStatus stt;
+  CycleCtl cc;
   info->outcome = LSBA_MAX_RESTARTS;
   bool finished = false;
   for (int cycle = 1; cycle <= max_restarts + 1 && !finished; ++cycle) {
     info->cycles = cycle;
-    TRY(io_begin(c, &stt));                                  // [V_1, beta] = IO(U)
-    if (stt.flag) { info->outcome = LSBA_DEAD; break; }      // R4
-    int k_used = 0;
-    enum { W_NONE, W_FLAG, W_CONV, W_KAPPA, W_M } why = W_NONE;
-    for (int k = 1; k <= m_cur; ++k) {
-      info->attempted_steps++;
-      const bool force = (c->force_flag_k > 0 && !c->forced_done && k == c->force_flag_k);
-      if (force) c->forced_done = true;
-      TRY(pip_step(c, k, force ? 1 : 0, &stt));
-      if (stt.flag || stt.proj_singular) {
-        if (!force) {
-          // R7: happy-breakdown candidate with H_{k+1,k} := 0 (M = 0), checked explicitly
-          int sing = 1;
-          TRY(cycle_solve(c, k, 0, 1, &sing));
-          if (!sing) {
-            TRY(project(c, slotp(c, 0), c->slot, k, c->d_Y, X, c->d_Xc, 0, nullptr, nullptr,
-                        nullptr, LSBA_K_COMBINE));
-            double rel;
-            TRY(true_relres(c->d_Xc, slotp(c, k), &rel));    // slot k (flagged W) is free
-            if (rel <= tol) {
-              CK(cudaMemcpyAsync(X, c->d_Xc, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
-              info->iterations++;
-              info->happy++;
-              info->true_relres = rel;
-              info->outcome = LSBA_CONVERGED;
-              finished = true;
-              break;
-            }
+    // enqueue IO(U) and all m_cur steps of the cycle; the step kernels take the
+    // continue/restart decision on the device and later launches no-op (one host sync)
+    CycleParams prm;
+    prm.m_cur = m_cur;
+    prm.gmres = gmres;
+    prm.force_k = c->force_flag_k;
+    prm.reset_forced = (cycle == 1) ? 1 : 0;
+    prm.tol_abs = tol * normB;                               // R5, R18
+    prm.tau = tau;                                           // R8
+    TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
+    for (int k = 1; k <= m_cur; ++k) TRY(pip_step_async(c, k));
+    TRY(read_status(c, nullptr, &cc));
+    if (cc.why == 5) { info->outcome = LSBA_DEAD; break; }   // IO flagged (R4)
+    int k_used = cc.k_used;
+    info->iterations += k_used;
+    info->attempted_steps += k_used + (cc.why == 1 ? 1 : 0);
+    if (k_used > 0) info->res_est = cc.res_est;
+    if (cc.why == 1) {
+      const int k = cc.k_flag;
+      if (!cc.forced_here) {
+        // R7: happy-breakdown candidate with H_{k+1,k} := 0 (M = 0), checked explicitly
+        int sing = 1;
+        TRY(cycle_solve(c, k, 0, 1, &sing));
+        if (!sing) {
+          TRY(project(c, slotp(c, 0), c->slot, k, c->d_Y, X, c->d_Xc, 0, nullptr, nullptr,
+                      nullptr, LSBA_K_COMBINE));
+          double rel;
+          TRY(true_relres(c->d_Xc, slotp(c, k), &rel));    // slot k (flagged W) is free
+          if (rel <= tol) {
+            CK(cudaMemcpyAsync(X, c->d_Xc, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+            info->iterations++;
+            info->happy++;
+            info->true_relres = rel;
+            info->outcome = LSBA_CONVERGED;
+            finished = true;
+            break;
           }
         }
-        info->nan_flags++;
-        k_used = k - 1;
-        m_cur = k - 1;                                       // R6
-        why = W_FLAG;
-        break;
       }
-      info->iterations++;
-      const double est = gmres ? stt.res_gmres : stt.res_fom;
-      info->res_est = est;
-      k_used = k;
-      if (est <= tol * normB) { why = W_CONV; break; }      // R5
-      if (std::isfinite(tau) && stt.kappa_F > tau) {         // R8
-        info->cond_restarts++;
-        why = W_KAPPA;
-        break;
-      }
-      why = W_M;
+      info->nan_flags++;
+      m_cur = k - 1;                                        // R6
+    } else if (cc.why == 3) {
+      info->cond_restarts++;
     }
-    if (finished) break;
     if (k_used == 0) { info->outcome = LSBA_DEAD; break; }
     int sing = 0;
     TRY(cycle_solve(c, k_used, gmres, 0, &sing));            // Xi, M, cos; C_acc <- cos C_acc
@@ -550,7 +608,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       info->outcome = LSBA_DEAD;
       break;
     }
-    if (why == W_CONV) {
+    if (cc.why == 2) {
       // X += V_k Xi C_acc, then confirm with the explicit residual (R19)
       TRY(project(c, slotp(c, 0), c->slot, k_used, c->d_Y, X, X, 0, nullptr, nullptr, nullptr,
                   LSBA_K_COMBINE));
@@ -696,12 +754,14 @@ static void release(lsba_ctx c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_G, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
-                  c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev};
+                  c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
+                  c->d_gpart, c->d_tickets, c->d_ctl};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_info) cudaFreeHost(c->h_info);
   if (c->h_scalar) cudaFreeHost(c->h_scalar);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
   for (int k = 0; k < LSBA_K_COUNT; ++k)
     for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   if (c->comm) ncclCommDestroy(c->comm);
@@ -819,8 +879,26 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->slot = (size_t)n_local * s;
   TRY(dalloc(c, &c->d_V, (size_t)(m_max + 1) * c->slot));
   TRY(dalloc(c, &c->d_Xc, c->slot));
-  c->part_cap = (size_t)(kGramCtas + 16 * (m_max + 1)) * s * s + 2 * (size_t)(m_max + 1) * s * s;
+  {
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess && sms > 0)
+      c->n_sms = sms;
+  }
+  // DMMA Gram: persistent grid of 2 CTAs per SM; partials [cta][E] and [group][E]
+  c->gram_grid = 4 * c->n_sms;
+  const size_t Emax = (size_t)(m_max + 1) * s * s;
+  c->part_cap = std::max((size_t)(kGramCtas + 16 * (m_max + 1)) * s * s + 2 * Emax,
+                         (size_t)c->gram_grid * Emax);
   TRY(dalloc(c, &c->d_part, c->part_cap));
+  {
+    const int ngroups = (c->gram_grid + kGramGroup - 1) / kGramGroup;
+    TRY(dalloc(c, &c->d_gpart, (size_t)ngroups * Emax));
+    TRY(dalloc(c, &c->d_tickets, (size_t)ngroups + 1));
+    CK(cudaMemset(c->d_tickets, 0, sizeof(unsigned) * (ngroups + 1)));
+  }
+  TRY(dalloc(c, &c->d_ctl, 1));
+  CK(cudaMemset(c->d_ctl, 0, sizeof(CycleCtl)));
+  CK(cudaMallocHost((void**)&c->h_ctl, sizeof(CycleCtl)));
   TRY(dalloc(c, &c->d_G, (size_t)(m_max + 1) * s * s));
   c->sq_cap = std::max(1, cdiv((long)n_local * 16, kThreads));
   TRY(dalloc(c, &c->d_sq, c->sq_cap));
@@ -850,6 +928,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.ldH = ldH;
   c->st.m = m_max;
   c->st.bmax = s;
+  c->st.ctl = c->d_ctl;
   TRY(dalloc(c, &c->st.status, 1));
   TRY(dalloc(c, &c->st.flag_dev, 1));
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
@@ -909,14 +988,22 @@ extern "C" lsba_status lsba_arnoldi_begin(lsba_ctx c, const double* B_dev, lsba_
   if ((uintptr_t)B_dev & 15) return fail(c, LSBA_E_ARG, "B not 16-byte aligned");
   CK(cudaSetDevice(c->device));
   set_ip(c, ip);
-  c->forced_done = false;
   if (c->n > 0)
     CK(cudaMemcpyAsync(slotp(c, 0), B_dev, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
   TRY(set_identity(c));
+  CycleParams prm;
+  prm.m_cur = c->m_max;
+  prm.gmres = 1;
+  prm.force_k = c->force_flag_k;
+  prm.reset_forced = 1;
+  prm.tol_abs = -1.0;            // the step API never declares convergence
+  prm.tau = INFINITY;
+  TRY(io_begin_async(c, prm));
   StepStatus stt;
-  TRY(io_begin(c, &stt));
+  TRY(read_status(c, &stt, nullptr));
   if (io_flag) *io_flag = stt.flag;
-  if (stt.flag) c->k = -1;
+  c->k = stt.flag ? -1 : 0;
+  c->flagged = false;
   return LSBA_OK;
 }
 
@@ -926,11 +1013,12 @@ extern "C" lsba_status lsba_block_arnoldi_step(lsba_ctx c, lsba_step_info* info)
   if (c->k >= c->m_max) return fail(c, LSBA_E_STATE, "basis full (k == m_max)");
   CK(cudaSetDevice(c->device));
   const int k = c->k + 1;
-  const bool force = (c->force_flag_k > 0 && !c->forced_done && k == c->force_flag_k);
-  if (force) c->forced_done = true;
+  TRY(pip_step_async(c, k));
   StepStatus stt;
-  TRY(pip_step(c, k, force ? 1 : 0, &stt));
-  if (stt.flag) c->flagged = true;
+  CycleCtl cc;
+  TRY(read_status(c, &stt, &cc));
+  const bool flagged = (cc.why == 1 && cc.k_flag == k);
+  if (flagged) c->flagged = true;
   else c->k = k;
   if (info) {
     info->k = k;
@@ -1051,7 +1139,7 @@ extern "C" lsba_status lsba_block_inner_product(lsba_ctx c, const double* V_dev,
   if (ip != LSBA_IP_CLASSICAL && ip != LSBA_IP_GLOBAL) return fail(c, LSBA_E_ARG, "bad inner product");
   if (((uintptr_t)V_dev | (uintptr_t)Y_dev) & 15) return fail(c, LSBA_E_ARG, "not 16-byte aligned");
   CK(cudaSetDevice(c->device));
-  TRY(gram(c, V_dev, c->slot, nblocks, Y_dev, ip));
+  TRY(gram(c, V_dev, c->slot, nblocks, const_cast<double*>(Y_dev), ip));
   const size_t E = (ip == LSBA_IP_GLOBAL) ? (size_t)nblocks : (size_t)nblocks * c->s * c->s;
   CK(cudaMemcpyAsync(G_host, c->d_G, sizeof(double) * E, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));

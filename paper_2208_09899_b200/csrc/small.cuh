@@ -35,7 +35,14 @@ struct SmallState2 {
   double* Cacc;    // b x b col-major
   StepStatus* status;
   int* flag_dev;
+  CycleCtl* ctl;
   int ldH, m, bmax;
+};
+
+// IO-time cycle parameters (k == 0 launch of k_step_small)
+struct CycleParams {
+  int m_cur, gmres, force_k, reset_forced;
+  double tol_abs, tau;
 };
 
 // ---------------------------------------------------------------------------- warp helpers
@@ -140,13 +147,20 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
 // blockDim = 32 * (B + 2).  dynamic smem: (k+1) B B doubles (copy of G).
 template <int B>
 __global__ void __launch_bounds__(32 * (B + 2))
-k_step_small(SmallState2 st, const double* __restrict__ G, int k, int force_flag, double rfac) {
+k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm, double rfac) {
   extern __shared__ double Gs[];
   __shared__ double Ss[B * B], Rs[B * B], Ris[B * B], Ht[B * B], Gh[B * B];
   __shared__ double red[32];
-  __shared__ int flag_s;
+  __shared__ int flag_s, sing_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int ldH = st.ldH, kb = k * B;
+  CycleCtl* ctl = st.ctl;
+  if (k > 0 && ctl->active == 0) {      // speculative launch after the cycle ended: no-op
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  int force_flag = 0;
+  if (k > 0 && k == ctl->force_k && !ctl->forced_done) force_flag = 1;
   for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
   __syncthreads();
   // Hcol -> Hbar column block k-1; S = Omega - Hcol^T Hcol
@@ -195,7 +209,29 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, int force_flag
     if (force_flag) f = true;
     if (lane == 0) {
       flag_s = f ? 1 : 0;
+      sing_s = 0;
       *st.flag_dev = flag_s;
+      if (k == 0) {   // IO of a new cycle: reset the control block
+        ctl->active = f ? 0 : 1;
+        ctl->why = f ? 5 : 0;
+        ctl->k_used = 0;
+        ctl->k_flag = 0;
+        ctl->forced_here = 0;
+        ctl->proj_singular = 0;
+        ctl->m_cur = prm.m_cur;
+        ctl->gmres = prm.gmres;
+        ctl->force_k = prm.force_k;
+        if (prm.reset_forced) ctl->forced_done = 0;
+        ctl->tol_abs = prm.tol_abs;
+        ctl->tau = prm.tau;
+        ctl->res_est = nan("");
+        ctl->kappa = nan("");
+      } else if (f) {
+        ctl->active = 0;
+        ctl->why = 1;
+        ctl->k_flag = k;
+        if (force_flag) { ctl->forced_here = 1; ctl->forced_done = 1; }
+      }
       st.status->k = k;
       st.status->flag = flag_s;
       st.status->proj_singular = 0;
@@ -310,6 +346,7 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, int force_flag
     if (lane == 0) {
       st.status->proj_singular = sing ? 1 : 0;
       st.status->res_fom = rf;
+      sing_s = sing ? 1 : 0;
     }
   } else if (warp == 1) {
     // Householder QR of the 2B x B stack [h~_k; H_{k+1,k}], applied to g rows (k-1)B..(k+1)B-1
@@ -409,7 +446,24 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, int force_flag
   if (tid == 0) {
     st.sc[0] += dr;
     st.sc[1] += di;
-    st.status->kappa_F = sqrt(st.sc[0] * st.sc[1]);
+    const double kap = sqrt(st.sc[0] * st.sc[1]);
+    st.status->kappa_F = kap;
+    // ---- device-side decision (readings R5, R8, R9, R22)
+    if (sing_s) {                       // FOM projected matrix singular: treated as a NaN-flag
+      *st.flag_dev = 1;
+      ctl->active = 0;
+      ctl->why = 1;
+      ctl->k_flag = k;
+      ctl->proj_singular = 1;
+    } else {
+      const double est = ctl->gmres ? st.status->res_gmres : st.status->res_fom;
+      ctl->k_used = k;
+      ctl->res_est = est;
+      ctl->kappa = kap;
+      if (est <= ctl->tol_abs) { ctl->active = 0; ctl->why = 2; }
+      else if (kap > ctl->tau) { ctl->active = 0; ctl->why = 3; }
+      else if (k >= ctl->m_cur) { ctl->active = 0; ctl->why = 4; }
+    }
   }
 }
 
@@ -422,7 +476,7 @@ __global__ void __launch_bounds__(512)
 k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double* __restrict__ Y,
             double* __restrict__ Z, int* __restrict__ info) {
   extern __shared__ double Xi[];             // kb x B, column-major (ld kb)
-  __shared__ double Db[B * B], Tb[B * B], HtH[B * B], cosC[B * B];
+  __shared__ double Tb[B * B], HtH[B * B], cosC[B * B];
   __shared__ int sing_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int ldH = st.ldH, kb = k * B;

@@ -9,16 +9,16 @@
 namespace lsba {
 
 template <>
-cudaError_t launch_step_small<LSBA_B>(const SmallState2& st, const double* G, int k, int force,
-                                      double rfac, cudaStream_t stream) {
+cudaError_t launch_step_small<LSBA_B>(const SmallState2& st, const double* G, int k,
+                                      const CycleParams& prm, double rfac, cudaStream_t stream) {
   constexpr int B = LSBA_B;
   const size_t smem = sizeof(double) * (size_t)(k + 1) * B * B;
   auto fn = k_step_small<B>;
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  fn<<<1, 32 * (B + 2), smem, stream>>>(st, G, k, force, rfac);
+  fn<<<1, 32 * (B + 2), smem, stream>>>(st, G, k, prm, rfac);
   return cudaGetLastError();
 }
 
@@ -28,7 +28,7 @@ cudaError_t launch_cycle_end<LSBA_B>(const SmallState2& st, int k, int gmres, in
   constexpr int B = LSBA_B;
   const size_t smem = sizeof(double) * (size_t)k * B * B;
   auto fn = k_cycle_end<B>;
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
