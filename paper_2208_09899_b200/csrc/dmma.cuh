@@ -31,12 +31,16 @@ struct GramCfg {
   static constexpr int NT = S >= 8 ? S / 8 : 1;        // N tiles
   static constexpr int T = S >= 8 ? 64 : 512 / S;      // rows per tile
   static constexpr int L = S >= 2 ? S / 2 : 1;         // SpMM lanes per row
-  static constexpr int RPP = 256 / L;                  // SpMM rows per pass (256 threads)
-  static constexpr int JMAX = S >= 16 ? 5 : 7;         // j-groups per warp (registers)
-  static constexpr int UF = S >= 16 ? 2 : 4;           // 4-row steps per unrolled batch
-  static constexpr int NW = 8;                         // warps per CTA
+  static constexpr int NWG = 8;                        // tensor-core (Gram) warps
+  static constexpr int NWS = 4;                        // gather (SpMM) warps
+  static constexpr int NTHR = 32 * (NWG + NWS);
+  static constexpr int RPP = 32 * NWS / L;             // SpMM rows per pass
+  static constexpr int JMAX = S >= 16 ? 5 : 7;         // j-groups per Gram warp (registers)
+  static constexpr int UF = S >= 16 ? 4 : 8;           // 4-row steps per unrolled batch
   static constexpr int NSTEP = T / 4;
 };
+// basis slots are padded to a multiple of this many rows (zero rows): branch-free tiles
+constexpr int kRowPad = 512;
 
 constexpr int kGramGroup = 16;  // CTAs per first-level reduction group
 
@@ -45,10 +49,12 @@ struct GramArgs {
   const int* rp; const int* ci; const double* va;   // CSR (local rows)
   const double* Vk;        // SpMM input block (fused mode) or nullptr (W = Y given)
   const double* Vghost;
-  const double* X;         // blocks X_0..X_{J-1} at X + j*xstride
+  const double* X;         // blocks X_0..X_{NVB-1} at X + j*xstride (rows padded to kRowPad)
   size_t xstride;
-  int J;
-  double* Y;               // W (written in fused mode; read otherwise); block J-1 if it aliases
+  int J;                   // total blocks in the Gram (including W if y_alias)
+  int y_alias;             // 1: block J-1 is Y itself (taken from the W tile in smem)
+  double* Y;               // W (written in fused mode; read otherwise; rows padded)
+  const double* zeros;     // >= 16 zero doubles (padding lanes of packed groups)
   double* part;            // [cta][E]
   double* gpart;           // [group][E]
   unsigned* tickets;       // [ngroups + 1], zero-initialised, reset by the last CTA
@@ -56,16 +62,24 @@ struct GramArgs {
   const int* active;       // nullable: skip when *active == 0
 };
 
-// W rows of one tile by CSR gather (row-local lane group of L lanes, 2 columns per lane);
-// column indices and values of up to 8 nonzeros are loaded before their V rows (MLP).
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// W rows of one tile by CSR gather, executed by the NWS gather warps (thread index gt).
+// Lane group of L lanes per row, 2 columns per lane; up to 8 nonzeros' indices are loaded
+// before their V rows.  Rows >= n produce zeros.
 template <int S>
-__device__ __forceinline__ void spmm_tile(const GramArgs& g, int row0, double* Ws) {
+__device__ __forceinline__ void spmm_tile(const GramArgs& g, int row0, double* Ws, int gt) {
   using C = GramCfg<S>;
-  const int tid = threadIdx.x, n = g.n;
-#pragma unroll
+  const int n = g.n;
+#pragma unroll 1
   for (int pass = 0; pass < (C::T + C::RPP - 1) / C::RPP; ++pass) {
-    const int rl = pass * C::RPP + tid / C::L;
-    const int ell = tid % C::L;
+    const int rl = pass * C::RPP + gt / C::L;
+    const int ell = gt % C::L;
     if (rl >= C::T) continue;
     const int row = row0 + rl;
     double a0 = 0.0, a1 = 0.0;
@@ -79,25 +93,18 @@ __device__ __forceinline__ void spmm_tile(const GramArgs& g, int row0, double* W
           cc[u] = (p + u < p1) ? __ldg(g.ci + p + u) : -1;
           av[u] = (p + u < p1) ? __ldg(g.va + p + u) : 0.0;
         }
-        double vx[8], vy[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          vx[u] = vy[u] = 0.0;
           if (cc[u] >= 0) {
             const double* src = (cc[u] < n) ? (g.Vk + (size_t)cc[u] * S) : (g.Vghost + (size_t)(cc[u] - n) * S);
             if constexpr (S >= 2) {
               const double2 v = __ldg(reinterpret_cast<const double2*>(src) + ell);
-              vx[u] = v.x;
-              vy[u] = v.y;
+              a0 = fma(av[u], v.x, a0);
+              a1 = fma(av[u], v.y, a1);
             } else {
-              vx[u] = __ldg(src);
+              a0 = fma(av[u], __ldg(src), a0);
             }
           }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          a0 = fma(av[u], vx[u], a0);
-          if constexpr (S >= 2) a1 = fma(av[u], vy[u], a1);
         }
       }
       if constexpr (S >= 2)
@@ -106,136 +113,198 @@ __device__ __forceinline__ void spmm_tile(const GramArgs& g, int row0, double* W
         g.Y[row] = a0;
     }
     if constexpr (S >= 2) {
-      Ws[rl * S + 2 * ell] = a0;
-      Ws[rl * S + 2 * ell + 1] = a1;
+      reinterpret_cast<double2*>(Ws + rl * S)[ell] = make_double2(a0, a1);
     } else {
       Ws[rl] = a0;
     }
   }
 }
 
-// grid: any size (persistent over row tiles); block 256; dyn smem T*S + J*S*S doubles.
-// Work of a tile = NG j-groups x NSTEP 4-row steps, split into 8 equal contiguous ranges
-// (one per warp; a warp touches at most JMAX groups).
+// grid: persistent over row tiles; block NTHR = 384 (8 Gram warps + 4 gather warps);
+// dyn smem (2 T S + J S S) doubles.  The gather warps produce W tile t+1 (double buffer)
+// while the Gram warps run tile t on the tensor cores (named barriers 1-4).  A tile's
+// Gram work = NG j-groups x NSTEP 4-row steps, split into 8 equal contiguous ranges.
 template <int S>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(GramCfg<S>::NTHR, (S >= 16 ? 1 : 2))
 k_spmm_gram(GramArgs g) {
   using C = GramCfg<S>;
   if (g.active && *g.active == 0) return;
   extern __shared__ double smem[];
-  double* Ws = smem;                       // T x S tile of W
-  double* Gp = smem + C::T * S;            // J S S partial (CTA)
+  double* Wbuf = smem;                     // 2 x (T x S)
+  double* Gp = smem + 2 * C::T * S;        // J S S CTA partial
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = g.n, J = g.J;
   const int E = J * S * S;
-  const int NG = (J + C::JP - 1) / C::JP;
-  const int U = NG * C::NSTEP;
-  const int u0 = (warp * U) / C::NW, u1 = ((warp + 1) * U) / C::NW;
-  const int gfirst = u0 / C::NSTEP;
-  const int glast = (u1 > u0) ? (u1 - 1) / C::NSTEP : gfirst - 1;
   const int ntiles = (n + C::T - 1) / C::T;
-  for (int e = tid; e < E; e += 256) Gp[e] = 0.0;
+  for (int e = tid; e < E; e += C::NTHR) Gp[e] = 0.0;
+  __syncthreads();
 
-  double acc[C::JMAX][C::MT][C::NT][2];
-#pragma unroll
-  for (int a = 0; a < C::JMAX; ++a)
-#pragma unroll
-    for (int b = 0; b < C::MT; ++b)
-#pragma unroll
-      for (int c = 0; c < C::NT; ++c) acc[a][b][c][0] = acc[a][b][c][1] = 0.0;
-
-  const int r4 = lane & 3, c8 = lane >> 2;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int row0 = t * C::T;
-    if (g.Vk) {
-      spmm_tile<S>(g, row0, Ws);
-    } else {
-      for (int e = tid; e < C::T * S; e += 256) {
-        const size_t gi = (size_t)row0 * S + e;
-        Ws[e] = (gi < (size_t)n * S) ? g.Y[gi] : 0.0;
+  if (warp >= C::NWG) {
+    // ======================= gather (SpMM) warps: producers of W tiles =======================
+    const int gt = tid - 32 * C::NWG;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      if (it >= 2) named_sync(3 + b, C::NTHR);          // Gram warps released buffer b
+      double* Ws = Wbuf + b * C::T * S;
+      if (g.Vk) {
+        spmm_tile<S>(g, t * C::T, Ws, gt);
+      } else {
+        for (int e = gt; e < C::T * S; e += 32 * C::NWS) Ws[e] = g.Y[(size_t)t * C::T * S + e];
       }
+      __threadfence_block();
+      named_arrive(1 + b, C::NTHR);                     // W tile of buffer b is full
     }
-    __syncthreads();
+    // drain the outstanding "empty" arrivals of the last (up to) two tiles
+    for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) named_sync(3 + (k2 & 1), C::NTHR);
+  } else {
+    // ======================= Gram warps: consumers on the tensor cores =======================
+    const int NVB = J - (g.y_alias ? 1 : 0);           // blocks read from global memory
+    const int NGV = (NVB + C::JP - 1) / C::JP;
+    const int NG = NGV + (g.y_alias ? 1 : 0);
+    const int U = NG * C::NSTEP;
+    const int u0 = (warp * U) / C::NWG, u1 = ((warp + 1) * U) / C::NWG;
+    const int gfirst = u0 / C::NSTEP;
+    const int glast = (u1 > u0) ? (u1 - 1) / C::NSTEP : gfirst - 1;
+    const int r4 = lane & 3, c8 = lane >> 2;
+    double acc[C::JMAX][C::MT][C::NT][2];
 #pragma unroll
-    for (int gi = 0; gi < C::JMAX; ++gi) {
-      const int grp = gfirst + gi;
-      if (grp > glast) break;
-      const int st0 = max(u0 - grp * C::NSTEP, 0);
-      const int st1 = min(u1 - grp * C::NSTEP, C::NSTEP);
-      // A-fragment source of this lane for each M tile (fixed for the group)
-      const double* src[C::MT];
-      bool alias[C::MT];
-      int colA[C::MT];
+    for (int a = 0; a < C::JMAX; ++a)
 #pragma unroll
-      for (int tm = 0; tm < C::MT; ++tm) {
-        int j;
-        if constexpr (S >= 8) { j = grp; colA[tm] = tm * 8 + c8; }
-        else { j = grp * C::JP + c8 / S; colA[tm] = c8 % S; }
-        const double* Xj = (j < J) ? g.X + (size_t)j * g.xstride : nullptr;
-        alias[tm] = (Xj == g.Y);
-        src[tm] = Xj;
-      }
-      for (int st = st0; st < st1; st += C::UF) {
-        double av[C::UF][C::MT], bf[C::UF][C::NT];
+      for (int bb = 0; bb < C::MT; ++bb)
 #pragma unroll
-        for (int u = 0; u < C::UF; ++u) {
-          const int rl = (st + u) * 4 + r4;
-          const int row = row0 + rl;
-          const bool in = (st + u < st1);
-#pragma unroll
-          for (int tn = 0; tn < C::NT; ++tn) {
-            const int col = tn * 8 + c8;
-            bf[u][tn] = (in && col < S) ? Ws[rl * S + col] : 0.0;
-          }
-#pragma unroll
-          for (int tm = 0; tm < C::MT; ++tm) {
-            double v = 0.0;
-            if (in && src[tm] != nullptr) {
-              if (alias[tm]) v = Ws[rl * S + colA[tm]];
-              else if (row < n) v = __ldg(src[tm] + (size_t)row * S + colA[tm]);
-            }
-            av[u][tm] = v;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < C::UF; ++u)
-#pragma unroll
-          for (int tm = 0; tm < C::MT; ++tm)
-#pragma unroll
-            for (int tn = 0; tn < C::NT; ++tn) dmma(acc[gi][tm][tn][0], acc[gi][tm][tn][1], av[u][tm], bf[u][tn]);
-      }
-    }
-    __syncthreads();
-  }
-  // ---- CTA partial: warps add their fragments in warp order (deterministic)
-  for (int w = 0; w < C::NW; ++w) {
-    if (warp == w) {
-#pragma unroll
+        for (int c = 0; c < C::NT; ++c) acc[a][bb][c][0] = acc[a][bb][c][1] = 0.0;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int b = it & 1;
+      named_sync(1 + b, C::NTHR);                       // wait for W tile t
+      const double* Ws = Wbuf + b * C::T * S;
+      const size_t row0 = (size_t)t * C::T;
+#pragma unroll 1
       for (int gi = 0; gi < C::JMAX; ++gi) {
         const int grp = gfirst + gi;
         if (grp > glast) break;
+        const int st0 = max(u0 - grp * C::NSTEP, 0);
+        const int st1 = min(u1 - grp * C::NSTEP, C::NSTEP);
+        double tacc[C::MT][C::NT][2];
 #pragma unroll
         for (int tm = 0; tm < C::MT; ++tm)
 #pragma unroll
-          for (int tn = 0; tn < C::NT; ++tn)
+          for (int tn = 0; tn < C::NT; ++tn) tacc[tm][tn][0] = tacc[tm][tn][1] = 0.0;
+        if (grp < NGV) {
+          // A fragments from global memory (branch-free: padded rows, zero source for
+          // padding lanes of packed groups)
+          const double* src[C::MT];
+          int rstride[C::MT];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const int m = c8, nn = 2 * r4 + i;
-              int j, a, b;
-              if constexpr (S >= 8) { j = grp; a = tm * 8 + m; b = tn * 8 + nn; }
-              else { j = grp * C::JP + m / S; a = m % S; b = nn; }
-              if (j < J && b < S) Gp[(j * S + a) * S + b] += acc[gi][tm][tn][i];
+          for (int tm = 0; tm < C::MT; ++tm) {
+            int j, col;
+            if constexpr (S >= 8) { j = grp; col = tm * 8 + c8; }
+            else { j = grp * C::JP + c8 / S; col = c8 % S; }
+            if (j < NVB) {
+              src[tm] = g.X + (size_t)j * g.xstride + (row0 + r4) * S + col;
+              rstride[tm] = 4 * S;
+            } else {
+              src[tm] = g.zeros;
+              rstride[tm] = 0;
             }
+          }
+#pragma unroll 1
+          for (int st = st0; st < st1; st += C::UF) {
+            double av[C::UF][C::MT], bf[C::UF][C::NT];
+#pragma unroll
+            for (int u = 0; u < C::UF; ++u) {
+              const int s2 = min(st + u, st1 - 1);      // clamp (duplicates masked below)
+#pragma unroll
+              for (int tm = 0; tm < C::MT; ++tm) av[u][tm] = __ldg(src[tm] + s2 * rstride[tm]);
+#pragma unroll
+              for (int tn = 0; tn < C::NT; ++tn) {
+                const int col = tn * 8 + c8;
+                bf[u][tn] = (col < S && st + u < st1) ? Ws[(s2 * 4 + r4) * S + col] : 0.0;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < C::UF; ++u)
+#pragma unroll
+              for (int tm = 0; tm < C::MT; ++tm)
+#pragma unroll
+                for (int tn = 0; tn < C::NT; ++tn)
+                  dmma(tacc[tm][tn][0], tacc[tm][tn][1], av[u][tm], bf[u][tn]);
+          }
+        } else {
+          // the W block itself (y_alias): both operands from the shared-memory tile; in a
+          // packed group (S < 8) only the first S rows of M carry W
+#pragma unroll 1
+          for (int st = st0; st < st1; ++st) {
+            const int rl = st * 4 + r4;
+#pragma unroll
+            for (int tm = 0; tm < C::MT; ++tm) {
+              double a;
+              if constexpr (S >= 8) a = Ws[rl * S + tm * 8 + c8];
+              else a = (c8 < S) ? Ws[rl * S + c8] : 0.0;
+#pragma unroll
+              for (int tn = 0; tn < C::NT; ++tn) {
+                const int col = tn * 8 + c8;
+                const double bv = (col < S) ? Ws[rl * S + col] : 0.0;
+                dmma(tacc[tm][tn][0], tacc[tm][tn][1], a, bv);
+              }
+            }
+          }
+        }
+        // fold into the per-group accumulator (static register indexing)
+#pragma unroll
+        for (int q = 0; q < C::JMAX; ++q)
+          if (q == gi) {
+#pragma unroll
+            for (int tm = 0; tm < C::MT; ++tm)
+#pragma unroll
+              for (int tn = 0; tn < C::NT; ++tn) {
+                acc[q][tm][tn][0] += tacc[tm][tn][0];
+                acc[q][tm][tn][1] += tacc[tm][tn][1];
+              }
+          }
       }
+      named_arrive(3 + b, C::NTHR);                     // buffer b may be refilled
     }
-    __syncthreads();
+    // CTA partial: Gram warps add their fragments in warp order (deterministic)
+    for (int w = 0; w < C::NWG; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int gi = 0; gi < C::JMAX; ++gi) {
+          const int grp = gfirst + gi;
+          if (grp > glast) break;
+#pragma unroll
+          for (int tm = 0; tm < C::MT; ++tm)
+#pragma unroll
+            for (int tn = 0; tn < C::NT; ++tn)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int m = c8, nn = 2 * r4 + i;
+                int j, a, bcol;
+                bool ok;
+                if (grp < NGV) {
+                  if constexpr (S >= 8) { j = grp; a = tm * 8 + m; bcol = tn * 8 + nn; }
+                  else { j = grp * C::JP + m / S; a = m % S; bcol = nn; }
+                  ok = (j < NVB) && (bcol < S);
+                } else {
+                  j = J - 1;
+                  if constexpr (S >= 8) { a = tm * 8 + m; bcol = tn * 8 + nn; ok = true; }
+                  else { a = m; bcol = nn; ok = (m < S) && (nn < S); }
+                }
+                if (ok) Gp[(j * S + a) * S + bcol] += acc[gi][tm][tn][i];
+              }
+        }
+      }
+      named_sync(5, 32 * C::NWG);
+    }
   }
+  __syncthreads();
   // ---- deterministic two-level reduction across CTAs
   const int P = gridDim.x;
   const int ngroups = (P + kGramGroup - 1) / kGramGroup;
   const int grp = blockIdx.x / kGramGroup;
   const int gsize = min(kGramGroup, P - grp * kGramGroup);
-  for (int e = tid; e < E; e += 256) g.part[(size_t)blockIdx.x * E + e] = Gp[e];
+  for (int e = tid; e < E; e += C::NTHR) g.part[(size_t)blockIdx.x * E + e] = Gp[e];
   __threadfence();
   __syncthreads();
   __shared__ unsigned ticket;
@@ -243,7 +312,7 @@ k_spmm_gram(GramArgs g) {
   __syncthreads();
   if (ticket != (unsigned)(gsize - 1)) return;
   __threadfence();
-  for (int e = tid; e < E; e += 256) {
+  for (int e = tid; e < E; e += C::NTHR) {
     double s = 0.0;
     for (int c = 0; c < gsize; ++c) s += __ldcg(g.part + (size_t)(grp * kGramGroup + c) * E + e);
     g.gpart[(size_t)grp * E + e] = s;
@@ -255,7 +324,7 @@ k_spmm_gram(GramArgs g) {
   __syncthreads();
   if (ticket != (unsigned)(ngroups - 1)) return;
   __threadfence();
-  for (int e = tid; e < E; e += 256) {
+  for (int e = tid; e < E; e += C::NTHR) {
     double s = 0.0;
     for (int c = 0; c < ngroups; ++c) s += __ldcg(g.gpart + (size_t)c * E + e);
     g.G[e] = s;

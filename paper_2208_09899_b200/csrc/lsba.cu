@@ -56,7 +56,9 @@ struct lsba_ctx_ {
   double* d_va = nullptr;
   // basis: (m_max+1) slots of n x s
   double* d_V = nullptr;
-  size_t slot = 0;  // elements per slot
+  size_t slot = 0;         // elements per block (n_local x s)
+  size_t slot_stride = 0;  // elements between consecutive basis slots (rows padded to kRowPad)
+  double* d_zeros = nullptr;
   // halo
   int n_ghost = 0;
   double* d_ghost = nullptr;
@@ -197,6 +199,10 @@ struct LaunchScope {
   }
 
 static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot_stride; }
+static inline bool in_basis(lsba_ctx c, const double* p) {
+  return p >= c->d_V && p < c->d_V + (size_t)(c->m_max + 1) * c->slot_stride;
+}
 
 // ---------------------------------------------------------------- halo exchange (P > 1)
 template <int S>
@@ -274,14 +280,15 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
 }
 
 template <int S>
-static bool dmma_gram_ok(lsba_ctx c, int J, int ip) {
+static bool dmma_gram_ok(lsba_ctx c, int J, int ip, const double* X, const double* Y) {
   if (ip == LSBA_IP_GLOBAL || c->variant != 0) return false;
+  if (!in_basis(c, X) || !in_basis(c, Y)) return false;   // padded rows required
   if constexpr (!(S == 1 || S == 2 || S == 4 || S == 8 || S == 16)) {
     return false;
   } else {
     using Cg = GramCfg<S>;
     const int NG = (J + Cg::JP - 1) / Cg::JP;
-    return (NG + Cg::NW - 1) / Cg::NW + 1 <= Cg::JMAX && c->d_tickets != nullptr &&
+    return (NG + 1 + Cg::NWG - 1) / Cg::NWG + 1 <= Cg::JMAX && c->d_tickets != nullptr &&
            (size_t)c->gram_grid * J * S * S <= c->part_cap;
   }
 }
@@ -295,7 +302,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
                           const double* Vk, const int* active) {
   const bool gl = (ip == LSBA_IP_GLOBAL);
   const size_t E = gl ? (size_t)J : (size_t)J * S * S;
-  if (dmma_gram_ok<S>(c, J, ip)) {
+  if (dmma_gram_ok<S>(c, J, ip, X, Y)) {
     if constexpr (S == 1 || S == 2 || S == 4 || S == 8 || S == 16) {
       if (Vk) TRY(halo_t<S>(c, Vk));
       const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
@@ -305,16 +312,17 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       if (c->n > 0) {
         GramArgs a;
         a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-        a.Vk = Vk; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J; a.Y = Y;
+        a.Vk = Vk; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
+        a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
         a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
         a.active = active;
-        const size_t smem = sizeof(double) * ((size_t)GramCfg<S>::T * S + E);
+        const size_t smem = sizeof(double) * (2 * (size_t)GramCfg<S>::T * S + E);
         auto fn = k_spmm_gram<S>;
         if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ = 1;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, GramCfg<S>::NTHR, smem));
         const int grid = std::max(1, std::min(occ * c->n_sms, c->gram_grid));
-        fn<<<grid, 256, smem, c->stream>>>(a);
+        fn<<<grid, GramCfg<S>::NTHR, smem, c->stream>>>(a);
         CKL();
       } else {
         CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
@@ -406,7 +414,6 @@ static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, 
   LSBA_DISPATCH_S(c->s, project_t, c, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr, kid);
 }
 
-static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot; }
 
 template <int B>
 static lsba_status small_step_t(lsba_ctx c, int k, const CycleParams& prm) {
@@ -431,9 +438,9 @@ static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
 // IO(U) with U in slot 0: Gram (1 sync), chol, scale in place (Alg 3 line 1).  Resets the
 // device cycle control with this cycle's parameters.  Asynchronous.
 static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
-  TRY(gram(c, slotp(c, 0), c->slot, 1, slotp(c, 0), c->ip));
+  TRY(gram(c, slotp(c, 0), c->slot_stride, 1, slotp(c, 0), c->ip));
   TRY(small_step(c, 0, prm));
-  TRY(project(c, slotp(c, 0), c->slot, 1, c->st.coef, nullptr, slotp(c, 0), 0, nullptr, nullptr,
+  TRY(project(c, slotp(c, 0), c->slot_stride, 1, c->st.coef, nullptr, slotp(c, 0), 0, nullptr, nullptr,
               c->st.flag_dev, LSBA_K_PROJECT));
   return LSBA_OK;
 }
@@ -442,10 +449,10 @@ static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
 // control says the cycle has ended (speculative enqueue of a whole cycle).
 static lsba_status pip_step_async(lsba_ctx c, int k) {
   const CycleParams none{};
-  TRY(gram(c, slotp(c, 0), c->slot, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
+  TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
            &c->d_ctl->active));                                                  // lines 3-4
   TRY(small_step(c, k, none));                                                   // line 5
-  TRY(project(c, slotp(c, 0), c->slot, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
+  TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
               nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
   return LSBA_OK;
 }
@@ -580,7 +587,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
         int sing = 1;
         TRY(cycle_solve(c, k, 0, 1, &sing));
         if (!sing) {
-          TRY(project(c, slotp(c, 0), c->slot, k, c->d_Y, X, c->d_Xc, 0, nullptr, nullptr,
+          TRY(project(c, slotp(c, 0), c->slot_stride, k, c->d_Y, X, c->d_Xc, 0, nullptr, nullptr,
                       nullptr, LSBA_K_COMBINE));
           double rel;
           TRY(true_relres(c->d_Xc, slotp(c, k), &rel));    // slot k (flagged W) is free
@@ -610,7 +617,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     }
     if (cc.why == 2) {
       // X += V_k Xi C_acc, then confirm with the explicit residual (R19)
-      TRY(project(c, slotp(c, 0), c->slot, k_used, c->d_Y, X, X, 0, nullptr, nullptr, nullptr,
+      TRY(project(c, slotp(c, 0), c->slot_stride, k_used, c->d_Y, X, X, 0, nullptr, nullptr, nullptr,
                   LSBA_K_COMBINE));
       double rel;
       TRY(true_relres(X, slotp(c, 0), &rel));                // slot 0 <- B - A X
@@ -625,7 +632,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       continue;
     }
     // X += V_k Xi C_acc ;  U = V_{k+1} [M; -H_{k+1,k}] -> slot 0
-    TRY(project(c, slotp(c, 0), c->slot, k_used, c->d_Y, X, X, k_used + 1, c->d_Z, slotp(c, 0),
+    TRY(project(c, slotp(c, 0), c->slot_stride, k_used, c->d_Y, X, X, k_used + 1, c->d_Z, slotp(c, 0),
                 nullptr, LSBA_K_COMBINE));
   }
   info->m_final = m_cur;
@@ -755,7 +762,7 @@ static void release(lsba_ctx c) {
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_G, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
-                  c->d_gpart, c->d_tickets, c->d_ctl};
+                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -877,7 +884,11 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   }
   // ---- basis and work buffers
   c->slot = (size_t)n_local * s;
-  TRY(dalloc(c, &c->d_V, (size_t)(m_max + 1) * c->slot));
+  c->slot_stride = (size_t)((n_local + kRowPad - 1) / kRowPad) * kRowPad * s;
+  TRY(dalloc(c, &c->d_V, (size_t)(m_max + 1) * c->slot_stride));
+  CK(cudaMemset(c->d_V, 0, sizeof(double) * (size_t)(m_max + 1) * c->slot_stride));   // zero pad rows
+  TRY(dalloc(c, &c->d_zeros, 64));
+  CK(cudaMemset(c->d_zeros, 0, sizeof(double) * 64));
   TRY(dalloc(c, &c->d_Xc, c->slot));
   {
     int sms = 148;
