@@ -169,8 +169,11 @@ lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t 
 
 /* Fault injection: make the Cholesky of step k_flag report a NaN-flag once (0 = off). */
 lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
-/* Kernel implementation choice: 0 = auto (tensor-core DMMA kernels where s >= 4),
- * 1 = force the plain DFMA kernels.  For parity tests of both paths. */
+/* Kernel implementation choice (classical inner product): 0 = auto (standalone SpMM +
+ * tensor-core Gram with 16-byte fragment loads + tensor-core projection), 1 = plain DFMA
+ * kernels, 2 = SpMM fused into the tensor-core Gram pass (gather warps), 3 = tensor-core Gram
+ * with 8-byte fragment loads, 4 = TMA-staged tensor-core Gram.  For parity tests and
+ * measurements of every path. */
 lsba_status lsba_set_kernel_variant(lsba_ctx ctx, int32_t variant);
 
 /* Per-kernel timing with CUDA events on the context stream.  Kernel ids: */

@@ -100,6 +100,8 @@ struct lsba_ctx_ {
   int force_flag_k = 0;
   bool forced_done = false;
   int variant = 0;
+  int fuse_spmm = 0;   // 1: SpMM fused into the tensor-core Gram pass (gather warps)
+  int gram_impl = 0;   // unfused mode: 0 v5 (16-byte fragment loads), 1 TMA-staged, 2 v3
   int64_t launches = 0;
   int64_t ws_bytes = 0;
   std::string err;
@@ -304,6 +306,63 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
   const size_t E = gl ? (size_t)J : (size_t)J * S * S;
   if (dmma_gram_ok<S>(c, J, ip, X, Y)) {
     if constexpr (S == 1 || S == 2 || S == 4 || S == 8 || S == 16) {
+      if (Vk && !c->fuse_spmm) {   // standalone high-occupancy SpMM, then the Gram pass
+        TRY(spmm_t<S>(c, Vk, Y, active));
+        Vk = nullptr;
+      }
+      if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
+        using G5 = G5Cfg<S>;
+        const int NG5 = (J - 1 + G5::PB - 1) / G5::PB + 1;
+        if (!Vk && c->gram_impl == 0 && (NG5 + G5::NW - 1) / G5::NW + 1 <= G5::JMAX) {
+          const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+          LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
+          if (c->n > 0) {
+            GramArgs a;
+            a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+            a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
+            a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
+            a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+            a.active = active;
+            const size_t smem = sizeof(double) * (2 * (size_t)G5::T * S + E);
+            auto fn = k_gram_v5<S>;
+            if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 1;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G5::NTHR, smem));
+            const int grid = std::max(1, std::min(std::min(occ, 4) * c->n_sms, cdiv(c->n, G5::T)));
+            fn<<<grid, G5::NTHR, smem, c->stream>>>(a);
+            CKL();
+          } else {
+            CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+          }
+          if (c->nranks > 1)
+            CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+          return LSBA_OK;
+        }
+      }
+      if (!Vk && c->gram_impl == 1) {    // TMA-staged tensor-core Gram
+        const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+        LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
+        if (c->n > 0) {
+          GramArgs a;
+          a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+          a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
+          a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
+          a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+          a.active = active;
+          using TC = TmaCfg<S>;
+          const size_t smem = (size_t)TC::R * TC::STAGE_BYTES + (size_t)TC::WR * TC::TILE_BYTES + sizeof(double) * E;
+          auto fn = k_gram_tma<S>;
+          CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          const int grid = std::min(c->n_sms, std::max(1, cdiv(c->n, TC::T)));
+          fn<<<grid, TC::NTHR, smem, c->stream>>>(a);
+          CKL();
+        } else {
+          CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+        }
+        if (c->nranks > 1)
+          CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+        return LSBA_OK;
+      }
       if (Vk) TRY(halo_t<S>(c, Vk));
       const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
       const double bytes = (Vk ? 12.0 * c->nnz + 4.0 * (c->n + 1) : 0.0) +
@@ -1167,8 +1226,10 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
 
 extern "C" lsba_status lsba_set_kernel_variant(lsba_ctx c, int32_t variant) {
   if (!c) return LSBA_E_ARG;
-  if (variant < 0 || variant > 1) return fail(c, LSBA_E_ARG, "variant must be 0 or 1");
-  c->variant = variant;
+  if (variant < 0 || variant > 4) return fail(c, LSBA_E_ARG, "variant must be 0..4");
+  c->variant = variant == 1 ? 1 : 0;
+  c->fuse_spmm = variant == 2 ? 1 : 0;
+  c->gram_impl = variant == 3 ? 2 : (variant == 4 ? 1 : 0);
   return LSBA_OK;
 }
 
