@@ -410,7 +410,8 @@ struct CycleCtl {
   int32_t proj_singular; // why == 1 because h~_k was singular (reading R22)
   int32_t m_cur;         // step budget of this cycle
   int32_t gmres;         // 1: BGMRES estimate, 0: BFOM estimate
-  int32_t pad0, pad1;
+  int32_t need_kappa;    // 1: maintain kappa_F each step
+  int32_t pad1;
   double tol_abs;        // tol * ||B||_F (negative: never converge)
   double tau;            // kappa_F threshold (inf: off)
   double res_est;        // estimate of the last accepted step (times C_acc)

@@ -507,7 +507,7 @@ static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
 // One Alg-3 step k (1-based), asynchronous; every kernel no-ops once the device cycle
 // control says the cycle has ended (speculative enqueue of a whole cycle).
 static lsba_status pip_step_async(lsba_ctx c, int k) {
-  const CycleParams none{};
+  const CycleParams none{};   // (k > 0 launches read their parameters from the device control)
   TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
            &c->d_ctl->active));                                                  // lines 3-4
   TRY(small_step(c, k, none));                                                   // line 5
@@ -631,6 +631,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     prm.reset_forced = (cycle == 1) ? 1 : 0;
     prm.tol_abs = tol * normB;                               // R5, R18
     prm.tau = tau;                                           // R8
+    prm.need_kappa = std::isfinite(tau) ? 1 : 0;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
     for (int k = 1; k <= m_cur; ++k) TRY(pip_step_async(c, k));
     TRY(read_status(c, nullptr, &cc));
@@ -1068,6 +1069,7 @@ extern "C" lsba_status lsba_arnoldi_begin(lsba_ctx c, const double* B_dev, lsba_
   prm.reset_forced = 1;
   prm.tol_abs = -1.0;            // the step API never declares convergence
   prm.tau = INFINITY;
+  prm.need_kappa = 1;
   TRY(io_begin_async(c, prm));
   StepStatus stt;
   TRY(read_status(c, &stt, nullptr));

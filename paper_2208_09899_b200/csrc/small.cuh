@@ -30,7 +30,7 @@ struct SmallState2 {
   double* Rfac;    // (m bmax)^2 upper block triangular R of Hbar, ld ldH
   double* htil;    // [step][b*b] col-major h~_k
   double* ghat;    // [step][b*b] col-major g^_k
-  double* Rinv;    // ((m+1)bmax)^2, ld ldH
+  double* Rinv;    // ((m+1)bmax)^2, ROW-major, ld ldH
   double* sc;      // [0] ||R||_F^2, [1] ||R^{-1}||_F^2
   double* Cacc;    // b x b col-major
   StepStatus* status;
@@ -43,6 +43,8 @@ struct SmallState2 {
 struct CycleParams {
   int m_cur, gmres, force_k, reset_forced;
   double tol_abs, tau;
+  int need_kappa;      // 1: maintain kappa_F every step (tau finite, or the step API)
+  int pad_;
 };
 
 // ---------------------------------------------------------------------------- warp helpers
@@ -148,7 +150,7 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
 template <int B>
 __global__ void __launch_bounds__(32 * (B + 2))
 k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm, double rfac) {
-  extern __shared__ double Gs[];
+  extern __shared__ double Gs[];         // (k+1) B B copy of G, then (k-1) reflector sets
   __shared__ double Ss[B * B], Rs[B * B], Ris[B * B], Ht[B * B], Gh[B * B];
   __shared__ double red[32];
   __shared__ int flag_s, sing_s;
@@ -162,6 +164,18 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
   int force_flag = 0;
   if (k > 0 && k == ctl->force_k && !ctl->forced_done) force_flag = 1;
   for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
+  // stage the reflector sets 1..k-1 (set j: B vectors of 2B) for the QR window sweep
+  double* Vs = Gs + (kb + B) * B;
+  double* Ts = Vs + (size_t)(k > 1 ? k - 1 : 0) * B * 2 * B;
+  if (k > 1) {
+    for (int e = tid; e < (k - 1) * B * 2 * B; e += nt) {
+      const int jset = e / (B * 2 * B), rem = e % (B * 2 * B);
+      const int q = rem / (2 * B), r = rem % (2 * B);
+      Vs[e] = st.qr_v[(size_t)jset * st.bmax * 2 * st.bmax + (size_t)q * 2 * st.bmax + r];
+    }
+    for (int e = tid; e < (k - 1) * B; e += nt) Ts[e] = st.qr_tau[(size_t)(e / B) * st.bmax + e % B];
+  }
+  const int need_kappa = (k == 0) ? prm.need_kappa : ctl->need_kappa;
   __syncthreads();
   // Hcol -> Hbar column block k-1; S = Omega - Hcol^T Hcol
   if (k > 0)
@@ -169,11 +183,15 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
       const int r = e / B, c = e % B;
       st.Hbar[r + (size_t)((k - 1) * B + c) * ldH] = Gs[e];
     }
-  for (int e = tid; e < B * B; e += nt) {
-    const int x = e % B, y = e / B;
-    double t = Gs[(kb + x) * B + y];
-    for (int r = 0; r < kb; ++r) t -= Gs[r * B + x] * Gs[r * B + y];
-    Ss[x + y * B] = t;
+  {  // S = Omega - Hcol^T Hcol: one output per warp at a time, lanes split the kb-long sum
+    const int nw = nt >> 5;
+    for (int e = warp; e < B * B; e += nw) {
+      const int x = e % B, y = e / B;
+      double t = 0.0;
+      for (int r = lane; r < kb; r += 32) t += Gs[r * B + x] * Gs[r * B + y];
+      t = warp_sum(t);
+      if (lane == 0) Ss[x + y * B] = Gs[(kb + x) * B + y] - t;
+    }
   }
   __syncthreads();
   if (warp == 0) {
@@ -224,6 +242,7 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
         if (prm.reset_forced) ctl->forced_done = 0;
         ctl->tol_abs = prm.tol_abs;
         ctl->tau = prm.tau;
+        ctl->need_kappa = prm.need_kappa;
         ctl->res_est = nan("");
         ctl->kappa = nan("");
       } else if (f) {
@@ -262,12 +281,12 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     const int colg = (k - 1) * B + c;   // global column index in Hbar / Rfac
     double w = (lane < 2 * B && lane < kb) ? Gs[lane * B + c] : 0.0;
     for (int j = 1; j <= k - 1; ++j) {
-      const double* V = st.qr_v + (size_t)(j - 1) * st.bmax * 2 * st.bmax;
-      const double* T = st.qr_tau + (size_t)(j - 1) * st.bmax;
+      const double* V = Vs + (size_t)(j - 1) * B * 2 * B;
+      const double* T = Ts + (size_t)(j - 1) * B;
       double v[B], tau[B];
 #pragma unroll
       for (int q = 0; q < B; ++q) {
-        v[q] = (lane < 2 * B) ? V[(size_t)q * 2 * st.bmax + lane] : 0.0;
+        v[q] = (lane < 2 * B) ? V[q * 2 * B + lane] : 0.0;
         tau[q] = T[q];
       }
 #pragma unroll
@@ -316,7 +335,7 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     for (int e = tid; e < B * B; e += nt) {
       const int x = e % B, y = e / B;
       st.beta[e] = Rs[e];
-      st.Rinv[x + (size_t)y * ldH] = Ris[e];
+      st.Rinv[(size_t)x * ldH + y] = Ris[e];      // row-major
     }
     const int rows = (st.m + 1) * B;
     for (int e = tid; e < rows * B; e += nt) {
@@ -405,48 +424,53 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     acc2 = warp_sum(acc2);
     if (lane == 0) st.status->res_gmres = sqrt(acc2) * rfac;
   }
-  // kappa_F (reading R8): T = R_k^{-1} Hcol (kb x B); X = -T R^{-1} -> Rinv[:, kb..kb+B)
-  double part_r = 0.0, part_i = 0.0;
-  for (int r = tid; r < kb; r += nt) {
-    double acc[B];
+  // kappa_F (reading R8): T = R_k^{-1} Hcol (kb x B); X = -T R^{-1} -> Rinv[:, kb..kb+B).
+  // Rinv is row-major: one warp per row, lanes over the contiguous row.  Skipped unless
+  // needed (no condition threshold in a solve: the decision does not use it).
+  double kap = nan("");
+  if (need_kappa) {
+    double part_r = 0.0, part_i = 0.0;
+    const int nw = nt >> 5;
+    for (int r = warp; r < kb; r += nw) {
+      double acc[B];
 #pragma unroll
-    for (int c = 0; c < B; ++c) acc[c] = 0.0;
-    const double* Rr = st.Rinv + r;
-    int q = r;
-    for (; q + 3 < kb; q += 4) {
-      const double a0 = Rr[(size_t)q * ldH], a1 = Rr[(size_t)(q + 1) * ldH];
-      const double a2 = Rr[(size_t)(q + 2) * ldH], a3 = Rr[(size_t)(q + 3) * ldH];
+      for (int c = 0; c < B; ++c) acc[c] = 0.0;
+      const double* Rr = st.Rinv + (size_t)r * ldH;
+      for (int q = r + lane; q < kb; q += 32) {
+        const double a = Rr[q];
 #pragma unroll
-      for (int c = 0; c < B; ++c)
-        acc[c] += a0 * Gs[q * B + c] + a1 * Gs[(q + 1) * B + c] + a2 * Gs[(q + 2) * B + c] + a3 * Gs[(q + 3) * B + c];
+        for (int c = 0; c < B; ++c) acc[c] += a * Gs[q * B + c];
+      }
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
+      if (lane < B) {
+        const int c = lane;
+        double x = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < B; ++q2)
+          if (q2 <= c) x -= acc[q2] * Ris[q2 + c * B];
+        st.Rinv[(size_t)r * ldH + kb + c] = x;
+        part_i += x * x;
+        part_r += Gs[r * B + c] * Gs[r * B + c];
+      }
     }
-    for (; q < kb; ++q) {
-      const double a0 = Rr[(size_t)q * ldH];
-#pragma unroll
-      for (int c = 0; c < B; ++c) acc[c] += a0 * Gs[q * B + c];
+    for (int e = tid; e < B * B; e += nt) {
+      const int x = e % B, y = e / B;
+      st.Rinv[(size_t)(kb + x) * ldH + kb + y] = Ris[e];
+      part_i += Ris[e] * Ris[e];
+      part_r += Rs[e] * Rs[e];
     }
-#pragma unroll
-    for (int c = 0; c < B; ++c) {
-      double x = 0.0;
-#pragma unroll
-      for (int q2 = 0; q2 <= c; ++q2) x -= acc[q2] * Ris[q2 + c * B];
-      st.Rinv[r + (size_t)(kb + c) * ldH] = x;
-      part_i += x * x;
-      part_r += Gs[r * B + c] * Gs[r * B + c];
+    const double dr = block_sum(part_r, red);
+    const double di = block_sum(part_i, red);
+    if (tid == 0) {
+      st.sc[0] += dr;
+      st.sc[1] += di;
+      kap = sqrt(st.sc[0] * st.sc[1]);
     }
+  } else {
+    __syncthreads();
   }
-  for (int e = tid; e < B * B; e += nt) {
-    const int x = e % B, y = e / B;
-    st.Rinv[(kb + x) + (size_t)(kb + y) * ldH] = Ris[e];
-    part_i += Ris[e] * Ris[e];
-    part_r += Rs[e] * Rs[e];
-  }
-  const double dr = block_sum(part_r, red);
-  const double di = block_sum(part_i, red);
   if (tid == 0) {
-    st.sc[0] += dr;
-    st.sc[1] += di;
-    const double kap = sqrt(st.sc[0] * st.sc[1]);
     st.status->kappa_F = kap;
     // ---- device-side decision (readings R5, R8, R9, R22)
     if (sing_s) {                       // FOM projected matrix singular: treated as a NaN-flag
