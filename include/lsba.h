@@ -170,17 +170,17 @@ lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t 
 /* Fault injection: make the Cholesky of step k_flag report a NaN-flag once (0 = off). */
 lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
 /* Kernel implementation choice (classical inner product): 0 = auto (standalone SpMM +
- * tensor-core Gram with 16-byte fragment loads + tensor-core projection), 1 = plain DFMA
+ * barrier-free streaming tensor-core Gram v6 + tensor-core projection), 1 = plain DFMA
  * kernels, 2 = SpMM fused into the tensor-core Gram pass (gather warps), 3 = tensor-core Gram
- * with 8-byte fragment loads, 4 = TMA-staged tensor-core Gram.  For parity tests and
- * measurements of every path. */
+ * with 8-byte fragment loads, 4 = TMA-staged tensor-core Gram, 5 = shared-memory-tiled
+ * tensor-core Gram v5.  For parity tests and measurements of every path. */
 lsba_status lsba_set_kernel_variant(lsba_ctx ctx, int32_t variant);
 
 /* Per-kernel timing with CUDA events on the context stream.  Kernel ids: */
 enum {
   LSBA_K_SPMM = 0, LSBA_K_GRAM = 1, LSBA_K_GRAM_FINALIZE = 2, LSBA_K_SMALL_STEP = 3,
   LSBA_K_PROJECT = 4, LSBA_K_CYCLE_SOLVE = 5, LSBA_K_COMBINE = 6, LSBA_K_RESIDUAL = 7,
-  LSBA_K_HALO_PACK = 8, LSBA_K_MISC = 9, LSBA_K_COUNT = 10
+  LSBA_K_HALO_PACK = 8, LSBA_K_MISC = 9, LSBA_K_STEP_UPDATE = 10, LSBA_K_COUNT = 11
 };
 /* enable != 0 starts recording events around every launch (resets the records). */
 lsba_status lsba_profile_enable(lsba_ctx ctx, int32_t enable);

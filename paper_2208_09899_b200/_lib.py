@@ -23,7 +23,7 @@ LSBA_IP_CLASSICAL, LSBA_IP_GLOBAL = 0, 1
 LSBA_SKEL_BCGS_PIP = 0
 LSBA_CONVERGED, LSBA_MAX_RESTARTS, LSBA_DEAD = 0, 1, 2
 KERNEL_IDS = dict(spmm=0, gram=1, gram_finalize=2, small_step=3, project=4, cycle_solve=5,
-                  combine=6, residual=7, halo_pack=8, misc=9)
+                  combine=6, residual=7, halo_pack=8, misc=9, step_update=10)
 _IP = {"cl": LSBA_IP_CLASSICAL, "gl": LSBA_IP_GLOBAL, 0: 0, 1: 1}
 
 

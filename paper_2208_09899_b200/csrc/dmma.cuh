@@ -818,6 +818,170 @@ k_gram_v5(GramArgs g) {
 }
 
 // ------------------------------------------------------------------------------------------
+// pass 1 (unfused), v6: barrier-free streaming Gram.  Warp (rs, qs) of a CTA owns the 4-row
+// steps rs, rs+RW, ... of the CTA's contiguous step range and the block groups of set qs
+// (QW sets x RW row slices = 8 warps).  Per step it loads the W (B) fragment from global
+// memory (shared through L1 with the QW-1 sibling warps) and one 16-byte A fragment per
+// group (even/odd column DMMA tiles, PB = 16/S blocks per group as in v5); two steps per
+// iteration keep ~2 (GMAX + 1) independent loads in flight per warp.  No shared-memory
+// tiles, no barriers until the final deterministic reduction.
+// ------------------------------------------------------------------------------------------
+template <int S>
+struct G6Cfg {
+  static constexpr int PB = S >= 16 ? 1 : 16 / S;
+  static constexpr int NT = S >= 8 ? S / 8 : 1;
+  static constexpr int GMAX = S >= 16 ? 4 : 6;
+  static constexpr int NW = 8;
+  static constexpr int NTHR = 256;
+  static constexpr int U = 2;                      // steps per iteration
+};
+
+template <int S>
+__global__ void __launch_bounds__(256, 2)
+k_gram_v6(GramArgs g) {
+  using C = G6Cfg<S>;
+  static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v6 Gram: s in {2,4,8,16}");
+  if (g.active && *g.active == 0) return;
+  extern __shared__ __align__(16) double Gp6[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int J = g.J, E = J * S * S;
+  const int NVB = J - (g.y_alias ? 1 : 0);
+  const int NGV = (NVB + C::PB - 1) / C::PB;
+  const int NG = NGV + (g.y_alias ? 1 : 0);
+  int QW = 1;
+  while (QW < C::NW && (NG + QW - 1) / QW > C::GMAX) QW *= 2;
+  const int RW = C::NW / QW;
+  const int rs = warp % RW, qs = warp / RW;
+  const int gA = (qs * NG) / QW, gB = ((qs + 1) * NG) / QW;
+  const int ng = gB - gA;
+  const int r4 = lane & 3, c8 = lane >> 2;
+  constexpr int LPB = S >= 16 ? 8 : S / 2;
+  const int jj = c8 / LPB, cp = c8 % LPB;
+  for (int e = tid; e < E; e += C::NTHR) Gp6[e] = 0.0;
+
+  // per-group A source of this lane (row r4 of step 0; + 4 S per step)
+  const double* src[C::GMAX];
+  int rstr[C::GMAX];
+#pragma unroll
+  for (int gi = 0; gi < C::GMAX; ++gi) {
+    const int grp = gA + gi;
+    src[gi] = g.zeros;
+    rstr[gi] = 0;
+    if (gi < ng) {
+      if (grp < NGV) {
+        const int j = grp * C::PB + (S >= 16 ? 0 : jj);
+        if (j < NVB) { src[gi] = g.X + (size_t)j * g.xstride + r4 * S + 2 * cp; rstr[gi] = 4 * S; }
+      } else if (S >= 16 || jj == 0) {      // the W block itself
+        src[gi] = g.Y + r4 * S + 2 * cp;
+        rstr[gi] = 4 * S;
+      }
+    }
+  }
+  double acc[C::GMAX][2][C::NT][2];
+#pragma unroll
+  for (int a = 0; a < C::GMAX; ++a)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn) acc[a][e][tn][0] = acc[a][e][tn][1] = 0.0;
+
+  const long NS = ((long)g.n + 3) / 4;                 // 4-row steps (rows padded)
+  const long s0 = NS * blockIdx.x / gridDim.x, s1 = NS * (blockIdx.x + 1) / gridDim.x;
+  for (long st = s0 + rs; st < s1; st += (long)C::U * RW) {
+    double2 av[C::U][C::GMAX];
+    double bw[C::U][C::NT];
+#pragma unroll
+    for (int u = 0; u < C::U; ++u) {
+      const long su = st + (long)u * RW;
+      const bool ok = su < s1;
+      const long sc = ok ? su : st;
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn) {
+        const int col = tn * 8 + c8;
+        bw[u][tn] = (ok && col < S) ? __ldg(g.Y + (size_t)(sc * 4 + r4) * S + col) : 0.0;
+      }
+#pragma unroll
+      for (int gi = 0; gi < C::GMAX; ++gi)
+        av[u][gi] = (gi < ng) ? __ldg(reinterpret_cast<const double2*>(src[gi] + (size_t)sc * rstr[gi]))
+                              : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < C::U; ++u)
+#pragma unroll
+      for (int gi = 0; gi < C::GMAX; ++gi) {
+        if (gi >= ng) continue;
+#pragma unroll
+        for (int tn = 0; tn < C::NT; ++tn) {
+          dmma(acc[gi][0][tn][0], acc[gi][0][tn][1], av[u][gi].x, bw[u][tn]);
+          dmma(acc[gi][1][tn][0], acc[gi][1][tn][1], av[u][gi].y, bw[u][tn]);
+        }
+      }
+  }
+  __syncthreads();
+  // CTA partial: row slices add in order rs = 0..RW-1 (group sets are disjoint)
+  for (int r = 0; r < RW; ++r) {
+    if (rs == r) {
+#pragma unroll
+      for (int gi = 0; gi < C::GMAX; ++gi) {
+        if (gi >= ng) continue;
+        const int grp = gA + gi;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int tn = 0; tn < C::NT; ++tn)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int a = 2 * cp + e;
+              const int bcol = tn * 8 + 2 * r4 + i;
+              int j;
+              bool ok = bcol < S;
+              if (grp < NGV) {
+                j = grp * C::PB + (S >= 16 ? 0 : jj);
+                ok = ok && (j < NVB);
+              } else {
+                j = J - 1;
+                ok = ok && (S >= 16 || jj == 0);
+              }
+              if (ok) Gp6[(j * S + a) * S + bcol] += acc[gi][e][tn][i];
+            }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- deterministic two-level reduction across CTAs
+  const int P = gridDim.x;
+  const int ngroups = (P + kGramGroup - 1) / kGramGroup;
+  const int grpi = blockIdx.x / kGramGroup;
+  const int gsize = min(kGramGroup, P - grpi * kGramGroup);
+  for (int e = tid; e < E; e += C::NTHR) g.part[(size_t)blockIdx.x * E + e] = Gp6[e];
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned ticket;
+  if (tid == 0) ticket = atomicAdd(&g.tickets[grpi], 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(gsize - 1)) return;
+  __threadfence();
+  for (int e = tid; e < E; e += C::NTHR) {
+    double s2 = 0.0;
+    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * E + e);
+    g.gpart[(size_t)grpi * E + e] = s2;
+  }
+  if (tid == 0) g.tickets[grpi] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(&g.tickets[ngroups], 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(ngroups - 1)) return;
+  __threadfence();
+  for (int e = tid; e < E; e += C::NTHR) {
+    double s2 = 0.0;
+    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * E + e);
+    g.G[e] = s2;
+  }
+  if (tid == 0) g.tickets[ngroups] = 0u;
+}
+
+// ------------------------------------------------------------------------------------------
 // pass 2 on the tensor cores (S in {4, 8, 16}).  A warp owns 8-row blocks (grid-stride);
 // per block j: A = X_j rows (8 x 4 chunks), B = C_j (4 x 8 chunks, shared memory), D in
 // registers.  out0/out1 may alias an input block (each warp reads its rows before writing).

@@ -12,6 +12,9 @@ template <int B>
 cudaError_t launch_step_small(const SmallState2& st, const double* G, int k, const CycleParams& prm,
                               double rfac, cudaStream_t stream);
 template <int B>
+cudaError_t launch_step_update(const SmallState2& st, const double* G, int k, double rfac,
+                               cudaStream_t stream);
+template <int B>
 cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy, int upd, double* Y,
                              double* Z, int* info, cudaStream_t stream);
 
@@ -19,6 +22,8 @@ cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy,
   template <>                                                                                           \
   cudaError_t launch_step_small<B>(const SmallState2&, const double*, int, const CycleParams&, double,  \
                                    cudaStream_t);                                                        \
+  template <>                                                                                           \
+  cudaError_t launch_step_update<B>(const SmallState2&, const double*, int, double, cudaStream_t);     \
   template <>                                                                                           \
   cudaError_t launch_cycle_end<B>(const SmallState2&, int, int, int, int, double*, double*, int*,     \
                                   cudaStream_t);

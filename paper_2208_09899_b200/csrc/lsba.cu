@@ -75,6 +75,8 @@ struct lsba_ctx_ {
   unsigned* d_tickets = nullptr;  // DMMA Gram: CTA arrival counters (self-resetting)
   int gram_grid = 0;              // DMMA Gram: persistent grid size
   CycleCtl* d_ctl = nullptr;      // device-side cycle control
+  cudaStream_t stream2 = nullptr;  // update kernels run here, concurrent with the projection
+  cudaEvent_t ev_coef = nullptr, ev_upd = nullptr;
   CycleCtl* h_ctl = nullptr;      // pinned copy
   int n_sms = 148;
   // small state
@@ -101,7 +103,7 @@ struct lsba_ctx_ {
   bool forced_done = false;
   int variant = 0;
   int fuse_spmm = 0;   // 1: SpMM fused into the tensor-core Gram pass (gather warps)
-  int gram_impl = 0;   // unfused mode: 0 v5 (16-byte fragment loads), 1 TMA-staged, 2 v3
+  int gram_impl = 0;   // unfused mode: 0 v6 (barrier-free), 3 v5, 1 TMA-staged, 2 v3
   int64_t launches = 0;
   int64_t ws_bytes = 0;
   std::string err;
@@ -156,7 +158,9 @@ struct LaunchScope {
   lsba_ctx c;
   int kid;
   EvPair* ev = nullptr;
-  LaunchScope(lsba_ctx c_, int kid_, double bytes) : c(c_), kid(kid_) {
+  cudaStream_t strm;
+  LaunchScope(lsba_ctx c_, int kid_, double bytes, cudaStream_t s_ = nullptr)
+      : c(c_), kid(kid_), strm(s_ ? s_ : c_->stream) {
     c->launches++;
     if (!c->prof.on) return;
     Prof& p = c->prof;
@@ -169,10 +173,10 @@ struct LaunchScope {
       p.ev[kid].push_back(e);
     }
     ev = &p.ev[kid][p.used[kid]++];
-    cudaEventRecord(ev->a, c->stream);
+    cudaEventRecord(ev->a, strm);
   }
   ~LaunchScope() {
-    if (ev) cudaEventRecord(ev->b, c->stream);
+    if (ev) cudaEventRecord(ev->b, strm);
   }
 };
 
@@ -311,9 +315,38 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
         Vk = nullptr;
       }
       if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
+        using G6 = G6Cfg<S>;
+        const int NG6 = (J - 1 + G6::PB - 1) / G6::PB + 1;
+        if (!Vk && c->gram_impl == 0 && (NG6 + G6::NW - 1) / G6::NW <= G6::GMAX) {
+          const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+          LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
+          if (c->n > 0) {
+            GramArgs a;
+            a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+            a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
+            a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
+            a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+            a.active = active;
+            const size_t smem = sizeof(double) * E;
+            auto fn = k_gram_v6<S>;
+            if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 1;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G6::NTHR, smem));
+            const int grid = std::max(1, std::min(std::min(occ, 4) * c->n_sms, cdiv(cdiv(c->n, 4), 64)));
+            fn<<<grid, G6::NTHR, smem, c->stream>>>(a);
+            CKL();
+          } else {
+            CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+          }
+          if (c->nranks > 1)
+            CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+          return LSBA_OK;
+        }
+      }
+      if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
         using G5 = G5Cfg<S>;
         const int NG5 = (J - 1 + G5::PB - 1) / G5::PB + 1;
-        if (!Vk && c->gram_impl == 0 && (NG5 + G5::NW - 1) / G5::NW + 1 <= G5::JMAX) {
+        if (!Vk && (c->gram_impl == 0 || c->gram_impl == 3) && (NG5 + G5::NW - 1) / G5::NW + 1 <= G5::JMAX) {
           const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
           LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
           if (c->n > 0) {
@@ -485,6 +518,15 @@ static lsba_status small_step(lsba_ctx c, int k, const CycleParams& prm) {
   LSBA_DISPATCH_S(c->b, small_step_t, c, k, prm);
 }
 
+template <int B>
+static lsba_status step_update_t(lsba_ctx c, int k) {
+  LaunchScope Ls(c, LSBA_K_STEP_UPDATE, 0.0, c->stream2);
+  const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
+  CK(launch_step_update<B>(c->st, c->d_G, k, rfac, c->stream2));
+  return LSBA_OK;
+}
+static lsba_status step_update(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, step_update_t, c, k); }
+
 static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
@@ -511,8 +553,14 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
            &c->d_ctl->active));                                                  // lines 3-4
   TRY(small_step(c, k, none));                                                   // line 5
+  // estimates / kappa_F / decision on stream 2, concurrent with the projection
+  CK(cudaEventRecord(c->ev_coef, c->stream));
+  CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
+  TRY(step_update(c, k));
+  CK(cudaEventRecord(c->ev_upd, c->stream2));
   TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
               nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
+  CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
   return LSBA_OK;
 }
 
@@ -822,13 +870,16 @@ static void release(lsba_ctx c) {
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_G, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
-                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros};
+                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_info) cudaFreeHost(c->h_info);
   if (c->h_scalar) cudaFreeHost(c->h_scalar);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->ev_coef) cudaEventDestroy(c->ev_coef);
+  if (c->ev_upd) cudaEventDestroy(c->ev_upd);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   for (int k = 0; k < LSBA_K_COUNT; ++k)
     for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1000,6 +1051,11 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.m = m_max;
   c->st.bmax = s;
   c->st.ctl = c->d_ctl;
+  TRY(dalloc(c, &c->st.rscr, 2 * (size_t)s * s));
+  TRY(dalloc(c, &c->st.iscr, 4));
+  CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_coef, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming));
   TRY(dalloc(c, &c->st.status, 1));
   TRY(dalloc(c, &c->st.flag_dev, 1));
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
@@ -1228,10 +1284,10 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
 
 extern "C" lsba_status lsba_set_kernel_variant(lsba_ctx c, int32_t variant) {
   if (!c) return LSBA_E_ARG;
-  if (variant < 0 || variant > 4) return fail(c, LSBA_E_ARG, "variant must be 0..4");
+  if (variant < 0 || variant > 5) return fail(c, LSBA_E_ARG, "variant must be 0..5");
   c->variant = variant == 1 ? 1 : 0;
   c->fuse_spmm = variant == 2 ? 1 : 0;
-  c->gram_impl = variant == 3 ? 2 : (variant == 4 ? 1 : 0);
+  c->gram_impl = variant == 3 ? 2 : (variant == 4 ? 1 : (variant == 5 ? 3 : 0));
   return LSBA_OK;
 }
 

@@ -36,6 +36,8 @@ struct SmallState2 {
   StepStatus* status;
   int* flag_dev;
   CycleCtl* ctl;
+  double* rscr;    // 2 b b: R and R^{-1} of the current step (coef -> update)
+  int* iscr;       // [0] flag, [1] forced
   int ldH, m, bmax;
 };
 
@@ -145,15 +147,23 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
   return sqrt(__shfl_sync(0xffffffffu, acc2, 0));
 }
 
-// ---------------------------------------------------------------------------- step kernel
-// blockDim = 32 * (B + 2).  dynamic smem: (k+1) B B doubles (copy of G).
+// ---------------------------------------------------------------------------- step kernels
+// Step k is split in two so that only what the projection needs sits on its critical path:
+//   k_step_coef   (stream A, between the Gram and the projection): H column -> Hbar,
+//                 S = sym(Omega - H^T H), Cholesky + NaN-flag, R^{-1}, coefficients
+//                 [-H R^{-1}; R^{-1}].  k == 0 is the IO of a new cycle (+ cycle-state init).
+//   k_step_update (stream B, concurrent with the projection): incremental QR of Hbar, BFOM /
+//                 BGMRES residual estimates, kappa_F, and the device-side decision.
+// The next step's kernels on stream A wait for the update (event), as they read the decision.
+
+// k_step_coef: blockDim 128; dyn smem (k+1) B B doubles.
 template <int B>
-__global__ void __launch_bounds__(32 * (B + 2))
-k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm, double rfac) {
-  extern __shared__ double Gs[];         // (k+1) B B copy of G, then (k-1) reflector sets
-  __shared__ double Ss[B * B], Rs[B * B], Ris[B * B], Ht[B * B], Gh[B * B];
+__global__ void __launch_bounds__(128)
+k_step_coef(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm, double rfac) {
+  extern __shared__ double Gs[];
+  __shared__ double Ss[B * B], Rs[B * B], Ris[B * B];
   __shared__ double red[32];
-  __shared__ int flag_s, sing_s;
+  __shared__ int flag_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int ldH = st.ldH, kb = k * B;
   CycleCtl* ctl = st.ctl;
@@ -161,23 +171,9 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     if (tid == 0) *st.flag_dev = 1;
     return;
   }
-  int force_flag = 0;
-  if (k > 0 && k == ctl->force_k && !ctl->forced_done) force_flag = 1;
+  const int force_flag = (k > 0 && k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
   for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
-  // stage the reflector sets 1..k-1 (set j: B vectors of 2B) for the QR window sweep
-  double* Vs = Gs + (kb + B) * B;
-  double* Ts = Vs + (size_t)(k > 1 ? k - 1 : 0) * B * 2 * B;
-  if (k > 1) {
-    for (int e = tid; e < (k - 1) * B * 2 * B; e += nt) {
-      const int jset = e / (B * 2 * B), rem = e % (B * 2 * B);
-      const int q = rem / (2 * B), r = rem % (2 * B);
-      Vs[e] = st.qr_v[(size_t)jset * st.bmax * 2 * st.bmax + (size_t)q * 2 * st.bmax + r];
-    }
-    for (int e = tid; e < (k - 1) * B; e += nt) Ts[e] = st.qr_tau[(size_t)(e / B) * st.bmax + e % B];
-  }
-  const int need_kappa = (k == 0) ? prm.need_kappa : ctl->need_kappa;
   __syncthreads();
-  // Hcol -> Hbar column block k-1; S = Omega - Hcol^T Hcol
   if (k > 0)
     for (int e = tid; e < kb * B; e += nt) {
       const int r = e / B, c = e % B;
@@ -198,12 +194,7 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     // symmetrise (R2) then right-looking Cholesky with NaN-flag; R^{-1}
     for (int e = lane; e < B * B; e += 32) {
       const int x = e % B, y = e / B;
-      if (x <= y) {
-        const double v = 0.5 * (Ss[x + y * B] + Ss[y + x * B]);
-        Rs[x + y * B] = v;  // work copy (upper part used)
-      } else {
-        Rs[x + y * B] = 0.0;
-      }
+      Rs[x + y * B] = (x <= y) ? 0.5 * (Ss[x + y * B] + Ss[y + x * B]) : 0.0;
     }
     __syncwarp();
     bool f = false;
@@ -227,8 +218,9 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     if (force_flag) f = true;
     if (lane == 0) {
       flag_s = f ? 1 : 0;
-      sing_s = 0;
       *st.flag_dev = flag_s;
+      st.iscr[0] = flag_s;
+      st.iscr[1] = force_flag;
       if (k == 0) {   // IO of a new cycle: reset the control block
         ctl->active = f ? 0 : 1;
         ctl->why = f ? 5 : 0;
@@ -245,11 +237,6 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
         ctl->need_kappa = prm.need_kappa;
         ctl->res_est = nan("");
         ctl->kappa = nan("");
-      } else if (f) {
-        ctl->active = 0;
-        ctl->why = 1;
-        ctl->k_flag = k;
-        if (force_flag) { ctl->forced_here = 1; ctl->forced_done = 1; }
       }
       st.status->k = k;
       st.status->flag = flag_s;
@@ -275,39 +262,6 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
 #pragma unroll
       for (int r = 0; r < B; ++r) Ris[r + c * B] = (r <= c) ? x[r] : 0.0;
     }
-  } else if (k > 0 && warp - 1 < B) {
-    // QR window for column c: apply reflector sets 1..k-1 (set j acts on block rows j-1, j)
-    const int c = warp - 1;
-    const int colg = (k - 1) * B + c;   // global column index in Hbar / Rfac
-    double w = (lane < 2 * B && lane < kb) ? Gs[lane * B + c] : 0.0;
-    for (int j = 1; j <= k - 1; ++j) {
-      const double* V = Vs + (size_t)(j - 1) * B * 2 * B;
-      const double* T = Ts + (size_t)(j - 1) * B;
-      double v[B], tau[B];
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        v[q] = (lane < 2 * B) ? V[q * 2 * B + lane] : 0.0;
-        tau[q] = T[q];
-      }
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        const double d = warp_sum(v[q] * w);
-        w -= tau[q] * d * v[q];
-      }
-      // rows (j-1)B.. of the window are final: R-factor entries
-      if (lane < B) st.Rfac[((j - 1) * B + lane) + (size_t)colg * ldH] = w;
-      // shift the window down by one block
-      const double up = __shfl_down_sync(0xffffffffu, w, B);
-      const int gr = (j + 1) * B + (lane - B);
-      w = (lane < B) ? up : ((lane < 2 * B && gr < kb) ? Gs[gr * B + c] : 0.0);
-    }
-    if (lane < B) {   // h~_k column c, and g^_k column c (g block k-1 before reflector k)
-      Ht[lane + c * B] = w;
-      st.htil[(size_t)(k - 1) * B * B + lane + c * B] = w;
-      const double gv = st.g[((k - 1) * B + lane) + (size_t)c * ldH];
-      Gh[lane + c * B] = gv;
-      st.ghat[(size_t)(k - 1) * B * B + lane + c * B] = gv;
-    }
   }
   __syncthreads();
   if (flag_s) {
@@ -329,6 +283,10 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
       t = Ris[(r - kb) + c * B];
     }
     st.coef[e] = t;
+  }
+  for (int e = tid; e < B * B; e += nt) {   // hand R and R^{-1} to the update kernel
+    st.rscr[e] = Rs[e];
+    st.rscr[B * B + e] = Ris[e];
   }
   if (k == 0) {
     // IO: beta = R; g = E_1 beta; R_1^{-1} = beta^{-1}; norms for kappa_F
@@ -352,6 +310,84 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
   for (int e = tid; e < B * B; e += nt) {
     const int x = e % B, y = e / B;
     st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
+  }
+}
+
+// k_step_update (k >= 1): blockDim 32 * (B + 2); dyn smem (k+1) B B + (k-1)(2 B B + B).
+template <int B>
+__global__ void __launch_bounds__(32 * (B + 2))
+k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) {
+  extern __shared__ double Gs[];         // (k+1) B B copy of G, then (k-1) reflector sets
+  __shared__ double Rs[B * B], Ris[B * B], Ht[B * B], Gh[B * B];
+  __shared__ double red[32];
+  __shared__ int flag_s, forced_s, sing_s;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int ldH = st.ldH, kb = k * B;
+  CycleCtl* ctl = st.ctl;
+  if (ctl->active == 0) return;          // speculative launch after the cycle ended
+  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
+  double* Vs = Gs + (kb + B) * B;
+  double* Ts = Vs + (size_t)(k > 1 ? k - 1 : 0) * B * 2 * B;
+  if (k > 1) {
+    for (int e = tid; e < (k - 1) * B * 2 * B; e += nt) {
+      const int jset = e / (B * 2 * B), rem = e % (B * 2 * B);
+      const int q = rem / (2 * B), r = rem % (2 * B);
+      Vs[e] = st.qr_v[(size_t)jset * st.bmax * 2 * st.bmax + (size_t)q * 2 * st.bmax + r];
+    }
+    for (int e = tid; e < (k - 1) * B; e += nt) Ts[e] = st.qr_tau[(size_t)(e / B) * st.bmax + e % B];
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    Rs[e] = st.rscr[e];
+    Ris[e] = st.rscr[B * B + e];
+  }
+  if (tid == 0) {
+    flag_s = st.iscr[0];
+    forced_s = st.iscr[1];
+    sing_s = 0;
+  }
+  const int need_kappa = ctl->need_kappa;
+  __syncthreads();
+  if (warp >= 1 && warp - 1 < B) {
+    // QR window for column c: apply reflector sets 1..k-1 (set j acts on block rows j-1, j)
+    const int c = warp - 1;
+    const int colg = (k - 1) * B + c;   // global column index in Hbar / Rfac
+    double w = (lane < 2 * B && lane < kb) ? Gs[lane * B + c] : 0.0;
+    for (int j = 1; j <= k - 1; ++j) {
+      const double* V = Vs + (size_t)(j - 1) * B * 2 * B;
+      const double* T = Ts + (size_t)(j - 1) * B;
+      double v[B], tau[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        v[q] = (lane < 2 * B) ? V[q * 2 * B + lane] : 0.0;
+        tau[q] = T[q];
+      }
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        const double d = warp_sum(v[q] * w);
+        w -= tau[q] * d * v[q];
+      }
+      if (lane < B) st.Rfac[((j - 1) * B + lane) + (size_t)colg * ldH] = w;
+      const double up = __shfl_down_sync(0xffffffffu, w, B);
+      const int gr = (j + 1) * B + (lane - B);
+      w = (lane < B) ? up : ((lane < 2 * B && gr < kb) ? Gs[gr * B + c] : 0.0);
+    }
+    if (lane < B) {   // h~_k column c, and g^_k column c (g block k-1 before reflector k)
+      Ht[lane + c * B] = w;
+      st.htil[(size_t)(k - 1) * B * B + lane + c * B] = w;
+      const double gv = st.g[((k - 1) * B + lane) + (size_t)c * ldH];
+      Gh[lane + c * B] = gv;
+      st.ghat[(size_t)(k - 1) * B * B + lane + c * B] = gv;
+    }
+  }
+  __syncthreads();
+  if (flag_s) {
+    if (tid == 0) {
+      ctl->active = 0;
+      ctl->why = 1;
+      ctl->k_flag = k;
+      if (forced_s) { ctl->forced_here = 1; ctl->forced_done = 1; }
+    }
+    return;
   }
   if (warp == 0) {
     // FOM estimate: cos_F = h~^{-1} g^ ; ||H_{k+1,k} cos_F C_acc||_F
@@ -474,7 +510,6 @@ k_step_small(SmallState2 st, const double* __restrict__ G, int k, CycleParams pr
     st.status->kappa_F = kap;
     // ---- device-side decision (readings R5, R8, R9, R22)
     if (sing_s) {                       // FOM projected matrix singular: treated as a NaN-flag
-      *st.flag_dev = 1;
       ctl->active = 0;
       ctl->why = 1;
       ctl->k_flag = k;

@@ -12,14 +12,28 @@ template <>
 cudaError_t launch_step_small<LSBA_B>(const SmallState2& st, const double* G, int k,
                                       const CycleParams& prm, double rfac, cudaStream_t stream) {
   constexpr int B = LSBA_B;
-  const size_t km1 = k > 1 ? (size_t)(k - 1) : 0;
-  const size_t smem = sizeof(double) * ((size_t)(k + 1) * B * B + km1 * B * 2 * B + km1 * B);
-  auto fn = k_step_small<B>;
+  const size_t smem = sizeof(double) * (size_t)(k + 1) * B * B;
+  auto fn = k_step_coef<B>;
   if (smem > 32 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  fn<<<1, 32 * (B + 2), smem, stream>>>(st, G, k, prm, rfac);
+  fn<<<1, 128, smem, stream>>>(st, G, k, prm, rfac);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_step_update<LSBA_B>(const SmallState2& st, const double* G, int k, double rfac,
+                                       cudaStream_t stream) {
+  constexpr int B = LSBA_B;
+  const size_t km1 = k > 1 ? (size_t)(k - 1) : 0;
+  const size_t smem = sizeof(double) * ((size_t)(k + 1) * B * B + km1 * B * 2 * B + km1 * B);
+  auto fn = k_step_update<B>;
+  if (smem > 32 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<1, 32 * (B + 2), smem, stream>>>(st, G, k, rfac);
   return cudaGetLastError();
 }
 

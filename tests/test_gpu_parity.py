@@ -348,12 +348,12 @@ def test_s1_and_s16_small_n(L):
 
 
 def test_dfma_variant_matches(L):
-    """Every kernel family (0: DMMA v5, 1: plain DFMA, 2: DMMA with fused SpMM, 3: DMMA with
-    8-byte fragments, 4: TMA-staged DMMA) matches the oracle."""
+    """Every kernel family (0: DMMA v6, 1: plain DFMA, 2: DMMA with fused SpMM, 3: DMMA with
+    8-byte fragments, 4: TMA-staged DMMA, 5: DMMA v5) matches the oracle."""
     from oracle import lsba_oracle as O
     A, B, _ = get_problem("random_16K")
     arn = oracle_steps(A, B, "cl", 5)
-    for variant in (0, 1, 2, 3, 4):
+    for variant in (0, 1, 2, 3, 4, 5):
         H, beta, Vs, _ = gpu_steps(L, A, B, "cl", 5, variant=variant)
         for j, (v, vo) in enumerate(zip(Vs, arn.V)):
             assert np.linalg.norm(v - vo) <= 1e-10 * np.linalg.norm(vo), (variant, j)
