@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU-box helper: parity tests + benches for the given configs (default 2 3 5); summaries on stdout.
-cd "$(dirname "$0")"
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"
 grep -E "passed|failed|FAILED" gpurun_out/pytest_gpu.log | head -30; grep -E "^E " gpurun_out/pytest_gpu.log | head -12
