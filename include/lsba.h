@@ -170,10 +170,11 @@ lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t 
 /* Fault injection: make the Cholesky of step k_flag report a NaN-flag once (0 = off). */
 lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
 /* Kernel implementation choice (classical inner product): 0 = auto (standalone SpMM +
- * barrier-free streaming tensor-core Gram v6 + tensor-core projection), 1 = plain DFMA
- * kernels, 2 = SpMM fused into the tensor-core Gram pass (gather warps), 3 = tensor-core Gram
- * with 8-byte fragment loads, 4 = TMA-staged tensor-core Gram, 5 = shared-memory-tiled
- * tensor-core Gram v5.  For parity tests and measurements of every path. */
+ * latency-tuned streaming tensor-core Gram v7 + projection: DMMA for s in {8,16}, DFMA
+ * otherwise), 1 = plain DFMA kernels, 2 = SpMM fused into the tensor-core Gram pass (gather
+ * warps), 3 = tensor-core Gram with 8-byte fragment loads, 4 = TMA-staged tensor-core Gram,
+ * 5 = shared-memory-tiled tensor-core Gram v5, 6 = barrier-free tensor-core Gram v6.
+ * For parity tests and measurements of every path. */
 lsba_status lsba_set_kernel_variant(lsba_ctx ctx, int32_t variant);
 
 /* Per-kernel timing with CUDA events on the context stream.  Kernel ids: */

@@ -1,0 +1,245 @@
+// gram7.cuh — the single-sync Gram pass G = <[X_0 .. X_{J-1}], Y> (Alg 3 line 4,
+// PAPER.md:268-269) as a latency-tuned streaming kernel on the FP64 tensor cores.
+//
+// Design rules measured on B200 (tools/microbench.cu, profiles/r01_microbench.md):
+//   * DMMA m8n8k4.f64 and DFMA both run at 64 MAC/clk/SM (37 TF/s): DMMA is used for its
+//     register efficiency (an 8x8 fp64 accumulator is 2 doubles per lane), not for flops;
+//   * a read stream reaches 7.3 TB/s only with >= 64 KB in flight per SM spread over
+//     >= 16 warps; 8 warps per SM cap it near 3.9 TB/s whatever the unroll.
+// So: no shared-memory tiles and no barriers in the main loop; each warp keeps U 4-row steps
+// of loads in flight (issued together, then consumed), register budget sized for MINB CTAs of
+// 256 threads per SM; the CTA partial is reduced through shared memory in one ordered pass
+// and the cross-CTA reduction is the deterministic two-level tree of k_gram_v6.
+//
+// Fragment mapping (as v5/v6): lane (r4 = lane & 3, c8 = lane >> 2) loads a 16-byte column
+// pair (2cp, 2cp+1) of row r4 of a block and feeds two DMMAs (M tile "even" columns, M tile
+// "odd" columns); a group packs PB = 16/S blocks (S <= 8) into the 8 M rows; W (B operand) is
+// W[r4][c8 (+8 tn)].  Inputs are basis slots (rows padded to kRowPad with zero rows).
+#pragma once
+#include <algorithm>
+
+#include "dmma.cuh"
+
+namespace lsba {
+
+constexpr int kMaxGramPasses = 64;  // ticket sets allocated per context (one per pass)
+
+template <int S, int GMAX_, int U_, int MINB_>
+struct G7Cfg {
+  static constexpr int PB = S >= 16 ? 1 : 16 / S;
+  static constexpr int NT = S >= 8 ? S / 8 : 1;
+  static constexpr int GMAX = GMAX_;
+  static constexpr int U = U_;
+  static constexpr int MINB = MINB_;
+  static constexpr int NW = 8;
+  static constexpr int NTHR = 256;
+};
+
+// Block groups of a J-block Gram: the J blocks (the last one is Y itself when y_alias) are
+// packed PB per group in order; a launch covers the groups in `passes` contiguous ranges of
+// at most 8 GMAX groups (blockIdx.x = pass + passes * row_chunk, so a chunk's passes run side
+// by side and share the W rows through L2).
+template <int S>
+__host__ __device__ inline int g7_groups(int J) {
+  constexpr int PB = S >= 16 ? 1 : 16 / S;
+  return (J + PB - 1) / PB;
+}
+__host__ __device__ inline int g7_passes(int NG, int GMAX) { return (NG + 8 * GMAX - 1) / (8 * GMAX); }
+__host__ __device__ inline int g7_qw(int ngp, int GMAX) {
+  int QW = 1;
+  while (QW < 8 && (ngp + QW - 1) / QW > GMAX) QW *= 2;
+  return QW;
+}
+
+template <int S, int GMAX, int U, int MINB, bool PIPE = false>
+__global__ void __launch_bounds__(256, MINB)
+k_gram_v7(GramArgs g) {
+  using C = G7Cfg<S, GMAX, U, MINB>;
+  static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v7 Gram: s in {2,4,8,16}");
+  if (g.active && *g.active == 0) return;
+  extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int J = g.J, E = J * S * S;
+  const int NG = g7_groups<S>(J);
+  const int passes = g7_passes(NG, C::GMAX);
+  const int pass = blockIdx.x % passes, chunk = blockIdx.x / passes, nchunks = gridDim.x / passes;
+  const int gp0 = (NG * pass) / passes, gp1 = (NG * (pass + 1)) / passes;
+  const int QW = g7_qw(gp1 - gp0, C::GMAX);
+  const int RW = C::NW / QW;
+  const int rs = warp % RW, qs = warp / RW;
+  const int gA = gp0 + ((gp1 - gp0) * qs) / QW, gB = gp0 + ((gp1 - gp0) * (qs + 1)) / QW;
+  const int ng = gB - gA;
+  const int jlo = gp0 * C::PB, jhi = min(J, gp1 * C::PB);   // blocks (entries) of this pass
+  const int e0 = jlo * S * S, EP = (jhi - jlo) * S * S;
+  const int r4 = lane & 3, c8 = lane >> 2;
+  constexpr int LPB = S >= 16 ? 8 : S / 2;
+  const int jj = c8 / LPB, cp = c8 % LPB;
+
+  const double* src[C::GMAX];
+#pragma unroll
+  for (int gi = 0; gi < C::GMAX; ++gi) {
+    const int j = (gA + gi) * C::PB + (S >= 16 ? 0 : jj);
+    src[gi] = (gi < ng && j < J) ? g.X + (size_t)j * g.xstride + r4 * S + 2 * cp : nullptr;
+  }
+  const double* wsrc = g.Y + r4 * S + c8;
+  double acc[C::GMAX][2][C::NT][2];
+#pragma unroll
+  for (int a = 0; a < C::GMAX; ++a)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn) acc[a][e][tn][0] = acc[a][e][tn][1] = 0.0;
+
+  const long NS = ((long)g.n + 3) / 4;                 // 4-row steps (rows padded)
+  const long s0 = NS * chunk / nchunks, s1 = NS * (chunk + 1) / nchunks;
+  long st = s0 + rs;
+  // U 4-row steps per batch: load the batch's fragments, then run its DMMAs.  PIPE: two
+  // batches in registers, the next batch's loads are issued before the current batch's DMMAs.
+  auto load_batch = [&](double2 (&av)[C::U][C::GMAX], double (&bw)[C::U][C::NT], long sb) {
+#pragma unroll
+    for (int u = 0; u < C::U; ++u) {
+      const size_t off = (size_t)(sb + (long)u * RW) * 4 * S;
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn)
+        bw[u][tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+#pragma unroll
+      for (int gi = 0; gi < C::GMAX; ++gi)
+        av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+    }
+  };
+  auto mma_batch = [&](const double2 (&av)[C::U][C::GMAX], const double (&bw)[C::U][C::NT]) {
+#pragma unroll
+    for (int u = 0; u < C::U; ++u)
+#pragma unroll
+      for (int gi = 0; gi < C::GMAX; ++gi) {
+        if (gi >= ng) continue;
+#pragma unroll
+        for (int tn = 0; tn < C::NT; ++tn) {
+          dmma(acc[gi][0][tn][0], acc[gi][0][tn][1], av[u][gi].x, bw[u][tn]);
+          dmma(acc[gi][1][tn][0], acc[gi][1][tn][1], av[u][gi].y, bw[u][tn]);
+        }
+      }
+  };
+  const long BS = (long)C::U * RW;                     // steps per batch (this warp's stride)
+  if constexpr (PIPE) {
+    double2 av0[C::U][C::GMAX], av1[C::U][C::GMAX];
+    double bw0[C::U][C::NT], bw1[C::U][C::NT];
+    if (st + (C::U - 1) * RW < s1) load_batch(av0, bw0, st);
+    while (st + (C::U - 1) * RW < s1) {
+      const bool has1 = st + BS + (C::U - 1) * RW < s1;
+      if (has1) load_batch(av1, bw1, st + BS);
+      mma_batch(av0, bw0);
+      st += BS;
+      if (!has1) break;
+      const bool has0 = st + BS + (C::U - 1) * RW < s1;
+      if (has0) load_batch(av0, bw0, st + BS);
+      mma_batch(av1, bw1);
+      st += BS;
+      if (!has0) break;
+    }
+  } else {
+    for (; st + (long)(C::U - 1) * RW < s1; st += BS) {
+      double2 av[C::U][C::GMAX];
+      double bw[C::U][C::NT];
+      load_batch(av, bw, st);
+      mma_batch(av, bw);
+    }
+  }
+  for (; st < s1; st += RW) {                          // remainder steps, one at a time
+    const size_t off = (size_t)st * 4 * S;
+    double bw[C::NT];
+#pragma unroll
+    for (int tn = 0; tn < C::NT; ++tn) bw[tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+#pragma unroll
+    for (int gi = 0; gi < C::GMAX; ++gi) {
+      if (gi >= ng) continue;
+      const double2 av = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn) {
+        dmma(acc[gi][0][tn][0], acc[gi][0][tn][1], av.x, bw[tn]);
+        dmma(acc[gi][1][tn][0], acc[gi][1][tn][1], av.y, bw[tn]);
+      }
+    }
+  }
+  // CTA partial: each row slice writes its own slot (group sets are disjoint and cover the
+  // pass), then one ordered sum over the RW slots (deterministic)
+  for (int e = tid; e < RW * EP; e += C::NTHR) sm7[e] = 0.0;
+  __syncthreads();
+  double* mine = sm7 + (size_t)rs * EP - e0;
+#pragma unroll
+  for (int gi = 0; gi < C::GMAX; ++gi) {
+    if (gi >= ng) continue;
+    const int j = (gA + gi) * C::PB + (S >= 16 ? 0 : jj);
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int a = 2 * cp + e;
+          const int bcol = tn * 8 + 2 * r4 + i;
+          if (bcol < S && j < J) mine[(j * S + a) * S + bcol] = acc[gi][e][tn][i];
+        }
+  }
+  __syncthreads();
+  const int ngroups = (nchunks + kGramGroup - 1) / kGramGroup;
+  const int grpi = chunk / kGramGroup;
+  const int gsize = min(kGramGroup, nchunks - grpi * kGramGroup);
+  unsigned* tk = g.tickets + (size_t)pass * (ngroups + 1);
+  for (int e = tid; e < EP; e += C::NTHR) {
+    double t = sm7[e];
+    for (int r = 1; r < RW; ++r) t += sm7[(size_t)r * EP + e];
+    g.part[(size_t)chunk * E + e0 + e] = t;
+  }
+  // ---- deterministic two-level reduction across the row chunks of this pass
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned ticket7;
+  if (tid == 0) ticket7 = atomicAdd(&tk[grpi], 1u);
+  __syncthreads();
+  if (ticket7 != (unsigned)(gsize - 1)) return;
+  __threadfence();
+  for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
+    double s2 = 0.0;
+    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * E + e);
+    g.gpart[(size_t)grpi * E + e] = s2;
+  }
+  if (tid == 0) tk[grpi] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket7 = atomicAdd(&tk[ngroups], 1u);
+  __syncthreads();
+  if (ticket7 != (unsigned)(ngroups - 1)) return;
+  __threadfence();
+  for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
+    double s2 = 0.0;
+    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * E + e);
+    g.G[e] = s2;
+  }
+  if (tid == 0) tk[ngroups] = 0u;
+}
+
+// launch geometry of k_gram_v7: grid (a multiple of the pass count) and dynamic smem bytes
+template <int S, int GMAX>
+struct G7Launch {
+  int passes, grid;
+  size_t smem;
+  G7Launch(int n, int J, int ctas_per_sm, int sms) {
+    const int NG = g7_groups<S>(J);
+    passes = g7_passes(NG, GMAX);
+    int maxEP = 0, maxRW = 1;
+    for (int p = 0; p < passes; ++p) {
+      const int gp0 = NG * p / passes, gp1 = NG * (p + 1) / passes;
+      const int ep = (std::min(J, gp1 * (S >= 16 ? 1 : 16 / S)) - gp0 * (S >= 16 ? 1 : 16 / S)) * S * S;
+      maxEP = std::max(maxEP, ep);
+      maxRW = std::max(maxRW, 8 / g7_qw(gp1 - gp0, GMAX));
+    }
+    smem = sizeof(double) * (size_t)maxRW * maxEP;
+    const long steps = ((long)n + 3) / 4;
+    int chunks = std::max(1, ctas_per_sm * sms / passes);
+    chunks = (int)std::max(1L, std::min<long>(chunks, (steps + 63) / 64));
+    grid = chunks * passes;
+  }
+};
+
+}  // namespace lsba

@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "small.cuh"  // SmallState2 / StepStatus layouts (kernels are in small_inst.cu)
 #include "dmma.cuh"
+#include "gram7.cuh"
 #include "launch_small.h"
 
 using namespace lsba;
@@ -292,10 +293,44 @@ static bool dmma_gram_ok(lsba_ctx c, int J, int ip, const double* X, const doubl
   if constexpr (!(S == 1 || S == 2 || S == 4 || S == 8 || S == 16)) {
     return false;
   } else {
+    if constexpr (S != 1) {
+      if (c->gram_impl == 0 && !c->fuse_spmm) return c->d_tickets != nullptr;   // v7: any J
+    }
     using Cg = GramCfg<S>;
     const int NG = (J + Cg::JP - 1) / Cg::JP;
     return (NG + 1 + Cg::NWG - 1) / Cg::NWG + 1 <= Cg::JMAX && c->d_tickets != nullptr &&
            (size_t)c->gram_grid * J * S * S <= c->part_cap;
+  }
+}
+
+// ---------------------------------------------------------------- a2: v7 streaming Gram
+// Tuned (GMAX groups per warp, U steps per batch, MINB CTAs per SM) per s and J from the
+// standalone sweep in tools/gram_bench.cu (profiles/r01_gram_sweep.md).
+template <int S, int GMAX, int U, int MINB>
+static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a) {
+  auto fn = k_gram_v7<S, GMAX, U, MINB>;
+  G7Launch<S, GMAX> geo(c->n, a.J, MINB, c->n_sms);
+  if ((size_t)geo.grid * a.J * S * S > c->part_cap || geo.passes > kMaxGramPasses)
+    return fail(c, LSBA_E_STATE, "v7 Gram workspace too small (J=%d)", a.J);
+  if (geo.smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
+  fn<<<geo.grid, 256, geo.smem, c->stream>>>(a);
+  CKL();
+  return LSBA_OK;
+}
+
+template <int S>
+static lsba_status gram_v7(lsba_ctx c, const GramArgs& a) {
+  if constexpr (S == 2 || S == 4) {
+    if (a.J <= 6) return gram_v7_launch<S, 1, 16, 3>(c, a);
+    return gram_v7_launch<S, 3, 4, 3>(c, a);
+  } else if constexpr (S == 8) {
+    if (a.J <= 4) return gram_v7_launch<S, 1, 16, 3>(c, a);
+    return gram_v7_launch<S, 3, 4, 3>(c, a);
+  } else if constexpr (S == 16) {
+    if (a.J <= 4 || a.J > 16) return gram_v7_launch<S, 2, 8, 3>(c, a);
+    return gram_v7_launch<S, 3, 4, 3>(c, a);
+  } else {
+    return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
   }
 }
 
@@ -317,7 +352,27 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
         using G6 = G6Cfg<S>;
         const int NG6 = (J - 1 + G6::PB - 1) / G6::PB + 1;
-        if (!Vk && c->gram_impl == 0 && (NG6 + G6::NW - 1) / G6::NW <= G6::GMAX) {
+        if (!Vk && c->gram_impl == 0) {
+          const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+          LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
+          if (c->n > 0) {
+            GramArgs a;
+            a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+            a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride;
+            // v7 takes the blocks uniformly: J blocks X_0..X_{J-1} (the last is Y itself when
+            // y_is_block) and Y as the B operand
+            a.J = J; a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
+            a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+            a.active = active;
+            TRY(gram_v7<S>(c, a));
+          } else {
+            CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+          }
+          if (c->nranks > 1)
+            CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+          return LSBA_OK;
+        }
+        if (!Vk && c->gram_impl == 6 && (NG6 + G6::NW - 1) / G6::NW <= G6::GMAX) {
           const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
           LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
           if (c->n > 0) {
@@ -463,7 +518,9 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
   const double bytes = 8.0 * c->n * S * (Jmax + (J0 > 0) + (J1 > 0) + (base0 ? 1 : 0));
   LaunchScope Ls(c, kid, bytes);
   if (c->n == 0) return LSBA_OK;
-  if constexpr (S == 4 || S == 8 || S == 16) {
+  // s = 4: the DFMA kernel streams faster than the DMMA one (5.8 vs 5.0 TB/s on config 2,
+  // profiles/r01_variants.md); s = 8, 16: DMMA (6.65 TB/s on configs 3 and 5)
+  if constexpr (S == 8 || S == 16) {
     if (!gl && c->variant == 0) {
       auto fn = k_project_dmma<S>;
       if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1015,8 +1072,8 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   {
     const int ngroups = (c->gram_grid + kGramGroup - 1) / kGramGroup;
     TRY(dalloc(c, &c->d_gpart, (size_t)ngroups * Emax));
-    TRY(dalloc(c, &c->d_tickets, (size_t)ngroups + 1));
-    CK(cudaMemset(c->d_tickets, 0, sizeof(unsigned) * (ngroups + 1)));
+    TRY(dalloc(c, &c->d_tickets, (size_t)kMaxGramPasses * (ngroups + 1)));
+    CK(cudaMemset(c->d_tickets, 0, sizeof(unsigned) * kMaxGramPasses * (ngroups + 1)));
   }
   TRY(dalloc(c, &c->d_ctl, 1));
   CK(cudaMemset(c->d_ctl, 0, sizeof(CycleCtl)));
@@ -1284,10 +1341,10 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
 
 extern "C" lsba_status lsba_set_kernel_variant(lsba_ctx c, int32_t variant) {
   if (!c) return LSBA_E_ARG;
-  if (variant < 0 || variant > 5) return fail(c, LSBA_E_ARG, "variant must be 0..5");
+  if (variant < 0 || variant > 6) return fail(c, LSBA_E_ARG, "variant must be 0..6");
   c->variant = variant == 1 ? 1 : 0;
   c->fuse_spmm = variant == 2 ? 1 : 0;
-  c->gram_impl = variant == 3 ? 2 : (variant == 4 ? 1 : (variant == 5 ? 3 : 0));
+  c->gram_impl = variant == 3 ? 2 : (variant == 4 ? 1 : (variant == 5 ? 3 : (variant == 6 ? 6 : 0)));
   return LSBA_OK;
 }
 
