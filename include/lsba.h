@@ -189,6 +189,11 @@ lsba_status lsba_profile_enable(lsba_ctx ctx, int32_t enable);
  * over the recorded launches.  Synchronises the stream. */
 lsba_status lsba_profile_read(lsba_ctx ctx, int32_t kid, int64_t* launches, double* ms,
                               double* bytes);
+/* The recorded launches in issue order (both streams): kernel id and start / end times in ms
+ * relative to the first recorded launch's start event.  Writes min(count, cap) entries;
+ * *count receives the number recorded.  Synchronises the context's streams. */
+lsba_status lsba_profile_timeline(lsba_ctx ctx, int32_t* kids, double* t_start_ms, double* t_end_ms,
+                                  int64_t cap, int64_t* count);
 /* Total kernel launches of this context since creation. */
 lsba_status lsba_launch_count(lsba_ctx ctx, int64_t* launches);
 /* Device workspace bytes held by the context. */

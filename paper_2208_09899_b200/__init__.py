@@ -38,6 +38,7 @@ from ._lib import (  # noqa: F401
     lsba_set_kernel_variant,
     lsba_profile_enable,
     lsba_profile_read,
+    lsba_profile_timeline,
     lsba_launch_count,
     lsba_workspace_bytes,
     lsba_ghost_plan,

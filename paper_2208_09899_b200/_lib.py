@@ -66,6 +66,7 @@ _sigs = {
     "lsba_set_kernel_variant": [_vp, _i32],
     "lsba_profile_enable": [_vp, _i32],
     "lsba_profile_read": [_vp, _i32, C.POINTER(_i64), C.POINTER(_d), C.POINTER(_d)],
+    "lsba_profile_timeline": [_vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
     "lsba_launch_count": [_vp, C.POINTER(_i64)],
     "lsba_workspace_bytes": [_vp, C.POINTER(_i64)],
     "lsba_ghost_plan": [_i64, _i64, _vp, _i64, _vp, _i32, _vp, _vp, C.POINTER(_i64), _vp],
@@ -236,6 +237,18 @@ def lsba_profile_read(ctx, kid):
     kid = KERNEL_IDS[kid] if isinstance(kid, str) else kid
     _check(lib.lsba_profile_read(ctx, int(kid), C.byref(n), C.byref(ms), C.byref(by)), ctx)
     return n.value, ms.value, by.value
+
+
+def lsba_profile_timeline(ctx):
+    """[(kernel name, start ms, end ms)] of the recorded launches in issue order."""
+    n = C.c_int64()
+    _check(lib.lsba_profile_timeline(ctx, None, None, None, 0, C.byref(n)), ctx)
+    kids = np.zeros(max(n.value, 1), dtype=np.int32)
+    t0 = np.zeros(max(n.value, 1))
+    t1 = np.zeros(max(n.value, 1))
+    _check(lib.lsba_profile_timeline(ctx, _hptr(kids), _hptr(t0), _hptr(t1), n.value, C.byref(n)), ctx)
+    names = {v: k for k, v in KERNEL_IDS.items()}
+    return [(names.get(int(k), str(k)), float(a), float(b)) for k, a, b in zip(kids[:n.value], t0, t1)]
 
 
 def lsba_launch_count(ctx):

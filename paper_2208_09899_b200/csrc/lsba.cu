@@ -38,6 +38,7 @@ struct Prof {
   size_t used[LSBA_K_COUNT] = {};
   double bytes[LSBA_K_COUNT] = {};
   int64_t launches[LSBA_K_COUNT] = {};
+  std::vector<std::pair<int, size_t>> order;   // launch order: (kernel id, index into ev[kid])
 };
 
 constexpr int kGramCtas = 4 * 148 * 2;  // target CTAs of the partial-Gram grid
@@ -71,7 +72,10 @@ struct lsba_ctx_ {
   // Gram
   double* d_part = nullptr;
   size_t part_cap = 0;
-  double* d_G = nullptr;
+  double* d_G = nullptr;          // current Gram result (one of the two halves of d_Gbase)
+  double* d_Gbase = nullptr;      // 2 x (m_max+1) s^2: step k uses half k & 1, so the Gram of
+                                  // step k+1 never overwrites what the update of step k reads
+  size_t g_half = 0;
   double* d_gpart = nullptr;     // DMMA Gram: first-level group partials
   unsigned* d_tickets = nullptr;  // DMMA Gram: CTA arrival counters (self-resetting)
   int gram_grid = 0;              // DMMA Gram: persistent grid size
@@ -173,6 +177,7 @@ struct LaunchScope {
       cudaEventCreate(&e.b);
       p.ev[kid].push_back(e);
     }
+    p.order.emplace_back(kid, p.used[kid]);
     ev = &p.ev[kid][p.used[kid]++];
     cudaEventRecord(ev->a, strm);
   }
@@ -607,8 +612,13 @@ static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
 // control says the cycle has ended (speculative enqueue of a whole cycle).
 static lsba_status pip_step_async(lsba_ctx c, int k) {
   const CycleParams none{};   // (k > 0 launches read their parameters from the device control)
+  // Lines 3-4 of step k run while the update kernel of step k-1 (stream 2) is still taking
+  // the continue/restart decision: they only write slot k and G, which are scratch if the
+  // cycle ended at step k-1.  The coefficient kernel reads the decision, so it waits.
+  c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
   TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
            &c->d_ctl->active));                                                  // lines 3-4
+  if (k > 1) CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
   TRY(small_step(c, k, none));                                                   // line 5
   // estimates / kappa_F / decision on stream 2, concurrent with the projection
   CK(cudaEventRecord(c->ev_coef, c->stream));
@@ -617,6 +627,11 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   CK(cudaEventRecord(c->ev_upd, c->stream2));
   TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
               nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
+  return LSBA_OK;
+}
+
+// join stream 2 (the last step's update) into the main stream
+static lsba_status join_update(lsba_ctx c) {
   CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
   return LSBA_OK;
 }
@@ -739,6 +754,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     prm.need_kappa = std::isfinite(tau) ? 1 : 0;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
     for (int k = 1; k <= m_cur; ++k) TRY(pip_step_async(c, k));
+    TRY(join_update(c));
     TRY(read_status(c, nullptr, &cc));
     if (cc.why == 5) { info->outcome = LSBA_DEAD; break; }   // IO flagged (R4)
     int k_used = cc.k_used;
@@ -925,7 +941,7 @@ static void release(lsba_ctx c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
-                  c->d_part, c->d_G, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
+                  c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr};
   for (void* p : ptrs)
@@ -1078,7 +1094,9 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   TRY(dalloc(c, &c->d_ctl, 1));
   CK(cudaMemset(c->d_ctl, 0, sizeof(CycleCtl)));
   CK(cudaMallocHost((void**)&c->h_ctl, sizeof(CycleCtl)));
-  TRY(dalloc(c, &c->d_G, (size_t)(m_max + 1) * s * s));
+  c->g_half = (size_t)(m_max + 1) * s * s;
+  TRY(dalloc(c, &c->d_Gbase, 2 * c->g_half));
+  c->d_G = c->d_Gbase;
   c->sq_cap = std::max(1, cdiv((long)n_local * 16, kThreads));
   TRY(dalloc(c, &c->d_sq, c->sq_cap));
   TRY(dalloc(c, &c->d_scalar, 4));
@@ -1110,7 +1128,11 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.ctl = c->d_ctl;
   TRY(dalloc(c, &c->st.rscr, 2 * (size_t)s * s));
   TRY(dalloc(c, &c->st.iscr, 4));
-  CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+  {  // the update kernel's single CTA should get an SM as soon as one frees up
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, hi));
+  }
   CK(cudaEventCreateWithFlags(&c->ev_coef, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming));
   TRY(dalloc(c, &c->st.status, 1));
@@ -1199,6 +1221,7 @@ extern "C" lsba_status lsba_block_arnoldi_step(lsba_ctx c, lsba_step_info* info)
   CK(cudaSetDevice(c->device));
   const int k = c->k + 1;
   TRY(pip_step_async(c, k));
+  TRY(join_update(c));
   StepStatus stt;
   CycleCtl cc;
   TRY(read_status(c, &stt, &cc));
@@ -1357,7 +1380,30 @@ extern "C" lsba_status lsba_profile_enable(lsba_ctx c, int32_t enable) {
     c->prof.bytes[k] = 0.0;
     c->prof.launches[k] = 0;
   }
+  c->prof.order.clear();
   c->prof.on = enable != 0;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_profile_timeline(lsba_ctx c, int32_t* kids, double* t_start_ms, double* t_end_ms,
+                                             int64_t cap, int64_t* count) {
+  if (!c || !count) return LSBA_E_ARG;
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->stream2));
+  const auto& ord = c->prof.order;
+  *count = (int64_t)ord.size();
+  if (ord.empty()) return LSBA_OK;
+  const cudaEvent_t origin = c->prof.ev[ord[0].first][ord[0].second].a;
+  for (size_t i = 0; i < ord.size() && (int64_t)i < cap; ++i) {
+    const EvPair& e = c->prof.ev[ord[i].first][ord[i].second];
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, origin, e.a));
+    CK(cudaEventElapsedTime(&b, origin, e.b));
+    if (kids) kids[i] = ord[i].first;
+    if (t_start_ms) t_start_ms[i] = a;
+    if (t_end_ms) t_end_ms[i] = b;
+  }
   return LSBA_OK;
 }
 
