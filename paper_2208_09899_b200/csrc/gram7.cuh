@@ -19,10 +19,21 @@
 #include <algorithm>
 
 #include "dmma.cuh"
+#include "small.cuh"
 
 namespace lsba {
 
 constexpr int kMaxGramPasses = 64;  // ticket sets allocated per context (one per pass)
+
+// Fused small step: on a single rank the Gram's last-finishing CTA goes straight on with
+// Alg 3 line 5 (S = Omega - H^T H, Cholesky + NaN-flag, R^-1, projection coefficients;
+// step_coef_body of small.cuh) instead of a separate 1-CTA launch.
+struct GramFuse {
+  SmallState2 st;
+  CycleParams prm;
+  int k;    // step index (0 = IO)
+  int on;   // 0: plain Gram
+};
 
 template <int S, int GMAX_, int U_, int MINB_>
 struct G7Cfg {
@@ -53,10 +64,13 @@ __host__ __device__ inline int g7_qw(int ngp, int GMAX) {
 
 template <int S, int GMAX, int U, int MINB, bool PIPE = false>
 __global__ void __launch_bounds__(256, MINB)
-k_gram_v7(GramArgs g) {
+k_gram_v7(GramArgs g, GramFuse f) {
   using C = G7Cfg<S, GMAX, U, MINB>;
   static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v7 Gram: s in {2,4,8,16}");
-  if (g.active && *g.active == 0) return;
+  if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
+    if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
+    return;
+  }
   extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int J = g.J, E = J * S * S;
@@ -217,6 +231,17 @@ k_gram_v7(GramArgs g) {
     g.G[e] = s2;
   }
   if (tid == 0) tk[ngroups] = 0u;
+  if (!f.on) return;
+  // ---- fused small step, run by the CTA that completes the last pass
+  __threadfence();
+  __syncthreads();
+  unsigned* tpass = g.tickets + (size_t)kMaxGramPasses * (ngroups + 1);
+  if (tid == 0) ticket7 = atomicAdd(tpass, 1u);
+  __syncthreads();
+  if (ticket7 != (unsigned)(passes - 1)) return;
+  __threadfence();
+  if (tid == 0) *tpass = 0u;
+  step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
 }
 
 // launch geometry of k_gram_v7: grid (a multiple of the pass count) and dynamic smem bytes
@@ -224,7 +249,7 @@ template <int S, int GMAX>
 struct G7Launch {
   int passes, grid;
   size_t smem;
-  G7Launch(int n, int J, int ctas_per_sm, int sms) {
+  G7Launch(int n, int J, int ctas_per_sm, int sms, bool fuse = false) {
     const int NG = g7_groups<S>(J);
     passes = g7_passes(NG, GMAX);
     int maxEP = 0, maxRW = 1;
@@ -235,6 +260,7 @@ struct G7Launch {
       maxRW = std::max(maxRW, 8 / g7_qw(gp1 - gp0, GMAX));
     }
     smem = sizeof(double) * (size_t)maxRW * maxEP;
+    if (fuse) smem = std::max(smem, sizeof(double) * (size_t)J * S * S);   // step_coef_body's Gs
     const long steps = ((long)n + 3) / 4;
     int chunks = std::max(1, ctas_per_sm * sms / passes);
     chunks = (int)std::max(1L, std::min<long>(chunks, (steps + 63) / 64));

@@ -108,6 +108,7 @@ struct lsba_ctx_ {
   bool forced_done = false;
   int variant = 0;
   int fuse_spmm = 0;   // 1: SpMM fused into the tensor-core Gram pass (gather warps)
+  bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int gram_impl = 0;   // unfused mode: 0 v6 (barrier-free), 3 v5, 1 TMA-staged, 2 v3
   int64_t launches = 0;
   int64_t ws_bytes = 0;
@@ -308,32 +309,42 @@ static bool dmma_gram_ok(lsba_ctx c, int J, int ip, const double* X, const doubl
   }
 }
 
+// The previous step's update kernel (stream 2) overlaps this step's SpMM; everything after the
+// SpMM reads its decision or the small state it writes, so the main stream joins it here.
+static lsba_status wait_update(lsba_ctx c) {
+  if (c->pending_upd) {
+    CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
+    c->pending_upd = false;
+  }
+  return LSBA_OK;
+}
+
 // ---------------------------------------------------------------- a2: v7 streaming Gram
 // Tuned (GMAX groups per warp, U steps per batch, MINB CTAs per SM) per s and J from the
 // standalone sweep in tools/gram_bench.cu (profiles/r01_gram_sweep.md).
 template <int S, int GMAX, int U, int MINB>
-static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a) {
+static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   auto fn = k_gram_v7<S, GMAX, U, MINB>;
-  G7Launch<S, GMAX> geo(c->n, a.J, MINB, c->n_sms);
+  G7Launch<S, GMAX> geo(c->n, a.J, MINB, c->n_sms, f.on != 0);
   if ((size_t)geo.grid * a.J * S * S > c->part_cap || geo.passes > kMaxGramPasses)
     return fail(c, LSBA_E_STATE, "v7 Gram workspace too small (J=%d)", a.J);
   if (geo.smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
-  fn<<<geo.grid, 256, geo.smem, c->stream>>>(a);
+  fn<<<geo.grid, 256, geo.smem, c->stream>>>(a, f);
   CKL();
   return LSBA_OK;
 }
 
 template <int S>
-static lsba_status gram_v7(lsba_ctx c, const GramArgs& a) {
+static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   if constexpr (S == 2 || S == 4) {
-    if (a.J <= 6) return gram_v7_launch<S, 1, 16, 3>(c, a);
-    return gram_v7_launch<S, 3, 4, 3>(c, a);
+    if (a.J <= 6) return gram_v7_launch<S, 1, 16, 3>(c, a, f);
+    return gram_v7_launch<S, 3, 4, 3>(c, a, f);
   } else if constexpr (S == 8) {
-    if (a.J <= 4) return gram_v7_launch<S, 1, 16, 3>(c, a);
-    return gram_v7_launch<S, 3, 4, 3>(c, a);
+    if (a.J <= 4) return gram_v7_launch<S, 1, 16, 3>(c, a, f);
+    return gram_v7_launch<S, 3, 4, 3>(c, a, f);
   } else if constexpr (S == 16) {
-    if (a.J <= 4 || a.J > 16) return gram_v7_launch<S, 2, 8, 3>(c, a);
-    return gram_v7_launch<S, 3, 4, 3>(c, a);
+    if (a.J <= 4 || a.J > 16) return gram_v7_launch<S, 2, 8, 3>(c, a, f);
+    return gram_v7_launch<S, 3, 4, 3>(c, a, f);
   } else {
     return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
   }
@@ -345,15 +356,18 @@ static lsba_status gram_v7(lsba_ctx c, const GramArgs& a) {
 // pass on the tensor-core path).  Exactly one allreduce when P > 1 (the step's single sync).
 template <int S>
 static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, double* Y, int ip,
-                          const double* Vk, const int* active) {
+                          const double* Vk, const int* active, int coef_k, const CycleParams* prm,
+                          bool* coef_fused) {
   const bool gl = (ip == LSBA_IP_GLOBAL);
   const size_t E = gl ? (size_t)J : (size_t)J * S * S;
+  if (coef_fused) *coef_fused = false;
   if (dmma_gram_ok<S>(c, J, ip, X, Y)) {
     if constexpr (S == 1 || S == 2 || S == 4 || S == 8 || S == 16) {
       if (Vk && !c->fuse_spmm) {   // standalone high-occupancy SpMM, then the Gram pass
         TRY(spmm_t<S>(c, Vk, Y, active));
         Vk = nullptr;
       }
+      TRY(wait_update(c));
       if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
         using G6 = G6Cfg<S>;
         const int NG6 = (J - 1 + G6::PB - 1) / G6::PB + 1;
@@ -369,9 +383,20 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
             a.J = J; a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
             a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
             a.active = active;
-            TRY(gram_v7<S>(c, a));
+            GramFuse f{};
+            // fuse the small step into the Gram tail on one rank (no allreduce in between)
+            // while its Gram copy fits next to the partials (<= 64 KB of shared memory)
+            if (coef_k >= 0 && coef_fused && c->nranks == 1 && E * sizeof(double) <= 64 * 1024) {
+              f.on = 1;
+              f.st = c->st;
+              f.k = coef_k;
+              f.prm = prm ? *prm : CycleParams{};
+              *coef_fused = true;
+            }
+            TRY(gram_v7<S>(c, a, f));
           } else {
             CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+            if (coef_fused) *coef_fused = false;
           }
           if (c->nranks > 1)
             CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
@@ -432,6 +457,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
           return LSBA_OK;
         }
       }
+      TRY(wait_update(c));
       if (!Vk && c->gram_impl == 1) {    // TMA-staged tensor-core Gram
         const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
         LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
@@ -482,6 +508,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
     }
   } else {
     if (Vk) TRY(spmm_t<S>(c, Vk, Y, active));
+    TRY(wait_update(c));
     const int gx = gl ? J : J * (S / GramTA<S>::value);
     int P = std::max(1, std::min(cdiv(std::max(c->n, 1), 256), cdiv(kGramCtas, gx)));
     if ((size_t)P * E > c->part_cap) P = std::max(1, (int)(c->part_cap / E));
@@ -559,8 +586,9 @@ static lsba_status residual(lsba_ctx c, const double* Bm, const double* X, doubl
   LSBA_DISPATCH_S(c->s, residual_t, c, Bm, X, out);
 }
 static lsba_status gram(lsba_ctx c, const double* X, size_t xstride, int J, double* Y, int ip,
-                        const double* Vk = nullptr, const int* active = nullptr) {
-  LSBA_DISPATCH_S(c->s, gram_t, c, X, xstride, J, Y, ip, Vk, active);
+                        const double* Vk = nullptr, const int* active = nullptr, int coef_k = -1,
+                        const CycleParams* prm = nullptr, bool* coef_fused = nullptr) {
+  LSBA_DISPATCH_S(c->s, gram_t, c, X, xstride, J, Y, ip, Vk, active, coef_k, prm, coef_fused);
 }
 static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, const double* C0,
                            const double* base0, double* out0, int J1, const double* C1, double* out1,
@@ -601,8 +629,9 @@ static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
 // IO(U) with U in slot 0: Gram (1 sync), chol, scale in place (Alg 3 line 1).  Resets the
 // device cycle control with this cycle's parameters.  Asynchronous.
 static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
-  TRY(gram(c, slotp(c, 0), c->slot_stride, 1, slotp(c, 0), c->ip));
-  TRY(small_step(c, 0, prm));
+  bool fused = false;
+  TRY(gram(c, slotp(c, 0), c->slot_stride, 1, slotp(c, 0), c->ip, nullptr, nullptr, 0, &prm, &fused));
+  if (!fused) TRY(small_step(c, 0, prm));
   TRY(project(c, slotp(c, 0), c->slot_stride, 1, c->st.coef, nullptr, slotp(c, 0), 0, nullptr, nullptr,
               c->st.flag_dev, LSBA_K_PROJECT));
   return LSBA_OK;
@@ -612,14 +641,16 @@ static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
 // control says the cycle has ended (speculative enqueue of a whole cycle).
 static lsba_status pip_step_async(lsba_ctx c, int k) {
   const CycleParams none{};   // (k > 0 launches read their parameters from the device control)
-  // Lines 3-4 of step k run while the update kernel of step k-1 (stream 2) is still taking
-  // the continue/restart decision: they only write slot k and G, which are scratch if the
-  // cycle ended at step k-1.  The coefficient kernel reads the decision, so it waits.
+  // The SpMM of step k runs while the update kernel of step k-1 (stream 2) is still taking
+  // the continue/restart decision: it only writes slot k, scratch if the cycle ended at step
+  // k-1.  The Gram (and the small step fused into its tail) waits for the update (wait_update).
   c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
+  c->pending_upd = (k > 1);
+  bool fused = false;
   TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
-           &c->d_ctl->active));                                                  // lines 3-4
-  if (k > 1) CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
-  TRY(small_step(c, k, none));                                                   // line 5
+           &c->d_ctl->active, k, &none, &fused));                                // lines 3-4 (+5)
+  TRY(wait_update(c));
+  if (!fused) TRY(small_step(c, k, none));                                       // line 5
   // estimates / kappa_F / decision on stream 2, concurrent with the projection
   CK(cudaEventRecord(c->ev_coef, c->stream));
   CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
@@ -1088,8 +1119,8 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   {
     const int ngroups = (c->gram_grid + kGramGroup - 1) / kGramGroup;
     TRY(dalloc(c, &c->d_gpart, (size_t)ngroups * Emax));
-    TRY(dalloc(c, &c->d_tickets, (size_t)kMaxGramPasses * (ngroups + 1)));
-    CK(cudaMemset(c->d_tickets, 0, sizeof(unsigned) * kMaxGramPasses * (ngroups + 1)));
+    TRY(dalloc(c, &c->d_tickets, (size_t)(kMaxGramPasses + 1) * (ngroups + 1)));
+    CK(cudaMemset(c->d_tickets, 0, sizeof(unsigned) * (kMaxGramPasses + 1) * (ngroups + 1)));
   }
   TRY(dalloc(c, &c->d_ctl, 1));
   CK(cudaMemset(c->d_ctl, 0, sizeof(CycleCtl)));

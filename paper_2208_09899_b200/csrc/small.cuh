@@ -156,11 +156,12 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
 //                 BGMRES residual estimates, kappa_F, and the device-side decision.
 // The next step's kernels on stream A wait for the update (event), as they read the decision.
 
-// k_step_coef: blockDim 128; dyn smem (k+1) B B doubles.
+// step_coef_body: the whole block runs it (any blockDim multiple of 32, >= 64); Gs is a
+// shared buffer of (k+1) B B doubles.  Called by k_step_coef and, fused, by the last CTA of
+// the Gram kernel (gram7.cuh) on a single rank.
 template <int B>
-__global__ void __launch_bounds__(128)
-k_step_coef(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm, double rfac) {
-  extern __shared__ double Gs[];
+__device__ __forceinline__ void step_coef_body(const SmallState2& st, const double* G, double* Gs, int k,
+                                               const CycleParams& prm, double rfac) {
   __shared__ double Ss[B * B], Rs[B * B], Ris[B * B];
   __shared__ double red[32];
   __shared__ int flag_s;
@@ -172,7 +173,7 @@ k_step_coef(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm
     return;
   }
   const int force_flag = (k > 0 && k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
-  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
+  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = __ldcg(G + e);
   __syncthreads();
   if (k > 0)
     for (int e = tid; e < kb * B; e += nt) {
@@ -311,6 +312,14 @@ k_step_coef(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm
     const int x = e % B, y = e / B;
     st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
   }
+}
+
+// k_step_coef: blockDim 128; dyn smem (k+1) B B doubles.
+template <int B>
+__global__ void __launch_bounds__(128)
+k_step_coef(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm, double rfac) {
+  extern __shared__ double Gs[];
+  step_coef_body<B>(st, G, Gs, k, prm, rfac);
 }
 
 // k_step_update (k >= 1): blockDim 32 * (B + 2); dyn smem (k+1) B B + (k-1)(2 B B + B).

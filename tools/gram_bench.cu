@@ -74,7 +74,8 @@ static std::vector<double> run_v7(const Bufs& B, int n, int J, double* us, int* 
   G7Launch<S, GMAX> geo(n, J, MINB, 148);
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(geo.smem, 48 * 1024)));
   *grid_out = geo.grid;
-  *us = time_it([&] { fn<<<geo.grid, 256, geo.smem>>>(a); }, 10);
+  GramFuse nf{};
+  *us = time_it([&] { fn<<<geo.grid, 256, geo.smem>>>(a, nf); }, 10);
   CK(cudaGetLastError());
   std::vector<double> G(J * S * S);
   CK(cudaMemcpy(G.data(), B.G, sizeof(double) * G.size(), cudaMemcpyDeviceToHost));
