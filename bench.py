@@ -166,16 +166,18 @@ def oracle_sample(wl, budget_s):
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
+    from threadpoolctl import threadpool_limits
     wl = build_workload(args.config, 0, 1)
     per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        oracle_sample(wl, per_step_budget / 4)
     tot_s, tot_b, tot_steps = 0.0, 0.0, 0
-    for _ in range(args.steps):
-        r = oracle_sample(wl, per_step_budget)
-        tot_s += r["seconds"]
-        tot_b += r["bytes"]
-        tot_steps += r["steps"]
+    with threadpool_limits(1):              # the oracle as it stands, on one host core
+        for _ in range(args.warmup):
+            oracle_sample(wl, per_step_budget / 4)
+        for _ in range(args.steps):
+            r = oracle_sample(wl, per_step_budget)
+            tot_s += r["seconds"]
+            tot_b += r["bytes"]
+            tot_steps += r["steps"]
     gbs = tot_b / tot_s / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
@@ -248,24 +250,33 @@ def main():
     if args.warmup:
         L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1)
     barrier()
+
+    def timed_cycles(profile):
+        """K cycles in one solve call, CUDA events on the library's stream, max over ranks."""
+        L.lsba_profile_enable(ctx.ctx, profile)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        inf = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.steps - 1)    # exactly K cycles
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_ms = e0.elapsed_time(e1)
+        pr = {k: L.lsba_profile_read(ctx.ctx, k) for k in L.KERNEL_IDS} if profile else None
+        L.lsba_profile_enable(ctx.ctx, False)
+        if dist is not None:
+            t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_ms = float(t.item())
+        return inf, t_ms, pr
+
+    # headline: un-instrumented (a CUDA event around every launch costs ~2 us of GPU idle each,
+    # ~8% of a config-2 step); then the same K cycles again with per-launch events for the
+    # per-kernel times behind `roofline`
     clocks = ClockSampler(local)
     clocks.start()
-    L.lsba_profile_enable(ctx.ctx, True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    info = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.steps - 1)    # exactly K cycles
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms_local = e0.elapsed_time(e1)
+    info, ms, _ = timed_cycles(False)
     clk = clocks.stop()
-    prof = {k: L.lsba_profile_read(ctx.ctx, k) for k in L.KERNEL_IDS}
-    L.lsba_profile_enable(ctx.ctx, False)
-    ms = ms_local
-    if dist is not None:
-        t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    info_p, ms_prof, prof = timed_cycles(True)
     cycles, iters = info.cycles, info.iterations
     assert cycles == args.steps, f"expected {args.steps} cycles, ran {cycles} (outcome {info.outcome})"
     # whole-job algorithmic bytes (global problem)
@@ -311,7 +322,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = oracle_sample(wl, 20.0)
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1):          # the oracle as it stands, on one host core
+            r = oracle_sample(wl, 20.0)
         cpu = {"value": r["bytes"] / r["seconds"] / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
                "block_steps_per_s": r["steps"] / r["seconds"],
                "sample": f"oracle IO + first {r['steps']} block steps of one cycle of {wl['name']} "
@@ -330,7 +343,9 @@ def main():
                        "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "launches": dn, "kernel_share_of_step": dms / tot_ms if tot_ms else None},
+                         "launches": dn, "kernel_share_of_step": dms / tot_ms if tot_ms else None,
+                         "measured_in": "instrumented re-run of the same K cycles (per-launch CUDA events "
+                                        f"on the launching streams; {ms_prof / args.steps:.3f} ms per cycle)"},
             "kernel_times_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
             "kernel_gbs": {k: round(v[2] / (v[1] / 1e3) / 1e9, 1) for k, v in prof.items() if v[1] > 0 and v[2] > 0},
             "gpu_launches": int(info.kernel_launches),

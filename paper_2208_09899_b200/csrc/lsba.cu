@@ -338,13 +338,14 @@ template <int S>
 static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   if constexpr (S == 2 || S == 4) {
     if (a.J <= 6) return gram_v7_launch<S, 1, 16, 3>(c, a, f);
+    if (a.J <= 16) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
     return gram_v7_launch<S, 3, 4, 3>(c, a, f);
   } else if constexpr (S == 8) {
     if (a.J <= 4) return gram_v7_launch<S, 1, 16, 3>(c, a, f);
     return gram_v7_launch<S, 3, 4, 3>(c, a, f);
   } else if constexpr (S == 16) {
-    if (a.J <= 4 || a.J > 16) return gram_v7_launch<S, 2, 8, 3>(c, a, f);
-    return gram_v7_launch<S, 3, 4, 3>(c, a, f);
+    if (a.J <= 4) return gram_v7_launch<S, 3, 6, 2>(c, a, f);
+    return gram_v7_launch<S, 2, 4, 3>(c, a, f);
   } else {
     return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
   }

@@ -122,21 +122,23 @@ static void sweep(int n, std::vector<int> Js) {
     printf("s=%d n=%d J=%d (%.0f MB)\n   v6               : %8.1f us %7.0f GB/s\n", S, n, J, bytes / 1e6, us6, bytes / us6 / 1e3);
     v7_line<S, 3, 4, 3>(B, n, J, ref, bytes);
     v7_line<S, 2, 8, 3>(B, n, J, ref, bytes);
-    v7_line<S, 3, 2, 3, true>(B, n, J, ref, bytes);
-    v7_line<S, 2, 4, 3, true>(B, n, J, ref, bytes);
-    v7_line<S, 2, 2, 4, true>(B, n, J, ref, bytes);
-    v7_line<S, 4, 2, 2, true>(B, n, J, ref, bytes);
-    v7_line<S, 2, 4, 2, true>(B, n, J, ref, bytes);
-    v7_line<S, 1, 4, 4, true>(B, n, J, ref, bytes);
+    v7_line<S, 1, 16, 3>(B, n, J, ref, bytes);
+    v7_line<S, 4, 4, 3>(B, n, J, ref, bytes);
+    v7_line<S, 2, 4, 3>(B, n, J, ref, bytes);
+    v7_line<S, 3, 6, 2>(B, n, J, ref, bytes);
+    v7_line<S, 3, 2, 4>(B, n, J, ref, bytes);
+    v7_line<S, 1, 8, 4>(B, n, J, ref, bytes);
+    v7_line<S, 2, 6, 3>(B, n, J, ref, bytes);
+    v7_line<S, 4, 2, 4>(B, n, J, ref, bytes);
   }
   cudaFree(B.V); cudaFree(B.part); cudaFree(B.gpart); cudaFree(B.G); cudaFree(B.zeros); cudaFree(B.tickets);
 }
 
 int main(int argc, char** argv) {
   const int which = argc > 1 ? atoi(argv[1]) : 0;
-  if (which == 0 || which == 2) sweep<4>(1 << 20, {2, 6, 11, 21});
+  if (which == 0 || which == 2) sweep<4>(1 << 20, {3, 6, 9, 13, 17, 21});
   if (which == 0 || which == 3) sweep<8>(1 << 21, {2, 11, 21, 31});
   if (which == 0 || which == 5) sweep<8>(1 << 24, {2, 21, 41});
-  if (which == 0 || which == 4) sweep<16>(1 << 22, {2, 11, 26});
+  if (which == 0 || which == 4) sweep<16>(1 << 22, {3, 7, 13, 19, 26});
   return 0;
 }
