@@ -47,6 +47,13 @@ def roof_cycle_extra(n, s, k_used):
     return 8.0 * n * s * (k_used + 7)
 
 
+def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks):
+    """sum_steps ROOF(k) + sum_cycles 8ns(k_used+7), from the solver's counters
+    (gram_blocks = sum over accepted steps of k+1)."""
+    return (iters * (12.0 * nnz + 4.0 * (n + 1) + 8.0 * n * s) + 16.0 * n * s * gram_blocks
+            + 8.0 * n * s * (iters + 7 * cycles))
+
+
 def cycle_bytes(nnz, n, s, m):
     return sum(roof_step(nnz, n, s, k) for k in range(1, m + 1)) + roof_cycle_extra(n, s, m)
 
@@ -206,6 +213,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
 
@@ -248,16 +256,31 @@ def main():
 
     # warm-up: W cycles (one solve call), not timed
     if args.warmup:
-        L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1)
+        L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1, ip=args.ip)
     barrier()
 
+    # configs 1 and 4 converge in a few cycles: a bench step is then one full solve from X0 = 0
+    full_solve = wl["spec"].get("max_restarts", 0) <= 50 or args.config == 4
+
     def timed_cycles(profile):
-        """K cycles in one solve call, CUDA events on the library's stream, max over ranks."""
+        """K cycles in one solve call (or K full solves), CUDA events on the library's stream,
+        max over ranks.  Returns (iterations, cycles, ms, per-kernel profile, last info)."""
         L.lsba_profile_enable(ctx.ctx, profile)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
-        inf = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.steps - 1)    # exactly K cycles
+        it = cy = nl = gb = 0
+        for _ in range(args.steps if full_solve else 1):
+            if full_solve:
+                X.zero_()
+            inf = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, 200 if full_solve else args.steps - 1,
+                                      ip=args.ip)
+            it += inf.iterations
+            cy += inf.cycles
+            nl += inf.kernel_launches
+            gb += inf.gram_blocks
+        timed_cycles.launches = nl
+        timed_cycles.gram_blocks = gb
         e1.record(stream)
         torch.cuda.synchronize()
         t_ms = e0.elapsed_time(e1)
@@ -267,20 +290,22 @@ def main():
             t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_ms = float(t.item())
-        return inf, t_ms, pr
+        return it, cy, t_ms, pr, inf
 
     # headline: un-instrumented (a CUDA event around every launch costs ~2 us of GPU idle each,
     # ~8% of a config-2 step); then the same K cycles again with per-launch events for the
     # per-kernel times behind `roofline`
     clocks = ClockSampler(local)
     clocks.start()
-    info, ms, _ = timed_cycles(False)
+    iters, cycles, ms, _, info = timed_cycles(False)
+    launches = timed_cycles.launches
     clk = clocks.stop()
-    info_p, ms_prof, prof = timed_cycles(True)
-    cycles, iters = info.cycles, info.iterations
-    assert cycles == args.steps, f"expected {args.steps} cycles, ran {cycles} (outcome {info.outcome})"
-    # whole-job algorithmic bytes (global problem)
-    total_bytes = cycle_bytes(wl["nnz"], n_glob, s, m) * iters / m
+    _, _, ms_prof, prof, _ = timed_cycles(True)
+    if not full_solve:
+        assert cycles == args.steps, f"expected {args.steps} cycles, ran {cycles} (outcome {info.outcome})"
+    # whole-job algorithmic bytes (global problem): sum over accepted steps of ROOF(k) =
+    # iters (A + 8ns) + 16ns sum(k+1), plus 8ns(k_used + 7) per cycle
+    total_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, iters, cycles, timed_cycles.gram_blocks)
     gbs = total_bytes / (ms / 1e3) / 1e9
     steps_per_s = iters / (ms / 1e3)
     peak, peak_kind = measured_peaks()
@@ -306,19 +331,25 @@ def main():
         barrier()
         t0 = time.perf_counter()
         e2e_iters = 0
+        e2e_cycles = e2e_gb = 0
         for _ in range(args.steps):
-            ih = L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 0)
+            if full_solve:
+                Xh[:] = 0.0
+            ih = L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 200 if full_solve else 0, ip=args.ip)
             e2e_iters += ih.iterations
+            e2e_cycles += ih.cycles
+            e2e_gb += ih.gram_blocks
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if dist is not None:
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e_bytes = cycle_bytes(wl["nnz"], n_glob, s, m) * e2e_iters / m
+        e2e_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, e2e_iters, e2e_cycles, e2e_gb)
         e2e = {"value": e2e_bytes / dt / 1e9, "unit": "GB/s", "block_steps_per_s": e2e_iters / dt,
                "h2d_bytes_per_step": 2 * n_loc * s * 8 * world, "d2h_bytes_per_step": n_loc * s * 8 * world,
-               "api": "lsba_solve_host (1 cycle per call, X0 = previous X)"}
+               "api": "lsba_solve_host (" + ("one full solve per step, X0 = 0" if full_solve
+                                             else "1 cycle per call, X0 = previous X") + ")"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -338,8 +369,10 @@ def main():
             "block_steps_per_s": steps_per_s, "ms_per_block_step": ms / iters,
             "pct_roofline": {"of_measured_hbm": gbs / (peak * world), "of_8TBps_nominal": gbs / (8000.0 * world)},
             "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
-                       "method": "cl-BGMRES, BCGS-PIP skeleton, CholQR IO",
-                       "timed_unit": f"restart cycle = IO + {m} block steps + cycle end",
+                       "method": f"{args.ip}-BGMRES, BCGS-PIP skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO"),
+                       "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
+                                      f"{iters / args.steps:.1f} block steps)") if full_solve
+                                     else f"restart cycle = IO + {m} block steps + cycle end",
                        "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
@@ -348,7 +381,7 @@ def main():
                                         f"on the launching streams; {ms_prof / args.steps:.3f} ms per cycle)"},
             "kernel_times_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
             "kernel_gbs": {k: round(v[2] / (v[1] / 1e3) / 1e9, 1) for k, v in prof.items() if v[1] > 0 and v[2] > 0},
-            "gpu_launches": int(info.kernel_launches),
+            "gpu_launches": int(launches),
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

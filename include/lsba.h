@@ -82,6 +82,8 @@ typedef struct {
   double res_est;             /* last residual estimate, ||.||_F (absolute)               */
   double true_relres;         /* ||B - A X||_F / ||B||_F at exit (explicit)               */
   double seconds;             /* wall time of the call                                    */
+  int64_t gram_blocks;        /* sum over accepted steps k of (k+1): n x s blocks read by the
+                                 single-sync Gram passes (algorithmic-bytes accounting)     */
 } lsba_solve_info;
 
 /* ---------------------------------------------------------------- lifecycle */

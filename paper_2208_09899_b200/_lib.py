@@ -40,7 +40,8 @@ class SolveInfo(C.Structure):
                 ("false_convergences", C.c_int32), ("m_final", C.c_int32),
                 ("syncs", C.c_int64), ("matvecs", C.c_int64), ("basis_evals", C.c_int64),
                 ("kernel_launches", C.c_int64),
-                ("res_est", C.c_double), ("true_relres", C.c_double), ("seconds", C.c_double)]
+                ("res_est", C.c_double), ("true_relres", C.c_double), ("seconds", C.c_double),
+                ("gram_blocks", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

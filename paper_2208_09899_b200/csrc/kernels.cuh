@@ -184,6 +184,16 @@ k_spmm_odd(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   }
 }
 
+// *flag |= (any x[i] != 0) over count doubles (flag zeroed by the caller); used to take
+// U = B without an SpMM when X0 = 0 (reading R13)
+static __global__ void k_any_nonzero(long count, const double* __restrict__ x, int* __restrict__ flag) {
+  int nz = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    nz |= (x[i] != 0.0);
+  nz = __syncthreads_or(nz);
+  if (threadIdx.x == 0 && nz) atomicOr(flag, 1);
+}
+
 // halo pack: send[i] = V[idx[i]] (rows)
 template <int S>
 __global__ void k_halo_pack(int cnt, const int* __restrict__ idx, const double* __restrict__ V,

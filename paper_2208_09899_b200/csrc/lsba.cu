@@ -83,6 +83,7 @@ struct lsba_ctx_ {
   cudaStream_t stream2 = nullptr;  // update kernels run here, concurrent with the projection
   cudaEvent_t ev_coef = nullptr, ev_upd = nullptr;
   CycleCtl* h_ctl = nullptr;      // pinned copy
+  volatile int* h_prog = nullptr; // mapped pinned {k_done, active} (see publish_progress)
   int n_sms = 148;
   // small state
   SmallState2 st{};
@@ -662,6 +663,20 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   return LSBA_OK;
 }
 
+// Host-side lookahead bound for the speculative enqueue of a cycle: step k is enqueued once
+// the device has decided step k - kLookahead (polling the mapped progress word).  Returns
+// false if the device already ended the cycle.
+constexpr int kLookahead = 3;
+static bool throttle(lsba_ctx c, int k) {
+  if (k <= kLookahead) return c->h_prog[1] != 0 || c->h_prog[0] < 0;
+  for (;;) {
+    const int done = c->h_prog[0], act = c->h_prog[1];
+    if (done >= 0 && act == 0) return false;
+    if (done >= k - kLookahead) return true;
+    if (cudaStreamQuery(c->stream) == cudaSuccess) return true;   // (device drained: no stall)
+  }
+}
+
 // join stream 2 (the last step's update) into the main stream
 static lsba_status join_update(lsba_ctx c) {
   CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
@@ -766,7 +781,24 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     return LSBA_OK;
   };
 
-  TRY(residual(c, B, X, slotp(c, 0)));   // U = B - A X0 (R13)
+  // U = B - A X0 (R13); U = B exactly when X0 = 0 (every rank must agree: one flag allreduce)
+  {
+    CK(cudaMemsetAsync(c->d_info, 0, sizeof(int), c->stream));
+    if (c->n > 0) {
+      LaunchScope Ls(c, LSBA_K_MISC, 8.0 * c->slot);
+      k_any_nonzero<<<std::min(4 * c->n_sms, cdiv((long)c->slot, kThreads)), kThreads, 0, c->stream>>>(
+          (long)c->slot, X, c->d_info);
+      CKL();
+    }
+    if (c->nranks > 1) CKN(ncclAllReduce(c->d_info, c->d_info, 1, ncclInt, ncclMax, c->comm, c->stream));
+    CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->h_info[0]) {
+      TRY(residual(c, B, X, slotp(c, 0)));
+    } else if (c->n > 0) {
+      CK(cudaMemcpyAsync(slotp(c, 0), B, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
   TRY(set_identity(c));                   // C_acc = I
   int m_cur = m;
   CycleCtl cc;
@@ -784,13 +816,21 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     prm.tol_abs = tol * normB;                               // R5, R18
     prm.tau = tau;                                           // R8
     prm.need_kappa = std::isfinite(tau) ? 1 : 0;
+    c->h_prog[0] = -1;                                       // (device idle: cycle boundary)
+    c->h_prog[1] = 1;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
-    for (int k = 1; k <= m_cur; ++k) TRY(pip_step_async(c, k));
+    for (int k = 1; k <= m_cur; ++k) {
+      // keep at most kLookahead steps enqueued beyond the last decided one; stop enqueueing
+      // once the device has ended the cycle (flag, convergence, kappa trigger)
+      if (!throttle(c, k)) break;
+      TRY(pip_step_async(c, k));
+    }
     TRY(join_update(c));
     TRY(read_status(c, nullptr, &cc));
     if (cc.why == 5) { info->outcome = LSBA_DEAD; break; }   // IO flagged (R4)
     int k_used = cc.k_used;
     info->iterations += k_used;
+    info->gram_blocks += (int64_t)k_used * (k_used + 3) / 2;    // sum_{k=1}^{k_used} (k+1)
     info->attempted_steps += k_used + (cc.why == 1 ? 1 : 0);
     if (k_used > 0) info->res_est = cc.res_est;
     if (cc.why == 1) {
@@ -982,6 +1022,7 @@ static void release(lsba_ctx c) {
   if (c->h_info) cudaFreeHost(c->h_info);
   if (c->h_scalar) cudaFreeHost(c->h_scalar);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->h_prog) cudaFreeHost((void*)c->h_prog);
   if (c->ev_coef) cudaEventDestroy(c->ev_coef);
   if (c->ev_upd) cudaEventDestroy(c->ev_upd);
   if (c->stream2) cudaStreamDestroy(c->stream2);
@@ -1158,6 +1199,14 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.m = m_max;
   c->st.bmax = s;
   c->st.ctl = c->d_ctl;
+  {  // progress word in mapped pinned host memory (written by the device, polled by the host)
+    CK(cudaHostAlloc((void**)&c->h_prog, 2 * sizeof(int), cudaHostAllocMapped));
+    c->h_prog[0] = -1;
+    c->h_prog[1] = 0;
+    int* dp = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&dp, (void*)c->h_prog, 0));
+    c->st.prog = dp;
+  }
   TRY(dalloc(c, &c->st.rscr, 2 * (size_t)s * s));
   TRY(dalloc(c, &c->st.iscr, 4));
   {  // the update kernel's single CTA should get an SM as soon as one frees up

@@ -39,7 +39,19 @@ struct SmallState2 {
   double* rscr;    // 2 b b: R and R^{-1} of the current step (coef -> update)
   int* iscr;       // [0] flag, [1] forced
   int ldH, m, bmax;
+  volatile int* prog;   // host-mapped progress word {k_done, active} read by the enqueueing host
 };
+
+// publish the step just decided to the host (mapped pinned memory; the host bounds how far
+// ahead of the device it enqueues speculative steps)
+__device__ __forceinline__ void publish_progress(const SmallState2& st, int k, int active) {
+  if (st.prog) {
+    st.prog[1] = active;
+    __threadfence_system();
+    st.prog[0] = k;
+    __threadfence_system();
+  }
+}
 
 // IO-time cycle parameters (k == 0 launch of k_step_small)
 struct CycleParams {
@@ -238,6 +250,7 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
         ctl->need_kappa = prm.need_kappa;
         ctl->res_est = nan("");
         ctl->kappa = nan("");
+        publish_progress(st, 0, f ? 0 : 1);
       }
       st.status->k = k;
       st.status->flag = flag_s;
@@ -395,6 +408,7 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
       ctl->why = 1;
       ctl->k_flag = k;
       if (forced_s) { ctl->forced_here = 1; ctl->forced_done = 1; }
+      publish_progress(st, k, 0);
     }
     return;
   }
@@ -532,6 +546,7 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
       else if (kap > ctl->tau) { ctl->active = 0; ctl->why = 3; }
       else if (k >= ctl->m_cur) { ctl->active = 0; ctl->why = 4; }
     }
+    publish_progress(st, k, ctl->active);
   }
 }
 

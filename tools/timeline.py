@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--cycles", type=int, default=2)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--cold", action="store_true", help="profile a full solve from X0 = 0")
+    ap.add_argument("--ip", default="cl")
     args = ap.parse_args()
     import torch
     import paper_2208_09899_b200 as L
@@ -30,10 +32,13 @@ def main():
     L.lsba_set_kernel_variant(ctx.ctx, args.variant)
     B = torch.from_numpy(wl["B"]).cuda()
     X = torch.zeros_like(B)
-    L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 0)
+    L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 0, ip=args.ip)
     torch.cuda.synchronize()
+    if args.cold:
+        X.zero_()
     L.lsba_profile_enable(ctx.ctx, True)
-    L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], args.cycles - 1)
+    info = L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 200 if args.cold else args.cycles - 1, ip=args.ip)
+    print("solve:", info.as_dict())
     tl = L.lsba_profile_timeline(ctx.ctx)
     L.lsba_profile_enable(ctx.ctx, False)
     lines = []
