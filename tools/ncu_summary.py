@@ -100,11 +100,16 @@ def full(rep, out):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     vals = {}
     name = ""
-    for r in csv.reader(det.splitlines()):
-        if len(r) > 5 and r[-3] in FULL_KEYS:
-            vals.setdefault(r[-3], f"{r[-1]} {r[-2]}")
-        if len(r) > 5 and not name and "lsba" in "".join(r):
-            name = next((x for x in r if "lsba::" in x), "")
+    rows = list(csv.reader(det.splitlines()))
+    if rows:
+        h = rows[0]
+        iN, iM, iU, iV = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
+        for r in rows[1:]:
+            if len(r) <= iV:
+                continue
+            name = name or r[iN]
+            if r[iM] in FULL_KEYS:
+                vals.setdefault(r[iM], f"{r[iV]} {r[iU]}".strip())
     rr = list(csv.reader(raw.splitlines()))
     d = dict(zip(rr[0], rr[2])) if len(rr) > 2 else {}
     units = dict(zip(rr[0], rr[1])) if len(rr) > 1 else {}
