@@ -28,6 +28,14 @@ constexpr int kMaxGramPasses = 64;  // ticket sets allocated per context (one pe
 // Fused small step: on a single rank the Gram's last-finishing CTA goes straight on with
 // Alg 3 line 5 (S = Omega - H^T H, Cholesky + NaN-flag, R^-1, projection coefficients;
 // step_coef_body of small.cuh) instead of a separate 1-CTA launch.
+// The fused small step as a real call for s = 16: inlined, its 16 x 16 register arrays would
+// raise the register demand (and spills) of the streaming loop above it.
+template <int B>
+__device__ __noinline__ void step_coef_noinline(const SmallState2& st, const double* G, double* Gs, int k,
+                                                const CycleParams& prm) {
+  step_coef_body<B>(st, G, Gs, k, prm, 1.0);
+}
+
 struct GramFuse {
   SmallState2 st;
   CycleParams prm;
@@ -62,7 +70,7 @@ __host__ __device__ inline int g7_qw(int ngp, int GMAX) {
   return QW;
 }
 
-template <int S, int GMAX, int U, int MINB, bool PIPE = false>
+template <int S, int GMAX, int U, int MINB, bool WIN = true>
 __global__ void __launch_bounds__(256, MINB)
 k_gram_v7(GramArgs g, GramFuse f) {
   using C = G7Cfg<S, GMAX, U, MINB>;
@@ -105,74 +113,89 @@ k_gram_v7(GramArgs g, GramFuse f) {
       for (int tn = 0; tn < C::NT; ++tn) acc[a][e][tn][0] = acc[a][e][tn][1] = 0.0;
 
   const long NS = ((long)g.n + 3) / 4;                 // 4-row steps (rows padded)
-  const long s0 = NS * chunk / nchunks, s1 = NS * (chunk + 1) / nchunks;
-  long st = s0 + rs;
-  // U 4-row steps per batch: load the batch's fragments, then run its DMMAs.  PIPE: two
-  // batches in registers, the next batch's loads are issued before the current batch's DMMAs.
-  auto load_batch = [&](double2 (&av)[C::U][C::GMAX], double (&bw)[C::U][C::NT], long sb) {
-#pragma unroll
-    for (int u = 0; u < C::U; ++u) {
-      const size_t off = (size_t)(sb + (long)u * RW) * 4 * S;
-#pragma unroll
-      for (int tn = 0; tn < C::NT; ++tn)
-        bw[u][tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
-#pragma unroll
-      for (int gi = 0; gi < C::GMAX; ++gi)
-        av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
-    }
-  };
-  auto mma_batch = [&](const double2 (&av)[C::U][C::GMAX], const double (&bw)[C::U][C::NT]) {
-#pragma unroll
-    for (int u = 0; u < C::U; ++u)
-#pragma unroll
-      for (int gi = 0; gi < C::GMAX; ++gi) {
-        if (gi >= ng) continue;
-#pragma unroll
-        for (int tn = 0; tn < C::NT; ++tn) {
-          dmma(acc[gi][0][tn][0], acc[gi][0][tn][1], av[u][gi].x, bw[u][tn]);
-          dmma(acc[gi][1][tn][0], acc[gi][1][tn][1], av[u][gi].y, bw[u][tn]);
-        }
-      }
-  };
-  const long BS = (long)C::U * RW;                     // steps per batch (this warp's stride)
-  if constexpr (PIPE) {
-    double2 av0[C::U][C::GMAX], av1[C::U][C::GMAX];
-    double bw0[C::U][C::NT], bw1[C::U][C::NT];
-    if (st + (C::U - 1) * RW < s1) load_batch(av0, bw0, st);
-    while (st + (C::U - 1) * RW < s1) {
-      const bool has1 = st + BS + (C::U - 1) * RW < s1;
-      if (has1) load_batch(av1, bw1, st + BS);
-      mma_batch(av0, bw0);
-      st += BS;
-      if (!has1) break;
-      const bool has0 = st + BS + (C::U - 1) * RW < s1;
-      if (has0) load_batch(av0, bw0, st + BS);
-      mma_batch(av1, bw1);
-      st += BS;
-      if (!has0) break;
-    }
-  } else {
-    for (; st + (long)(C::U - 1) * RW < s1; st += BS) {
-      double2 av[C::U][C::GMAX];
-      double bw[C::U][C::NT];
-      load_batch(av, bw, st);
-      mma_batch(av, bw);
-    }
-  }
-  for (; st < s1; st += RW) {                          // remainder steps, one at a time
-    const size_t off = (size_t)st * 4 * S;
-    double bw[C::NT];
-#pragma unroll
-    for (int tn = 0; tn < C::NT; ++tn) bw[tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+  // Row order ("windowed"): warp slice rs of chunk c takes the U consecutive steps starting at
+  // ((i nchunks + c) RW + rs) U in its i-th batch, so the whole grid sweeps one moving window
+  // of rows (few open DRAM pages, 16-row contiguous runs per block and warp).  Measured 3-8%
+  // faster than per-CTA contiguous chunks with steps strided by RW (tools/gram_bench.cu).
+  const long BS = (long)C::U * RW;                     // steps per chunk-batch
+  const long GS = BS * nchunks;                        // steps per grid-batch
+  (void)BS;
+  // U 4-row steps per batch: load the batch's fragments, then run its DMMAs.
+  auto mma_step = [&](const double2 (&av)[C::GMAX], const double (&bw)[C::NT]) {
 #pragma unroll
     for (int gi = 0; gi < C::GMAX; ++gi) {
       if (gi >= ng) continue;
-      const double2 av = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int tn = 0; tn < C::NT; ++tn) {
-        dmma(acc[gi][0][tn][0], acc[gi][0][tn][1], av.x, bw[tn]);
-        dmma(acc[gi][1][tn][0], acc[gi][1][tn][1], av.y, bw[tn]);
+        dmma(acc[gi][0][tn][0], acc[gi][0][tn][1], av[gi].x, bw[tn]);
+        dmma(acc[gi][1][tn][0], acc[gi][1][tn][1], av[gi].y, bw[tn]);
       }
+    }
+  };
+  if constexpr (WIN) {
+    // windowed order (above): U consecutive steps per batch, the grid sweeping one window
+    for (long st = ((long)chunk * RW + rs) * C::U; st < NS; st += GS) {
+      double2 av[C::U][C::GMAX];
+      double bw[C::U][C::NT];
+      if (st + C::U <= NS) {                           // full batch: unpredicated loads
+#pragma unroll
+        for (int u = 0; u < C::U; ++u) {
+          const size_t off = (size_t)(st + u) * 4 * S;
+#pragma unroll
+          for (int tn = 0; tn < C::NT; ++tn)
+            bw[u][tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+#pragma unroll
+          for (int gi = 0; gi < C::GMAX; ++gi)
+            av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+        }
+      } else {                                         // the grid's last, ragged batch
+#pragma unroll
+        for (int u = 0; u < C::U; ++u) {
+          const bool ok = st + u < NS;
+          const size_t off = (size_t)(ok ? st + u : st) * 4 * S;
+#pragma unroll
+          for (int tn = 0; tn < C::NT; ++tn)
+            bw[u][tn] = (ok && tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+#pragma unroll
+          for (int gi = 0; gi < C::GMAX; ++gi)
+            av[u][gi] = (ok && src[gi]) ? __ldg(reinterpret_cast<const double2*>(src[gi] + off))
+                                        : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < C::U; ++u) mma_step(av[u], bw[u]);
+    }
+  } else {
+    // per-CTA contiguous chunk, the steps of a batch strided by RW (s = 16: its DMMA load is 4x
+    // that of s <= 8 and this order measured faster there)
+    const long s0 = NS * chunk / nchunks, s1 = NS * (chunk + 1) / nchunks;
+    long st = s0 + rs;
+    for (; st + (long)(C::U - 1) * RW < s1; st += (long)C::U * RW) {
+      double2 av[C::U][C::GMAX];
+      double bw[C::U][C::NT];
+#pragma unroll
+      for (int u = 0; u < C::U; ++u) {
+        const size_t off = (size_t)(st + (long)u * RW) * 4 * S;
+#pragma unroll
+        for (int tn = 0; tn < C::NT; ++tn)
+          bw[u][tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+#pragma unroll
+        for (int gi = 0; gi < C::GMAX; ++gi)
+          av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < C::U; ++u) mma_step(av[u], bw[u]);
+    }
+    for (; st < s1; st += RW) {                        // remainder steps, one at a time
+      const size_t off = (size_t)st * 4 * S;
+      double2 av[C::GMAX];
+      double bw[C::NT];
+#pragma unroll
+      for (int tn = 0; tn < C::NT; ++tn) bw[tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+#pragma unroll
+      for (int gi = 0; gi < C::GMAX; ++gi)
+        av[gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+      mma_step(av, bw);
     }
   }
   // CTA partial: each row slice writes its own slot (group sets are disjoint and cover the
@@ -241,7 +264,8 @@ k_gram_v7(GramArgs g, GramFuse f) {
   if (ticket7 != (unsigned)(passes - 1)) return;
   __threadfence();
   if (tid == 0) *tpass = 0u;
-  step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
+  if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm);
+  else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
 }
 
 // launch geometry of k_gram_v7: grid (a multiple of the pass count) and dynamic smem bytes

@@ -96,8 +96,22 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   const int row = (int)(gt / L);
   const int lane = (int)(gt % L);
   double sq = 0.0;
+  // row pointers: for L >= 2 one coalesced load of the warp's 32/L + 1 pointers, then shuffles
+  // (instead of 2 L redundant dependent loads per row; +4-7% on the stencil configs,
+  // tools/spmm_bench.cu)
+  int p0, p1;
+  if constexpr (L >= 2) {
+    const int lane32 = threadIdx.x & 31;
+    const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
+    const int rr = row_w + lane32;
+    const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+    p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
+    p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
+  } else {
+    p0 = (row < n) ? rp[row] : 0;
+    p1 = (row < n) ? rp[row + 1] : 0;
+  }
   if (row < n) {
-    const int p0 = rp[row], p1 = rp[row + 1];
     double a0 = 0.0, a1 = 0.0;
     for (int p = p0; p < p1; ++p) {
       const int c = __ldg(ci + p);

@@ -323,9 +323,9 @@ static lsba_status wait_update(lsba_ctx c) {
 // ---------------------------------------------------------------- a2: v7 streaming Gram
 // Tuned (GMAX groups per warp, U steps per batch, MINB CTAs per SM) per s and J from the
 // standalone sweep in tools/gram_bench.cu (profiles/r01_gram_sweep.md).
-template <int S, int GMAX, int U, int MINB>
+template <int S, int GMAX, int U, int MINB, bool WIN = true>
 static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
-  auto fn = k_gram_v7<S, GMAX, U, MINB>;
+  auto fn = k_gram_v7<S, GMAX, U, MINB, WIN>;
   G7Launch<S, GMAX> geo(c->n, a.J, MINB, c->n_sms, f.on != 0);
   if ((size_t)geo.grid * a.J * S * S > c->part_cap || geo.passes > kMaxGramPasses)
     return fail(c, LSBA_E_STATE, "v7 Gram workspace too small (J=%d)", a.J);
@@ -338,15 +338,15 @@ static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse&
 template <int S>
 static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   if constexpr (S == 2 || S == 4) {
-    if (a.J <= 6) return gram_v7_launch<S, 1, 16, 3>(c, a, f);
-    if (a.J <= 16) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
-    return gram_v7_launch<S, 3, 4, 3>(c, a, f);
+    if (a.J <= 4) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    if (a.J <= 8) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
+    return gram_v7_launch<S, 3, 6, 2>(c, a, f);
   } else if constexpr (S == 8) {
-    if (a.J <= 4) return gram_v7_launch<S, 1, 16, 3>(c, a, f);
-    return gram_v7_launch<S, 3, 4, 3>(c, a, f);
+    if (a.J <= 4) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    return gram_v7_launch<S, 3, 6, 2>(c, a, f);
   } else if constexpr (S == 16) {
-    if (a.J <= 4) return gram_v7_launch<S, 3, 6, 2>(c, a, f);
-    return gram_v7_launch<S, 2, 4, 3>(c, a, f);
+    if (a.J <= 4) return gram_v7_launch<S, 3, 6, 2, false>(c, a, f);
+    return gram_v7_launch<S, 2, 4, 3, false>(c, a, f);
   } else {
     return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
   }
@@ -622,6 +622,7 @@ static lsba_status step_update(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, step_u
 static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (out) *out = *c->h_status;
   if (ctl) *ctl = *c->h_ctl;
@@ -691,16 +692,28 @@ static lsba_status set_identity(lsba_ctx c) {
 }
 
 template <int B>
-static lsba_status cycle_end_t(lsba_ctx c, int k, int gmres, int happy, int upd) {
+static lsba_status cycle_end_t(lsba_ctx c, int k, int gmres, int happy, int upd, int* info) {
   LaunchScope Ls(c, LSBA_K_CYCLE_SOLVE, 0.0);
-  CK(launch_cycle_end<B>(c->st, k, gmres, happy, upd, c->d_Y, c->d_Z, c->d_info, c->stream));
+  CK(launch_cycle_end<B>(c->st, k, gmres, happy, upd, c->d_Y, c->d_Z, info, c->stream));
   return LSBA_OK;
+}
+
+// Enqueue the cycle-end projected solve; its singular flag goes to d_info[1] and guards the
+// combine that follows (no host round trip; the flag is read with the next cycle's status).
+static lsba_status cycle_solve_async(lsba_ctx c, int k, int gmres) {
+  switch (c->b) {
+#define CASE(B) case B: return cycle_end_t<B>(c, k, gmres, 0, 1, c->d_info + 1);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return LSBA_E_ARG;
+  }
 }
 
 static lsba_status cycle_solve(lsba_ctx c, int k, int gmres, int happy, int* singular, int upd = 1) {
   lsba_status st;
   switch (c->b) {
-#define CASE(B) case B: st = cycle_end_t<B>(c, k, gmres, happy, upd); break;
+#define CASE(B) case B: st = cycle_end_t<B>(c, k, gmres, happy, upd, c->d_info); break;
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
 #undef CASE
@@ -801,6 +814,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   }
   TRY(set_identity(c));                   // C_acc = I
   int m_cur = m;
+  bool sing_pending = false;   // a guarded combine was enqueued; its flag is read later
   CycleCtl cc;
   info->outcome = LSBA_MAX_RESTARTS;
   bool finished = false;
@@ -827,6 +841,13 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     }
     TRY(join_update(c));
     TRY(read_status(c, nullptr, &cc));
+    if (sing_pending && c->h_info[1]) {                     // last cycle end was singular:
+      fail(c, LSBA_OK, "projected system singular at cycle end");   // its combine no-op'd,
+      info->cycles = cycle - 1;                             // this cycle ran on stale data
+      info->outcome = LSBA_DEAD;
+      break;
+    }
+    sing_pending = false;
     if (cc.why == 5) { info->outcome = LSBA_DEAD; break; }   // IO flagged (R4)
     int k_used = cc.k_used;
     info->iterations += k_used;
@@ -861,6 +882,15 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       info->cond_restarts++;
     }
     if (k_used == 0) { info->outcome = LSBA_DEAD; break; }
+    if (cc.why != 2) {
+      // X += V_k Xi C_acc ;  U = V_{k+1} [M; -H_{k+1,k}] -> slot 0,
+      // enqueued behind the projected solve without a host round trip (guarded by its flag)
+      TRY(cycle_solve_async(c, k_used, gmres));               // Xi, M, cos; C_acc <- cos C_acc
+      TRY(project(c, slotp(c, 0), c->slot_stride, k_used, c->d_Y, X, X, k_used + 1, c->d_Z, slotp(c, 0),
+                  c->d_info + 1, LSBA_K_COMBINE));
+      sing_pending = true;
+      continue;
+    }
     int sing = 0;
     TRY(cycle_solve(c, k_used, gmres, 0, &sing));            // Xi, M, cos; C_acc <- cos C_acc
     if (sing) {
@@ -868,7 +898,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       info->outcome = LSBA_DEAD;
       break;
     }
-    if (cc.why == 2) {
+    {
       // X += V_k Xi C_acc, then confirm with the explicit residual (R19)
       TRY(project(c, slotp(c, 0), c->slot_stride, k_used, c->d_Y, X, X, 0, nullptr, nullptr, nullptr,
                   LSBA_K_COMBINE));
@@ -884,9 +914,14 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       TRY(set_identity(c));                                  // restart from the true residual
       continue;
     }
-    // X += V_k Xi C_acc ;  U = V_{k+1} [M; -H_{k+1,k}] -> slot 0
-    TRY(project(c, slotp(c, 0), c->slot_stride, k_used, c->d_Y, X, X, k_used + 1, c->d_Z, slotp(c, 0),
-                nullptr, LSBA_K_COMBINE));
+  }
+  if (sing_pending) {                                        // the last cycle's combine
+    CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->h_info[1]) {
+      fail(c, LSBA_OK, "projected system singular at cycle end");
+      info->outcome = LSBA_DEAD;
+    }
   }
   info->m_final = m_cur;
   if (!(info->outcome == LSBA_CONVERGED)) {

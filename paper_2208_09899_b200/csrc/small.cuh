@@ -557,14 +557,27 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
 template <int B>
 __global__ void __launch_bounds__(512)
 k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double* __restrict__ Y,
-            double* __restrict__ Z, int* __restrict__ info) {
-  extern __shared__ double Xi[];             // kb x B, column-major (ld kb)
+            double* __restrict__ Z, int* __restrict__ info, int stage_r) {
+  extern __shared__ double Xi[];             // kb x B, column-major (ld kb) [+ kb x kb R copy]
   __shared__ double Tb[B * B], HtH[B * B], cosC[B * B];
   __shared__ int sing_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int ldH = st.ldH, kb = k * B;
   const bool use_fom = happy || !gmres;
   if (tid == 0) sing_s = 0;
+  // the R factor of Hbar: staged into shared memory when the launcher gave room for it (one
+  // coalesced pass instead of two dependent global round trips per block row below)
+  const double* Rm = st.Rfac;
+  int ldR = ldH;
+  if (stage_r) {
+    double* Rsm = Xi + (size_t)kb * B;
+    for (int e = tid; e < kb * kb; e += nt) {
+      const int r = e % kb, c = e / kb;
+      Rsm[e] = (r <= c) ? st.Rfac[r + (size_t)c * ldH] : 0.0;
+    }
+    Rm = Rsm;
+    ldR = kb;
+  }
   // rhs -> Xi
   for (int e = tid; e < kb * B; e += nt) {
     const int r = e % kb, c = e / kb;
@@ -582,7 +595,7 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
         double a;
         if (lane < B) {
           a = (use_fom && j == k - 1) ? st.htil[(size_t)(k - 1) * B * B + r + lane * B]
-                                     : st.Rfac[(j * B + r) + (size_t)(j * B + lane) * ldH];
+                                     : Rm[(j * B + r) + (size_t)(j * B + lane) * ldR];
         } else if (lane < 2 * B) {
           a = Xi[(j * B + r) + (size_t)(lane - B) * kb];
         } else {
@@ -604,7 +617,7 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
       const int r = e % rows, c = e / rows;
       double t = 0.0;
 #pragma unroll
-      for (int q = 0; q < B; ++q) t += st.Rfac[r + (size_t)(j * B + q) * ldH] * Xi[(j * B + q) + (size_t)c * kb];
+      for (int q = 0; q < B; ++q) t += Rm[r + (size_t)(j * B + q) * ldR] * Xi[(j * B + q) + (size_t)c * kb];
       Xi[r + (size_t)c * kb] -= t;
     }
     __syncthreads();

@@ -41,13 +41,16 @@ template <>
 cudaError_t launch_cycle_end<LSBA_B>(const SmallState2& st, int k, int gmres, int happy, int upd,
                                      double* Y, double* Z, int* info, cudaStream_t stream) {
   constexpr int B = LSBA_B;
-  const size_t smem = sizeof(double) * (size_t)k * B * B;
+  const size_t kb = (size_t)k * B;
+  size_t smem = sizeof(double) * kb * B;
+  const int stage_r = (smem + sizeof(double) * kb * kb <= 200 * 1024) ? 1 : 0;
+  if (stage_r) smem += sizeof(double) * kb * kb;
   auto fn = k_cycle_end<B>;
   if (smem > 32 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  fn<<<1, 32 * (B > 8 ? B : 8), smem, stream>>>(st, k, gmres, happy, upd, Y, Z, info);
+  fn<<<1, 32 * (B > 8 ? B : 8), smem, stream>>>(st, k, gmres, happy, upd, Y, Z, info, stage_r);
   return cudaGetLastError();
 }
 
