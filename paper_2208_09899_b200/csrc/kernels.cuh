@@ -364,6 +364,48 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
   double o0[S], o1[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) { o0[c] = 0.0; o1[c] = 0.0; }
+  if (J1 == 0 && !base0) {
+    // the step projection (one output): blocks in batches of 4 so that a thread has four
+    // rows in flight.  Every thread reads only its own row of every block before writing that
+    // row (the output may be the last input block), so the read-only path is safe here.
+    int j = 0;
+    for (; j + 4 <= J0; j += 4) {
+      double x[4][S];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_row<S>(X + (size_t)(j + u) * xstride + (size_t)i * S, x[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if constexpr (GLOBAL) {
+          const double cj = c0[j + u];
+#pragma unroll
+          for (int c = 0; c < S; ++c) o0[c] = fma(x[u][c], cj, o0[c]);
+        } else {
+          const double* cj = c0 + (size_t)(j + u) * S * S;
+#pragma unroll
+          for (int a = 0; a < S; ++a)
+#pragma unroll
+            for (int c = 0; c < S; ++c) o0[c] = fma(x[u][a], cj[a * S + c], o0[c]);
+        }
+      }
+    }
+    for (; j < J0; ++j) {
+      double x[S];
+      load_row<S>(X + (size_t)j * xstride + (size_t)i * S, x);
+      if constexpr (GLOBAL) {
+        const double cj = c0[j];
+#pragma unroll
+        for (int c = 0; c < S; ++c) o0[c] = fma(x[c], cj, o0[c]);
+      } else {
+        const double* cj = c0 + (size_t)j * S * S;
+#pragma unroll
+        for (int a = 0; a < S; ++a)
+#pragma unroll
+          for (int c = 0; c < S; ++c) o0[c] = fma(x[a], cj[a * S + c], o0[c]);
+      }
+    }
+    store_row<S>(out0 + (size_t)i * S, o0);
+    return;
+  }
   const int Jmax = max(J0, J1);
   for (int j = 0; j < Jmax; ++j) {
     double x[S];
