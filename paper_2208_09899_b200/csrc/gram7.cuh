@@ -268,6 +268,102 @@ k_gram_v7(GramArgs g, GramFuse f) {
   else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
 }
 
+// ------------------------------------------------------------------------------------------
+// Global block inner product (Table 1): g_j = (1/s) tr(X_j^T Y) = (1/s) sum of
+// the elementwise products of two n x s blocks, for the J blocks of a step in ONE pass.  Each
+// thread streams 16-byte pieces of Y and of up to JM blocks (the grid sweeps one window of the
+// flattened blocks), keeping JM dot-product partials in registers; blocks beyond JM run as
+// further passes over Y.  CTA partials: warp shuffle + ordered warp sum; cross-CTA: the same
+// deterministic two-level ticketed tree as k_gram_v7; the small step can be fused the same way.
+// Inputs are basis slots (rows padded to kRowPad with zero rows); S even.
+// ------------------------------------------------------------------------------------------
+constexpr int kGlJM = 8;
+
+template <int S>
+__global__ void __launch_bounds__(256, 3)
+k_gram_gl2(GramArgs g, GramFuse f) {
+  static_assert(S % 2 == 0, "gl2: even s");
+  if (g.active && *g.active == 0) {
+    if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;
+    return;
+  }
+  __shared__ double red[8][kGlJM];
+  __shared__ double gsm[4 * kGlJM];     // fused small step (b = 1): (k+1) <= ... handled below
+  __shared__ unsigned ticket;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int J = g.J;
+  const long npad = ((long)g.n + kRowPad - 1) / kRowPad * kRowPad;
+  const long N2 = npad * S / 2;                       // double2 per block
+  const long gstride = (long)gridDim.x * blockDim.x;
+  const int P = gridDim.x;
+  const int ngroups = (P + kGramGroup - 1) / kGramGroup;
+  const int grpi = blockIdx.x / kGramGroup;
+  const int gsize = min(kGramGroup, P - grpi * kGramGroup);
+  const double2* Y2 = reinterpret_cast<const double2*>(g.Y);
+  for (int j0 = 0; j0 < J; j0 += kGlJM) {
+    const int nb = min(kGlJM, J - j0);
+    double acc[kGlJM];
+#pragma unroll
+    for (int q = 0; q < kGlJM; ++q) acc[q] = 0.0;
+    for (long e = (long)blockIdx.x * blockDim.x + tid; e < N2; e += gstride) {
+      const double2 y0 = __ldg(Y2 + e);
+      double2 x0[kGlJM];
+#pragma unroll
+      for (int q = 0; q < kGlJM; ++q) {
+        const double2* Xq = reinterpret_cast<const double2*>(g.X + (size_t)(j0 + q) * g.xstride);
+        x0[q] = (q < nb) ? __ldg(Xq + e) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < kGlJM; ++q) {
+        acc[q] = fma(x0[q].x, y0.x, acc[q]);
+        acc[q] = fma(x0[q].y, y0.y, acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kGlJM; ++q) {
+      const double v = warp_sum(acc[q]);
+      if (lane == 0) red[warp][q] = v;
+    }
+    __syncthreads();
+    if (tid < nb) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w][tid];
+      g.part[(size_t)blockIdx.x * J + j0 + tid] = t;
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(&g.tickets[grpi], 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(gsize - 1)) return;
+  __threadfence();
+  for (int e = tid; e < J; e += blockDim.x) {
+    double s2 = 0.0;
+    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * J + e);
+    g.gpart[(size_t)grpi * J + e] = s2;
+  }
+  if (tid == 0) g.tickets[grpi] = 0u;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(&g.tickets[ngroups], 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(ngroups - 1)) return;
+  __threadfence();
+  for (int e = tid; e < J; e += blockDim.x) {
+    double s2 = 0.0;
+    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * J + e);
+    g.G[e] = s2 * (1.0 / S);                          // Table 1: (1/s) tr(X^T Y)
+  }
+  if (tid == 0) g.tickets[ngroups] = 0u;
+  (void)gsm;
+  if (!f.on) return;
+  __threadfence();
+  __syncthreads();
+  extern __shared__ double gl2_dyn[];                 // (k+1) doubles for the small step
+  step_coef_body<1>(f.st, g.G, gl2_dyn, f.k, f.prm, sqrt((double)S));
+}
+
 // launch geometry of k_gram_v7: grid (a multiple of the pass count) and dynamic smem bytes
 template <int S, int GMAX>
 struct G7Launch {

@@ -511,6 +511,38 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
   } else {
     if (Vk) TRY(spmm_t<S>(c, Vk, Y, active));
     TRY(wait_update(c));
+    if constexpr (S % 2 == 0) {
+      if (gl && c->variant == 0 && in_basis(c, X) && in_basis(c, Y) && c->d_tickets) {
+        // streaming global Gram (gram7.cuh), small step fused on one rank
+        const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+        LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
+        if (c->n > 0) {
+          GramArgs a;
+          a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+          a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride;
+          a.J = J; a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
+          a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+          a.active = active;
+          GramFuse f{};
+          if (coef_k >= 0 && coef_fused && c->nranks == 1) {
+            f.on = 1;
+            f.st = c->st;
+            f.k = coef_k;
+            f.prm = prm ? *prm : CycleParams{};
+            *coef_fused = true;
+          }
+          const int grid = std::max(1, std::min(3 * c->n_sms, cdiv(cdiv((long)c->slot, 2), 256)));
+          k_gram_gl2<S><<<grid, 256, sizeof(double) * (J + 1), c->stream>>>(a, f);
+          CKL();
+        } else {
+          CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+          if (coef_fused) *coef_fused = false;
+        }
+        if (c->nranks > 1)
+          CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+        return LSBA_OK;
+      }
+    }
     const int gx = gl ? J : J * (S / GramTA<S>::value);
     int P = std::max(1, std::min(cdiv(std::max(c->n, 1), 256), cdiv(kGramCtas, gx)));
     if ((size_t)P * E > c->part_cap) P = std::max(1, (int)(c->part_cap / E));
