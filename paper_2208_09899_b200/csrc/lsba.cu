@@ -700,11 +700,15 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
 // the device has decided step k - kLookahead (polling the mapped progress word).  Returns
 // false if the device already ended the cycle.
 constexpr int kLookahead = 3;
+// With P > 1 ranks every speculative step still contains its allreduce and halo exchange, and
+// the count of collectives must match across ranks, so there the host only paces (it never
+// stops early: which step a rank's host is at when its device ends the cycle is timing).
 static bool throttle(lsba_ctx c, int k) {
-  if (k <= kLookahead) return c->h_prog[1] != 0 || c->h_prog[0] < 0;
+  const bool may_stop = (c->nranks == 1);
+  if (k <= kLookahead) return !may_stop || c->h_prog[1] != 0 || c->h_prog[0] < 0;
   for (;;) {
     const int done = c->h_prog[0], act = c->h_prog[1];
-    if (done >= 0 && act == 0) return false;
+    if (done >= 0 && act == 0) return !may_stop;
     if (done >= k - kLookahead) return true;
     if (cudaStreamQuery(c->stream) == cudaSuccess) return true;   // (device drained: no stall)
   }
