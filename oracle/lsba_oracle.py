@@ -310,6 +310,115 @@ class PipArnoldi:
 
 
 # --------------------------------------------------------------------------------------
+# BMGS-CWY / BMGS-ICWY-Arnoldi, Alg 6, Sec 3.3 — the NEXT skeleton (§8(f) f1)
+# --------------------------------------------------------------------------------------
+
+
+class CwyArnoldi:
+    """Alg 6 as a resumable object with the same interface as PipArnoldi.
+
+    Alg 6 lags the normalisation by one iteration: loop iteration i >= 2 applies A to the
+    unnormalised U (= V_i H_{i,i-1}), computes ONE block inner product
+    [Y Z; Omega Pt] = <[V_1..V_{i-1} U], [U W]>, H_{i,i-1} = chol(Omega),
+    P = H_{i,i-1}^{-*} Pt, the new block column of T (CWY: -T Y H^{-1}; ICWY: Y H^{-1}), the
+    column H_{1:i,i} = T^* [Z; P] H^{-1} (CWY) or T^{-*} [Z; P] H^{-1} (ICWY), V_i = U H^{-1}
+    and U = W H^{-1} - V_i-stack H_{1:i,i}.  Iteration 1 (W = A V_1,
+    H_11 = <V_1, W>, U = W - V_1 H_11) is done by ``begin`` after IO, so ``step`` number k is
+    Alg 6 iteration k+1: it completes Hessenberg column k (its subdiagonal H_{k+1,k}) and
+    returns V_{k+1}.  Reading R24: Alg 6 line 15 writes V_{k-1} H_{1:k,k}; the k blocks of
+    H_{1:k,k} need V_1..V_k (V_k set on line 14 of the same iteration), so it is read as the
+    k-block stack.  Per cycle: m+1 A-applications and m+2 syncs (Table 1 PAPER.md:109-118;
+    tridiag table).  Global inner product: scalars, chol = sqrt (R3)."""
+
+    def __init__(self, A, ip: str, m_max: int, s: int, inverse: bool = False):
+        self.A, self.ip, self.m_max, self.s = A, ip, m_max, s
+        self.inverse = inverse                       # False: CWY, True: ICWY
+        self.b = s if ip == "cl" else 1
+        self.V: list[np.ndarray] = []
+        self.Hbar = np.zeros(((m_max + 1) * self.b, m_max * self.b))
+        self.T = np.eye((m_max + 1) * self.b)
+        self.beta = None
+        self.U = None
+        self.k = 0
+
+    def _ip(self, Xs, Y):
+        if self.ip == "cl":
+            return ip_cl(Xs, Y)
+        return ip_gl(Xs, Y).reshape(-1, 1)
+
+    def _mul(self, X, C):
+        return X @ C if self.ip == "cl" else X * C[0, 0]
+
+    def begin(self, B):
+        """IO(B) (line 2), U = V_1 (line 3), and loop iteration 1 (lines 5-8)."""
+        b = self.b
+        if self.ip == "cl":
+            V1, beta, flag = io_cl(B)
+        else:
+            V1, beta, flag = io_gl(B)
+            beta = np.array([[beta]])
+        self.beta = beta
+        self.Hbar[:] = 0.0
+        self.T = np.eye((self.m_max + 1) * b)
+        self.k = 0
+        if flag:
+            self.V = []
+            return flag
+        self.V = [V1]
+        W = spmm(*self.A, V1)                                  # line 5
+        H11 = self._ip([V1], W)                                # line 7 (its own sync)
+        self.Hbar[:b, :b] = H11
+        self.U = W - self._mul(V1, H11)                        # line 8
+        return False
+
+    def step(self, force_flag: bool = False) -> StepResult:
+        """Alg 6 iteration k+1 for Arnoldi step k = len(V)."""
+        b, k = self.b, len(self.V)
+        Hcol = self.Hbar[: k * b, (k - 1) * b: k * b].copy()
+        U = self.U
+        W = spmm(*self.A, U)                                   # line 5
+        G = self._ip(list(self.V) + [U], np.concatenate([U, W], axis=1)) if self.ip == "cl" else None
+        if self.ip == "cl":
+            s = self.s
+            Y, Z = G[: k * s, :s], G[: k * s, s:]
+            Omega, Pt = G[k * s:, :s], G[k * s:, s:]           # line 10: ONE block inner product
+            R, flag = chol_flag(Omega)                         # line 11
+        else:
+            gU = ip_gl(list(self.V) + [U], U)
+            gW = ip_gl(list(self.V) + [U], W)
+            Y, Z = gU[:k].reshape(-1, 1), gW[:k].reshape(-1, 1)
+            Omega, Pt = gU[k], gW[k]
+            flag = not (Omega > 0.0) or not math.isfinite(Omega)
+            R = np.array([[math.sqrt(Omega)]]) if not flag else np.array([[float("nan")]])
+        flag = flag or force_flag
+        if flag:
+            return StepResult(Hcol, R if self.ip == "cl" else float("nan"), None, True, W)
+        Rinv = right_trsm_upper(np.eye(b), R)                  # H_{k+1,k}^{-1}
+        P = np.linalg.solve(R.T, Pt) if self.ip == "cl" else np.array([[Pt / R[0, 0]]])   # line 12
+        T = self.T
+        YR = Y @ Rinv
+        if self.inverse:
+            T[: k * b, k * b:(k + 1) * b] = YR                 # line 13 (ICWY)
+        else:
+            T[: k * b, k * b:(k + 1) * b] = -T[: k * b, : k * b] @ YR   # line 13 (CWY)
+        ZP = np.vstack([Z, P]) @ Rinv
+        Tk = T[:(k + 1) * b, :(k + 1) * b]
+        Hnext = np.linalg.solve(Tk.T, ZP) if self.inverse else Tk.T @ ZP   # line 14
+        Vn = self._mul(U, Rinv)                                # line 16: V_{k+1} = U H^{-1}
+        self.Hbar[k * b:(k + 1) * b, (k - 1) * b: k * b] = R
+        if k < self.m_max:
+            self.Hbar[:(k + 1) * b, k * b:(k + 1) * b] = Hnext
+        self.V.append(Vn)
+        # line 17: U = W H^{-1} - [V_1..V_{k+1}] H_{1:k+1,k+1}  (reading R24)
+        Un = self._mul(W, Rinv)
+        for j, Vj in enumerate(self.V):
+            Un = Un - self._mul(Vj, Hnext[j * b:(j + 1) * b])
+        self.U = Un
+        self.k = k
+        return StepResult(Hcol, R if self.ip == "cl" else float(R[0, 0]), Vn, False, W)
+
+
+# --------------------------------------------------------------------------------------
 # BMGS-Arnoldi, Alg 2 (PAPER.md:164-178) — independent cross-check only (pin P5)
 # --------------------------------------------------------------------------------------
 
@@ -427,19 +536,22 @@ class SolveInfo:
     cycle_lengths: list = field(default_factory=list)  # k_used per cycle
     history: list = field(default_factory=list)        # (cycle, k, res_est/normB, kappa_F)
 
-    # Paper accounting (PAPER.md:650 tables; pin P14): sync = iterations + cycles,
-    # A-ct = iterations, V-ct = 3 * iterations for BCGS-PIP.
+    skel: str = "pip"
+
+    # Paper accounting (PAPER.md:650 tables; pin P14): BCGS-PIP: sync = iterations + cycles,
+    # A-ct = iterations, V-ct = 3 iterations; BMGS-(I)CWY: one
+    # more A-application, sync and block evaluation per cycle (the lagged normalisation).
     @property
     def syncs(self):
-        return self.iterations + self.cycles
+        return self.iterations + (2 if self.skel != "pip" else 1) * self.cycles
 
     @property
     def matvecs(self):
-        return self.iterations
+        return self.iterations + (self.cycles if self.skel != "pip" else 0)
 
     @property
     def basis_evals(self):
-        return 3 * self.iterations
+        return 3 * self.iterations + (self.cycles if self.skel != "pip" else 0)
 
     @property
     def restarts(self):
@@ -449,8 +561,10 @@ class SolveInfo:
 def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
           ip: str = "cl", mod: str = "gmres", cond_threshold: float = float("inf"),
           stop_on: str = "residual", X_star=None, force_flag_at=None,
-          happy_check: bool = True, confirm_true: bool = True, record_kappa: bool = False):
-    """Restarted modified BFOM/BGMRES with BCGS-PIP-Arnoldi and adaptive restart.
+          happy_check: bool = True, confirm_true: bool = True, record_kappa: bool = False,
+          skel: str = "pip"):
+    """Restarted modified BFOM/BGMRES with BCGS-PIP-Arnoldi (skel='pip', Alg 3) or
+    BMGS-CWY / BMGS-ICWY-Arnoldi (skel='cwy' / 'icwy', Alg 6) and adaptive restart.
 
     Follows SURVEY.md 8(c) "Step list" literally; readings cited inline.  ``A`` is the CSR
     triple (row_ptr, col_idx, vals).  ``stop_on='error'`` (test-only, pin P13) stops on
@@ -467,9 +581,14 @@ def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
         return np.zeros_like(B), SolveInfo(outcome=CONVERGED, true_relres=0.0, m_final=m)
     U = B.copy() if X0 is None else B - spmm(row_ptr, col_idx, vals, X)       # R13
     Cacc = np.eye(b)
-    info = SolveInfo()
+    info = SolveInfo(skel=skel)
     m_cur = m
-    arn = PipArnoldi(A, ip, m, s)
+    if skel == "pip":
+        arn = PipArnoldi(A, ip, m, s)
+    elif skel in ("cwy", "icwy"):
+        arn = CwyArnoldi(A, ip, m, s, inverse=(skel == "icwy"))
+    else:
+        raise ValueError(f"unknown skeleton {skel!r}")
     forced_done = False
 
     def true_relres(Xc):

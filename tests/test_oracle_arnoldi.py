@@ -383,3 +383,75 @@ def test_dead_when_io_flags():
     assert info.outcome == O.DEAD and info.iterations == 0
     X, info = O.solve(A, np.zeros((10, 2)), m=3, tol=1e-8)     # B = 0: X = 0 exactly
     assert info.outcome == O.CONVERGED and not X.any()
+
+
+# ---------------------------------------------------------------- BMGS-CWY / BMGS-ICWY (Alg 6)
+@pytest.mark.parametrize("skel", ["cwy", "icwy"])
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+def test_cwy_equals_bmgs_in_exact_arithmetic(ip, skel):
+    """Alg 6 builds the same Arnoldi decomposition as BMGS-Arnoldi (Alg 2) in exact arithmetic
+    (PAPER.md:316-320): on a well-conditioned case H and the basis agree to rounding."""
+    A, B = tridiag(100), tridiag_rhs(100)
+    V, H, beta = O.bmgs_arnoldi(A, B, 10, ip)
+    arn = O.CwyArnoldi(A, ip, 10, 2, inverse=(skel == "icwy"))
+    assert not arn.begin(B)
+    for _ in range(10):
+        assert not arn.step().flag
+    assert np.linalg.norm(arn.Hbar - H) <= 1e-10 * np.linalg.norm(H)
+    for v, vo in zip(arn.V, V):
+        assert np.linalg.norm(v - vo) <= 1e-10 * np.linalg.norm(vo)
+    assert np.allclose(arn.beta, beta, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("skel", ["cwy", "icwy"])
+def test_cwy_arnoldi_relation_and_orthogonality(skel):
+    """A V_k = V_{k+1} Hbar_k and small LOO for Alg 6 on a twin."""
+    from lsba_inputs import make_twin
+    p = make_twin(3)
+    A = (p.row_ptr, p.col_idx, p.vals)
+    arn = O.CwyArnoldi(A, "cl", 8, p.s, inverse=(skel == "icwy"))
+    assert not arn.begin(p.B)
+    for _ in range(8):
+        assert not arn.step().flag
+    AV = np.concatenate([O.spmm(*A, v) for v in arn.V[:8]], axis=1)
+    VH = np.concatenate(arn.V, axis=1) @ arn.Hbar
+    assert np.linalg.norm(AV - VH) <= 1e-12 * np.linalg.norm(AV)
+    assert O.loss_of_orthogonality(arn.V, "cl") <= 1e-12
+
+
+def test_paper_tridiag1000_cwy_counts(golden_dir):
+    """Appendix tridiag table: gl-BMGS-CWY/ICWY-FOM reproduce
+    9 cycles / 621 iterations / A-ct 630 / V-ct 1872 / sync 639 exactly under the paper's error
+    measure; cl-BMGS-CWY/ICWY-FOM finish in 2 cycles with no NaN-flag."""
+    tab = json.load(open(os.path.join(golden_dir, "paper_tridiag_table3.json")))["rows"]
+    n = 1000
+    A, B = tridiag(n), tridiag_rhs(n)
+    Xs = np.linalg.solve(dense(A, n), B)
+    for skel, key in (("cwy", "BMGSCWY"), ("icwy", "BMGSICWY")):
+        X, info = O.solve(A, B, m=70, tol=1e-10, max_restarts=100, ip="gl", mod="fom",
+                          stop_on="error", X_star=Xs, skel=skel)
+        row = tab[f"gl-{key}-gl-FOM"]
+        assert (info.cycles, info.iterations, info.matvecs, info.basis_evals, info.syncs) == \
+            (row["cycles"], row["iterations"], row["A_ct"], row["V_ct"], row["sync_ct"])
+        X, info = O.solve(A, B, m=70, tol=1e-10, max_restarts=100, ip="cl", mod="fom",
+                          stop_on="error", X_star=Xs, skel=skel)
+        row = tab[f"cl-{key}-CholQR-FOM"]
+        assert info.outcome == O.CONVERGED and info.cycles == row["cycles"] and info.nan_flags == 0
+        assert abs(info.iterations - row["iterations"]) <= 3
+        assert info.matvecs == info.iterations + info.cycles and info.syncs == info.iterations + 2 * info.cycles
+        X, info = O.solve(A, B, m=70, tol=1e-10, max_restarts=100, ip="cl", mod="fom", skel=skel)
+        assert info.outcome == O.CONVERGED and info.cycles == row["cycles"] and info.nan_flags == 0
+
+
+@pytest.mark.parametrize("skel", ["cwy", "icwy"])
+@pytest.mark.parametrize("ip,mod", [("cl", "gmres"), ("gl", "gmres"), ("cl", "fom")])
+def test_cwy_tiny_config_vs_dense_lu(ip, mod, skel):
+    """Restarted solve with Alg 6 on the tiny config: converged, error vs a dense LU within
+    kappa(A) tol."""
+    from lsba_inputs import make_twin
+    p = make_twin(1)
+    A = (p.row_ptr, p.col_idx, p.vals)
+    X, info = O.solve(A, p.B, m=p.m, tol=p.tol, max_restarts=p.max_restarts, ip=ip, mod=mod, skel=skel)
+    assert info.outcome == O.CONVERGED and info.true_relres <= p.tol
+    Xs = np.linalg.solve(dense(A, p.n), p.B)
+    assert np.linalg.norm(X - Xs) <= 100 * p.tol * np.linalg.norm(Xs)
