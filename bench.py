@@ -47,11 +47,17 @@ def roof_cycle_extra(n, s, k_used):
     return 8.0 * n * s * (k_used + 7)
 
 
-def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks):
-    """sum_steps ROOF(k) + sum_cycles 8ns(k_used+7), from the solver's counters
-    (gram_blocks = sum over accepted steps of k+1)."""
-    return (iters * (12.0 * nnz + 4.0 * (n + 1) + 8.0 * n * s) + 16.0 * n * s * gram_blocks
-            + 8.0 * n * s * (iters + 7 * cycles))
+def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks, skel="pip"):
+    """sum_steps ROOF(k) + per-cycle bytes, from the solver's counters (gram_blocks = sum over
+    accepted steps of k+1).  BCGS-PIP: ROOF(k) = A + 8ns(2k+3), + 8ns(k_used+7) per cycle.
+    BMGS-(I)CWY (Alg 6): per step the SpMM of U (2 blocks), the Gram over [V_1..V_k U] and W
+    (k+2) and the two-output pass (k+2 reads, 2 writes): A + 8ns(2k+8); per cycle IO (3), loop
+    iteration 1 (7) and the cycle end (k_used+4): 8ns(k_used+14)."""
+    A = 12.0 * nnz + 4.0 * (n + 1)
+    blk = 8.0 * n * s
+    if skel == "pip":
+        return iters * (A + blk) + 2 * blk * gram_blocks + blk * (iters + 7 * cycles)
+    return iters * (A + 6 * blk) + 2 * blk * gram_blocks + blk * (iters + 14 * cycles)
 
 
 def cycle_bytes(nnz, n, s, m):
@@ -214,6 +220,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
+    ap.add_argument("--skel", default="pip", choices=["pip", "cwy", "icwy"],
+                    help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3) or BMGS-CWY / -ICWY (Alg 6)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
 
@@ -243,6 +251,7 @@ def main():
                     row_end=wl["row_end"], rank=rank, nranks=world, nccl_id=nccl_id, device=local,
                     stream=stream.cuda_stream)
     L.lsba_set_kernel_variant(ctx.ctx, args.variant)
+    L.lsba_set_skeleton(ctx.ctx, args.skel)
     B = torch.from_numpy(wl["B"]).cuda()
     X = torch.zeros_like(B)
     m, tol, s = wl["m"], wl["tol"], wl["s"]
@@ -256,7 +265,7 @@ def main():
 
     # warm-up: W cycles (one solve call), not timed
     if args.warmup:
-        L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1, ip=args.ip)
+        L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1, ip=args.ip, skel=args.skel)
     barrier()
 
     # configs 1 and 4 converge in a few cycles: a bench step is then one full solve from X0 = 0
@@ -274,7 +283,7 @@ def main():
             if full_solve:
                 X.zero_()
             inf = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, 200 if full_solve else args.steps - 1,
-                                      ip=args.ip)
+                                      ip=args.ip, skel=args.skel)
             it += inf.iterations
             cy += inf.cycles
             nl += inf.kernel_launches
@@ -305,7 +314,7 @@ def main():
         assert cycles == args.steps, f"expected {args.steps} cycles, ran {cycles} (outcome {info.outcome})"
     # whole-job algorithmic bytes (global problem): sum over accepted steps of ROOF(k) =
     # iters (A + 8ns) + 16ns sum(k+1), plus 8ns(k_used + 7) per cycle
-    total_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, iters, cycles, timed_cycles.gram_blocks)
+    total_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, iters, cycles, timed_cycles.gram_blocks, args.skel)
     gbs = total_bytes / (ms / 1e3) / 1e9
     steps_per_s = iters / (ms / 1e3)
     peak, peak_kind = measured_peaks()
@@ -345,7 +354,7 @@ def main():
             t = torch.tensor([dt], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, e2e_iters, e2e_cycles, e2e_gb)
+        e2e_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, e2e_iters, e2e_cycles, e2e_gb, args.skel)
         e2e = {"value": e2e_bytes / dt / 1e9, "unit": "GB/s", "block_steps_per_s": e2e_iters / dt,
                "h2d_bytes_per_step": 2 * n_loc * s * 8 * world, "d2h_bytes_per_step": n_loc * s * 8 * world,
                "api": "lsba_solve_host (" + ("one full solve per step, X0 = 0" if full_solve
@@ -369,7 +378,8 @@ def main():
             "block_steps_per_s": steps_per_s, "ms_per_block_step": ms / iters,
             "pct_roofline": {"of_measured_hbm": gbs / (peak * world), "of_8TBps_nominal": gbs / (8000.0 * world)},
             "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
-                       "method": f"{args.ip}-BGMRES, BCGS-PIP skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO"),
+                       "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY"}[args.skel]
+                                 + " skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO"),
                        "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
                                       f"{iters / args.steps:.1f} block steps)") if full_solve
                                      else f"restart cycle = IO + {m} block steps + cycle end",

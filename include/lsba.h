@@ -47,8 +47,10 @@ typedef enum {
 /* Table 1. */
 typedef enum { LSBA_IP_CLASSICAL = 0, LSBA_IP_GLOBAL = 1 } lsba_ip;
 
-/* Gram-Schmidt skeleton (Table 2).  Only BCGS-PIP (Alg 3) is built. */
-typedef enum { LSBA_SKEL_BCGS_PIP = 0 } lsba_skel;
+/* Gram-Schmidt skeleton (Table 2): BCGS-PIP (Alg 3) and
+ * BMGS-CWY / BMGS-ICWY (Alg 6; one block inner product per iteration with the
+ * normalisation lagged by one iteration: m+1 A-applications and m+2 syncs per cycle). */
+typedef enum { LSBA_SKEL_BCGS_PIP = 0, LSBA_SKEL_BMGS_CWY = 1, LSBA_SKEL_BMGS_ICWY = 2 } lsba_skel;
 
 /* SPEC.md:327 outcome of a solve. */
 typedef enum { LSBA_CONVERGED = 0, LSBA_MAX_RESTARTS = 1, LSBA_DEAD = 2 } lsba_outcome;
@@ -64,8 +66,9 @@ typedef struct {
   int32_t pad_;
 } lsba_step_info;
 
-/* Result of a solve.  Counters follow the paper's accounting (PAPER.md:650 tables):
- * syncs = iterations + cycles, matvecs (A-ct) = iterations, basis_evals (V-ct) = 3 iterations. */
+/* Result of a solve.  Counters follow the paper's accounting (PAPER.md:650 tables): BCGS-PIP
+ * syncs = iterations + cycles, matvecs (A-ct) = iterations, basis_evals (V-ct) = 3 iterations;
+ * BMGS-(I)CWY one more of each per cycle. */
 typedef struct {
   int32_t outcome;            /* lsba_outcome                                             */
   int32_t cycles;             /* restart cycles run                                       */
@@ -137,8 +140,8 @@ lsba_status lsba_copy_basis_block(lsba_ctx ctx, int32_t j, double* dst_dev);
 
 /* ---------------------------------------------------------------- solvers */
 
-/* Restarted BGMRES / BFOM (modification M of PAPER.md:191 / M = 0) with BCGS-PIP and the
- * adaptive restart of Sec 4 (NaN-flag -> restart from the last safe block, m <- k-1;
+/* Restarted BGMRES / BFOM (modification M of PAPER.md:191 / M = 0) with the skeleton `skel`
+ * and the adaptive restart of Sec 4 (NaN-flag -> restart from the last safe block, m <- k-1;
  * PAPER.md:405) plus cond_threshold (kappa_F trigger, +inf = off; reading R8).
  *   B_dev : n_local x s (device);  X_dev : in X0, out X (device)
  *   m <= m_max; tol > 0 relative to ||B||_F; at most max_restarts+1 cycles.
@@ -171,6 +174,11 @@ lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t 
 
 /* Fault injection: make the Cholesky of step k_flag report a NaN-flag once (0 = off). */
 lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
+/* Skeleton of the step API (lsba_arnoldi_begin / lsba_block_arnoldi_step) and of
+ * lsba_solve_host (default BCGS-PIP); the *_solve calls take theirs as an argument.
+ * With BMGS-(I)CWY, lsba_arnoldi_begin also runs Alg 6's first loop iteration, and step k
+ * (its iteration k+1) completes Hessenberg column k and forms V_{k+1}. */
+lsba_status lsba_set_skeleton(lsba_ctx ctx, lsba_skel skel);
 /* Kernel implementation choice (classical inner product): 0 = auto (standalone SpMM +
  * latency-tuned streaming tensor-core Gram v7 + projection: DMMA for s in {8,16}, DFMA
  * otherwise), 1 = plain DFMA kernels, 2 = SpMM fused into the tensor-core Gram pass (gather

@@ -16,6 +16,8 @@ from ._lib import (  # noqa: F401
     LSBA_IP_CLASSICAL,
     LSBA_IP_GLOBAL,
     LSBA_SKEL_BCGS_PIP,
+    LSBA_SKEL_BMGS_CWY,
+    LSBA_SKEL_BMGS_ICWY,
     LSBA_CONVERGED,
     LSBA_MAX_RESTARTS,
     LSBA_DEAD,
@@ -36,6 +38,7 @@ from ._lib import (  # noqa: F401
     lsba_block_inner_product,
     lsba_set_force_flag,
     lsba_set_kernel_variant,
+    lsba_set_skeleton,
     lsba_profile_enable,
     lsba_profile_read,
     lsba_profile_timeline,

@@ -20,7 +20,8 @@ lib = C.CDLL(library_path)
 
 LSBA_OK, LSBA_E_ARG, LSBA_E_CUDA, LSBA_E_NCCL, LSBA_E_OOM, LSBA_E_STATE = range(6)
 LSBA_IP_CLASSICAL, LSBA_IP_GLOBAL = 0, 1
-LSBA_SKEL_BCGS_PIP = 0
+LSBA_SKEL_BCGS_PIP, LSBA_SKEL_BMGS_CWY, LSBA_SKEL_BMGS_ICWY = 0, 1, 2
+_SKEL = {"pip": 0, "cwy": 1, "icwy": 2, 0: 0, 1: 1, 2: 2}
 LSBA_CONVERGED, LSBA_MAX_RESTARTS, LSBA_DEAD = 0, 1, 2
 KERNEL_IDS = dict(spmm=0, gram=1, gram_finalize=2, small_step=3, project=4, cycle_solve=5,
                   combine=6, residual=7, halo_pack=8, misc=9, step_update=10)
@@ -65,6 +66,7 @@ _sigs = {
     "lsba_block_inner_product": [_vp, _vp, _i32, _vp, C.c_int, _vp],
     "lsba_set_force_flag": [_vp, _i32],
     "lsba_set_kernel_variant": [_vp, _i32],
+    "lsba_set_skeleton": [_vp, C.c_int],
     "lsba_profile_enable": [_vp, _i32],
     "lsba_profile_read": [_vp, _i32, C.POINTER(_i64), C.POINTER(_d), C.POINTER(_d)],
     "lsba_profile_timeline": [_vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
@@ -184,19 +186,23 @@ def lsba_copy_basis_block(ctx, j, dst):
     return dst
 
 
-def _solve(fn, ctx, B, X, m, tol, max_restarts, ip, cond_threshold):
+def _solve(fn, ctx, B, X, m, tol, max_restarts, ip, cond_threshold, skel):
     info = SolveInfo()
     _check(fn(ctx, _dptr(B, "B"), _dptr(X, "X"), int(m), float(tol), int(max_restarts),
-              LSBA_SKEL_BCGS_PIP, _IP[ip], float(cond_threshold), C.byref(info)), ctx)
+              _SKEL[skel], _IP[ip], float(cond_threshold), C.byref(info)), ctx)
     return info
 
 
-def lsba_bgmres_solve(ctx, B, X, m, tol, max_restarts, ip="cl", cond_threshold=float("inf")):
-    return _solve(lib.lsba_bgmres_solve, ctx, B, X, m, tol, max_restarts, ip, cond_threshold)
+def lsba_bgmres_solve(ctx, B, X, m, tol, max_restarts, ip="cl", cond_threshold=float("inf"), skel="pip"):
+    return _solve(lib.lsba_bgmres_solve, ctx, B, X, m, tol, max_restarts, ip, cond_threshold, skel)
 
 
-def lsba_bfom_solve(ctx, B, X, m, tol, max_restarts, ip="cl", cond_threshold=float("inf")):
-    return _solve(lib.lsba_bfom_solve, ctx, B, X, m, tol, max_restarts, ip, cond_threshold)
+def lsba_bfom_solve(ctx, B, X, m, tol, max_restarts, ip="cl", cond_threshold=float("inf"), skel="pip"):
+    return _solve(lib.lsba_bfom_solve, ctx, B, X, m, tol, max_restarts, ip, cond_threshold, skel)
+
+
+def lsba_set_skeleton(ctx, skel):
+    _check(lib.lsba_set_skeleton(ctx, _SKEL[skel]), ctx)
 
 
 def lsba_solve_host(ctx, B, X, m, tol, max_restarts, fom=False, ip="cl", cond_threshold=float("inf")):
@@ -347,6 +353,6 @@ class Context:
         W = torch.empty_like(V)
         return lsba_spmm(self.ctx, V, W)
 
-    def solve(self, B, X, m, tol, max_restarts, ip="cl", mod="gmres", cond_threshold=float("inf")):
+    def solve(self, B, X, m, tol, max_restarts, ip="cl", mod="gmres", cond_threshold=float("inf"), skel="pip"):
         fn = lsba_bgmres_solve if mod == "gmres" else lsba_bfom_solve
-        return fn(self.ctx, B, X, m, tol, max_restarts, ip, cond_threshold)
+        return fn(self.ctx, B, X, m, tol, max_restarts, ip, cond_threshold, skel)

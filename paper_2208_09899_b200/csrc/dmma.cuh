@@ -60,6 +60,7 @@ struct GramArgs {
   unsigned* tickets;       // [ngroups + 1], zero-initialised, reset by the last CTA
   double* G;               // result, E = J S S doubles, row-major [(j S + a) S + b]
   const int* active;       // nullable: skip when *active == 0
+  const double* Y2 = nullptr;  // k_gram_v7<.., NY = 2>: second B-operand block, G = X^T [Y Y2]
 };
 
 __device__ __forceinline__ void named_sync(int id, int count) {

@@ -43,10 +43,12 @@ struct GramFuse {
   int on;   // 0: plain Gram
 };
 
-template <int S, int GMAX_, int U_, int MINB_>
+template <int S, int GMAX_, int U_, int MINB_, int NY_ = 1>
 struct G7Cfg {
   static constexpr int PB = S >= 16 ? 1 : 16 / S;
-  static constexpr int NT = S >= 8 ? S / 8 : 1;
+  static constexpr int NY = NY_;                       // B-operand blocks: G = X^T [Y (Y2)]
+  static constexpr int NCOL = NY * S;
+  static constexpr int NT = (NCOL + 7) / 8;
   static constexpr int GMAX = GMAX_;
   static constexpr int U = U_;
   static constexpr int MINB = MINB_;
@@ -70,10 +72,10 @@ __host__ __device__ inline int g7_qw(int ngp, int GMAX) {
   return QW;
 }
 
-template <int S, int GMAX, int U, int MINB, bool WIN = true>
+template <int S, int GMAX, int U, int MINB, bool WIN = true, int NY = 1>
 __global__ void __launch_bounds__(256, MINB)
 k_gram_v7(GramArgs g, GramFuse f) {
-  using C = G7Cfg<S, GMAX, U, MINB>;
+  using C = G7Cfg<S, GMAX, U, MINB, NY>;
   static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v7 Gram: s in {2,4,8,16}");
   if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
     if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
@@ -81,7 +83,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
   }
   extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int J = g.J, E = J * S * S;
+  const int J = g.J, E = J * S * C::NCOL;
   const int NG = g7_groups<S>(J);
   const int passes = g7_passes(NG, C::GMAX);
   const int pass = blockIdx.x % passes, chunk = blockIdx.x / passes, nchunks = gridDim.x / passes;
@@ -92,7 +94,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
   const int gA = gp0 + ((gp1 - gp0) * qs) / QW, gB = gp0 + ((gp1 - gp0) * (qs + 1)) / QW;
   const int ng = gB - gA;
   const int jlo = gp0 * C::PB, jhi = min(J, gp1 * C::PB);   // blocks (entries) of this pass
-  const int e0 = jlo * S * S, EP = (jhi - jlo) * S * S;
+  const int e0 = jlo * S * C::NCOL, EP = (jhi - jlo) * S * C::NCOL;
   const int r4 = lane & 3, c8 = lane >> 2;
   constexpr int LPB = S >= 16 ? 8 : S / 2;
   const int jj = c8 / LPB, cp = c8 % LPB;
@@ -103,7 +105,14 @@ k_gram_v7(GramArgs g, GramFuse f) {
     const int j = (gA + gi) * C::PB + (S >= 16 ? 0 : jj);
     src[gi] = (gi < ng && j < J) ? g.X + (size_t)j * g.xstride + r4 * S + 2 * cp : nullptr;
   }
-  const double* wsrc = g.Y + r4 * S + c8;
+  // B operand column tn*8 + c8 of [Y (Y2)] at row r4 of a step (nullptr: zero column)
+  const double* wsrc[C::NT];
+#pragma unroll
+  for (int tn = 0; tn < C::NT; ++tn) {
+    const int col = tn * 8 + c8;
+    wsrc[tn] = (col < S) ? g.Y + r4 * S + col
+                         : ((NY == 2 && col < 2 * S) ? g.Y2 + r4 * S + (col - S) : nullptr);
+  }
   double acc[C::GMAX][2][C::NT][2];
 #pragma unroll
   for (int a = 0; a < C::GMAX; ++a)
@@ -143,7 +152,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
           const size_t off = (size_t)(st + u) * 4 * S;
 #pragma unroll
           for (int tn = 0; tn < C::NT; ++tn)
-            bw[u][tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+            bw[u][tn] = wsrc[tn] ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
           for (int gi = 0; gi < C::GMAX; ++gi)
             av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
@@ -155,7 +164,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
           const size_t off = (size_t)(ok ? st + u : st) * 4 * S;
 #pragma unroll
           for (int tn = 0; tn < C::NT; ++tn)
-            bw[u][tn] = (ok && tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+            bw[u][tn] = (ok && wsrc[tn]) ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
           for (int gi = 0; gi < C::GMAX; ++gi)
             av[u][gi] = (ok && src[gi]) ? __ldg(reinterpret_cast<const double2*>(src[gi] + off))
@@ -178,7 +187,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
         const size_t off = (size_t)(st + (long)u * RW) * 4 * S;
 #pragma unroll
         for (int tn = 0; tn < C::NT; ++tn)
-          bw[u][tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+          bw[u][tn] = wsrc[tn] ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
         for (int gi = 0; gi < C::GMAX; ++gi)
           av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
@@ -191,7 +200,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
       double2 av[C::GMAX];
       double bw[C::NT];
 #pragma unroll
-      for (int tn = 0; tn < C::NT; ++tn) bw[tn] = (tn * 8 + c8 < S) ? __ldg(wsrc + off + tn * 8) : 0.0;
+      for (int tn = 0; tn < C::NT; ++tn) bw[tn] = wsrc[tn] ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
       for (int gi = 0; gi < C::GMAX; ++gi)
         av[gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
@@ -215,7 +224,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
         for (int i = 0; i < 2; ++i) {
           const int a = 2 * cp + e;
           const int bcol = tn * 8 + 2 * r4 + i;
-          if (bcol < S && j < J) mine[(j * S + a) * S + bcol] = acc[gi][e][tn][i];
+          if (bcol < C::NCOL && j < J) mine[(j * S + a) * C::NCOL + bcol] = acc[gi][e][tn][i];
         }
   }
   __syncthreads();
@@ -264,8 +273,10 @@ k_gram_v7(GramArgs g, GramFuse f) {
   if (ticket7 != (unsigned)(passes - 1)) return;
   __threadfence();
   if (tid == 0) *tpass = 0u;
-  if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm);
-  else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
+  if constexpr (NY == 1) {
+    if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm);
+    else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -279,7 +290,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
 // ------------------------------------------------------------------------------------------
 constexpr int kGlJM = 8;
 
-template <int S>
+template <int S, int NY = 1>
 __global__ void __launch_bounds__(256, 3)
 k_gram_gl2(GramArgs g, GramFuse f) {
   static_assert(S % 2 == 0, "gl2: even s");
@@ -287,11 +298,11 @@ k_gram_gl2(GramArgs g, GramFuse f) {
     if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;
     return;
   }
-  __shared__ double red[8][kGlJM];
+  __shared__ double red[8][kGlJM * NY];
   __shared__ double gsm[4 * kGlJM];     // fused small step (b = 1): (k+1) <= ... handled below
   __shared__ unsigned ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int J = g.J;
+  const int J = g.J, E = J * NY;                      // G[j NY + y] = <X_j, Y_y>
   const long npad = ((long)g.n + kRowPad - 1) / kRowPad * kRowPad;
   const long N2 = npad * S / 2;                       // double2 per block
   const long gstride = (long)gridDim.x * blockDim.x;
@@ -299,14 +310,19 @@ k_gram_gl2(GramArgs g, GramFuse f) {
   const int ngroups = (P + kGramGroup - 1) / kGramGroup;
   const int grpi = blockIdx.x / kGramGroup;
   const int gsize = min(kGramGroup, P - grpi * kGramGroup);
-  const double2* Y2 = reinterpret_cast<const double2*>(g.Y);
+  const double2* Ya = reinterpret_cast<const double2*>(g.Y);
+  const double2* Yb = reinterpret_cast<const double2*>(NY == 2 ? g.Y2 : g.Y);
   for (int j0 = 0; j0 < J; j0 += kGlJM) {
     const int nb = min(kGlJM, J - j0);
-    double acc[kGlJM];
+    double acc[kGlJM][NY];
 #pragma unroll
-    for (int q = 0; q < kGlJM; ++q) acc[q] = 0.0;
+    for (int q = 0; q < kGlJM; ++q)
+#pragma unroll
+      for (int y = 0; y < NY; ++y) acc[q][y] = 0.0;
     for (long e = (long)blockIdx.x * blockDim.x + tid; e < N2; e += gstride) {
-      const double2 y0 = __ldg(Y2 + e);
+      double2 yv[NY];
+      yv[0] = __ldg(Ya + e);
+      if constexpr (NY == 2) yv[NY - 1] = __ldg(Yb + e);
       double2 x0[kGlJM];
 #pragma unroll
       for (int q = 0; q < kGlJM; ++q) {
@@ -314,21 +330,25 @@ k_gram_gl2(GramArgs g, GramFuse f) {
         x0[q] = (q < nb) ? __ldg(Xq + e) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int q = 0; q < kGlJM; ++q) {
-        acc[q] = fma(x0[q].x, y0.x, acc[q]);
-        acc[q] = fma(x0[q].y, y0.y, acc[q]);
-      }
+      for (int q = 0; q < kGlJM; ++q)
+#pragma unroll
+        for (int y = 0; y < NY; ++y) {
+          acc[q][y] = fma(x0[q].x, yv[y].x, acc[q][y]);
+          acc[q][y] = fma(x0[q].y, yv[y].y, acc[q][y]);
+        }
     }
 #pragma unroll
-    for (int q = 0; q < kGlJM; ++q) {
-      const double v = warp_sum(acc[q]);
-      if (lane == 0) red[warp][q] = v;
-    }
+    for (int q = 0; q < kGlJM; ++q)
+#pragma unroll
+      for (int y = 0; y < NY; ++y) {
+        const double v = warp_sum(acc[q][y]);
+        if (lane == 0) red[warp][q * NY + y] = v;
+      }
     __syncthreads();
-    if (tid < nb) {
+    if (tid < nb * NY) {
       double t = 0.0;
       for (int w = 0; w < 8; ++w) t += red[w][tid];
-      g.part[(size_t)blockIdx.x * J + j0 + tid] = t;
+      g.part[(size_t)blockIdx.x * E + j0 * NY + tid] = t;
     }
     __syncthreads();
   }
@@ -338,10 +358,10 @@ k_gram_gl2(GramArgs g, GramFuse f) {
   __syncthreads();
   if (ticket != (unsigned)(gsize - 1)) return;
   __threadfence();
-  for (int e = tid; e < J; e += blockDim.x) {
+  for (int e = tid; e < E; e += blockDim.x) {
     double s2 = 0.0;
-    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * J + e);
-    g.gpart[(size_t)grpi * J + e] = s2;
+    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * E + e);
+    g.gpart[(size_t)grpi * E + e] = s2;
   }
   if (tid == 0) g.tickets[grpi] = 0u;
   __threadfence();
@@ -350,14 +370,14 @@ k_gram_gl2(GramArgs g, GramFuse f) {
   __syncthreads();
   if (ticket != (unsigned)(ngroups - 1)) return;
   __threadfence();
-  for (int e = tid; e < J; e += blockDim.x) {
+  for (int e = tid; e < E; e += blockDim.x) {
     double s2 = 0.0;
-    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * J + e);
+    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * E + e);
     g.G[e] = s2 * (1.0 / S);                          // Table 1: (1/s) tr(X^T Y)
   }
   if (tid == 0) g.tickets[ngroups] = 0u;
   (void)gsm;
-  if (!f.on) return;
+  if (NY != 1 || !f.on) return;
   __threadfence();
   __syncthreads();
   extern __shared__ double gl2_dyn[];                 // (k+1) doubles for the small step
@@ -365,7 +385,7 @@ k_gram_gl2(GramArgs g, GramFuse f) {
 }
 
 // launch geometry of k_gram_v7: grid (a multiple of the pass count) and dynamic smem bytes
-template <int S, int GMAX>
+template <int S, int GMAX, int NY = 1>
 struct G7Launch {
   int passes, grid;
   size_t smem;
@@ -375,12 +395,12 @@ struct G7Launch {
     int maxEP = 0, maxRW = 1;
     for (int p = 0; p < passes; ++p) {
       const int gp0 = NG * p / passes, gp1 = NG * (p + 1) / passes;
-      const int ep = (std::min(J, gp1 * (S >= 16 ? 1 : 16 / S)) - gp0 * (S >= 16 ? 1 : 16 / S)) * S * S;
+      const int ep = (std::min(J, gp1 * (S >= 16 ? 1 : 16 / S)) - gp0 * (S >= 16 ? 1 : 16 / S)) * S * S * NY;
       maxEP = std::max(maxEP, ep);
       maxRW = std::max(maxRW, 8 / g7_qw(gp1 - gp0, GMAX));
     }
     smem = sizeof(double) * (size_t)maxRW * maxEP;
-    if (fuse) smem = std::max(smem, sizeof(double) * (size_t)J * S * S);   // step_coef_body's Gs
+    if (fuse) smem = std::max(smem, sizeof(double) * (size_t)J * S * S * NY);   // step_coef_body's Gs
     const long steps = ((long)n + 3) / 4;
     int chunks = std::max(1, ctas_per_sm * sms / passes);
     chunks = (int)std::max(1L, std::min<long>(chunks, (steps + 63) / 64));

@@ -18,6 +18,11 @@ template <int B>
 cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy, int upd, double* Y,
                              double* Z, int* info, cudaStream_t stream);
 
+template <int B>
+cudaError_t launch_cwy_iter1(const SmallState2& st, const double* G, cudaStream_t stream);
+template <int B>
+cudaError_t launch_cwy_coef(const SmallState2& st, const double* G, int k, int inverse, cudaStream_t stream);
+
 #define LSBA_DECL_SMALL(B)                                                                              \
   template <>                                                                                           \
   cudaError_t launch_step_small<B>(const SmallState2&, const double*, int, const CycleParams&, double,  \
@@ -26,7 +31,11 @@ cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy,
   cudaError_t launch_step_update<B>(const SmallState2&, const double*, int, double, cudaStream_t);     \
   template <>                                                                                           \
   cudaError_t launch_cycle_end<B>(const SmallState2&, int, int, int, int, double*, double*, int*,     \
-                                  cudaStream_t);
+                                  cudaStream_t);                                                        \
+  template <>                                                                                           \
+  cudaError_t launch_cwy_iter1<B>(const SmallState2&, const double*, cudaStream_t);                    \
+  template <>                                                                                           \
+  cudaError_t launch_cwy_coef<B>(const SmallState2&, const double*, int, int, cudaStream_t);
 LSBA_DECL_SMALL(1) LSBA_DECL_SMALL(2) LSBA_DECL_SMALL(3) LSBA_DECL_SMALL(4)
 LSBA_DECL_SMALL(5) LSBA_DECL_SMALL(6) LSBA_DECL_SMALL(7) LSBA_DECL_SMALL(8)
 LSBA_DECL_SMALL(9) LSBA_DECL_SMALL(10) LSBA_DECL_SMALL(11) LSBA_DECL_SMALL(12)

@@ -110,6 +110,8 @@ struct lsba_ctx_ {
   int variant = 0;
   int fuse_spmm = 0;   // 1: SpMM fused into the tensor-core Gram pass (gather warps)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
+  int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
+  int skel_default = LSBA_SKEL_BCGS_PIP;  // lsba_set_skeleton: step API and lsba_solve_host
   int gram_impl = 0;   // unfused mode: 0 v6 (barrier-free), 3 v5, 1 TMA-staged, 2 v3
   int64_t launches = 0;
   int64_t ws_bytes = 0;
@@ -215,7 +217,7 @@ struct LaunchScope {
 static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot_stride; }
 static inline bool in_basis(lsba_ctx c, const double* p) {
-  return p >= c->d_V && p < c->d_V + (size_t)(c->m_max + 1) * c->slot_stride;
+  return p >= c->d_V && p < c->d_V + (size_t)(c->m_max + 2) * c->slot_stride;
 }
 
 // ---------------------------------------------------------------- halo exchange (P > 1)
@@ -323,11 +325,11 @@ static lsba_status wait_update(lsba_ctx c) {
 // ---------------------------------------------------------------- a2: v7 streaming Gram
 // Tuned (GMAX groups per warp, U steps per batch, MINB CTAs per SM) per s and J from the
 // standalone sweep in tools/gram_bench.cu (profiles/r01_gram_sweep.md).
-template <int S, int GMAX, int U, int MINB, bool WIN = true>
+template <int S, int GMAX, int U, int MINB, bool WIN = true, int NY = 1>
 static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
-  auto fn = k_gram_v7<S, GMAX, U, MINB, WIN>;
-  G7Launch<S, GMAX> geo(c->n, a.J, MINB, c->n_sms, f.on != 0);
-  if ((size_t)geo.grid * a.J * S * S > c->part_cap || geo.passes > kMaxGramPasses)
+  auto fn = k_gram_v7<S, GMAX, U, MINB, WIN, NY>;
+  G7Launch<S, GMAX, NY> geo(c->n, a.J, MINB, c->n_sms, f.on != 0);
+  if ((size_t)geo.grid * a.J * S * S * NY > c->part_cap || geo.passes > kMaxGramPasses)
     return fail(c, LSBA_E_STATE, "v7 Gram workspace too small (J=%d)", a.J);
   if (geo.smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
   fn<<<geo.grid, 256, geo.smem, c->stream>>>(a, f);
@@ -350,6 +352,30 @@ static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   } else {
     return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
   }
+}
+
+// BMGS-(I)CWY Gram: G = X^T [Y Y2] ((J s) x 2s) in one pass (v7 with two B-operand blocks)
+template <int S>
+static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
+  const GramFuse f{};
+  if constexpr (S == 2 || S == 4) {
+    if (a.J <= 8) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
+    return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
+  } else if constexpr (S == 8) {
+    return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
+  } else if constexpr (S == 16) {
+    return gram_v7_launch<S, 1, 4, 2, false, 2>(c, a, f);
+  } else {
+    return fail(c, LSBA_E_STATE, "v7 Gram (2 blocks): s=%d unsupported", S);
+  }
+}
+
+__global__ void k_interleave2(int R, int b, const double* __restrict__ G1, const double* __restrict__ G2,
+                              double* __restrict__ G) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;   // G[r][0..2b) = [G1[r] G2[r]]
+  if (e >= R * 2 * b) return;
+  const int r = e / (2 * b), c = e % (2 * b);
+  G[e] = (c < b) ? G1[(size_t)r * b + c] : G2[(size_t)r * b + c - b];
 }
 
 // ---------------------------------------------------------------- a1+a2: (SpMM +) Gram (+ allreduce)
@@ -615,7 +641,9 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
 }
 
 // dispatch wrappers (runtime s)
-static lsba_status spmm(lsba_ctx c, const double* V, double* W) { LSBA_DISPATCH_S(c->s, spmm_t, c, V, W, nullptr); }
+static lsba_status spmm(lsba_ctx c, const double* V, double* W, const int* active = nullptr) {
+  LSBA_DISPATCH_S(c->s, spmm_t, c, V, W, active);
+}
 static lsba_status residual(lsba_ctx c, const double* Bm, const double* X, double* out) {
   LSBA_DISPATCH_S(c->s, residual_t, c, Bm, X, out);
 }
@@ -624,6 +652,67 @@ static lsba_status gram(lsba_ctx c, const double* X, size_t xstride, int J, doub
                         const CycleParams* prm = nullptr, bool* coef_fused = nullptr) {
   LSBA_DISPATCH_S(c->s, gram_t, c, X, xstride, J, Y, ip, Vk, active, coef_k, prm, coef_fused);
 }
+// BMGS-(I)CWY block inner product <[X_0..X_{J-1}], [Y Y2]> ((J b) x 2b, row-major; global:
+// J pairs) into c->d_G, one pass and one allreduce (Alg 6 line 10).
+template <int S>
+static lsba_status gram2_t(lsba_ctx c, const double* X, size_t xstride, int J, const double* Y,
+                           const double* Y2, int ip, const int* active) {
+  const bool gl = (ip == LSBA_IP_GLOBAL);
+  const size_t E = gl ? 2 * (size_t)J : 2 * (size_t)J * S * S;
+  const bool slots = in_basis(c, X) && in_basis(c, Y) && in_basis(c, Y2) && c->d_tickets;
+  bool done = false;
+  if (c->variant == 0 && slots) {
+    LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J + 1));
+    GramArgs a;
+    a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+    a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride;
+    a.J = J; a.y_alias = 0; a.Y = const_cast<double*>(Y); a.Y2 = Y2; a.zeros = c->d_zeros;
+    a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+    a.active = active;
+    if (c->n == 0) {
+      CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+      done = true;
+    } else if (!gl) {
+      if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
+        TRY(gram2_v7<S>(c, a));
+        done = true;
+      }
+    } else {
+      if constexpr (S % 2 == 0) {
+        const int grid = std::max(1, std::min(3 * c->n_sms, cdiv(cdiv((long)c->slot, 2), 256)));
+        k_gram_gl2<S, 2><<<grid, 256, 0, c->stream>>>(a, GramFuse{});
+        CKL();
+        done = true;
+      }
+    }
+  }
+  if (done) {
+    if (c->nranks > 1) CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+    return LSBA_OK;
+  }
+  // fallback (odd s, DFMA variant, non-slot inputs): two block inner products (two syncs on
+  // P > 1), interleaved; the other half of the G double buffer is free in a CWY step
+  double* const Gdst = c->d_G;
+  double* const T1 = (Gdst == c->d_Gbase) ? c->d_Gbase + c->g_half : c->d_Gbase;
+  double* const T2 = T1 + E / 2;
+  c->d_G = T1;
+  TRY(gram_t<S>(c, X, xstride, J, const_cast<double*>(Y), ip, nullptr, active, -1, nullptr, nullptr));
+  c->d_G = T2;
+  TRY(gram_t<S>(c, X, xstride, J, const_cast<double*>(Y2), ip, nullptr, active, -1, nullptr, nullptr));
+  c->d_G = Gdst;
+  {
+    LaunchScope Ls(c, LSBA_K_MISC, 16.0 * E);
+    const int bb = gl ? 1 : S;
+    k_interleave2<<<cdiv((long)E, 256), 256, 0, c->stream>>>(J * bb, bb, T1, T2, Gdst);
+    CKL();
+  }
+  return LSBA_OK;
+}
+static lsba_status gram2(lsba_ctx c, const double* X, size_t xstride, int J, const double* Y,
+                         const double* Y2, int ip, const int* active) {
+  LSBA_DISPATCH_S(c->s, gram2_t, c, X, xstride, J, Y, Y2, ip, active);
+}
+
 static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, const double* C0,
                            const double* base0, double* out0, int J1, const double* C1, double* out1,
                            const int* flag_ptr, int kid) {
@@ -643,13 +732,31 @@ static lsba_status small_step(lsba_ctx c, int k, const CycleParams& prm) {
 }
 
 template <int B>
-static lsba_status step_update_t(lsba_ctx c, int k) {
+static lsba_status step_update_t(lsba_ctx c, int k, const double* G) {
   LaunchScope Ls(c, LSBA_K_STEP_UPDATE, 0.0, c->stream2);
   const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
-  CK(launch_step_update<B>(c->st, c->d_G, k, rfac, c->stream2));
+  CK(launch_step_update<B>(c->st, G, k, rfac, c->stream2));
   return LSBA_OK;
 }
-static lsba_status step_update(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, step_update_t, c, k); }
+static lsba_status step_update(lsba_ctx c, int k, const double* G) {
+  LSBA_DISPATCH_S(c->b, step_update_t, c, k, G);
+}
+
+// ---------------------------------------------------------------- BMGS-(I)CWY small kernels
+template <int B>
+static lsba_status cwy_iter1_t(lsba_ctx c) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  CK(launch_cwy_iter1<B>(c->st, c->d_G, c->stream));
+  return LSBA_OK;
+}
+template <int B>
+static lsba_status cwy_coef_t(lsba_ctx c, int k) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  CK(launch_cwy_coef<B>(c->st, c->d_G, k, c->skel == LSBA_SKEL_BMGS_ICWY ? 1 : 0, c->stream));
+  return LSBA_OK;
+}
+static lsba_status cwy_iter1_small(lsba_ctx c) { LSBA_DISPATCH_S(c->b, cwy_iter1_t, c); }
+static lsba_status cwy_coef(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, cwy_coef_t, c, k); }
 
 static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
@@ -689,7 +796,7 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   // estimates / kappa_F / decision on stream 2, concurrent with the projection
   CK(cudaEventRecord(c->ev_coef, c->stream));
   CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
-  TRY(step_update(c, k));
+  TRY(step_update(c, k, c->d_G));
   CK(cudaEventRecord(c->ev_upd, c->stream2));
   TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
               nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
@@ -712,6 +819,46 @@ static bool throttle(lsba_ctx c, int k) {
     if (done >= k - kLookahead) return true;
     if (cudaStreamQuery(c->stream) == cudaSuccess) return true;   // (device drained: no stall)
   }
+}
+
+// BMGS-(I)CWY (Alg 6): loop iteration 1 after IO(U): W = A V_1 (slot 1),
+// H_11 = <V_1, W>, U = W - V_1 H_11 over W (slot 1).  Asynchronous.
+static lsba_status cwy_iter1_async(lsba_ctx c) {
+  const int* act = &c->d_ctl->active;
+  TRY(spmm(c, slotp(c, 0), slotp(c, 1), act));                                    // line 5
+  TRY(gram(c, slotp(c, 0), c->slot_stride, 2, slotp(c, 1), c->ip, nullptr, act));  // line 7
+  TRY(cwy_iter1_small(c));
+  TRY(project(c, slotp(c, 0), c->slot_stride, 2, c->st.coef, nullptr, slotp(c, 1), 0, nullptr, nullptr,
+              c->st.flag_dev, LSBA_K_PROJECT));                                     // line 8
+  return LSBA_OK;
+}
+
+// Arnoldi step k >= 1 = Alg 6 loop iteration k+1: U (unnormalised V_{k+1}) sits in slot k.
+// W = A U -> slot k+1; ONE block inner product <[V_1..V_k U], [U W]> (+ one allreduce); the
+// small step (chol, T column, H_{1:k+1,k+1}, coefficients); the update kernel (QR, estimates,
+// decision) on stream 2 for the now complete Hessenberg column k; and one two-output pass
+// V_{k+1} = U H^{-1} (over slot k), U' = W H^{-1} - V H_{1:k+1,k+1} (over slot k+1; skipped on
+// the cycle's last step).  Asynchronous.
+static lsba_status cwy_step_async(lsba_ctx c, int k, bool last) {
+  const int* act = &c->d_ctl->active;
+  const size_t bb = (size_t)c->b * c->b;
+  c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
+  c->pending_upd = (k > 1);
+  TRY(spmm(c, slotp(c, k), slotp(c, k + 1), act));                                 // line 5
+  TRY(wait_update(c));
+  TRY(gram2(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), slotp(c, k + 1), c->ip, act));  // line 10
+  TRY(cwy_coef(c, k));                                                              // lines 11-14
+  CK(cudaEventRecord(c->ev_coef, c->stream));
+  CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
+  TRY(step_update(c, k, c->st.gpip));
+  CK(cudaEventRecord(c->ev_upd, c->stream2));
+  TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), last ? 0 : k + 2,
+              c->st.coef + (size_t)(k + 1) * bb, slotp(c, k + 1), c->st.flag_dev, LSBA_K_PROJECT));  // 16-17
+  return LSBA_OK;
+}
+
+static lsba_status step_async(lsba_ctx c, int k, bool last) {
+  return c->skel == LSBA_SKEL_BCGS_PIP ? pip_step_async(c, k) : cwy_step_async(c, k, last);
 }
 
 // join stream 2 (the last step's update) into the main stream
@@ -779,7 +926,7 @@ static void set_ip(lsba_ctx c, int ip) {
 
 static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, double tol,
                               int max_restarts, int gmres, int ip, double tau,
-                              lsba_solve_info* info) {
+                              lsba_solve_info* info, int skel = LSBA_SKEL_BCGS_PIP) {
   if (!c) return LSBA_E_ARG;
   if (!info) return fail(c, LSBA_E_ARG, "info is NULL");
   if (m < 1 || m > c->m_max) return fail(c, LSBA_E_ARG, "m=%d outside [1, m_max=%d]", m, c->m_max);
@@ -794,15 +941,20 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   std::memset(info, 0, sizeof *info);
   info->true_relres = NAN;
   info->res_est = NAN;
+  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BMGS_ICWY) return fail(c, LSBA_E_ARG, "bad skeleton");
   set_ip(c, ip);
+  c->skel = skel;
   c->forced_done = false;
   c->k = -1;
   c->flagged = false;
   auto finish = [&]() {
+    // the paper's counters (PAPER.md:650 tables): BMGS-(I)CWY applies A, syncs and evaluates
+    // one more block per cycle than BCGS-PIP (the lagged normalisation)
+    const int64_t extra = (skel == LSBA_SKEL_BCGS_PIP) ? 0 : info->cycles;
     info->restarts = info->cycles > 0 ? info->cycles - 1 : 0;
-    info->syncs = (int64_t)info->iterations + info->cycles;
-    info->matvecs = info->iterations;
-    info->basis_evals = 3 * (int64_t)info->iterations;
+    info->syncs = (int64_t)info->iterations + info->cycles + extra;
+    info->matvecs = info->iterations + extra;
+    info->basis_evals = 3 * (int64_t)info->iterations + extra;
     info->kernel_launches = c->launches - launches0;
     info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   };
@@ -869,11 +1021,12 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     c->h_prog[0] = -1;                                       // (device idle: cycle boundary)
     c->h_prog[1] = 1;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
+    if (c->skel != LSBA_SKEL_BCGS_PIP) TRY(cwy_iter1_async(c));   // Alg 6 iteration 1
     for (int k = 1; k <= m_cur; ++k) {
       // keep at most kLookahead steps enqueued beyond the last decided one; stop enqueueing
       // once the device has ended the cycle (flag, convergence, kappa trigger)
       if (!throttle(c, k)) break;
-      TRY(pip_step_async(c, k));
+      TRY(step_async(c, k, k == m_cur));
     }
     TRY(join_update(c));
     TRY(read_status(c, nullptr, &cc));
@@ -1086,7 +1239,8 @@ static void release(lsba_ctx c) {
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
-                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr};
+                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
+                  c->st.Tm, c->st.gpip};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1213,8 +1367,10 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   // ---- basis and work buffers
   c->slot = (size_t)n_local * s;
   c->slot_stride = (size_t)((n_local + kRowPad - 1) / kRowPad) * kRowPad * s;
-  TRY(dalloc(c, &c->d_V, (size_t)(m_max + 1) * c->slot_stride));
-  CK(cudaMemset(c->d_V, 0, sizeof(double) * (size_t)(m_max + 1) * c->slot_stride));   // zero pad rows
+  // m_max + 2 slots: V_1..V_{m+1} plus W of the last step of a BMGS-(I)CWY cycle (Alg 6 applies
+  // A to the unnormalised V_{k+1} one slot ahead)
+  TRY(dalloc(c, &c->d_V, (size_t)(m_max + 2) * c->slot_stride));
+  CK(cudaMemset(c->d_V, 0, sizeof(double) * (size_t)(m_max + 2) * c->slot_stride));   // zero pad rows
   TRY(dalloc(c, &c->d_zeros, 64));
   CK(cudaMemset(c->d_zeros, 0, sizeof(double) * 64));
   TRY(dalloc(c, &c->d_Xc, c->slot));
@@ -1225,7 +1381,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   }
   // DMMA Gram: persistent grid of 2 CTAs per SM; partials [cta][E] and [group][E]
   c->gram_grid = 4 * c->n_sms;
-  const size_t Emax = (size_t)(m_max + 1) * s * s;
+  const size_t Emax = 2 * (size_t)(m_max + 2) * s * s;      // (k+1)s x 2s for BMGS-(I)CWY
   c->part_cap = std::max((size_t)(kGramCtas + 16 * (m_max + 1)) * s * s + 2 * Emax,
                          (size_t)c->gram_grid * Emax);
   TRY(dalloc(c, &c->d_part, c->part_cap));
@@ -1238,7 +1394,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   TRY(dalloc(c, &c->d_ctl, 1));
   CK(cudaMemset(c->d_ctl, 0, sizeof(CycleCtl)));
   CK(cudaMallocHost((void**)&c->h_ctl, sizeof(CycleCtl)));
-  c->g_half = (size_t)(m_max + 1) * s * s;
+  c->g_half = Emax;
   TRY(dalloc(c, &c->d_Gbase, 2 * c->g_half));
   c->d_G = c->d_Gbase;
   c->sq_cap = std::max(1, cdiv((long)n_local * 16, kThreads));
@@ -1246,7 +1402,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   TRY(dalloc(c, &c->d_scalar, 4));
   // ---- small state (sized for b = s)
   const int ldH = (m_max + 1) * s;
-  const size_t nH = (size_t)ldH * m_max * s, nBeta = (size_t)s * s, nCoef = 2 * (size_t)(m_max + 1) * s * s,
+  const size_t nH = (size_t)ldH * m_max * s, nBeta = (size_t)s * s, nCoef = 2 * (size_t)(m_max + 2) * s * s,
                nQv = (size_t)m_max * s * 2 * s, nQt = (size_t)m_max * s, nG = (size_t)ldH * s,
                nRf = (size_t)ldH * ldH, nHt = (size_t)m_max * s * s, nGh = (size_t)m_max * s * s,
                nRi = (size_t)ldH * ldH, nSc = 4, nCacc = (size_t)s * s;
@@ -1269,6 +1425,8 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.ldH = ldH;
   c->st.m = m_max;
   c->st.bmax = s;
+  TRY(dalloc(c, &c->st.Tm, (size_t)ldH * ldH));
+  TRY(dalloc(c, &c->st.gpip, (size_t)ldH * s));
   c->st.ctl = c->d_ctl;
   {  // progress word in mapped pinned host memory (written by the device, polled by the host)
     CK(cudaHostAlloc((void**)&c->h_prog, 2 * sizeof(int), cudaHostAllocMapped));
@@ -1357,7 +1515,9 @@ extern "C" lsba_status lsba_arnoldi_begin(lsba_ctx c, const double* B_dev, lsba_
   prm.tol_abs = -1.0;            // the step API never declares convergence
   prm.tau = INFINITY;
   prm.need_kappa = 1;
+  c->skel = c->skel_default;
   TRY(io_begin_async(c, prm));
+  if (c->skel != LSBA_SKEL_BCGS_PIP) TRY(cwy_iter1_async(c));     // Alg 6 loop iteration 1
   StepStatus stt;
   TRY(read_status(c, &stt, nullptr));
   if (io_flag) *io_flag = stt.flag;
@@ -1372,7 +1532,7 @@ extern "C" lsba_status lsba_block_arnoldi_step(lsba_ctx c, lsba_step_info* info)
   if (c->k >= c->m_max) return fail(c, LSBA_E_STATE, "basis full (k == m_max)");
   CK(cudaSetDevice(c->device));
   const int k = c->k + 1;
-  TRY(pip_step_async(c, k));
+  TRY(step_async(c, k, k == c->m_max));
   TRY(join_update(c));
   StepStatus stt;
   CycleCtl cc;
@@ -1444,16 +1604,14 @@ extern "C" lsba_status lsba_bgmres_solve(lsba_ctx c, const double* B, double* X,
                                          int32_t max_restarts, lsba_skel skel, lsba_ip ip,
                                          double cond_threshold, lsba_solve_info* info) {
   if (!c) return LSBA_E_ARG;
-  if (skel != LSBA_SKEL_BCGS_PIP) return fail(c, LSBA_E_ARG, "only BCGS-PIP is built");
-  return solve_impl(c, B, X, m, tol, max_restarts, 1, ip, cond_threshold, info);
+  return solve_impl(c, B, X, m, tol, max_restarts, 1, ip, cond_threshold, info, skel);
 }
 
 extern "C" lsba_status lsba_bfom_solve(lsba_ctx c, const double* B, double* X, int32_t m, double tol,
                                        int32_t max_restarts, lsba_skel skel, lsba_ip ip,
                                        double cond_threshold, lsba_solve_info* info) {
   if (!c) return LSBA_E_ARG;
-  if (skel != LSBA_SKEL_BCGS_PIP) return fail(c, LSBA_E_ARG, "only BCGS-PIP is built");
-  return solve_impl(c, B, X, m, tol, max_restarts, 0, ip, cond_threshold, info);
+  return solve_impl(c, B, X, m, tol, max_restarts, 0, ip, cond_threshold, info, skel);
 }
 
 extern "C" lsba_status lsba_solve_host(lsba_ctx c, const double* B_host, double* X_host, int32_t m,
@@ -1471,7 +1629,8 @@ extern "C" lsba_status lsba_solve_host(lsba_ctx c, const double* B_host, double*
     CK(cudaMemcpyAsync(c->d_Bh, B_host, sizeof(double) * c->slot, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_Xh, X_host, sizeof(double) * c->slot, cudaMemcpyHostToDevice, c->stream));
   }
-  TRY(solve_impl(c, c->d_Bh, c->d_Xh, m, tol, max_restarts, fom ? 0 : 1, ip, cond_threshold, info));
+  TRY(solve_impl(c, c->d_Bh, c->d_Xh, m, tol, max_restarts, fom ? 0 : 1, ip, cond_threshold, info,
+                 c->skel_default));
   if (c->n > 0)
     CK(cudaMemcpyAsync(X_host, c->d_Xh, sizeof(double) * c->slot, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -1511,6 +1670,13 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
   if (k_flag < 0) return fail(c, LSBA_E_ARG, "k_flag < 0");
   c->force_flag_k = k_flag;
   c->forced_done = false;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_set_skeleton(lsba_ctx c, lsba_skel skel) {
+  if (!c) return LSBA_E_ARG;
+  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BMGS_ICWY) return fail(c, LSBA_E_ARG, "bad skeleton");
+  c->skel_default = skel;
   return LSBA_OK;
 }
 

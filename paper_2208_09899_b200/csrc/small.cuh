@@ -40,6 +40,8 @@ struct SmallState2 {
   int* iscr;       // [0] flag, [1] forced
   int ldH, m, bmax;
   volatile int* prog;   // host-mapped progress word {k_done, active} read by the enqueueing host
+  double* Tm;           // BMGS-(I)CWY: T ((m+1)b square, col-major, ld ldH)
+  double* gpip;         // BMGS-(I)CWY: H_{1:k,k} in the Gram layout the update kernel reads
 };
 
 // publish the step just decided to the host (mapped pinned memory; the host bounds how far
@@ -547,6 +549,225 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
       else if (k >= ctl->m_cur) { ctl->active = 0; ctl->why = 4; }
     }
     publish_progress(st, k, ctl->active);
+  }
+}
+
+// ---------------------------------------------------------------------------- BMGS-(I)CWY
+// Alg 6.  Loop iteration 1 (after IO): G = <[V_1 W], W> (the PIP Gram with
+// J = 2); H_11 = its first block; coefficients [-H_11; I] for U = W - V_1 H_11 (written over W).
+// blockDim 128.
+template <int B>
+__global__ void __launch_bounds__(128)
+k_cwy_iter1(SmallState2 st, const double* __restrict__ G) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (st.ctl->active == 0) {            // IO flagged: nothing to project
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int r = e / B, c = e % B;     // G row-major (j B + a) B + b, block 0 = <V_1, W>
+    const double h = __ldcg(G + e);
+    st.Hbar[r + (size_t)c * st.ldH] = h;
+    st.coef[e] = -h;                                   // block 0 (V_1): -H_11
+    st.coef[B * B + e] = (r == c) ? 1.0 : 0.0;         // block 1 (W): I
+    st.Tm[r + (size_t)c * st.ldH] = (r == c) ? 1.0 : 0.0;   // T_11 = I (line 1)
+  }
+  if (tid == 0) *st.flag_dev = 0;
+}
+
+// Loop iteration k+1 = Arnoldi step k >= 1.  G ((k+1)B x 2B, row-major) = <[V_1..V_k U], [U W]>:
+// rows < kB: [Y Z], rows kB..: [Omega Pt].  R = H_{k+1,k} = chol(Omega) with NaN-flag (R2);
+// P = R^{-*} Pt; T column (CWY: -T Y R^{-1}; ICWY: Y R^{-1}); H_{1:k+1,k+1} = T^* ZP (CWY) or
+// T^{-*} ZP (ICWY) with ZP = [Z; P] R^{-1}.  Writes Hbar (subdiagonal of column k, top of
+// column k+1), the update kernel's inputs (gpip = H_{1:k,k}, rscr = [R, R^{-1}], iscr) and the
+// coefficients of the two-output projection over [V_1..V_k, U, W]:
+//   V_{k+1} = U R^{-1}                        (C0: k+1 blocks, zero but the last)
+//   U' = W R^{-1} - V H_{1:k+1,k+1}            (C1: k+2 blocks; V_{k+1} folded in as U R^{-1})
+// blockDim 256; dyn smem (k+1)B x 2B (G) + 2 (k+1)B x B (ZP, Hn) doubles.
+template <int B>
+__global__ void __launch_bounds__(256)
+k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
+  extern __shared__ double cw[];
+  __shared__ double Rs[B * B], Ris[B * B], Ps[B * B];
+  __shared__ int flag_s;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int ldH = st.ldH, kb = k * B, k1b = kb + B;
+  CycleCtl* ctl = st.ctl;
+  if (ctl->active == 0) {               // speculative launch after the cycle ended: no-op
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  const int force_flag = (k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
+  double* Gs = cw;                       // k1b x 2B
+  double* ZP = cw + (size_t)k1b * 2 * B; // k1b x B
+  double* Hn = ZP + (size_t)k1b * B;     // k1b x B
+  for (int e = tid; e < k1b * 2 * B; e += nt) Gs[e] = __ldcg(G + e);
+  // the update kernel reads H_{1:k,k} (column k, computed one iteration earlier) as a Gram
+  for (int e = tid; e < kb * B; e += nt) {
+    const int r = e / B, c = e % B;
+    st.gpip[e] = st.Hbar[r + (size_t)((k - 1) * B + c) * ldH];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    // R = chol(sym(Omega)) (R2), column-major upper
+    for (int e = lane; e < B * B; e += 32) {
+      const int x = e % B, y = e / B;
+      Rs[x + y * B] = (x <= y) ? 0.5 * (Gs[(kb + x) * 2 * B + y] + Gs[(kb + y) * 2 * B + x]) : 0.0;
+    }
+    __syncwarp();
+    bool f = false;
+    for (int j = 0; j < B; ++j) {
+      const double d = Rs[j + j * B];
+      if (!(d > 0.0) || !isfinite(d)) { f = true; break; }
+      const double r = sqrt(d);
+      __syncwarp();
+      for (int c = j + lane; c < B; c += 32) Rs[j + c * B] = (c == j) ? r : Rs[j + c * B] / r;
+      __syncwarp();
+      const int rem = B - j - 1;
+      for (int e = lane; e < rem * rem; e += 32) {
+        const int x = j + 1 + e % rem, y = j + 1 + e / rem;
+        if (x <= y) Rs[x + y * B] -= Rs[j + x * B] * Rs[j + y * B];
+      }
+      __syncwarp();
+    }
+    if (!f)
+      for (int e = 0; e < B * B; ++e)
+        if (!isfinite(Rs[e])) f = true;
+    if (force_flag) f = true;
+    if (lane == 0) {
+      flag_s = f ? 1 : 0;
+      *st.flag_dev = flag_s;
+      st.iscr[0] = flag_s;
+      st.iscr[1] = force_flag;
+      st.status->k = k;
+      st.status->flag = flag_s;
+      st.status->proj_singular = 0;
+      st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
+    }
+    __syncwarp();
+    if (!f && lane < B) {               // R^{-1}, column `lane`
+      const int c = lane;
+      double x[B];
+#pragma unroll
+      for (int r = B - 1; r >= 0; --r) {
+        double t = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = r + 1; q < B; ++q) t -= Rs[r + q * B] * x[q];
+        x[r] = (r <= c) ? t / Rs[r + r * B] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < B; ++r) Ris[r + c * B] = (r <= c) ? x[r] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (flag_s) {
+    for (int e = tid; e < B * B; e += nt) {
+      const int x = e % B, y = e / B;
+      st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = 0.0;
+    }
+    return;
+  }
+  // P = R^{-T} Pt  (P[x][y] = sum_q (R^{-1})[q][x] Pt[q][y])
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int q = 0; q <= x; ++q) t += Ris[q + x * B] * Gs[(kb + q) * 2 * B + B + y];
+    Ps[x + y * B] = t;
+  }
+  __syncthreads();
+  // T column k (block rows 0..k-1): YR = Y R^{-1}; CWY: -T_{1:k,1:k} YR, ICWY: YR
+  double* Tm = st.Tm;
+  const int Tcol = kb;                   // first column of block column k (0-based) of T
+  for (int e = tid; e < kb * B; e += nt) {
+    const int r = e % kb, c = e / kb;
+    double t = 0.0;
+    for (int q = 0; q <= c; ++q) t += Gs[r * 2 * B + q] * Ris[q + c * B];
+    ZP[r + (size_t)c * kb] = t;          // (scratch: YR, column-major kb x B)
+  }
+  __syncthreads();
+  if (inverse) {
+    for (int e = tid; e < kb * B; e += nt) {
+      const int r = e % kb, c = e / kb;
+      Tm[r + (size_t)(Tcol + c) * ldH] = ZP[r + (size_t)c * kb];
+    }
+  } else {
+    for (int e = tid; e < kb * B; e += nt) {
+      const int r = e % kb, c = e / kb;
+      double t = 0.0;
+      for (int q = r - r % B; q < kb; ++q)           // T block upper triangular (unit diagonal)
+        t += Tm[r + (size_t)q * ldH] * ZP[q + (size_t)c * kb];
+      Tm[r + (size_t)(Tcol + c) * ldH] = -t;
+    }
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    Tm[(kb + x) + (size_t)(Tcol + y) * ldH] = (x == y) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // ZP = [Z; P] R^{-1}  (column-major k1b x B)
+  for (int e = tid; e < k1b * B; e += nt) {
+    const int r = e % k1b, c = e / k1b;
+    double t = 0.0;
+    for (int q = 0; q <= c; ++q) {
+      const double zp = (r < kb) ? Gs[r * 2 * B + B + q] : Ps[(r - kb) + q * B];
+      t += zp * Ris[q + c * B];
+    }
+    ZP[r + (size_t)c * k1b] = t;
+  }
+  __syncthreads();
+  if (!inverse) {
+    // Hn = T^T ZP: Hn[r][c] = sum_q T[q][r] ZP[q][c], T[q][r] nonzero for q < (r/B + 1) B
+    for (int e = tid; e < k1b * B; e += nt) {
+      const int r = e % k1b, c = e / k1b;
+      const int qend = (r / B + 1) * B;
+      double t = 0.0;
+      for (int q = 0; q < qend; ++q) t += Tm[q + (size_t)r * ldH] * ZP[q + (size_t)c * k1b];
+      Hn[r + (size_t)c * k1b] = t;
+    }
+  } else {
+    // Hn = T^{-T} ZP: forward substitution over block rows (T^T lower, unit diagonal blocks)
+    for (int i = 0; i <= k; ++i) {
+      for (int e = tid; e < B * B; e += nt) {
+        const int rl = e % B, c = e / B, r = i * B + rl;
+        double t = ZP[r + (size_t)c * k1b];
+        for (int q = 0; q < i * B; ++q) t -= Tm[q + (size_t)r * ldH] * Hn[q + (size_t)c * k1b];
+        Hn[r + (size_t)c * k1b] = t;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // Hbar: subdiagonal of column k = R; top of column k+1 = Hn (if it exists)
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
+    st.rscr[e] = Rs[e];
+    st.rscr[B * B + e] = Ris[e];
+  }
+  if (k < st.m)
+    for (int e = tid; e < k1b * B; e += nt) {
+      const int r = e % k1b, c = e / k1b;
+      st.Hbar[r + (size_t)(kb + c) * ldH] = Hn[r + (size_t)c * k1b];
+    }
+  // projection coefficients (row-major blocks [j][a][c]): C0 then C1
+  double* C0 = st.coef;
+  double* C1 = st.coef + (size_t)(k + 1) * B * B;
+  for (int e = tid; e < (k + 1) * B * B; e += nt) {
+    const int j = e / (B * B), a = (e / B) % B, c = e % B;
+    C0[e] = (j == k) ? Ris[a + c * B] : 0.0;
+  }
+  for (int e = tid; e < (k + 2) * B * B; e += nt) {
+    const int j = e / (B * B), a = (e / B) % B, c = e % B;
+    double t;
+    if (j < k) {
+      t = -Hn[(j * B + a) + (size_t)c * k1b];
+    } else if (j == k) {                 // -R^{-1} H_{k+1,k+1}
+      t = 0.0;
+      for (int q = a; q < B; ++q) t -= Ris[a + q * B] * Hn[(kb + q) + (size_t)c * k1b];
+    } else {
+      t = Ris[a + c * B];
+    }
+    C1[e] = t;
   }
 }
 

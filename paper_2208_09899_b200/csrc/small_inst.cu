@@ -54,4 +54,25 @@ cudaError_t launch_cycle_end<LSBA_B>(const SmallState2& st, int k, int gmres, in
   return cudaGetLastError();
 }
 
+template <>
+cudaError_t launch_cwy_iter1<LSBA_B>(const SmallState2& st, const double* G, cudaStream_t stream) {
+  k_cwy_iter1<LSBA_B><<<1, 128, 0, stream>>>(st, G);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_cwy_coef<LSBA_B>(const SmallState2& st, const double* G, int k, int inverse,
+                                    cudaStream_t stream) {
+  constexpr int B = LSBA_B;
+  const size_t k1b = (size_t)(k + 1) * B;
+  const size_t smem = sizeof(double) * (k1b * 2 * B + 2 * k1b * B);
+  auto fn = k_cwy_coef<B>;
+  if (smem > 32 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<1, 256, smem, stream>>>(st, G, k, inverse);
+  return cudaGetLastError();
+}
+
 }  // namespace lsba
