@@ -362,7 +362,7 @@ static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
     if (a.J <= 8) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
   } else if constexpr (S == 8) {
-    return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
+    return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
   } else if constexpr (S == 16) {
     return gram_v7_launch<S, 1, 4, 2, false, 2>(c, a, f);
   } else {
@@ -1240,7 +1240,7 @@ static void release(lsba_ctx c) {
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
-                  c->st.Tm, c->st.gpip};
+                  c->st.Tm, c->st.TmT, c->st.gpip};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1426,6 +1426,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   c->st.m = m_max;
   c->st.bmax = s;
   TRY(dalloc(c, &c->st.Tm, (size_t)ldH * ldH));
+  TRY(dalloc(c, &c->st.TmT, (size_t)ldH * ldH));
   TRY(dalloc(c, &c->st.gpip, (size_t)ldH * s));
   c->st.ctl = c->d_ctl;
   {  // progress word in mapped pinned host memory (written by the device, polled by the host)

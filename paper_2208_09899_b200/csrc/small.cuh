@@ -41,6 +41,7 @@ struct SmallState2 {
   int ldH, m, bmax;
   volatile int* prog;   // host-mapped progress word {k_done, active} read by the enqueueing host
   double* Tm;           // BMGS-(I)CWY: T ((m+1)b square, col-major, ld ldH)
+  double* TmT;          // and its transpose (T row-major), for row-wise dot products
   double* gpip;         // BMGS-(I)CWY: H_{1:k,k} in the Gram layout the update kernel reads
 };
 
@@ -571,6 +572,7 @@ k_cwy_iter1(SmallState2 st, const double* __restrict__ G) {
     st.coef[e] = -h;                                   // block 0 (V_1): -H_11
     st.coef[B * B + e] = (r == c) ? 1.0 : 0.0;         // block 1 (W): I
     st.Tm[r + (size_t)c * st.ldH] = (r == c) ? 1.0 : 0.0;   // T_11 = I (line 1)
+    st.TmT[r + (size_t)c * st.ldH] = (r == c) ? 1.0 : 0.0;
   }
   if (tid == 0) *st.flag_dev = 0;
 }
@@ -685,23 +687,39 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     ZP[r + (size_t)c * kb] = t;          // (scratch: YR, column-major kb x B)
   }
   __syncthreads();
+  double* TmT = st.TmT;
+  const int nw = nt >> 5;
   if (inverse) {
     for (int e = tid; e < kb * B; e += nt) {
       const int r = e % kb, c = e / kb;
-      Tm[r + (size_t)(Tcol + c) * ldH] = ZP[r + (size_t)c * kb];
+      const double v = ZP[r + (size_t)c * kb];
+      Tm[r + (size_t)(Tcol + c) * ldH] = v;
+      TmT[(Tcol + c) + (size_t)r * ldH] = v;
     }
   } else {
-    for (int e = tid; e < kb * B; e += nt) {
-      const int r = e % kb, c = e / kb;
-      double t = 0.0;
-      for (int q = r - r % B; q < kb; ++q)           // T block upper triangular (unit diagonal)
-        t += Tm[r + (size_t)q * ldH] * ZP[q + (size_t)c * kb];
-      Tm[r + (size_t)(Tcol + c) * ldH] = -t;
+    // new column = -T_{1:k,1:k} YR: one warp per row r of T (contiguous in TmT), lanes over q
+    for (int r = warp; r < kb; r += nw) {
+      double acc[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] = 0.0;
+      for (int q = (r - r % B) + lane; q < kb; q += 32) {   // T block upper triangular
+        const double t = TmT[q + (size_t)r * ldH];
+#pragma unroll
+        for (int c = 0; c < B; ++c) acc[c] += t * ZP[q + (size_t)c * kb];
+      }
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
+      if (lane < B) {
+        const double v = -sel<B>(acc, lane);
+        Tm[r + (size_t)(Tcol + lane) * ldH] = v;
+        TmT[(Tcol + lane) + (size_t)r * ldH] = v;
+      }
     }
   }
   for (int e = tid; e < B * B; e += nt) {
     const int x = e % B, y = e / B;
     Tm[(kb + x) + (size_t)(Tcol + y) * ldH] = (x == y) ? 1.0 : 0.0;
+    TmT[(Tcol + y) + (size_t)(kb + x) * ldH] = (x == y) ? 1.0 : 0.0;
   }
   __syncthreads();
   // ZP = [Z; P] R^{-1}  (column-major k1b x B)
@@ -716,13 +734,21 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
   }
   __syncthreads();
   if (!inverse) {
-    // Hn = T^T ZP: Hn[r][c] = sum_q T[q][r] ZP[q][c], T[q][r] nonzero for q < (r/B + 1) B
-    for (int e = tid; e < k1b * B; e += nt) {
-      const int r = e % k1b, c = e / k1b;
+    // Hn = T^T ZP: Hn[r][c] = sum_q T[q][r] ZP[q][c] (column r of T, contiguous in Tm), one warp
+    // per r, lanes over q; T[q][r] nonzero for q < (r/B + 1) B
+    for (int r = warp; r < k1b; r += nw) {
+      double acc[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] = 0.0;
       const int qend = (r / B + 1) * B;
-      double t = 0.0;
-      for (int q = 0; q < qend; ++q) t += Tm[q + (size_t)r * ldH] * ZP[q + (size_t)c * k1b];
-      Hn[r + (size_t)c * k1b] = t;
+      for (int q = lane; q < qend; q += 32) {
+        const double t = Tm[q + (size_t)r * ldH];
+#pragma unroll
+        for (int c = 0; c < B; ++c) acc[c] += t * ZP[q + (size_t)c * k1b];
+      }
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
+      if (lane < B) Hn[r + (size_t)lane * k1b] = sel<B>(acc, lane);
     }
   } else {
     // Hn = T^{-T} ZP: forward substitution over block rows (T^T lower, unit diagonal blocks)
