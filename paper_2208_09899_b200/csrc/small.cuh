@@ -835,7 +835,27 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
   __syncthreads();
   // block back substitution, column-oriented
   for (int j = k - 1; j >= 0; --j) {
-    if (warp == 0) {
+    if (warp == 0 && !(use_fom && j == k - 1)) {
+      // the diagonal blocks of the R factor are upper triangular (block-Householder QR):
+      // lane c < B back-substitutes right-hand-side column c
+      if (lane < B) {
+        const int c = lane;
+        double x[B];
+        bool sg = false;
+#pragma unroll
+        for (int r = B - 1; r >= 0; --r) {
+          double t = Xi[(j * B + r) + (size_t)c * kb];
+#pragma unroll
+          for (int q = r + 1; q < B; ++q) t -= Rm[(j * B + r) + (size_t)(j * B + q) * ldR] * x[q];
+          const double d = Rm[(j * B + r) + (size_t)(j * B + r) * ldR];
+          x[r] = t / d;
+          if (!(d != 0.0) || !isfinite(x[r])) sg = true;
+        }
+#pragma unroll
+        for (int r = 0; r < B; ++r) Xi[(j * B + r) + (size_t)c * kb] = x[r];
+        if (sg) sing_s = 1;
+      }
+    } else if (warp == 0) {
       double colv[B];
 #pragma unroll
       for (int r = 0; r < B; ++r) {
