@@ -933,14 +933,30 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
       if (k == 1) {
         if (lane >= B && lane < 2 * B) Z[(size_t)(lane - B) * B + c] = w;
       }
-      for (int j = k - 1; j >= 1; --j) {
+      // reflector set j's vectors and taus are prefetched one set ahead (the sets are applied
+      // in sequence; their loads are independent of the window)
+      auto load_set = [&](int j, double (&v)[B], double (&tau)[B]) {
         const double* V = st.qr_v + (size_t)(j - 1) * st.bmax * 2 * st.bmax;
         const double* T = st.qr_tau + (size_t)(j - 1) * st.bmax;
 #pragma unroll
+        for (int q = 0; q < B; ++q) {
+          v[q] = (lane < 2 * B) ? V[(size_t)q * 2 * st.bmax + lane] : 0.0;
+          tau[q] = T[q];
+        }
+      };
+      double vcur[B], tcur[B];
+      if (k >= 2) load_set(k - 1, vcur, tcur);
+      for (int j = k - 1; j >= 1; --j) {
+        double vnx[B], tnx[B];
+        if (j >= 2) load_set(j - 1, vnx, tnx);
+#pragma unroll
         for (int q = B - 1; q >= 0; --q) {
-          const double v = (lane < 2 * B) ? V[(size_t)q * 2 * st.bmax + lane] : 0.0;
-          const double d = warp_sum(v * w);
-          w -= T[q] * d * v;
+          const double d = warp_sum(vcur[q] * w);
+          w -= tcur[q] * d * vcur[q];
+        }
+        if (j >= 2) {
+#pragma unroll
+          for (int q = 0; q < B; ++q) { vcur[q] = vnx[q]; tcur[q] = tnx[q]; }
         }
         // bottom block (block j) final -> M rows jB..(j+1)B-1
         if (lane >= B && lane < 2 * B) Z[(size_t)(j * B + lane - B) * B + c] = w;
