@@ -179,12 +179,9 @@ lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
  * With BMGS-(I)CWY, lsba_arnoldi_begin also runs Alg 6's first loop iteration, and step k
  * (its iteration k+1) completes Hessenberg column k and forms V_{k+1}. */
 lsba_status lsba_set_skeleton(lsba_ctx ctx, lsba_skel skel);
-/* Kernel implementation choice (classical inner product): 0 = auto (standalone SpMM +
- * latency-tuned streaming tensor-core Gram v7 + projection: DMMA for s in {8,16}, DFMA
- * otherwise), 1 = plain DFMA kernels, 2 = SpMM fused into the tensor-core Gram pass (gather
- * warps), 3 = tensor-core Gram with 8-byte fragment loads, 4 = TMA-staged tensor-core Gram,
- * 5 = shared-memory-tiled tensor-core Gram v5, 6 = barrier-free tensor-core Gram v6.
- * For parity tests and measurements of every path. */
+/* Kernel implementation choice: 0 = default (streaming tensor-core v7 Gram / streaming global
+ * Gram, DMMA projection for s in {8, 16}, DFMA otherwise, small step fused into the Gram on one
+ * rank), 1 = plain DFMA Gram and projection kernels (for parity tests of both paths). */
 lsba_status lsba_set_kernel_variant(lsba_ctx ctx, int32_t variant);
 
 /* Per-kernel timing with CUDA events on the context stream.  Kernel ids: */

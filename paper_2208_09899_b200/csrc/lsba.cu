@@ -108,11 +108,9 @@ struct lsba_ctx_ {
   int force_flag_k = 0;
   bool forced_done = false;
   int variant = 0;
-  int fuse_spmm = 0;   // 1: SpMM fused into the tensor-core Gram pass (gather warps)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
   int skel_default = LSBA_SKEL_BCGS_PIP;  // lsba_set_skeleton: step API and lsba_solve_host
-  int gram_impl = 0;   // unfused mode: 0 v6 (barrier-free), 3 v5, 1 TMA-staged, 2 v3
   int64_t launches = 0;
   int64_t ws_bytes = 0;
   std::string err;
@@ -295,23 +293,6 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
   return LSBA_OK;
 }
 
-template <int S>
-static bool dmma_gram_ok(lsba_ctx c, int J, int ip, const double* X, const double* Y) {
-  if (ip == LSBA_IP_GLOBAL || c->variant != 0) return false;
-  if (!in_basis(c, X) || !in_basis(c, Y)) return false;   // padded rows required
-  if constexpr (!(S == 1 || S == 2 || S == 4 || S == 8 || S == 16)) {
-    return false;
-  } else {
-    if constexpr (S != 1) {
-      if (c->gram_impl == 0 && !c->fuse_spmm) return c->d_tickets != nullptr;   // v7: any J
-    }
-    using Cg = GramCfg<S>;
-    const int NG = (J + Cg::JP - 1) / Cg::JP;
-    return (NG + 1 + Cg::NWG - 1) / Cg::NWG + 1 <= Cg::JMAX && c->d_tickets != nullptr &&
-           (size_t)c->gram_grid * J * S * S <= c->part_cap;
-  }
-}
-
 // The previous step's update kernel (stream 2) overlaps this step's SpMM; everything after the
 // SpMM reads its decision or the small state it writes, so the main stream joins it here.
 static lsba_status wait_update(lsba_ctx c) {
@@ -380,8 +361,9 @@ __global__ void k_interleave2(int R, int b, const double* __restrict__ G1, const
 
 // ---------------------------------------------------------------- a1+a2: (SpMM +) Gram (+ allreduce)
 // G (device, c->d_G) = <[X_0..X_{J-1}], Y>; classical (J s) x s row-major; global J scalars
-// (scaled by 1/s).  If Vk != nullptr, Y = W is first computed as A Vk (fused into the Gram
-// pass on the tensor-core path).  Exactly one allreduce when P > 1 (the step's single sync).
+// (scaled by 1/s).  If Vk != nullptr, Y = W is first computed as A Vk.  Exactly one allreduce
+// when P > 1 (the step's single sync).  coef_k >= 0: the small step of step coef_k may be fused
+// into the Gram's tail (one rank); *coef_fused says whether it was.
 template <int S>
 static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, double* Y, int ip,
                           const double* Vk, const int* active, int coef_k, const CycleParams* prm,
@@ -389,191 +371,52 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
   const bool gl = (ip == LSBA_IP_GLOBAL);
   const size_t E = gl ? (size_t)J : (size_t)J * S * S;
   if (coef_fused) *coef_fused = false;
-  if (dmma_gram_ok<S>(c, J, ip, X, Y)) {
-    if constexpr (S == 1 || S == 2 || S == 4 || S == 8 || S == 16) {
-      if (Vk && !c->fuse_spmm) {   // standalone high-occupancy SpMM, then the Gram pass
-        TRY(spmm_t<S>(c, Vk, Y, active));
-        Vk = nullptr;
+  if (Vk) TRY(spmm_t<S>(c, Vk, Y, active));
+  TRY(wait_update(c));
+  const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
+  const bool slots = c->variant == 0 && in_basis(c, X) && in_basis(c, Y) && c->d_tickets;
+  constexpr bool v7_s = (S == 2 || S == 4 || S == 8 || S == 16);
+  if (slots && ((!gl && v7_s) || (gl && S % 2 == 0))) {
+    LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
+    if (c->n > 0) {
+      GramArgs a;
+      a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
+      a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride;
+      // the J blocks X_0..X_{J-1} (the last is Y itself when y_is_block), Y as the B operand
+      a.J = J; a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
+      a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
+      a.active = active;
+      GramFuse f{};
+      // fuse the small step into the Gram tail on one rank (no allreduce in between) while its
+      // Gram copy fits next to the partials (<= 64 KB of shared memory)
+      if (coef_k >= 0 && coef_fused && c->nranks == 1 && E * sizeof(double) <= 64 * 1024) {
+        f.on = 1;
+        f.st = c->st;
+        f.k = coef_k;
+        f.prm = prm ? *prm : CycleParams{};
+        *coef_fused = true;
       }
-      TRY(wait_update(c));
-      if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
-        using G6 = G6Cfg<S>;
-        const int NG6 = (J - 1 + G6::PB - 1) / G6::PB + 1;
-        if (!Vk && c->gram_impl == 0) {
-          const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
-          LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
-          if (c->n > 0) {
-            GramArgs a;
-            a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-            a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride;
-            // v7 takes the blocks uniformly: J blocks X_0..X_{J-1} (the last is Y itself when
-            // y_is_block) and Y as the B operand
-            a.J = J; a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
-            a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
-            a.active = active;
-            GramFuse f{};
-            // fuse the small step into the Gram tail on one rank (no allreduce in between)
-            // while its Gram copy fits next to the partials (<= 64 KB of shared memory)
-            if (coef_k >= 0 && coef_fused && c->nranks == 1 && E * sizeof(double) <= 64 * 1024) {
-              f.on = 1;
-              f.st = c->st;
-              f.k = coef_k;
-              f.prm = prm ? *prm : CycleParams{};
-              *coef_fused = true;
-            }
-            TRY(gram_v7<S>(c, a, f));
-          } else {
-            CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
-            if (coef_fused) *coef_fused = false;
-          }
-          if (c->nranks > 1)
-            CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
-          return LSBA_OK;
-        }
-        if (!Vk && c->gram_impl == 6 && (NG6 + G6::NW - 1) / G6::NW <= G6::GMAX) {
-          const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
-          LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
-          if (c->n > 0) {
-            GramArgs a;
-            a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-            a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
-            a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
-            a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
-            a.active = active;
-            const size_t smem = sizeof(double) * E;
-            auto fn = k_gram_v6<S>;
-            if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int occ = 1;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G6::NTHR, smem));
-            const int grid = std::max(1, std::min(std::min(occ, 4) * c->n_sms, cdiv(cdiv(c->n, 4), 64)));
-            fn<<<grid, G6::NTHR, smem, c->stream>>>(a);
-            CKL();
-          } else {
-            CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
-          }
-          if (c->nranks > 1)
-            CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
-          return LSBA_OK;
-        }
-      }
-      if constexpr (S == 2 || S == 4 || S == 8 || S == 16) {
-        using G5 = G5Cfg<S>;
-        const int NG5 = (J - 1 + G5::PB - 1) / G5::PB + 1;
-        if (!Vk && (c->gram_impl == 0 || c->gram_impl == 3) && (NG5 + G5::NW - 1) / G5::NW + 1 <= G5::JMAX) {
-          const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
-          LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
-          if (c->n > 0) {
-            GramArgs a;
-            a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-            a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
-            a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
-            a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
-            a.active = active;
-            const size_t smem = sizeof(double) * (2 * (size_t)G5::T * S + E);
-            auto fn = k_gram_v5<S>;
-            if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int occ = 1;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G5::NTHR, smem));
-            const int grid = std::max(1, std::min(std::min(occ, 4) * c->n_sms, cdiv(c->n, G5::T)));
-            fn<<<grid, G5::NTHR, smem, c->stream>>>(a);
-            CKL();
-          } else {
-            CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
-          }
-          if (c->nranks > 1)
-            CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
-          return LSBA_OK;
-        }
-      }
-      TRY(wait_update(c));
-      if (!Vk && c->gram_impl == 1) {    // TMA-staged tensor-core Gram
-        const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
-        LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
-        if (c->n > 0) {
-          GramArgs a;
-          a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-          a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
-          a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
-          a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
-          a.active = active;
-          using TC = TmaCfg<S>;
-          const size_t smem = (size_t)TC::R * TC::STAGE_BYTES + (size_t)TC::WR * TC::TILE_BYTES + sizeof(double) * E;
-          auto fn = k_gram_tma<S>;
-          CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          const int grid = std::min(c->n_sms, std::max(1, cdiv(c->n, TC::T)));
-          fn<<<grid, TC::NTHR, smem, c->stream>>>(a);
-          CKL();
-        } else {
-          CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
-        }
-        if (c->nranks > 1)
-          CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
-        return LSBA_OK;
-      }
-      if (Vk) TRY(halo_t<S>(c, Vk));
-      const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
-      const double bytes = (Vk ? 12.0 * c->nnz + 4.0 * (c->n + 1) : 0.0) +
-                           8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S;
-      LaunchScope Ls(c, LSBA_K_GRAM, bytes);
-      if (c->n > 0) {
-        GramArgs a;
-        a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-        a.Vk = Vk; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride; a.J = J;
-        a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
-        a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
-        a.active = active;
-        const size_t smem = sizeof(double) * (2 * (size_t)GramCfg<S>::T * S + E);
-        auto fn = k_spmm_gram<S>;
-        if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int occ = 1;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, GramCfg<S>::NTHR, smem));
-        const int grid = std::max(1, std::min(occ * c->n_sms, c->gram_grid));
-        fn<<<grid, GramCfg<S>::NTHR, smem, c->stream>>>(a);
-        CKL();
+      if (!gl) {
+        if constexpr (v7_s) TRY(gram_v7<S>(c, a, f));
       } else {
-        CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
-      }
-    }
-  } else {
-    if (Vk) TRY(spmm_t<S>(c, Vk, Y, active));
-    TRY(wait_update(c));
-    if constexpr (S % 2 == 0) {
-      if (gl && c->variant == 0 && in_basis(c, X) && in_basis(c, Y) && c->d_tickets) {
-        // streaming global Gram (gram7.cuh), small step fused on one rank
-        const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
-        LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
-        if (c->n > 0) {
-          GramArgs a;
-          a.n = c->n; a.rp = c->d_rp; a.ci = c->d_ci; a.va = c->d_va;
-          a.Vk = nullptr; a.Vghost = c->d_ghost; a.X = X; a.xstride = xstride;
-          a.J = J; a.y_alias = y_is_block ? 1 : 0; a.Y = Y; a.zeros = c->d_zeros;
-          a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
-          a.active = active;
-          GramFuse f{};
-          if (coef_k >= 0 && coef_fused && c->nranks == 1) {
-            f.on = 1;
-            f.st = c->st;
-            f.k = coef_k;
-            f.prm = prm ? *prm : CycleParams{};
-            *coef_fused = true;
-          }
+        if constexpr (S % 2 == 0) {
+          // streaming global Gram (gram7.cuh)
           const int grid = std::max(1, std::min(3 * c->n_sms, cdiv(cdiv((long)c->slot, 2), 256)));
           k_gram_gl2<S><<<grid, 256, sizeof(double) * (J + 1), c->stream>>>(a, f);
           CKL();
-        } else {
-          CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
-          if (coef_fused) *coef_fused = false;
         }
-        if (c->nranks > 1)
-          CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
-        return LSBA_OK;
       }
+    } else {
+      CK(cudaMemsetAsync(c->d_G, 0, sizeof(double) * E, c->stream));
+      if (coef_fused) *coef_fused = false;
     }
+  } else {
+    // DFMA fallback (odd s, s = 1, variant 1, non-slot inputs): per-CTA partials + fixed-order sum
     const int gx = gl ? J : J * (S / GramTA<S>::value);
     int P = std::max(1, std::min(cdiv(std::max(c->n, 1), 256), cdiv(kGramCtas, gx)));
     if ((size_t)P * E > c->part_cap) P = std::max(1, (int)(c->part_cap / E));
     {
-      LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * J + ((X + (size_t)(J - 1) * xstride == Y) ? 0.0 : 8.0 * c->n * S));
+      LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * J + (y_is_block ? 0.0 : 8.0 * c->n * S));
       dim3 grid(gx, P);
       if (gl)
         k_gram_gl<S><<<grid, kThreads, 0, c->stream>>>(c->n, X, xstride, J, Y, c->d_part, active);
@@ -1683,10 +1526,8 @@ extern "C" lsba_status lsba_set_skeleton(lsba_ctx c, lsba_skel skel) {
 
 extern "C" lsba_status lsba_set_kernel_variant(lsba_ctx c, int32_t variant) {
   if (!c) return LSBA_E_ARG;
-  if (variant < 0 || variant > 6) return fail(c, LSBA_E_ARG, "variant must be 0..6");
-  c->variant = variant == 1 ? 1 : 0;
-  c->fuse_spmm = variant == 2 ? 1 : 0;
-  c->gram_impl = variant == 3 ? 2 : (variant == 4 ? 1 : (variant == 5 ? 3 : (variant == 6 ? 6 : 0)));
+  if (variant < 0 || variant > 1) return fail(c, LSBA_E_ARG, "variant must be 0 or 1");
+  c->variant = variant;
   return LSBA_OK;
 }
 

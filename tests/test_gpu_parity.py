@@ -353,7 +353,7 @@ def test_dfma_variant_matches(L):
     from oracle import lsba_oracle as O
     A, B, _ = get_problem("random_16K")
     arn = oracle_steps(A, B, "cl", 5)
-    for variant in (0, 1, 2, 3, 4, 5, 6):
+    for variant in (0, 1):
         H, beta, Vs, _ = gpu_steps(L, A, B, "cl", 5, variant=variant)
         for j, (v, vo) in enumerate(zip(Vs, arn.V)):
             assert np.linalg.norm(v - vo) <= 1e-10 * np.linalg.norm(vo), (variant, j)

@@ -1,7 +1,7 @@
 // gram_bench.cu — standalone timing of the Gram-pass kernel candidates on the bench shapes
 // (dev tool; the product path is liblsba.so).  For (n, s, J): basis of J padded slots with the
 // last slot aliased as W, G = [X_0..X_{J-1}]^T W.  Reports us/launch and algorithmic GB/s
-// (8 n s J bytes), and the max relative difference of G against k_gram_v6.
+// (8 n s J bytes), and the max relative difference of G against k_gram_v7<S, 2, 4, 3>.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include -o build_tools/gram_bench tools/gram_bench.cu
 #include <cstdio>
 #include <cstdlib>
@@ -48,23 +48,6 @@ static GramArgs args(const Bufs& B, int n, int J) {
   a.Y = B.V + (size_t)(J - 1) * B.stride; a.zeros = B.zeros;
   a.part = B.part; a.gpart = B.gpart; a.tickets = B.tickets; a.G = B.G; a.active = nullptr;
   return a;
-}
-
-template <int S>
-static std::vector<double> run_v6(const Bufs& B, int n, int J, double* us) {
-  using G6 = G6Cfg<S>;
-  GramArgs a = args(B, n, J);
-  const size_t smem = sizeof(double) * J * S * S;
-  auto fn = k_gram_v6<S>;
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 * 1024)));
-  int occ = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G6::NTHR, smem));
-  const int grid = std::max(1, std::min(std::min(occ, 4) * 148, (n / 4 + 63) / 64));
-  *us = time_it([&] { fn<<<grid, G6::NTHR, smem>>>(a); }, 10);
-  CK(cudaGetLastError());
-  std::vector<double> G(J * S * S);
-  CK(cudaMemcpy(G.data(), B.G, sizeof(double) * G.size(), cudaMemcpyDeviceToHost));
-  return G;
 }
 
 template <int S, int GMAX, int U, int MINB, bool WIN = true>
@@ -166,9 +149,10 @@ static void sweep(int n, std::vector<int> Js) {
   CK(cudaMemset(B.tickets, 0, 4096 * sizeof(unsigned)));
   for (int J : Js) {
     const double bytes = 8.0 * n * S * J;
-    double us6;
-    auto ref = run_v6<S>(B, n, J, &us6);
-    printf("s=%d n=%d J=%d (%.0f MB)\n   v6               : %8.1f us %7.0f GB/s\n", S, n, J, bytes / 1e6, us6, bytes / us6 / 1e3);
+    double us0;
+    int grid0;
+    auto ref = run_v7<S, 2, 4, 3>(B, n, J, &us0, &grid0);   // reference for the diffs
+    printf("s=%d n=%d J=%d (%.0f MB)\n", S, n, J, bytes / 1e6);
     v7_line<S, 3, 4, 3>(B, n, J, ref, bytes);
     v7_line<S, 2, 4, 3>(B, n, J, ref, bytes);
     v7_line<S, 2, 8, 3>(B, n, J, ref, bytes);
