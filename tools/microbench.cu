@@ -42,6 +42,28 @@ __global__ void k_dmma(double* out, int iters, double a) {
   if (s == 1234.5) out[0] = s;
 }
 
+__global__ void k_mixed(double* out, int iters, double a) {
+  double d[4][2];
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) d[i][0] = d[i][1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  double b = threadIdx.x * 1e-3;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dmma(d[i][0], d[i][1], a, b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, 1.0);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s += d[i][0] + d[i][1];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1234.5) out[0] = s;
+}
+
 template <int U>
 __global__ void k_read(const double2* __restrict__ p, size_t n2, double* out) {
   double2 acc = make_double2(0, 0);
@@ -101,6 +123,17 @@ int main() {
     double mac = (double)grid * (block / 32) * iters * 8 * 256;
     printf("DMMA  grid %5d: %.2f TFLOP/s (%.1f MAC/clk/SM)\n", grid, 2 * mac / ms / 1e9,
            mac / (ms * 1e-3) / sms / (clk * 1e3));
+  }
+  for (int occ : {8, 16}) {
+    const int grid = sms * occ, block = 256;
+    k_mixed<<<grid, block>>>(out, 16, 1.0);
+    cudaEventRecord(a); k_mixed<<<grid, block>>>(out, iters, 1.0); cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    // per warp-iteration: 4 DMMA (4 x 256 MAC) + 8 DFMA per lane (8 x 32 FMA)
+    const double mac = (double)grid * (block / 32) * iters * (4.0 * 256 + 8.0 * 32);
+    printf("MIXED grid %5d: %.1f MAC/clk/SM (DMMA share %.0f%%)\n", grid,
+           mac / (ms * 1e-3) / sms / (clk * 1e3), 100.0 * 1024 / 1280);
   }
   const size_t bytes = (size_t)4 << 30;
   double2* p; CK(cudaMalloc(&p, bytes));
