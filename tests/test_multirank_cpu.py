@@ -9,7 +9,8 @@ and checks it against the single-rank oracle:
   * the halo-extended local SpMM equals the global SpMM rows bitwise (same CSR order);
   * the allreduced partial Gram equals the global Gram to rounding;
   * K distributed BCGS-PIP steps (one halo + one allreduce each) reproduce the single-rank
-    H and basis, with exactly K + 1 Gram allreduces (IO + K steps).
+    H and basis, with exactly K + 1 Gram allreduces (IO + K steps);
+  * the same for K BMGS-CWY steps (Alg 6): loop iteration 1 + K steps, K + 1 allreduces.
 """
 import os
 import socket
@@ -126,7 +127,34 @@ def _worker(rank, world, port, kind, K, out):
             Hbar[:k * s, (k - 1) * s:k * s] = Hcol
             Hbar[k * s:(k + 1) * s, (k - 1) * s:k * s] = R
         assert n_allreduce[0] == K + 1
-        out[rank] = dict(H=Hbar, beta=beta, V=np.stack(Vs), rows=(r0, r1))
+
+        # (4) BMGS-CWY (Alg 6): after IO and loop iteration 1, every Arnoldi step is one halo
+        # exchange + ONE allreduce of the two-block Gram <[V_1..V_k U], [U W]>
+        n_allreduce[0] = 0
+        Vc = [Vs[0]]
+        W = spmm_dist(Vc[0])
+        H11 = allreduce(O.ip_cl([Vc[0]], W))                           # iteration 1
+        U = W - Vc[0] @ H11
+        Hc = np.zeros(((K + 1) * s, K * s))
+        Hc[:s, :s] = H11
+        T = np.eye((K + 1) * s)
+        for k in range(1, K + 1):
+            W = spmm_dist(U)
+            Gk = allreduce(O.ip_cl(Vc + [U], np.concatenate([U, W], axis=1)))   # the single sync
+            Y, Z, Om, Pt = Gk[:k * s, :s], Gk[:k * s, s:], Gk[k * s:, :s], Gk[k * s:, s:]
+            R, flag = O.chol_flag(Om)
+            assert not flag
+            Ri = O.right_trsm_upper(np.eye(s), R)
+            P = np.linalg.solve(R.T, Pt)
+            T[:k * s, k * s:(k + 1) * s] = -T[:k * s, :k * s] @ (Y @ Ri)
+            Hn = T[:(k + 1) * s, :(k + 1) * s].T @ (np.vstack([Z, P]) @ Ri)
+            Vc.append(U @ Ri)
+            Hc[k * s:(k + 1) * s, (k - 1) * s:k * s] = R
+            if k < K:
+                Hc[:(k + 1) * s, k * s:(k + 1) * s] = Hn
+            U = W @ Ri - np.concatenate(Vc, axis=1) @ Hn
+        assert n_allreduce[0] == K + 1
+        out[rank] = dict(H=Hbar, beta=beta, V=np.stack(Vs), rows=(r0, r1), Hc=Hc, Vc=np.stack(Vc))
     finally:
         dist.destroy_process_group()
 
@@ -162,8 +190,17 @@ def test_distributed_pip_steps_match_single_rank(world, kind):
     assert not arn.begin(B)
     for _ in range(K):
         assert not arn.step().flag
+    cwy = O.CwyArnoldi(A, "cl", K, s)
+    assert not cwy.begin(B)
+    for _ in range(K):
+        assert not cwy.step().flag
     for r in range(world):
         d = res[r]
+        assert np.array_equal(d["Hc"], res[0]["Hc"])
+        np.testing.assert_allclose(d["Hc"], cwy.Hbar, rtol=0, atol=1e-11 * np.abs(cwy.Hbar).max())
+        for j in range(K + 1):
+            r0, r1 = d["rows"]
+            assert np.linalg.norm(d["Vc"][j] - cwy.V[j][r0:r1]) <= 1e-11 * np.linalg.norm(cwy.V[j])
         # replicated small state: identical on every rank (same allreduce results)
         assert np.array_equal(d["H"], res[0]["H"]) and np.array_equal(d["beta"], res[0]["beta"])
         np.testing.assert_allclose(d["H"], arn.Hbar, rtol=0, atol=1e-11 * np.abs(arn.Hbar).max())
