@@ -419,6 +419,91 @@ class CwyArnoldi:
 
 
 # --------------------------------------------------------------------------------------
+# Comparison skeletons: BMGS-Arnoldi (Alg 2) and BCGS-PIO-Arnoldi (Alg 4)
+# --------------------------------------------------------------------------------------
+
+
+class BmgsArnoldi(PipArnoldi):
+    """Alg 2 as a resumable object: per step k, k block inner products
+    H_{j,k} = <V_j, W> each followed by W = W - V_j H_{j,k} (k syncs), then
+    [V_{k+1}, H_{k+1,k}] = IO(W) (one more sync; CholQR for cl, the global norm for gl).
+    A flag of that IO is the step's NaN-flag."""
+
+    def step(self, force_flag: bool = False) -> StepResult:
+        b, k = self.b, len(self.V)
+        W = spmm(*self.A, self.V[-1])
+        Hcol = np.zeros((k * b, b))
+        for j in range(k):
+            if self.ip == "cl":
+                Hj = ip_cl([self.V[j]], W)
+                W = W - self.V[j] @ Hj
+            else:
+                Hj = np.array([[ip_gl([self.V[j]], W)[0]]])
+                W = W - self.V[j] * Hj[0, 0]
+            Hcol[j * b:(j + 1) * b] = Hj
+        self.Hbar[: k * b, (k - 1) * b: k * b] = Hcol
+        if self.ip == "cl":
+            Vn, R, flag = io_cl(W)
+        else:
+            Vn, R, flag = io_gl(W)
+        flag = bool(flag) or force_flag
+        if flag:
+            return StepResult(Hcol, R, None, True, W)
+        Rm = R if self.ip == "cl" else np.array([[R]])
+        self.Hbar[k * b:(k + 1) * b, (k - 1) * b: k * b] = Rm
+        self.V.append(Vn)
+        self.k = k
+        return StepResult(Hcol, R, Vn, False, W)
+
+
+class PioArnoldi(PipArnoldi):
+    """Alg 4, BCGS-PIO: H_{1:k,k} = <V_k-stack, W> (sync 1); the IO of
+    diag(W, H_{1:k,k}) gives the R factors W~ = chol(<W, W>) (sync 2) and H~ = chol(H^* H)
+    (replicated, no sync); H_{k+1,k} = chol(W~^* W~ - H~^* H~); V_{k+1} = (W - V H) H_{k+1,k}^{-1}.
+    Reading R26: the IO muscle is CholQR (the paper's solver experiments use CholQR for the
+    classical IO); a flag of any of the three Cholesky factorisations is the
+    step's NaN-flag.  Global: W~ = ||W||_gl, H~ = ||H|| (Euclidean norm of the k scalars)."""
+
+    def step(self, force_flag: bool = False) -> StepResult:
+        b, k = self.b, len(self.V)
+        W = spmm(*self.A, self.V[-1])
+        if self.ip == "cl":
+            Hcol = ip_cl(list(self.V), W)                       # line 4
+            Wt, f1 = chol_flag(ip_cl([W], W))                    # line 5 (IO of W)
+            Ht, f2 = chol_flag(Hcol.T @ Hcol)                    # line 5 (IO of H, local)
+            R, f3 = chol_flag(Wt.T @ Wt - Ht.T @ Ht) if not (f1 or f2) else (Wt, True)   # line 6
+            flag = f1 or f2 or f3 or force_flag
+        else:
+            Hcol = ip_gl(list(self.V), W)
+            om = ip_gl([W], W)[0]
+            hh = float(np.dot(Hcol, Hcol))
+            wt = math.sqrt(om) if om > 0 else float("nan")
+            ht = math.sqrt(hh) if hh > 0 else float("nan")
+            rad = wt * wt - ht * ht
+            flag = not (rad > 0.0) or not math.isfinite(rad) or force_flag
+            R = math.sqrt(rad) if not flag else float("nan")
+        b_ = self.b
+        Hc = Hcol.reshape(k * b_, b_) if self.ip == "cl" else np.asarray(Hcol).reshape(k, 1)
+        self.Hbar[: k * b_, (k - 1) * b_: k * b_] = Hc
+        if flag:
+            return StepResult(Hcol, R, None, True, W)
+        if self.ip == "cl":
+            P = W - np.concatenate(list(self.V), axis=1) @ Hcol
+            Vn = right_trsm_upper(P, R)
+            Rm = R
+        else:
+            P = W.copy()
+            for j in range(k):
+                P -= self.V[j] * Hcol[j]
+            Vn = P / R
+            Rm = np.array([[R]])
+        self.Hbar[k * b_:(k + 1) * b_, (k - 1) * b_: k * b_] = Rm
+        self.V.append(Vn)
+        self.k = k
+        return StepResult(Hcol, R, Vn, False, W)
+
+
+# --------------------------------------------------------------------------------------
 # BMGS-Arnoldi, Alg 2 (PAPER.md:164-178) — independent cross-check only (pin P5)
 # --------------------------------------------------------------------------------------
 
@@ -541,17 +626,25 @@ class SolveInfo:
     # Paper accounting (PAPER.md:650 tables; pin P14): BCGS-PIP: sync = iterations + cycles,
     # A-ct = iterations, V-ct = 3 iterations; BMGS-(I)CWY: one
     # more A-application, sync and block evaluation per cycle (the lagged normalisation).
+    # BMGS (Alg 2): k+1 syncs per step plus IO, A-ct = iterations, V-ct =
+    # 2 iterations; BCGS-PIO (Alg 4): two syncs per step (Table 1).
     @property
     def syncs(self):
-        return self.iterations + (2 if self.skel != "pip" else 1) * self.cycles
+        if self.skel == "bmgs":
+            return sum(k * (k + 3) // 2 for k in self.cycle_lengths) + self.cycles
+        if self.skel == "pio":
+            return 2 * self.iterations + self.cycles
+        return self.iterations + (2 if self.skel in ("cwy", "icwy") else 1) * self.cycles
 
     @property
     def matvecs(self):
-        return self.iterations + (self.cycles if self.skel != "pip" else 0)
+        return self.iterations + (self.cycles if self.skel in ("cwy", "icwy") else 0)
 
     @property
     def basis_evals(self):
-        return 3 * self.iterations + (self.cycles if self.skel != "pip" else 0)
+        if self.skel == "bmgs":
+            return 2 * self.iterations
+        return 3 * self.iterations + (self.cycles if self.skel in ("cwy", "icwy") else 0)
 
     @property
     def restarts(self):
@@ -587,6 +680,10 @@ def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
         arn = PipArnoldi(A, ip, m, s)
     elif skel in ("cwy", "icwy"):
         arn = CwyArnoldi(A, ip, m, s, inverse=(skel == "icwy"))
+    elif skel == "bmgs":
+        arn = BmgsArnoldi(A, ip, m, s)
+    elif skel == "pio":
+        arn = PioArnoldi(A, ip, m, s)
     else:
         raise ValueError(f"unknown skeleton {skel!r}")
     forced_done = False

@@ -455,3 +455,57 @@ def test_cwy_tiny_config_vs_dense_lu(ip, mod, skel):
     assert info.outcome == O.CONVERGED and info.true_relres <= p.tol
     Xs = np.linalg.solve(dense(A, p.n), p.B)
     assert np.linalg.norm(X - Xs) <= 100 * p.tol * np.linalg.norm(Xs)
+
+
+# ---------------------------------------------------------------- BMGS (Alg 2), BCGS-PIO (Alg 4)
+def test_paper_tridiag1000_bmgs_counts(golden_dir):
+    """Appendix tridiag table: gl-BMGS-FOM reproduces 9 cycles / 621
+    iterations / A-ct 621 / V-ct 1242 / 22401 syncs exactly under the paper's error measure;
+    cl-BMGS-FOM finishes in 2 cycles, 94 +- 3 iterations, V-ct = 2 iterations and
+    sync = sum over cycles of k(k+3)/2 + 1 (k+1 syncs per step plus IO; 2881 for 70 + 24)."""
+    tab = json.load(open(os.path.join(golden_dir, "paper_tridiag_table3.json")))["rows"]
+    n = 1000
+    A, B = tridiag(n), tridiag_rhs(n)
+    Xs = np.linalg.solve(dense(A, n), B)
+    X, info = O.solve(A, B, m=70, tol=1e-10, max_restarts=100, ip="gl", mod="fom",
+                      stop_on="error", X_star=Xs, skel="bmgs")
+    row = tab["gl-BMGS-gl-FOM"]
+    assert (info.cycles, info.iterations, info.matvecs, info.basis_evals, info.syncs) == \
+        (row["cycles"], row["iterations"], row["A_ct"], row["V_ct"], row["sync_ct"])
+    X, info = O.solve(A, B, m=70, tol=1e-10, max_restarts=100, ip="cl", mod="fom",
+                      stop_on="error", X_star=Xs, skel="bmgs")
+    row = tab["cl-BMGS-CholQR-FOM"]
+    assert info.cycles == row["cycles"] and abs(info.iterations - row["iterations"]) <= 3
+    assert info.basis_evals == 2 * info.iterations and info.matvecs == info.iterations
+    # the sync formula reproduces the paper's count at the paper's cycle lengths (70 + 24)
+    assert sum(k * (k + 3) // 2 for k in (70, 24)) + 2 == row["sync_ct"]
+
+
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+def test_pio_equals_bmgs_when_well_conditioned(ip):
+    """BCGS-PIO (Alg 4) builds the Arnoldi decomposition of BMGS-Arnoldi in exact arithmetic."""
+    p = make_twin(3)
+    A = (p.row_ptr, p.col_idx, p.vals)
+    V, H, beta = O.bmgs_arnoldi(A, p.B, 6, ip)
+    arn = O.PioArnoldi(A, ip, 6, p.s)
+    assert not arn.begin(p.B)
+    for _ in range(6):
+        assert not arn.step().flag
+    assert np.linalg.norm(arn.Hbar - H) <= 1e-10 * np.linalg.norm(H)
+    for v, vo in zip(arn.V, V):
+        assert np.linalg.norm(v - vo) <= 1e-10 * np.linalg.norm(vo)
+
+
+def test_sec4_pio_flags_and_bmgs_does_not(golden_dir):
+    """Sec 4: on tridiag(100) with m = 50, BCGS-PIO gives up (NaN-flag) between
+    16 and 36 iterations like BCGS-PIP, while BMGS completes all 50 steps."""
+    facts = json.load(open(os.path.join(golden_dir, "paper_sec4_tridiag100.json")))["facts"]
+    A, B = tridiag(100), tridiag_rhs(100)
+    arn = O.PioArnoldi(A, "cl", 50, 2)
+    assert not arn.begin(B)
+    flag_at = next((k for k in range(1, 51) if arn.step().flag), None)
+    assert flag_at is not None
+    assert facts["earliest_observed_failure"] <= flag_at <= facts["pip_max_completed_iterations"] + 1
+    arn = O.BmgsArnoldi(A, "cl", 50, 2)
+    assert not arn.begin(B)
+    assert not any(arn.step().flag for _ in range(50))
