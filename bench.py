@@ -57,6 +57,10 @@ def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks, skel="pip"):
     blk = 8.0 * n * s
     if skel == "pip":
         return iters * (A + blk) + 2 * blk * gram_blocks + blk * (iters + 7 * cycles)
+    if skel == "bmgs":     # per step: SpMM 2, k x (Gram 2 + update of W 3), IO 3: A + 8ns(5k+5)
+        return iters * A + 5 * blk * gram_blocks + blk * (iters + 7 * cycles)
+    if skel == "pio":      # per step: SpMM 2, Gram k+1, <W,W> 1, projection k+2: A + 8ns(2k+5)
+        return iters * (A + 3 * blk) + 2 * blk * gram_blocks + blk * (iters + 7 * cycles)
     return iters * (A + 6 * blk) + 2 * blk * gram_blocks + blk * (iters + 14 * cycles)
 
 
@@ -220,8 +224,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
-    ap.add_argument("--skel", default="pip", choices=["pip", "cwy", "icwy"],
-                    help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3) or BMGS-CWY / -ICWY (Alg 6)")
+    ap.add_argument("--skel", default="pip", choices=["pip", "cwy", "icwy", "bmgs", "pio"],
+                    help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3), BMGS-CWY / -ICWY (Alg 6), or the "
+                         "comparison baselines BMGS (Alg 2) and BCGS-PIO (Alg 4)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
 
@@ -378,7 +383,8 @@ def main():
             "block_steps_per_s": steps_per_s, "ms_per_block_step": ms / iters,
             "pct_roofline": {"of_measured_hbm": gbs / (peak * world), "of_8TBps_nominal": gbs / (8000.0 * world)},
             "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
-                       "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY"}[args.skel]
+                       "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY",
+                                                          "bmgs": "BMGS", "pio": "BCGS-PIO"}[args.skel]
                                  + " skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO"),
                        "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
                                       f"{iters / args.steps:.1f} block steps)") if full_solve

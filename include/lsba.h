@@ -49,8 +49,15 @@ typedef enum { LSBA_IP_CLASSICAL = 0, LSBA_IP_GLOBAL = 1 } lsba_ip;
 
 /* Gram-Schmidt skeleton (Table 2): BCGS-PIP (Alg 3) and
  * BMGS-CWY / BMGS-ICWY (Alg 6; one block inner product per iteration with the
- * normalisation lagged by one iteration: m+1 A-applications and m+2 syncs per cycle). */
-typedef enum { LSBA_SKEL_BCGS_PIP = 0, LSBA_SKEL_BMGS_CWY = 1, LSBA_SKEL_BMGS_ICWY = 2 } lsba_skel;
+ * normalisation lagged by one iteration: m+1 A-applications and m+2 syncs per cycle), and the
+ * comparison skeletons BMGS (Alg 2) and BCGS-PIO (Alg 4). */
+typedef enum {
+  LSBA_SKEL_BCGS_PIP = 0,    /* Alg 3: one sync per step (the north star's skeleton)          */
+  LSBA_SKEL_BMGS_CWY = 1,    /* Alg 6 (red): one sync per step, normalisation lagged           */
+  LSBA_SKEL_BMGS_ICWY = 2,   /* Alg 6 (blue)                                                   */
+  LSBA_SKEL_BMGS = 3,        /* Alg 2: k+1 syncs per step (comparison baseline)                */
+  LSBA_SKEL_BCGS_PIO = 4     /* Alg 4: two syncs per step (comparison baseline)                */
+} lsba_skel;
 
 /* SPEC.md:327 outcome of a solve. */
 typedef enum { LSBA_CONVERGED = 0, LSBA_MAX_RESTARTS = 1, LSBA_DEAD = 2 } lsba_outcome;
@@ -68,7 +75,9 @@ typedef struct {
 
 /* Result of a solve.  Counters follow the paper's accounting (PAPER.md:650 tables): BCGS-PIP
  * syncs = iterations + cycles, matvecs (A-ct) = iterations, basis_evals (V-ct) = 3 iterations;
- * BMGS-(I)CWY one more of each per cycle. */
+ * BMGS-(I)CWY one more of each per cycle; BMGS sum over steps of (k+1)
+ * syncs plus one per cycle and V-ct = 2 iterations; BCGS-PIO 2 iterations
+ * + cycles syncs. */
 typedef struct {
   int32_t outcome;            /* lsba_outcome                                             */
   int32_t cycles;             /* restart cycles run                                       */

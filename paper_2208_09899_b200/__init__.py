@@ -18,6 +18,8 @@ from ._lib import (  # noqa: F401
     LSBA_SKEL_BCGS_PIP,
     LSBA_SKEL_BMGS_CWY,
     LSBA_SKEL_BMGS_ICWY,
+    LSBA_SKEL_BMGS,
+    LSBA_SKEL_BCGS_PIO,
     LSBA_CONVERGED,
     LSBA_MAX_RESTARTS,
     LSBA_DEAD,

@@ -22,6 +22,12 @@ template <int B>
 cudaError_t launch_cwy_iter1(const SmallState2& st, const double* G, cudaStream_t stream);
 template <int B>
 cudaError_t launch_cwy_coef(const SmallState2& st, const double* G, int k, int inverse, cudaStream_t stream);
+template <int B>
+cudaError_t launch_bmgs_h(const SmallState2& st, const double* G, int j, int k, cudaStream_t stream);
+template <int B>
+cudaError_t launch_bmgs_r(const SmallState2& st, const double* G, int k, cudaStream_t stream);
+template <int B>
+cudaError_t launch_pio_coef(const SmallState2& st, const double* G1, const double* G2, int k, cudaStream_t stream);
 
 #define LSBA_DECL_SMALL(B)                                                                              \
   template <>                                                                                           \
@@ -35,7 +41,13 @@ cudaError_t launch_cwy_coef(const SmallState2& st, const double* G, int k, int i
   template <>                                                                                           \
   cudaError_t launch_cwy_iter1<B>(const SmallState2&, const double*, cudaStream_t);                    \
   template <>                                                                                           \
-  cudaError_t launch_cwy_coef<B>(const SmallState2&, const double*, int, int, cudaStream_t);
+  cudaError_t launch_cwy_coef<B>(const SmallState2&, const double*, int, int, cudaStream_t);           \
+  template <>                                                                                           \
+  cudaError_t launch_bmgs_h<B>(const SmallState2&, const double*, int, int, cudaStream_t);             \
+  template <>                                                                                           \
+  cudaError_t launch_bmgs_r<B>(const SmallState2&, const double*, int, cudaStream_t);                  \
+  template <>                                                                                           \
+  cudaError_t launch_pio_coef<B>(const SmallState2&, const double*, const double*, int, cudaStream_t);
 LSBA_DECL_SMALL(1) LSBA_DECL_SMALL(2) LSBA_DECL_SMALL(3) LSBA_DECL_SMALL(4)
 LSBA_DECL_SMALL(5) LSBA_DECL_SMALL(6) LSBA_DECL_SMALL(7) LSBA_DECL_SMALL(8)
 LSBA_DECL_SMALL(9) LSBA_DECL_SMALL(10) LSBA_DECL_SMALL(11) LSBA_DECL_SMALL(12)

@@ -601,6 +601,31 @@ static lsba_status cwy_coef_t(lsba_ctx c, int k) {
 static lsba_status cwy_iter1_small(lsba_ctx c) { LSBA_DISPATCH_S(c->b, cwy_iter1_t, c); }
 static lsba_status cwy_coef(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, cwy_coef_t, c, k); }
 
+// ---------------------------------------------------------------- BMGS / BCGS-PIO small kernels
+template <int B>
+static lsba_status bmgs_h_t(lsba_ctx c, int j, int k) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  CK(launch_bmgs_h<B>(c->st, c->d_G, j, k, c->stream));
+  return LSBA_OK;
+}
+template <int B>
+static lsba_status bmgs_r_t(lsba_ctx c, int k) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  CK(launch_bmgs_r<B>(c->st, c->d_G, k, c->stream));
+  return LSBA_OK;
+}
+template <int B>
+static lsba_status pio_coef_t(lsba_ctx c, const double* G1, const double* G2, int k) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  CK(launch_pio_coef<B>(c->st, G1, G2, k, c->stream));
+  return LSBA_OK;
+}
+static lsba_status bmgs_h(lsba_ctx c, int j, int k) { LSBA_DISPATCH_S(c->b, bmgs_h_t, c, j, k); }
+static lsba_status bmgs_r(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, bmgs_r_t, c, k); }
+static lsba_status pio_coef(lsba_ctx c, const double* G1, const double* G2, int k) {
+  LSBA_DISPATCH_S(c->b, pio_coef_t, c, G1, G2, k);
+}
+
 static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
@@ -700,8 +725,65 @@ static lsba_status cwy_step_async(lsba_ctx c, int k, bool last) {
   return LSBA_OK;
 }
 
+// BMGS-Arnoldi step k (Alg 2; comparison baseline):
+// W = A V_k; for j = 1..k: H_{j,k} = <V_j, W> (a sync each), W = W - V_j H_{j,k}; then
+// [V_{k+1}, H_{k+1,k}] = IO(W) (one more sync).  Asynchronous.
+static lsba_status bmgs_step_async(lsba_ctx c, int k) {
+  const int* act = &c->d_ctl->active;
+  c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
+  c->pending_upd = (k > 1);
+  TRY(spmm(c, slotp(c, k - 1), slotp(c, k), act));                                 // line 3
+  TRY(wait_update(c));
+  for (int j = 1; j <= k; ++j) {
+    TRY(gram(c, slotp(c, j - 1), c->slot_stride, 1, slotp(c, k), c->ip, nullptr, act));   // line 5
+    TRY(bmgs_h(c, j, k));
+    TRY(project(c, slotp(c, j - 1), (size_t)(k - j + 1) * c->slot_stride, 2, c->st.coef, nullptr,
+                slotp(c, k), 0, nullptr, nullptr, c->st.flag_dev, LSBA_K_PROJECT));   // line 6
+  }
+  TRY(gram(c, slotp(c, k), c->slot_stride, 1, slotp(c, k), c->ip, nullptr, act));  // line 7: IO
+  TRY(bmgs_r(c, k));
+  CK(cudaEventRecord(c->ev_coef, c->stream));
+  CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
+  TRY(step_update(c, k, c->st.gpip));
+  CK(cudaEventRecord(c->ev_upd, c->stream2));
+  TRY(project(c, slotp(c, k), c->slot_stride, 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr, nullptr,
+              c->st.flag_dev, LSBA_K_PROJECT));
+  return LSBA_OK;
+}
+
+// BCGS-PIO step k (Alg 4; comparison baseline): W = A V_k; H = <[V_1..V_k], W>
+// (sync 1); <W, W> (sync 2); H_{k+1,k} = chol(W~^T W~ - H~^T H~); V_{k+1} as BCGS-PIP.
+static lsba_status pio_step_async(lsba_ctx c, int k) {
+  const int* act = &c->d_ctl->active;
+  double* const G1 = c->d_Gbase + (size_t)(k & 1) * c->g_half;
+  double* const G2 = G1 + (size_t)k * c->b * c->b;
+  c->pending_upd = (k > 1);
+  c->d_G = G1;
+  TRY(spmm(c, slotp(c, k - 1), slotp(c, k), act));                                 // line 3
+  TRY(wait_update(c));
+  TRY(gram(c, slotp(c, 0), c->slot_stride, k, slotp(c, k), c->ip, nullptr, act));  // line 4
+  c->d_G = G2;
+  TRY(gram(c, slotp(c, k), c->slot_stride, 1, slotp(c, k), c->ip, nullptr, act));  // line 5 (IO of W)
+  c->d_G = G1;
+  TRY(pio_coef(c, G1, G2, k));                                                      // lines 5-6
+  CK(cudaEventRecord(c->ev_coef, c->stream));
+  CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
+  TRY(step_update(c, k, G1));
+  CK(cudaEventRecord(c->ev_upd, c->stream2));
+  TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
+              nullptr, c->st.flag_dev, LSBA_K_PROJECT));                           // line 7
+  return LSBA_OK;
+}
+
 static lsba_status step_async(lsba_ctx c, int k, bool last) {
-  return c->skel == LSBA_SKEL_BCGS_PIP ? pip_step_async(c, k) : cwy_step_async(c, k, last);
+  switch (c->skel) {
+    case LSBA_SKEL_BCGS_PIP: return pip_step_async(c, k);
+    case LSBA_SKEL_BMGS_CWY:
+    case LSBA_SKEL_BMGS_ICWY: return cwy_step_async(c, k, last);
+    case LSBA_SKEL_BMGS: return bmgs_step_async(c, k);
+    case LSBA_SKEL_BCGS_PIO: return pio_step_async(c, k);
+    default: return fail(c, LSBA_E_ARG, "bad skeleton");
+  }
 }
 
 // join stream 2 (the last step's update) into the main stream
@@ -784,7 +866,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   std::memset(info, 0, sizeof *info);
   info->true_relres = NAN;
   info->res_est = NAN;
-  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BMGS_ICWY) return fail(c, LSBA_E_ARG, "bad skeleton");
+  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BCGS_PIO) return fail(c, LSBA_E_ARG, "bad skeleton");
   set_ip(c, ip);
   c->skel = skel;
   c->forced_done = false;
@@ -793,11 +875,18 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   auto finish = [&]() {
     // the paper's counters (PAPER.md:650 tables): BMGS-(I)CWY applies A, syncs and evaluates
     // one more block per cycle than BCGS-PIP (the lagged normalisation)
-    const int64_t extra = (skel == LSBA_SKEL_BCGS_PIP) ? 0 : info->cycles;
+    const bool cwy = (skel == LSBA_SKEL_BMGS_CWY || skel == LSBA_SKEL_BMGS_ICWY);
+    const int64_t extra = cwy ? info->cycles : 0;
     info->restarts = info->cycles > 0 ? info->cycles - 1 : 0;
     info->syncs = (int64_t)info->iterations + info->cycles + extra;
     info->matvecs = info->iterations + extra;
     info->basis_evals = 3 * (int64_t)info->iterations + extra;
+    if (skel == LSBA_SKEL_BMGS) {          // k+1 syncs per step
+      info->syncs = info->gram_blocks + info->cycles;
+      info->basis_evals = 2 * (int64_t)info->iterations;
+    } else if (skel == LSBA_SKEL_BCGS_PIO) {   // two syncs per step (Table 1)
+      info->syncs = 2 * (int64_t)info->iterations + info->cycles;
+    }
     info->kernel_launches = c->launches - launches0;
     info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   };
@@ -864,7 +953,8 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     c->h_prog[0] = -1;                                       // (device idle: cycle boundary)
     c->h_prog[1] = 1;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
-    if (c->skel != LSBA_SKEL_BCGS_PIP) TRY(cwy_iter1_async(c));   // Alg 6 iteration 1
+    if (c->skel == LSBA_SKEL_BMGS_CWY || c->skel == LSBA_SKEL_BMGS_ICWY)
+      TRY(cwy_iter1_async(c));                               // Alg 6 iteration 1
     for (int k = 1; k <= m_cur; ++k) {
       // keep at most kLookahead steps enqueued beyond the last decided one; stop enqueueing
       // once the device has ended the cycle (flag, convergence, kappa trigger)
@@ -1361,7 +1451,8 @@ extern "C" lsba_status lsba_arnoldi_begin(lsba_ctx c, const double* B_dev, lsba_
   prm.need_kappa = 1;
   c->skel = c->skel_default;
   TRY(io_begin_async(c, prm));
-  if (c->skel != LSBA_SKEL_BCGS_PIP) TRY(cwy_iter1_async(c));     // Alg 6 loop iteration 1
+  if (c->skel == LSBA_SKEL_BMGS_CWY || c->skel == LSBA_SKEL_BMGS_ICWY)
+    TRY(cwy_iter1_async(c));                                       // Alg 6 loop iteration 1
   StepStatus stt;
   TRY(read_status(c, &stt, nullptr));
   if (io_flag) *io_flag = stt.flag;
@@ -1519,7 +1610,7 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
 
 extern "C" lsba_status lsba_set_skeleton(lsba_ctx c, lsba_skel skel) {
   if (!c) return LSBA_E_ARG;
-  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BMGS_ICWY) return fail(c, LSBA_E_ARG, "bad skeleton");
+  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BCGS_PIO) return fail(c, LSBA_E_ARG, "bad skeleton");
   c->skel_default = skel;
   return LSBA_OK;
 }

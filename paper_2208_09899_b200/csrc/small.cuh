@@ -797,6 +797,207 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
   }
 }
 
+// ---------------------------------------------------------------------------- BMGS / BCGS-PIO
+// Warp 0 only: R = chol(sym(S)) with the NaN-flag of reading R2 (S, R, R^{-1} B x B col-major
+// in shared memory; R, R^{-1} upper triangular).  Returns the flag on every lane.
+template <int B>
+__device__ bool warp_chol_inv(const double* S, double* Rs, double* Ris, bool force) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < B * B; e += 32) {
+    const int x = e % B, y = e / B;
+    Rs[x + y * B] = (x <= y) ? 0.5 * (S[x + y * B] + S[y + x * B]) : 0.0;
+  }
+  __syncwarp();
+  bool f = false;
+  for (int j = 0; j < B; ++j) {
+    const double d = Rs[j + j * B];
+    if (!(d > 0.0) || !isfinite(d)) { f = true; break; }
+    const double r = sqrt(d);
+    __syncwarp();
+    for (int c = j + lane; c < B; c += 32) Rs[j + c * B] = (c == j) ? r : Rs[j + c * B] / r;
+    __syncwarp();
+    const int rem = B - j - 1;
+    for (int e = lane; e < rem * rem; e += 32) {
+      const int x = j + 1 + e % rem, y = j + 1 + e / rem;
+      if (x <= y) Rs[x + y * B] -= Rs[j + x * B] * Rs[j + y * B];
+    }
+    __syncwarp();
+  }
+  if (!f)
+    for (int e = 0; e < B * B; ++e)
+      if (!isfinite(Rs[e])) f = true;
+  f = f || force;
+  if (!f && lane < B) {
+    const int c = lane;
+    double x[B];
+#pragma unroll
+    for (int r = B - 1; r >= 0; --r) {
+      double t = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = r + 1; q < B; ++q) t -= Rs[r + q * B] * x[q];
+      x[r] = (r <= c) ? t / Rs[r + r * B] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < B; ++r) Ris[r + c * B] = (r <= c) ? x[r] : 0.0;
+  }
+  __syncwarp();
+  return f;
+}
+
+// Step status and flag words of a step-closing small kernel (k >= 1); thread 0.
+__device__ __forceinline__ void close_status(const SmallState2& st, int k, int flag, int forced) {
+  *st.flag_dev = flag;
+  st.iscr[0] = flag;
+  st.iscr[1] = forced;
+  st.status->k = k;
+  st.status->flag = flag;
+  st.status->proj_singular = 0;
+  st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
+}
+
+// BMGS-Arnoldi (Alg 2), inner step j of step k: H_{j,k} = G (B x B, row-major),
+// stored in Hbar; coefficients [-H_{j,k}; I] for W = W - V_j H_{j,k} over [V_j, W].  blockDim 64.
+template <int B>
+__global__ void __launch_bounds__(64)
+k_bmgs_h(SmallState2 st, const double* __restrict__ G, int j, int k) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (st.ctl->active == 0) {
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int r = e / B, c = e % B;
+    const double h = __ldcg(G + e);
+    st.Hbar[((j - 1) * B + r) + (size_t)((k - 1) * B + c) * st.ldH] = h;
+    st.coef[e] = -h;
+    st.coef[B * B + e] = (r == c) ? 1.0 : 0.0;
+  }
+  if (tid == 0) *st.flag_dev = 0;
+}
+
+// BMGS-Arnoldi line 7: [V_{k+1}, H_{k+1,k}] = IO(W) with CholQR (global: the norm): G = <W, W>;
+// R = chol(G) with NaN-flag; coefficient R^{-1}; the update kernel's inputs.  blockDim 64.
+template <int B>
+__global__ void __launch_bounds__(64)
+k_bmgs_r(SmallState2 st, const double* __restrict__ G, int k) {
+  __shared__ double Ss[B * B], Rs[B * B], Ris[B * B];
+  __shared__ int flag_s;
+  const int tid = threadIdx.x, nt = blockDim.x, ldH = st.ldH, kb = k * B;
+  CycleCtl* ctl = st.ctl;
+  if (ctl->active == 0) {
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  const int force_flag = (k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    Ss[x + y * B] = __ldcg(G + x * B + y);
+  }
+  for (int e = tid; e < kb * B; e += nt) {        // H_{1:k,k} for the update kernel
+    const int r = e / B, c = e % B;
+    st.gpip[e] = st.Hbar[r + (size_t)((k - 1) * B + c) * ldH];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const bool f = warp_chol_inv<B>(Ss, Rs, Ris, force_flag != 0);
+    if (tid == 0) {
+      flag_s = f ? 1 : 0;
+      close_status(st, k, flag_s, force_flag);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = flag_s ? 0.0 : Rs[e];
+    if (!flag_s) {
+      st.rscr[e] = Rs[e];
+      st.rscr[B * B + e] = Ris[e];
+      st.coef[y * B + x] = Ris[y + x * B];       // row-major block: coef[a][c] = (R^{-1})[a][c]
+    }
+  }
+}
+
+// BCGS-PIO (Alg 4): G1 = H_{1:k,k} ((kB) x B, row-major), G2 = <W, W>.
+// W~ = chol(G2), H~ = chol(H^T H), R = chol(W~^T W~ - H~^T H~) (each with the NaN-flag);
+// coefficients [-H R^{-1}; R^{-1}] as BCGS-PIP.  blockDim 128.
+template <int B>
+__global__ void __launch_bounds__(128)
+k_pio_coef(SmallState2 st, const double* __restrict__ G1, const double* __restrict__ G2, int k) {
+  __shared__ double S1[B * B], W1[B * B], Wi[B * B], H1[B * B], Hi[B * B], Rs[B * B], Ris[B * B];
+  __shared__ int flag_s;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+  const int ldH = st.ldH, kb = k * B;
+  CycleCtl* ctl = st.ctl;
+  if (ctl->active == 0) {
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  const int force_flag = (k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
+  for (int e = tid; e < kb * B; e += nt) {
+    const int r = e / B, c = e % B;
+    st.Hbar[r + (size_t)((k - 1) * B + c) * ldH] = __ldcg(G1 + e);
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    S1[x + y * B] = __ldcg(G2 + x * B + y);
+  }
+  // H^T H (one warp per output, lanes over the kB rows)
+  __shared__ double HtH[B * B];
+  for (int e = warp; e < B * B; e += nt >> 5) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int r = lane; r < kb; r += 32) t += __ldcg(G1 + r * B + x) * __ldcg(G1 + r * B + y);
+    t = warp_sum(t);
+    if (lane == 0) HtH[x + y * B] = t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    bool f = warp_chol_inv<B>(S1, W1, Wi, false);          // W~
+    if (!f) f = warp_chol_inv<B>(HtH, H1, Hi, false);       // H~
+    if (!f) {
+      for (int e = lane; e < B * B; e += 32) {               // W~^T W~ - H~^T H~
+        const int x = e % B, y = e / B;
+        double t = 0.0;
+        for (int q = 0; q < B; ++q) t += W1[q + x * B] * W1[q + y * B] - H1[q + x * B] * H1[q + y * B];
+        S1[x + y * B] = t;
+      }
+      __syncwarp();
+      f = warp_chol_inv<B>(S1, Rs, Ris, force_flag != 0);
+    } else {
+      f = true;
+    }
+    if (lane == 0) {
+      flag_s = f ? 1 : 0;
+      close_status(st, k, flag_s, force_flag);
+    }
+  }
+  __syncthreads();
+  if (flag_s) {
+    for (int e = tid; e < B * B; e += nt) {
+      const int x = e % B, y = e / B;
+      st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = 0.0;
+    }
+    return;
+  }
+  for (int e = tid; e < (kb + B) * B; e += nt) {
+    const int r = e / B, c = e % B;
+    double t;
+    if (r < kb) {
+      t = 0.0;
+      for (int q = 0; q <= c; ++q) t -= __ldcg(G1 + r * B + q) * Ris[q + c * B];
+    } else {
+      t = Ris[(r - kb) + c * B];
+    }
+    st.coef[e] = t;
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
+    st.rscr[e] = Rs[e];
+    st.rscr[B * B + e] = Ris[e];
+  }
+}
+
 // ---------------------------------------------------------------------------- cycle end
 // blockDim = 32 * max(8, B).  dynamic smem: k B B (Xi) doubles.
 // gmres: 1 -> R Xi = g (least squares); 0 -> FOM (last diagonal block h~_k, rhs g^_k).

@@ -75,4 +75,23 @@ cudaError_t launch_cwy_coef<LSBA_B>(const SmallState2& st, const double* G, int 
   return cudaGetLastError();
 }
 
+template <>
+cudaError_t launch_bmgs_h<LSBA_B>(const SmallState2& st, const double* G, int j, int k, cudaStream_t stream) {
+  k_bmgs_h<LSBA_B><<<1, 64, 0, stream>>>(st, G, j, k);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_bmgs_r<LSBA_B>(const SmallState2& st, const double* G, int k, cudaStream_t stream) {
+  k_bmgs_r<LSBA_B><<<1, 64, 0, stream>>>(st, G, k);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_pio_coef<LSBA_B>(const SmallState2& st, const double* G1, const double* G2, int k,
+                                    cudaStream_t stream) {
+  k_pio_coef<LSBA_B><<<1, 128, 0, stream>>>(st, G1, G2, k);
+  return cudaGetLastError();
+}
+
 }  // namespace lsba
