@@ -153,16 +153,20 @@ static void sweep(int n, std::vector<int> Js) {
     int grid0;
     auto ref = run_v7<S, 2, 4, 3>(B, n, J, &us0, &grid0);   // reference for the diffs
     printf("s=%d n=%d J=%d (%.0f MB)\n", S, n, J, bytes / 1e6);
-    v7_line<S, 3, 4, 3>(B, n, J, ref, bytes);
-    v7_line<S, 2, 4, 3>(B, n, J, ref, bytes);
-    v7_line<S, 2, 8, 3>(B, n, J, ref, bytes);
-    v7_line<S, 1, 16, 3>(B, n, J, ref, bytes);
-    v7_line<S, 4, 4, 2>(B, n, J, ref, bytes);
-    v7_line<S, 3, 6, 2>(B, n, J, ref, bytes);
-    v7_line<S, 1, 8, 4>(B, n, J, ref, bytes);
-    v7_line<S, 2, 4, 4>(B, n, J, ref, bytes);
-    v7_line<S, 2, 4, 3, false>(B, n, J, ref, bytes);
-    v7_line<S, 3, 6, 2, false>(B, n, J, ref, bytes);
+    if constexpr (S == 16) {
+      v7_line<S, 2, 4, 3, false>(B, n, J, ref, bytes);
+      v7_line<S, 1, 4, 4, false>(B, n, J, ref, bytes);
+      v7_line<S, 1, 8, 3, false>(B, n, J, ref, bytes);
+      v7_line<S, 2, 2, 4, false>(B, n, J, ref, bytes);
+      v7_line<S, 1, 2, 4, false>(B, n, J, ref, bytes);
+      v7_line<S, 1, 4, 4, true>(B, n, J, ref, bytes);
+      v7_line<S, 4, 2, 3, false>(B, n, J, ref, bytes);
+      v7_line<S, 2, 6, 2, false>(B, n, J, ref, bytes);
+    } else {
+      v7_line<S, 3, 4, 3>(B, n, J, ref, bytes);
+      v7_line<S, 2, 4, 3>(B, n, J, ref, bytes);
+      v7_line<S, 3, 6, 2>(B, n, J, ref, bytes);
+    }
     read_line<S>(B, n, J, bytes);
   }
   cudaFree(B.V); cudaFree(B.part); cudaFree(B.gpart); cudaFree(B.G); cudaFree(B.zeros); cudaFree(B.tickets);
