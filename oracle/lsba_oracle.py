@@ -418,6 +418,57 @@ class CwyArnoldi:
         return StepResult(Hcol, R if self.ip == "cl" else float(R[0, 0]), Vn, False, W)
 
 
+class IrolsArnoldi(CwyArnoldi):
+    """BCGS-IRO-LS-Arnoldi, Alg 7: the block DCGS2 — the same lagged loop and
+    single block inner product <[V_1..V_k U], [U W]> as Alg 6, with the re-orthogonalisation
+    folded into it: Omega = Omega~ - Y^* Y, H_{k+1,k} = chol(Omega), column k finalised as
+    H_{1:k,k} = J + Y, P = H^{-*}(P~ - Y^* Z), J = ([Z; P] - H_{1:k+1,1:k} Y) H^{-1},
+    V_{k+1} = (U - V Y) H^{-1}, U = (W - [V_1..V_{k+1}] [Z; P]) H^{-1}.  (Step k = loop
+    iteration k+1, as in CwyArnoldi; J is the tentative next column.)  Per cycle m+1
+    A-applications, m+2 syncs and 4 block evaluations per step."""
+
+    def begin(self, B):
+        flag = super().begin(B)
+        if not flag:
+            self.J = self.Hbar[: self.b, : self.b].copy()      # line 6: J = <U, W>, H_11 = J
+        return flag
+
+    def step(self, force_flag: bool = False) -> StepResult:
+        b, k = self.b, len(self.V)
+        U = self.U
+        W = spmm(*self.A, U)                                   # line 4
+        if self.ip == "cl":
+            s = self.s
+            G = ip_cl(list(self.V) + [U], np.concatenate([U, W], axis=1))   # line 10: one sync
+            Y, Z = G[: k * s, :s], G[: k * s, s:]
+            Om_t, Pt = G[k * s:, :s], G[k * s:, s:]
+            R, flag = chol_flag(Om_t - Y.T @ Y)                # lines 11-12
+        else:
+            gU = ip_gl(list(self.V) + [U], U)
+            gW = ip_gl(list(self.V) + [U], W)
+            Y, Z = gU[:k].reshape(-1, 1), gW[:k].reshape(-1, 1)
+            om = gU[k] - float(Y[:, 0] @ Y[:, 0])
+            Pt = np.array([[gW[k]]])
+            flag = not (om > 0.0) or not math.isfinite(om)
+            R = np.array([[math.sqrt(om)]]) if not flag else np.array([[float("nan")]])
+        Hcol = self.J + Y                                      # line 13: column k final
+        self.Hbar[: k * b, (k - 1) * b: k * b] = Hcol
+        flag = bool(flag) or force_flag
+        if flag:
+            return StepResult(Hcol, R if self.ip == "cl" else float("nan"), None, True, W)
+        Rinv = right_trsm_upper(np.eye(b), R)
+        P = np.linalg.solve(R.T, Pt - Y.T @ Z)                 # line 14
+        self.Hbar[k * b:(k + 1) * b, (k - 1) * b: k * b] = R
+        Hk = self.Hbar[:(k + 1) * b, : k * b]                  # H_{1:k+1,1:k}
+        ZP = np.vstack([Z, P])
+        self.J = (ZP - Hk @ Y) @ Rinv                          # line 15
+        Vn = self._mul(U - _basis_combine(self.V, Y, b), Rinv)  # line 16
+        self.V.append(Vn)
+        self.U = self._mul(W - _basis_combine(self.V, ZP, b), Rinv)   # line 17
+        self.k = k
+        return StepResult(Hcol, R if self.ip == "cl" else float(R[0, 0]), Vn, False, W)
+
+
 # --------------------------------------------------------------------------------------
 # Comparison skeletons (SURVEY.md 8(f) f3): BMGS-Arnoldi (Alg 2) and BCGS-PIO-Arnoldi (Alg 4)
 # --------------------------------------------------------------------------------------
@@ -634,16 +685,18 @@ class SolveInfo:
             return sum(k * (k + 3) // 2 for k in self.cycle_lengths) + self.cycles
         if self.skel == "pio":
             return 2 * self.iterations + self.cycles
-        return self.iterations + (2 if self.skel in ("cwy", "icwy") else 1) * self.cycles
+        return self.iterations + (2 if self.skel in ("cwy", "icwy", "irols") else 1) * self.cycles
 
     @property
     def matvecs(self):
-        return self.iterations + (self.cycles if self.skel in ("cwy", "icwy") else 0)
+        return self.iterations + (self.cycles if self.skel in ("cwy", "icwy", "irols") else 0)
 
     @property
     def basis_evals(self):
         if self.skel == "bmgs":
             return 2 * self.iterations
+        if self.skel == "irols":                  # 4 per step
+            return 4 * self.iterations + self.cycles
         return 3 * self.iterations + (self.cycles if self.skel in ("cwy", "icwy") else 0)
 
     @property
@@ -680,6 +733,8 @@ def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
         arn = PipArnoldi(A, ip, m, s)
     elif skel in ("cwy", "icwy"):
         arn = CwyArnoldi(A, ip, m, s, inverse=(skel == "icwy"))
+    elif skel == "irols":
+        arn = IrolsArnoldi(A, ip, m, s)
     elif skel == "bmgs":
         arn = BmgsArnoldi(A, ip, m, s)
     elif skel == "pio":
