@@ -50,7 +50,7 @@ def roof_cycle_extra(n, s, k_used):
 def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks, skel="pip"):
     """sum_steps ROOF(k) + per-cycle bytes, from the solver's counters (gram_blocks = sum over
     accepted steps of k+1).  BCGS-PIP: ROOF(k) = A + 8ns(2k+3), + 8ns(k_used+7) per cycle.
-    BMGS-(I)CWY (Alg 6): per step the SpMM of U (2 blocks), the Gram over [V_1..V_k U] and W
+    BMGS-(I)CWY (Alg 6) and BCGS-IRO-LS (Alg 7): per step the SpMM of U (2 blocks), the Gram over [V_1..V_k U] and W
     (k+2) and the two-output pass (k+2 reads, 2 writes): A + 8ns(2k+8); per cycle IO (3), loop
     iteration 1 (7) and the cycle end (k_used+4): 8ns(k_used+14)."""
     A = 12.0 * nnz + 4.0 * (n + 1)
@@ -224,9 +224,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
-    ap.add_argument("--skel", default="pip", choices=["pip", "cwy", "icwy", "bmgs", "pio"],
-                    help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3), BMGS-CWY / -ICWY (Alg 6), or the "
-                         "comparison baselines BMGS (Alg 2) and BCGS-PIO (Alg 4)")
+    ap.add_argument("--skel", default="pip", choices=["pip", "cwy", "icwy", "irols", "bmgs", "pio"],
+                    help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3), BMGS-CWY / -ICWY (Alg 6), BCGS-IRO-LS "
+                         "(Alg 7), or the comparison baselines BMGS (Alg 2) and BCGS-PIO (Alg 4)")
     args = ap.parse_args()
     assert args.warmup >= 0 and args.steps >= 1
 
@@ -384,7 +384,8 @@ def main():
             "pct_roofline": {"of_measured_hbm": gbs / (peak * world), "of_8TBps_nominal": gbs / (8000.0 * world)},
             "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
                        "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY",
-                                                          "bmgs": "BMGS", "pio": "BCGS-PIO"}[args.skel]
+                                                          "irols": "BCGS-IRO-LS", "bmgs": "BMGS",
+                                                          "pio": "BCGS-PIO"}[args.skel]
                                  + " skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO"),
                        "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
                                       f"{iters / args.steps:.1f} block steps)") if full_solve

@@ -50,13 +50,15 @@ typedef enum { LSBA_IP_CLASSICAL = 0, LSBA_IP_GLOBAL = 1 } lsba_ip;
 /* Gram-Schmidt skeleton (Table 2): BCGS-PIP (Alg 3) and
  * BMGS-CWY / BMGS-ICWY (Alg 6; one block inner product per iteration with the
  * normalisation lagged by one iteration: m+1 A-applications and m+2 syncs per cycle), and the
- * comparison skeletons BMGS (Alg 2) and BCGS-PIO (Alg 4). */
+ * comparison skeletons BMGS (Alg 2) and BCGS-PIO (Alg 4),
+ * and BCGS-IRO-LS (Alg 7). */
 typedef enum {
   LSBA_SKEL_BCGS_PIP = 0,    /* Alg 3: one sync per step (the north star's skeleton)          */
   LSBA_SKEL_BMGS_CWY = 1,    /* Alg 6 (red): one sync per step, normalisation lagged           */
   LSBA_SKEL_BMGS_ICWY = 2,   /* Alg 6 (blue)                                                   */
   LSBA_SKEL_BMGS = 3,        /* Alg 2: k+1 syncs per step (comparison baseline)                */
-  LSBA_SKEL_BCGS_PIO = 4     /* Alg 4: two syncs per step (comparison baseline)                */
+  LSBA_SKEL_BCGS_PIO = 4,    /* Alg 4: two syncs per step (comparison baseline)                */
+  LSBA_SKEL_BCGS_IROLS = 5   /* Alg 7: BCGS-IRO-LS (block DCGS2), one sync per step, lagged    */
 } lsba_skel;
 
 /* SPEC.md:327 outcome of a solve. */

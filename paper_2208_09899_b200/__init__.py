@@ -20,6 +20,7 @@ from ._lib import (  # noqa: F401
     LSBA_SKEL_BMGS_ICWY,
     LSBA_SKEL_BMGS,
     LSBA_SKEL_BCGS_PIO,
+    LSBA_SKEL_BCGS_IROLS,
     LSBA_CONVERGED,
     LSBA_MAX_RESTARTS,
     LSBA_DEAD,

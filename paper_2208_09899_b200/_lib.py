@@ -20,8 +20,9 @@ lib = C.CDLL(library_path)
 
 LSBA_OK, LSBA_E_ARG, LSBA_E_CUDA, LSBA_E_NCCL, LSBA_E_OOM, LSBA_E_STATE = range(6)
 LSBA_IP_CLASSICAL, LSBA_IP_GLOBAL = 0, 1
-LSBA_SKEL_BCGS_PIP, LSBA_SKEL_BMGS_CWY, LSBA_SKEL_BMGS_ICWY, LSBA_SKEL_BMGS, LSBA_SKEL_BCGS_PIO = 0, 1, 2, 3, 4
-_SKEL = {"pip": 0, "cwy": 1, "icwy": 2, "bmgs": 3, "pio": 4, 0: 0, 1: 1, 2: 2, 3: 3, 4: 4}
+(LSBA_SKEL_BCGS_PIP, LSBA_SKEL_BMGS_CWY, LSBA_SKEL_BMGS_ICWY, LSBA_SKEL_BMGS, LSBA_SKEL_BCGS_PIO,
+ LSBA_SKEL_BCGS_IROLS) = 0, 1, 2, 3, 4, 5
+_SKEL = {"pip": 0, "cwy": 1, "icwy": 2, "bmgs": 3, "pio": 4, "irols": 5, 0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5}
 LSBA_CONVERGED, LSBA_MAX_RESTARTS, LSBA_DEAD = 0, 1, 2
 KERNEL_IDS = dict(spmm=0, gram=1, gram_finalize=2, small_step=3, project=4, cycle_solve=5,
                   combine=6, residual=7, halo_pack=8, misc=9, step_update=10)

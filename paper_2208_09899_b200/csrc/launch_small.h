@@ -23,6 +23,8 @@ cudaError_t launch_cwy_iter1(const SmallState2& st, const double* G, cudaStream_
 template <int B>
 cudaError_t launch_cwy_coef(const SmallState2& st, const double* G, int k, int inverse, cudaStream_t stream);
 template <int B>
+cudaError_t launch_irols_coef(const SmallState2& st, const double* G, int k, cudaStream_t stream);
+template <int B>
 cudaError_t launch_bmgs_h(const SmallState2& st, const double* G, int j, int k, cudaStream_t stream);
 template <int B>
 cudaError_t launch_bmgs_r(const SmallState2& st, const double* G, int k, cudaStream_t stream);
@@ -42,6 +44,8 @@ cudaError_t launch_pio_coef(const SmallState2& st, const double* G1, const doubl
   cudaError_t launch_cwy_iter1<B>(const SmallState2&, const double*, cudaStream_t);                    \
   template <>                                                                                           \
   cudaError_t launch_cwy_coef<B>(const SmallState2&, const double*, int, int, cudaStream_t);           \
+  template <>                                                                                           \
+  cudaError_t launch_irols_coef<B>(const SmallState2&, const double*, int, cudaStream_t);              \
   template <>                                                                                           \
   cudaError_t launch_bmgs_h<B>(const SmallState2&, const double*, int, int, cudaStream_t);             \
   template <>                                                                                           \

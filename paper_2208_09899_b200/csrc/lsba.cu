@@ -214,6 +214,10 @@ struct LaunchScope {
 
 static inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
 static inline double* slotp(lsba_ctx c, int j) { return c->d_V + (size_t)j * c->slot_stride; }
+// skeletons with Alg 6's lagged loop (iteration 1 after IO, the two-block Gram per step)
+static inline bool lagged(int skel) {
+  return skel == LSBA_SKEL_BMGS_CWY || skel == LSBA_SKEL_BMGS_ICWY || skel == LSBA_SKEL_BCGS_IROLS;
+}
 static inline bool in_basis(lsba_ctx c, const double* p) {
   return p >= c->d_V && p < c->d_V + (size_t)(c->m_max + 2) * c->slot_stride;
 }
@@ -598,8 +602,17 @@ static lsba_status cwy_coef_t(lsba_ctx c, int k) {
   CK(launch_cwy_coef<B>(c->st, c->d_G, k, c->skel == LSBA_SKEL_BMGS_ICWY ? 1 : 0, c->stream));
   return LSBA_OK;
 }
+template <int B>
+static lsba_status irols_coef_t(lsba_ctx c, int k) {
+  LaunchScope Ls(c, LSBA_K_SMALL_STEP, 0.0);
+  CK(launch_irols_coef<B>(c->st, c->d_G, k, c->stream));
+  return LSBA_OK;
+}
 static lsba_status cwy_iter1_small(lsba_ctx c) { LSBA_DISPATCH_S(c->b, cwy_iter1_t, c); }
-static lsba_status cwy_coef(lsba_ctx c, int k) { LSBA_DISPATCH_S(c->b, cwy_coef_t, c, k); }
+static lsba_status cwy_coef(lsba_ctx c, int k) {
+  if (c->skel == LSBA_SKEL_BCGS_IROLS) { LSBA_DISPATCH_S(c->b, irols_coef_t, c, k); }
+  LSBA_DISPATCH_S(c->b, cwy_coef_t, c, k);
+}
 
 // ---------------------------------------------------------------- BMGS / BCGS-PIO small kernels
 template <int B>
@@ -779,7 +792,8 @@ static lsba_status step_async(lsba_ctx c, int k, bool last) {
   switch (c->skel) {
     case LSBA_SKEL_BCGS_PIP: return pip_step_async(c, k);
     case LSBA_SKEL_BMGS_CWY:
-    case LSBA_SKEL_BMGS_ICWY: return cwy_step_async(c, k, last);
+    case LSBA_SKEL_BMGS_ICWY:
+    case LSBA_SKEL_BCGS_IROLS: return cwy_step_async(c, k, last);
     case LSBA_SKEL_BMGS: return bmgs_step_async(c, k);
     case LSBA_SKEL_BCGS_PIO: return pio_step_async(c, k);
     default: return fail(c, LSBA_E_ARG, "bad skeleton");
@@ -866,7 +880,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   std::memset(info, 0, sizeof *info);
   info->true_relres = NAN;
   info->res_est = NAN;
-  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BCGS_PIO) return fail(c, LSBA_E_ARG, "bad skeleton");
+  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BCGS_IROLS) return fail(c, LSBA_E_ARG, "bad skeleton");
   set_ip(c, ip);
   c->skel = skel;
   c->forced_done = false;
@@ -875,7 +889,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   auto finish = [&]() {
     // the paper's counters (PAPER.md:650 tables): BMGS-(I)CWY applies A, syncs and evaluates
     // one more block per cycle than BCGS-PIP (the lagged normalisation)
-    const bool cwy = (skel == LSBA_SKEL_BMGS_CWY || skel == LSBA_SKEL_BMGS_ICWY);
+    const bool cwy = lagged(skel);
     const int64_t extra = cwy ? info->cycles : 0;
     info->restarts = info->cycles > 0 ? info->cycles - 1 : 0;
     info->syncs = (int64_t)info->iterations + info->cycles + extra;
@@ -886,6 +900,8 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       info->basis_evals = 2 * (int64_t)info->iterations;
     } else if (skel == LSBA_SKEL_BCGS_PIO) {   // two syncs per step (Table 1)
       info->syncs = 2 * (int64_t)info->iterations + info->cycles;
+    } else if (skel == LSBA_SKEL_BCGS_IROLS) { // 4 block evaluations per step
+      info->basis_evals = 4 * (int64_t)info->iterations + info->cycles;
     }
     info->kernel_launches = c->launches - launches0;
     info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -953,7 +969,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     c->h_prog[0] = -1;                                       // (device idle: cycle boundary)
     c->h_prog[1] = 1;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
-    if (c->skel == LSBA_SKEL_BMGS_CWY || c->skel == LSBA_SKEL_BMGS_ICWY)
+    if (lagged(c->skel))
       TRY(cwy_iter1_async(c));                               // Alg 6 iteration 1
     for (int k = 1; k <= m_cur; ++k) {
       // keep at most kLookahead steps enqueued beyond the last decided one; stop enqueueing
@@ -1173,7 +1189,7 @@ static void release(lsba_ctx c) {
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
-                  c->st.Tm, c->st.TmT, c->st.gpip};
+                  c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1361,6 +1377,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   TRY(dalloc(c, &c->st.Tm, (size_t)ldH * ldH));
   TRY(dalloc(c, &c->st.TmT, (size_t)ldH * ldH));
   TRY(dalloc(c, &c->st.gpip, (size_t)ldH * s));
+  TRY(dalloc(c, &c->st.Jb, (size_t)ldH * s));
   c->st.ctl = c->d_ctl;
   {  // progress word in mapped pinned host memory (written by the device, polled by the host)
     CK(cudaHostAlloc((void**)&c->h_prog, 2 * sizeof(int), cudaHostAllocMapped));
@@ -1451,7 +1468,7 @@ extern "C" lsba_status lsba_arnoldi_begin(lsba_ctx c, const double* B_dev, lsba_
   prm.need_kappa = 1;
   c->skel = c->skel_default;
   TRY(io_begin_async(c, prm));
-  if (c->skel == LSBA_SKEL_BMGS_CWY || c->skel == LSBA_SKEL_BMGS_ICWY)
+  if (lagged(c->skel))
     TRY(cwy_iter1_async(c));                                       // Alg 6 loop iteration 1
   StepStatus stt;
   TRY(read_status(c, &stt, nullptr));
@@ -1610,7 +1627,7 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
 
 extern "C" lsba_status lsba_set_skeleton(lsba_ctx c, lsba_skel skel) {
   if (!c) return LSBA_E_ARG;
-  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BCGS_PIO) return fail(c, LSBA_E_ARG, "bad skeleton");
+  if (skel < LSBA_SKEL_BCGS_PIP || skel > LSBA_SKEL_BCGS_IROLS) return fail(c, LSBA_E_ARG, "bad skeleton");
   c->skel_default = skel;
   return LSBA_OK;
 }

@@ -43,6 +43,7 @@ struct SmallState2 {
   double* Tm;           // BMGS-(I)CWY: T ((m+1)b square, col-major, ld ldH)
   double* TmT;          // and its transpose (T row-major), for row-wise dot products
   double* gpip;         // BMGS-(I)CWY: H_{1:k,k} in the Gram layout the update kernel reads
+  double* Jb;           // BCGS-IRO-LS: the tentative next Hessenberg column J ((k+1)b x b, row-major)
 };
 
 // publish the step just decided to the host (mapped pinned memory; the host bounds how far
@@ -571,6 +572,7 @@ k_cwy_iter1(SmallState2 st, const double* __restrict__ G) {
     st.Hbar[r + (size_t)c * st.ldH] = h;
     st.coef[e] = -h;                                   // block 0 (V_1): -H_11
     st.coef[B * B + e] = (r == c) ? 1.0 : 0.0;         // block 1 (W): I
+    st.Jb[e] = h;                                      // BCGS-IRO-LS: J = <U, W> (Alg 7 l.6)
     st.Tm[r + (size_t)c * st.ldH] = (r == c) ? 1.0 : 0.0;   // T_11 = I (line 1)
     st.TmT[r + (size_t)c * st.ldH] = (r == c) ? 1.0 : 0.0;
   }
@@ -995,6 +997,159 @@ k_pio_coef(SmallState2 st, const double* __restrict__ G1, const double* __restri
     st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
     st.rscr[e] = Rs[e];
     st.rscr[B * B + e] = Ris[e];
+  }
+}
+
+// ---------------------------------------------------------------------------- BCGS-IRO-LS
+// Alg 7 step k (loop iteration k+1): G ((k+1)B x 2B) = <[V_1..V_k U], [U W]>.
+// Omega = Omega~ - Y^T Y, R = H_{k+1,k} = chol(Omega) (NaN-flag); column k final = J + Y;
+// P = R^{-T}(P~ - Y^T Z); J = ([Z; P] - H_{1:k+1,1:k} Y) R^{-1}; coefficients over
+// [V_1..V_k, U, W] of V_{k+1} = (U - V Y) R^{-1} (C0) and U' = (W - [V V_{k+1}][Z; P]) R^{-1}
+// (C1, V_{k+1} folded in).  blockDim 256; dyn smem (k+1)B x 2B (G) + (k+1)B x B (ZP) doubles.
+template <int B>
+__global__ void __launch_bounds__(256)
+k_irols_coef(SmallState2 st, const double* __restrict__ G, int k) {
+  extern __shared__ double iw[];
+  __shared__ double Om[B * B], Rs[B * B], Ris[B * B], Ps[B * B], PR[B * B], RPR[B * B];
+  __shared__ int flag_s;
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const int ldH = st.ldH, kb = k * B, k1b = kb + B;
+  CycleCtl* ctl = st.ctl;
+  if (ctl->active == 0) {
+    if (tid == 0) *st.flag_dev = 1;
+    return;
+  }
+  const int force_flag = (k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
+  double* Gs = iw;                        // k1b x 2B row-major
+  double* ZP = iw + (size_t)k1b * 2 * B;  // k1b x B row-major: [Z; P]
+  for (int e = tid; e < k1b * 2 * B; e += nt) Gs[e] = __ldcg(G + e);
+  __syncthreads();
+  // column k final: H_{1:k,k} = J + Y (Hbar and the update kernel's copy)
+  for (int e = tid; e < kb * B; e += nt) {
+    const int r = e / B, c = e % B;
+    const double h = st.Jb[e] + Gs[r * 2 * B + c];
+    st.Hbar[r + (size_t)((k - 1) * B + c) * ldH] = h;
+    st.gpip[e] = h;
+  }
+  // Omega = Omega~ - Y^T Y  (one warp per entry, lanes over the kB rows)
+  for (int e = warp; e < B * B; e += nw) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int r = lane; r < kb; r += 32) t += Gs[r * 2 * B + x] * Gs[r * 2 * B + y];
+    t = warp_sum(t);
+    if (lane == 0) Om[x + y * B] = Gs[(kb + x) * 2 * B + y] - t;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool f = warp_chol_inv<B>(Om, Rs, Ris, force_flag != 0);
+    if (lane == 0) {
+      flag_s = f ? 1 : 0;
+      close_status(st, k, flag_s, force_flag);
+    }
+  }
+  __syncthreads();
+  if (flag_s) {
+    for (int e = tid; e < B * B; e += nt) {
+      const int x = e % B, y = e / B;
+      st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = 0.0;
+    }
+    return;
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
+    st.rscr[e] = Rs[e];
+    st.rscr[B * B + e] = Ris[e];
+  }
+  // P = R^{-T} (P~ - Y^T Z): first Q = P~ - Y^T Z (warp per entry), then the triangular product
+  for (int e = warp; e < B * B; e += nw) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int r = lane; r < kb; r += 32) t += Gs[r * 2 * B + x] * Gs[r * 2 * B + B + y];
+    t = warp_sum(t);
+    if (lane == 0) Om[x + y * B] = Gs[(kb + x) * 2 * B + B + y] - t;   // (Om reused for Q)
+  }
+  __syncthreads();
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int q = 0; q <= x; ++q) t += Ris[q + x * B] * Om[q + y * B];
+    Ps[x + y * B] = t;
+  }
+  __syncthreads();
+  // ZP = [Z; P] (row-major); PR = P R^{-1}; RPR = R^{-1} P R^{-1}
+  for (int e = tid; e < k1b * B; e += nt) {
+    const int r = e / B, c = e % B;
+    ZP[e] = (r < kb) ? Gs[r * 2 * B + B + c] : Ps[(r - kb) + c * B];
+  }
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int q = 0; q <= y; ++q) t += Ps[x + q * B] * Ris[q + y * B];
+    PR[x + y * B] = t;
+  }
+  __syncthreads();
+  for (int e = tid; e < B * B; e += nt) {
+    const int x = e % B, y = e / B;
+    double t = 0.0;
+    for (int q = x; q < B; ++q) t += Ris[x + q * B] * PR[q + y * B];
+    RPR[x + y * B] = t;
+  }
+  // J = ([Z; P] - H_{1:k+1,1:k} Y) R^{-1}: one warp per row r of Hbar, lanes over the columns
+  for (int r = warp; r < k1b; r += nw) {
+    double acc[B];
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
+    const int q0 = max(0, (r / B - 1) * B);              // block upper Hessenberg
+    for (int q = q0 + lane; q < kb; q += 32) {
+      const double h = st.Hbar[r + (size_t)q * ldH];
+#pragma unroll
+      for (int c = 0; c < B; ++c) acc[c] += h * Gs[q * 2 * B + c];
+    }
+#pragma unroll
+    for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
+    if (lane < B) {
+      const int c = lane;
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        const double v = ZP[r * B + q] - sel<B>(acc, q);
+        t += (q <= c) ? v * Ris[q + c * B] : 0.0;
+      }
+      st.Jb[r * B + c] = t;
+    }
+  }
+  __syncthreads();
+  // coefficients over [V_1..V_k, U, W]
+  double* C0 = st.coef;
+  double* C1 = st.coef + (size_t)(k + 1) * B * B;
+  for (int e = tid; e < (k + 1) * B * B; e += nt) {
+    const int j = e / (B * B), a = (e / B) % B, c = e % B;
+    double t;
+    if (j < k) {                      // -Y_j R^{-1}
+      t = 0.0;
+      for (int q = 0; q <= c; ++q) t -= Gs[(j * B + a) * 2 * B + q] * Ris[q + c * B];
+    } else {
+      t = Ris[a + c * B];
+    }
+    C0[e] = t;
+  }
+  for (int e = tid; e < (k + 2) * B * B; e += nt) {
+    const int j = e / (B * B), a = (e / B) % B, c = e % B;
+    double t = 0.0;
+    if (j < k) {                      // -Z_j R^{-1} + Y_j R^{-1} P R^{-1}
+      for (int q = 0; q <= c; ++q) t -= Gs[(j * B + a) * 2 * B + B + q] * Ris[q + c * B];
+      for (int q = 0; q < B; ++q) {
+        double yr = 0.0;              // (Y_j R^{-1})[a][q]
+        for (int w = 0; w <= q; ++w) yr += Gs[(j * B + a) * 2 * B + w] * Ris[w + q * B];
+        t += yr * PR[q + c * B];
+      }
+    } else if (j == k) {              // -R^{-1} P R^{-1}
+      t = -RPR[a + c * B];
+    } else {                          // R^{-1}
+      t = Ris[a + c * B];
+    }
+    C1[e] = t;
   }
 }
 

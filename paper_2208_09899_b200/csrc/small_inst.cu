@@ -76,6 +76,20 @@ cudaError_t launch_cwy_coef<LSBA_B>(const SmallState2& st, const double* G, int 
 }
 
 template <>
+cudaError_t launch_irols_coef<LSBA_B>(const SmallState2& st, const double* G, int k, cudaStream_t stream) {
+  constexpr int B = LSBA_B;
+  const size_t k1b = (size_t)(k + 1) * B;
+  const size_t smem = sizeof(double) * (k1b * 3 * B);
+  auto fn = k_irols_coef<B>;
+  if (smem > 32 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  fn<<<1, 256, smem, stream>>>(st, G, k);
+  return cudaGetLastError();
+}
+
+template <>
 cudaError_t launch_bmgs_h<LSBA_B>(const SmallState2& st, const double* G, int j, int k, cudaStream_t stream) {
   k_bmgs_h<LSBA_B><<<1, 64, 0, stream>>>(st, G, j, k);
   return cudaGetLastError();

@@ -1,6 +1,7 @@
 """GPU parity of the comparison skeletons through the C ABI against the
 oracle on the same seeded inputs: BMGS-Arnoldi (Alg 2; k+1 syncs per step) and
-BCGS-PIO (Alg 4; two syncs per step) — the first steps' Hessenberg columns and
+BCGS-PIO (Alg 4; two syncs per step) and BCGS-IRO-LS (Alg 7,
+PAPER.md:350-379; block DCGS2, one sync per step, lagged like Alg 6) — the first steps' Hessenberg columns and
 basis normwise (reading R16), restarted solves and the paper's counters."""
 import numpy as np
 import pytest
@@ -30,11 +31,11 @@ def twin(name):
 
 def oracle_cls(skel):
     from oracle import lsba_oracle as O
-    return {"bmgs": O.BmgsArnoldi, "pio": O.PioArnoldi}[skel]
+    return {"bmgs": O.BmgsArnoldi, "pio": O.PioArnoldi, "irols": O.IrolsArnoldi}[skel]
 
 
 CASES = [(name, ip, skel) for name in ("tiny", "lapl2d", "cd3d", "random", "lapl3d")
-         for ip in ("cl", "gl") for skel in ("bmgs", "pio")]
+         for ip in ("cl", "gl") for skel in ("bmgs", "pio", "irols")]
 
 
 @pytest.mark.parametrize("name,ip,skel", CASES)
@@ -65,7 +66,7 @@ SOLVES = [("tiny", "cl", "gmres"), ("tiny", "gl", "gmres"), ("lapl2d", "cl", "fo
           ("random", "cl", "gmres"), ("cd3d", "cl", "gmres")]
 
 
-@pytest.mark.parametrize("skel", ["bmgs", "pio"])
+@pytest.mark.parametrize("skel", ["bmgs", "pio", "irols"])
 @pytest.mark.parametrize("name,ip,mod", SOLVES)
 def test_skeleton_solve_vs_oracle(L, name, ip, mod, skel):
     from oracle import lsba_oracle as O
@@ -79,6 +80,13 @@ def test_skeleton_solve_vs_oracle(L, name, ip, mod, skel):
     rel = np.linalg.norm(B - O.spmm(*A, Xg)) / np.linalg.norm(B)
     assert rel <= p.tol * (1 + 1e-6) and info.true_relres <= p.tol
     assert abs(info.cycles - io.cycles) <= 1
+    if skel == "irols":                   # Alg 6's lagged loop: m+1 A, m+2 syncs, 4 evaluations
+        assert info.matvecs == info.iterations + info.cycles                     # per step
+        assert info.syncs == info.iterations + 2 * info.cycles
+        assert info.basis_evals == 4 * info.iterations + info.cycles
+        if (info.cycles, info.iterations) == (io.cycles, io.iterations):
+            assert (info.matvecs, info.syncs, info.basis_evals) == (io.matvecs, io.syncs, io.basis_evals)
+        return
     assert info.matvecs == info.iterations
     if skel == "bmgs":                    # k+1 syncs per step plus IO
         assert info.syncs == info.gram_blocks + info.cycles and info.basis_evals == 2 * info.iterations

@@ -11,7 +11,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-SKELS = {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY", "pio": "BCGS-PIO", "bmgs": "BMGS"}
+SKELS = {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY", "irols": "BCGS-IRO-LS", "pio": "BCGS-PIO", "bmgs": "BMGS"}
 
 
 def problems(names):
@@ -24,7 +24,7 @@ def problems(names):
         else:
             i = {"tiny": 1, "c2": 2, "c3": 3, "c4": 4, "c5": 5}[nm]
             p = make_config(i)
-            skels = list(SKELS) if i in (1, 3, 4) else ["pip", "cwy", "icwy", "pio"]
+            skels = list(SKELS) if i in (1, 3, 4) else ["pip", "cwy", "icwy", "irols", "pio"]
             yield (p.name, (p.row_ptr, p.col_idx, p.vals), p.B, p.m, p.tol,
                    [(ip, md) for ip in p.ips for md in p.mods], p.cond_threshold, skels)
 
