@@ -69,6 +69,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int Jmax = max(J0, J1);
+  const uint64_t xpol = l2pol(c_l2hint & 4, false);
   for (int sb = gw; sb < nsup; sb += nwarps) {
     double d0[RB][NT][2], d1[RB][NT][2];
 #pragma unroll
@@ -82,7 +83,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
       for (int rb = 0; rb < RB; ++rb) {
         const int row = (sb * RB + rb) * 8 + r8;
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) a[rb][kc] = (row < n) ? Xj[(size_t)row * S + kc * 4 + k4] : 0.0;
+        for (int kc = 0; kc < KC; ++kc) a[rb][kc] = (row < n) ? ldh_rw(Xj + (size_t)row * S + kc * 4 + k4, xpol) : 0.0;
       }
       if (j < J0) {
         const double* cj = c0 + (size_t)j * S * S;

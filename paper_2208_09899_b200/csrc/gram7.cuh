@@ -83,6 +83,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
   }
   extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t xpol = l2pol(c_l2hint & 2, false);
   const int J = g.J, E = J * S * C::NCOL;
   const int NG = g7_groups<S>(J);
   const int passes = g7_passes(NG, C::GMAX);
@@ -155,7 +156,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
             bw[u][tn] = wsrc[tn] ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
           for (int gi = 0; gi < C::GMAX; ++gi)
-            av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+            av[u][gi] = src[gi] ? ldh2(src[gi] + off, xpol) : make_double2(0.0, 0.0);
         }
       } else {                                         // the grid's last, ragged batch
 #pragma unroll
@@ -167,7 +168,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
             bw[u][tn] = (ok && wsrc[tn]) ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
           for (int gi = 0; gi < C::GMAX; ++gi)
-            av[u][gi] = (ok && src[gi]) ? __ldg(reinterpret_cast<const double2*>(src[gi] + off))
+            av[u][gi] = (ok && src[gi]) ? ldh2(src[gi] + off, xpol)
                                         : make_double2(0.0, 0.0);
         }
       }
@@ -190,7 +191,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
           bw[u][tn] = wsrc[tn] ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
         for (int gi = 0; gi < C::GMAX; ++gi)
-          av[u][gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+          av[u][gi] = src[gi] ? ldh2(src[gi] + off, xpol) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int u = 0; u < C::U; ++u) mma_step(av[u], bw[u]);
@@ -203,7 +204,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
       for (int tn = 0; tn < C::NT; ++tn) bw[tn] = wsrc[tn] ? __ldg(wsrc[tn] + off) : 0.0;
 #pragma unroll
       for (int gi = 0; gi < C::GMAX; ++gi)
-        av[gi] = src[gi] ? __ldg(reinterpret_cast<const double2*>(src[gi] + off)) : make_double2(0.0, 0.0);
+        av[gi] = src[gi] ? ldh2(src[gi] + off, xpol) : make_double2(0.0, 0.0);
       mma_step(av, bw);
     }
   }

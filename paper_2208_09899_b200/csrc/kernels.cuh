@@ -25,6 +25,46 @@ namespace lsba {
 constexpr int kThreads = 256;
 
 // ------------------------------------------------------------------------------------------
+// L2 eviction-priority hints (createpolicy + ld.global.nc.L2::cache_hint).  c_l2hint bits:
+// 1 = the SpMM's CSR streams (row_ptr, col_idx, vals) evict_last, so A can stay L2-resident
+// across the step while the basis streams through; 2 = the Gram's basis reads evict_first;
+// 4 = the projection's basis reads evict_first; 8 = the SpMM output W and the projection output
+// V_{k+1} stored evict_last (the next kernel re-reads them).  Default 14 (measured: config 2
+// +8%, config 5 +1.5%, configs 3/4 neutral; tools/l2exp.sh); LSBA_L2HINT overrides per context.
+// ------------------------------------------------------------------------------------------
+static __constant__ int c_l2hint = 14;
+__device__ __forceinline__ uint64_t l2pol(bool hint, bool last) {
+  uint64_t p;
+  if (!hint) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else if (last) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ldh(const int* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldh(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldh_rw(const double* p, uint64_t pol) {   // coherent (not .nc)
+  double v;
+  asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void sth2(double* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" :: "l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ double2 ldh2(const double* p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+// ------------------------------------------------------------------------------------------
 // row access helpers: S doubles per row, loaded as double2 when S is even
 // ------------------------------------------------------------------------------------------
 template <int S>
@@ -40,6 +80,21 @@ __device__ __forceinline__ void load_row(const double* __restrict__ p, double (&
   } else {
 #pragma unroll
     for (int t = 0; t < S; ++t) v[t] = __ldg(p + t);
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void load_row_h(const double* __restrict__ p, double (&v)[S], uint64_t pol) {
+  if constexpr (S % 2 == 0) {
+#pragma unroll
+    for (int t = 0; t < S / 2; ++t) {
+      double2 d = ldh2(p + 2 * t, pol);
+      v[2 * t] = d.x;
+      v[2 * t + 1] = d.y;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < S; ++t) v[t] = ldh(p + t, pol);
   }
 }
 
@@ -96,6 +151,7 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   const int row = (int)(gt / L);
   const int lane = (int)(gt % L);
   double sq = 0.0;
+  const uint64_t apol = l2pol(c_l2hint & 1, true);
   // row pointers: for L >= 2 one coalesced load of the warp's 32/L + 1 pointers, then shuffles
   // (instead of 2 L redundant dependent loads per row; +4-7% on the stencil configs,
   // tools/spmm_bench.cu)
@@ -104,7 +160,7 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
     const int lane32 = threadIdx.x & 31;
     const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
     const int rr = row_w + lane32;
-    const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+    const int pv = (lane32 <= 32 / L && rr <= n) ? ldh(rp + rr, apol) : 0;
     p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
     p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
   } else {
@@ -114,8 +170,8 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   if (row < n) {
     double a0 = 0.0, a1 = 0.0;
     for (int p = p0; p < p1; ++p) {
-      const int c = __ldg(ci + p);
-      const double a = __ldg(va + p);
+      const int c = ldh(ci + p, apol);
+      const double a = ldh(va + p, apol);
       const double* src = (c < n) ? (V + (size_t)c * S) : (Vghost + (size_t)(c - n) * S);
       if constexpr (C == 2) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(src) + lane);
@@ -137,7 +193,7 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
       sq = a0 * a0 + (C == 2 ? a1 * a1 : 0.0);
     }
     if constexpr (C == 2)
-      reinterpret_cast<double2*>(dst)[lane] = make_double2(a0, a1);
+      sth2(dst + 2 * lane, make_double2(a0, a1), l2pol(c_l2hint & 8, true));
     else
       dst[0] = a0;
   }
@@ -369,10 +425,11 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
     // rows in flight.  Every thread reads only its own row of every block before writing that
     // row (the output may be the last input block), so the read-only path is safe here.
     int j = 0;
+    const uint64_t xpol = l2pol(c_l2hint & 4, false);
     for (; j + 4 <= J0; j += 4) {
       double x[4][S];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load_row<S>(X + (size_t)(j + u) * xstride + (size_t)i * S, x[u]);
+      for (int u = 0; u < 4; ++u) load_row_h<S>(X + (size_t)(j + u) * xstride + (size_t)i * S, x[u], xpol);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if constexpr (GLOBAL) {
@@ -403,7 +460,13 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
           for (int c = 0; c < S; ++c) o0[c] = fma(x[a], cj[a * S + c], o0[c]);
       }
     }
-    store_row<S>(out0 + (size_t)i * S, o0);
+    if constexpr (S % 2 == 0) {
+      const uint64_t opol = l2pol(c_l2hint & 8, true);
+#pragma unroll
+      for (int t = 0; t < S / 2; ++t) sth2(out0 + (size_t)i * S + 2 * t, make_double2(o0[2 * t], o0[2 * t + 1]), opol);
+    } else {
+      store_row<S>(out0 + (size_t)i * S, o0);
+    }
     return;
   }
   const int Jmax = max(J0, J1);

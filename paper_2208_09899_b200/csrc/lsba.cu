@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -108,6 +109,8 @@ struct lsba_ctx_ {
   int force_flag_k = 0;
   bool forced_done = false;
   int variant = 0;
+  bool no_fuse = false;          // diagnostics: LSBA_NO_FUSE=1 keeps the small step a separate launch
+  int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
   int skel_default = LSBA_SKEL_BCGS_PIP;  // lsba_set_skeleton: step API and lsba_solve_host
@@ -393,7 +396,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       GramFuse f{};
       // fuse the small step into the Gram tail on one rank (no allreduce in between) while its
       // Gram copy fits next to the partials (<= 64 KB of shared memory)
-      if (coef_k >= 0 && coef_fused && c->nranks == 1 && E * sizeof(double) <= 64 * 1024) {
+      if (coef_k >= 0 && coef_fused && c->nranks == 1 && !c->no_fuse && E * sizeof(double) <= 64 * 1024) {
         f.on = 1;
         f.st = c->st;
         f.k = coef_k;
@@ -1294,6 +1297,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
       if (send_idx[i] < 0 || send_idx[i] >= n_local) return fail(c, LSBA_E_ARG, "peer requested a row this rank does not own");
     }
   }
+  CK(cudaMemcpyToSymbol(c_l2hint, &c->l2hint, sizeof(int)));
   // ---- device CSR
   std::vector<int32_t> rp32(n_local + 1);
   for (int64_t i = 0; i <= n_local; ++i) rp32[i] = (int32_t)row_ptr[i];
@@ -1418,6 +1422,8 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   lsba_ctx c = new (std::nothrow) lsba_ctx_();
   if (!c) return LSBA_E_OOM;
   *out = c;  // returned even on failure so that lsba_last_error works; destroy it
+  if (const char* e = std::getenv("LSBA_NO_FUSE")) c->no_fuse = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
   if (n < s) return fail(c, LSBA_E_ARG, "n < s");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, LSBA_E_ARG, "bad rank/nranks");

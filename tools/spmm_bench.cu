@@ -144,6 +144,50 @@ k_spmm_pf(int n, const int* __restrict__ rp, const int* __restrict__ ci, const d
   reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
 }
 
+// H: batched entries: per chunk of NB entries of the row, all index/value loads first, then all
+// NB gathers, then the FMAs (NB independent gathers in flight per thread); register budget
+// from MINB CTAs of 256 per SM.  NA: index/value loads bypass L1 allocation.
+template <bool NA>
+__device__ __forceinline__ int ld_i(const int* p) {
+  if constexpr (NA) { int v; asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p)); return v; }
+  else return __ldg(p);
+}
+template <bool NA>
+__device__ __forceinline__ double ld_d(const double* p) {
+  if constexpr (NA) { double v; asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v; }
+  else return __ldg(p);
+}
+template <int S, int NB, int MINB, bool NA>
+__global__ void __launch_bounds__(256, MINB)
+k_spmm_batch(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+             const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 2;
+  const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / L), lane = (int)(gt % L);
+  const int lane32 = threadIdx.x & 31;
+  const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
+  const int rr = row_w + lane32;
+  const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+  const int me = lane32 / L;
+  const int p0 = __shfl_sync(0xffffffffu, pv, me), p1 = __shfl_sync(0xffffffffu, pv, me + 1);
+  if (row >= n) return;
+  double a0 = 0, a1 = 0;
+  for (int p = p0; p < p1; p += NB) {
+    int c[NB]; double a[NB]; double2 v[NB];
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+      const bool ok = p + t < p1;
+      c[t] = ok ? ld_i<NA>(ci + p + t) : row;
+      a[t] = ok ? ld_d<NA>(va + p + t) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < NB; ++t) v[t] = __ldg(reinterpret_cast<const double2*>(V + (size_t)c[t] * S) + lane);
+#pragma unroll
+    for (int t = 0; t < NB; ++t) { a0 = fma(a[t], v[t].x, a0); a1 = fma(a[t], v[t].y, a1); }
+  }
+  reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
+}
+
 template <typename F>
 static double time_it(F launch) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -201,6 +245,11 @@ static void run(int dims, int N) {
   check("pf", us);
   us = time_it([&] { k_spmm_pf<S, true><<<gA, 256>>>((int)n, drp, dci, dva, dV, dW); });
   check("pfV", us);
+#define HB(NB, MINB, NA) \
+  us = time_it([&] { k_spmm_batch<S, NB, MINB, NA><<<gA, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
+  check("b" #NB "m" #MINB #NA, us);
+  HB(4, 8, false) HB(4, 4, false) HB(8, 4, false) HB(8, 3, false) HB(4, 8, true) HB(8, 4, true)
+#undef HB
   cudaFree(drp); cudaFree(dci); cudaFree(dva); cudaFree(dV); cudaFree(dW); cudaFree(dW2);
 }
 
