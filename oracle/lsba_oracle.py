@@ -84,6 +84,140 @@ def spmm(row_ptr, col_idx, vals, V, chunk_rows: int = 1 << 16) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------------------
+# ILU(0) left preconditioning ("an incomplete LU (ILU)
+# preconditioner with no fill"; SPEC.md:512-528 for the interface and the side: LEFT, with
+# every residual and tolerance in the preconditioned norm — DESIGN.md reading R28)
+# --------------------------------------------------------------------------------------
+
+
+class ZeroPivot(ValueError):
+    """ILU(0) met a zero (or missing) pivot: the problem is reported unpreconditionable."""
+
+
+@dataclass
+class Ilu0Factors:
+    """L (unit lower, strictly-lower entries) and U (upper incl. diagonal) stored together in
+    the pattern of A: ``lu[p]`` for CSR position p (same row_ptr / col_idx as A)."""
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    lu: np.ndarray
+    diag: np.ndarray          # CSR position of a_ii per row
+    _plans: dict = field(default_factory=dict, repr=False)
+
+    def lower_solve(self, X):
+        """Y with L Y = X (unit diagonal): y_i = x_i - sum_{k<i} l_ik y_k (CSR order)."""
+        return _tri_solve(self, X, lower=True)
+
+    def upper_solve(self, Y):
+        """Z with U Z = Y: z_i = (y_i - sum_{j>i} u_ij z_j) / u_ii (CSR order)."""
+        return _tri_solve(self, Y, lower=False)
+
+    def solve(self, X):
+        """M^{-1} X = U^{-1} L^{-1} X."""
+        return self.upper_solve(self.lower_solve(X))
+
+
+def ilu0(row_ptr, col_idx, vals) -> Ilu0Factors:
+    """ILU(0), the IKJ variant (Saad, Iterative Methods, Alg 10.4) restricted to pattern(A):
+        for i = 2..n, for k < i with a_ik in the pattern (ascending):
+            a_ik = a_ik / a_kk
+            for j > k with a_ij in the pattern:  a_ij = a_ij - a_ik a_kj   (if a_kj is too)
+    Zero or structurally missing pivot -> ZeroPivot.  Plain row loops."""
+    n = len(row_ptr) - 1
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col_idx = np.asarray(col_idx, dtype=np.int64)
+    a = np.array(vals, dtype=np.float64)
+    pos = []
+    diag = np.full(n, -1, dtype=np.int64)
+    for i in range(n):
+        cols = col_idx[row_ptr[i]:row_ptr[i + 1]].tolist()
+        pos.append({c: row_ptr[i] + t for t, c in enumerate(cols)})
+        if i in pos[i]:
+            diag[i] = pos[i][i]
+    if np.any(diag < 0):
+        raise ZeroPivot(f"structurally missing diagonal in row {int(np.argmax(diag < 0))}")
+    for i in range(n):
+        p0, p1 = int(row_ptr[i]), int(row_ptr[i + 1])
+        for p in range(p0, p1):
+            k = int(col_idx[p])
+            if k >= i:
+                break
+            piv = a[diag[k]]
+            if piv == 0.0 or not math.isfinite(piv):
+                raise ZeroPivot(f"zero pivot u_{k}{k}")
+            a[p] = a[p] / piv
+            rk = pos[k]
+            for q in range(p + 1, p1):
+                r = rk.get(int(col_idx[q]))
+                if r is not None:
+                    a[q] = a[q] - a[p] * a[r]
+        if a[diag[i]] == 0.0 or not math.isfinite(a[diag[i]]):
+            raise ZeroPivot(f"zero pivot u_{i}{i}")
+    return Ilu0Factors(row_ptr, col_idx, a, diag)
+
+
+def _tri_plan(F: Ilu0Factors, lower: bool):
+    """Level sets of the triangular factor (rows whose dependencies are all in earlier levels)
+    and, per level, the off-diagonal CSR positions in CSR order.  Evaluating a level's rows
+    together changes no row's arithmetic (each row sums its own terms in CSR order)."""
+    if lower in F._plans:
+        return F._plans[lower]
+    rp, ci = F.row_ptr, F.col_idx
+    n = len(rp) - 1
+    lev = np.zeros(n, dtype=np.int64)
+    rows = range(n) if lower else range(n - 1, -1, -1)
+    for i in rows:
+        cols = ci[rp[i]:rp[i + 1]]
+        dep = cols[cols < i] if lower else cols[cols > i]
+        lev[i] = 1 + int(lev[dep].max()) if dep.size else 0
+    plan = []
+    for L in range(int(lev.max()) + 1 if n else 0):
+        R = np.nonzero(lev == L)[0]
+        ps, starts, nz_rows = [], [], []
+        for i in R:
+            seg = np.arange(rp[i], rp[i + 1])
+            seg = seg[ci[seg] < i] if lower else seg[ci[seg] > i]
+            if seg.size:
+                starts.append(sum(len(x) for x in ps))
+                ps.append(seg)
+                nz_rows.append(i)
+        plan.append((R, np.concatenate(ps) if ps else np.zeros(0, np.int64),
+                     np.array(starts, np.int64), np.array(nz_rows, np.int64)))
+    F._plans[lower] = plan
+    return plan
+
+
+def _tri_solve(F: Ilu0Factors, X, lower: bool):
+    X = np.asarray(X, dtype=np.float64)
+    Y = X.copy()
+    for R, ps, starts, nz_rows in _tri_plan(F, lower):
+        if ps.size:
+            contrib = F.lu[ps][:, None] * Y[F.col_idx[ps]]
+            Y[nz_rows] = Y[nz_rows] - np.add.reduceat(contrib, starts, axis=0)
+        if not lower:
+            Y[R] = Y[R] / F.lu[F.diag[R]][:, None]
+    return Y
+
+
+class IluOperator:
+    """The left-preconditioned operator X -> U^{-1} L^{-1} (A X)."""
+
+    def __init__(self, A, factors: Ilu0Factors):
+        self.A = A
+        self.F = factors
+
+    def __call__(self, V):
+        return self.F.solve(spmm(*self.A, V))
+
+
+def apply_A(A, V):
+    """The operator of the Krylov method: A V for a CSR triple, M^{-1} A V for an IluOperator."""
+    if isinstance(A, IluOperator):
+        return A(V)
+    return spmm(*A, V)
+
+
+# --------------------------------------------------------------------------------------
 # Near-exactly-rounded Gram  X^T Y  (parity note; DESIGN.md R23)
 # --------------------------------------------------------------------------------------
 
@@ -243,9 +377,8 @@ def pip_step(A, Vs, ip: str, force_flag: bool = False) -> StepResult:
         V_{k+1} = (W - V_k H_{1:k,k}) H_{k+1,k}^{-1}.
     Reading R1: Sec 3.1's "W - W H" is read as W - V_k H (line 6).
     Global (R3): H_{k+1,k} = sqrt(omega - sum_j h_j^2) I_s, flag iff radicand not > 0."""
-    row_ptr, col_idx, vals = A
     k = len(Vs)
-    W = spmm(row_ptr, col_idx, vals, Vs[-1])
+    W = apply_A(A, Vs[-1])
     s = W.shape[1]
     if ip == "cl":
         G = ip_cl(list(Vs) + [W], W)                  # ONE call: the step's single sync
@@ -365,7 +498,7 @@ class CwyArnoldi:
             self.V = []
             return flag
         self.V = [V1]
-        W = spmm(*self.A, V1)                                  # line 5
+        W = apply_A(self.A, V1)                                # line 5
         H11 = self._ip([V1], W)                                # line 7 (its own sync)
         self.Hbar[:b, :b] = H11
         self.U = W - self._mul(V1, H11)                        # line 8
@@ -376,7 +509,7 @@ class CwyArnoldi:
         b, k = self.b, len(self.V)
         Hcol = self.Hbar[: k * b, (k - 1) * b: k * b].copy()
         U = self.U
-        W = spmm(*self.A, U)                                   # line 5
+        W = apply_A(self.A, U)                                 # line 5
         G = self._ip(list(self.V) + [U], np.concatenate([U, W], axis=1)) if self.ip == "cl" else None
         if self.ip == "cl":
             s = self.s
@@ -436,7 +569,7 @@ class IrolsArnoldi(CwyArnoldi):
     def step(self, force_flag: bool = False) -> StepResult:
         b, k = self.b, len(self.V)
         U = self.U
-        W = spmm(*self.A, U)                                   # line 4
+        W = apply_A(self.A, U)                                 # line 4
         if self.ip == "cl":
             s = self.s
             G = ip_cl(list(self.V) + [U], np.concatenate([U, W], axis=1))   # line 10: one sync
@@ -482,7 +615,7 @@ class BmgsArnoldi(PipArnoldi):
 
     def step(self, force_flag: bool = False) -> StepResult:
         b, k = self.b, len(self.V)
-        W = spmm(*self.A, self.V[-1])
+        W = apply_A(self.A, self.V[-1])
         Hcol = np.zeros((k * b, b))
         for j in range(k):
             if self.ip == "cl":
@@ -517,7 +650,7 @@ class PioArnoldi(PipArnoldi):
 
     def step(self, force_flag: bool = False) -> StepResult:
         b, k = self.b, len(self.V)
-        W = spmm(*self.A, self.V[-1])
+        W = apply_A(self.A, self.V[-1])
         if self.ip == "cl":
             Hcol = ip_cl(list(self.V), W)                       # line 4
             Wt, f1 = chol_flag(ip_cl([W], W))                    # line 5 (IO of W)
@@ -561,7 +694,6 @@ class PioArnoldi(PipArnoldi):
 
 def bmgs_arnoldi(A, B, m: int, ip: str):
     """Alg 2 with the CholQR (cl) or global (gl) muscle.  Returns (V list, Hbar, beta)."""
-    row_ptr, col_idx, vals = A
     s = B.shape[1]
     b = s if ip == "cl" else 1
     io = io_cl if ip == "cl" else io_gl
@@ -570,7 +702,7 @@ def bmgs_arnoldi(A, B, m: int, ip: str):
     V = [V1]
     Hbar = np.zeros(((m + 1) * b, m * b))
     for k in range(1, m + 1):
-        W = spmm(row_ptr, col_idx, vals, V[k - 1])
+        W = apply_A(A, V[k - 1])
         for j in range(1, k + 1):
             if ip == "cl":
                 Hjk = ip_cl([V[j - 1]], W)
@@ -708,24 +840,31 @@ def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
           ip: str = "cl", mod: str = "gmres", cond_threshold: float = float("inf"),
           stop_on: str = "residual", X_star=None, force_flag_at=None,
           happy_check: bool = True, confirm_true: bool = True, record_kappa: bool = False,
-          skel: str = "pip"):
+          skel: str = "pip", prec=None):
     """Restarted modified BFOM/BGMRES with BCGS-PIP-Arnoldi (skel='pip', Alg 3) or
     BMGS-CWY / BMGS-ICWY-Arnoldi (skel='cwy' / 'icwy', Alg 6) and adaptive restart.
+    ``prec='ilu0'`` (or an Ilu0Factors) runs the same method on M^{-1} A X = M^{-1} B with
+    M = LU from ILU(0) (left preconditioning; tolerances in the preconditioned norm, R28).
 
     Follows SURVEY.md 8(c) "Step list" literally; readings cited inline.  ``A`` is the CSR
     triple (row_ptr, col_idx, vals).  ``stop_on='error'`` (test-only, pin P13) stops on
     ||X - X*||_F / ||X*||_F <= tol with X* given (PAPER.md:424-428).  ``force_flag_at`` is
     the fault-injection hook (a NaN-flag at that step k of the first cycle reaching it).
     Returns (X, SolveInfo)."""
-    row_ptr, col_idx, vals = A
     n, s = B.shape
     b = s if ip == "cl" else 1
     B = np.asarray(B, dtype=np.float64)
+    if prec is not None:      # left ILU(0): solve M^{-1} A X = M^{-1} B (R28, SPEC.md:518-522)
+        F = ilu0(*A) if isinstance(prec, str) else prec
+        if isinstance(prec, str) and prec != "ilu0":
+            raise ValueError(f"unknown preconditioner {prec!r}")
+        A = IluOperator(A, F)
+        B = F.solve(B)
     normB = math.sqrt(float(gram(B.reshape(-1, 1), B.reshape(-1, 1))[0, 0]))   # ||B||_F (R18)
     X = np.zeros_like(B) if X0 is None else np.array(X0, dtype=np.float64)
     if normB == 0.0:                               # B = 0: X = 0 is exact; nothing to do
         return np.zeros_like(B), SolveInfo(outcome=CONVERGED, true_relres=0.0, m_final=m)
-    U = B.copy() if X0 is None else B - spmm(row_ptr, col_idx, vals, X)       # R13
+    U = B.copy() if X0 is None else B - apply_A(A, X)                          # R13
     Cacc = np.eye(b)
     info = SolveInfo(skel=skel)
     m_cur = m
@@ -744,7 +883,7 @@ def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
     forced_done = False
 
     def true_relres(Xc):
-        Rr = B - spmm(row_ptr, col_idx, vals, Xc)
+        Rr = B - apply_A(A, Xc)
         return float(np.linalg.norm(Rr)) / normB
 
     for cycle in range(1, max_restarts + 2):
@@ -832,7 +971,7 @@ def solve(A, B, X0=None, m: int = 10, tol: float = 1e-8, max_restarts: int = 50,
                 break
             # R19: the estimate drifted; restart from the true residual
             info.false_convergences += 1
-            U = B - spmm(row_ptr, col_idx, vals, X)
+            U = B - apply_A(A, X)
             Cacc = np.eye(b)
             continue
         # U = V_{k+1} [M; -H_{k+1,k}]  and  C_acc <- cos C_acc  (R10)
