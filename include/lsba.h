@@ -41,7 +41,8 @@ typedef enum {
   LSBA_E_CUDA = 2,   /* a CUDA runtime call or kernel launch failed              */
   LSBA_E_NCCL = 3,   /* an NCCL call failed                                      */
   LSBA_E_OOM = 4,    /* device or pinned-host allocation failed                  */
-  LSBA_E_STATE = 5   /* call out of order (e.g. step before arnoldi_begin)       */
+  LSBA_E_STATE = 5,  /* call out of order (e.g. step before arnoldi_begin)       */
+  LSBA_E_NUMERIC = 6 /* ILU(0) zero pivot: the problem is unpreconditionable     */
 } lsba_status;
 
 /* Table 1. */
@@ -190,6 +191,28 @@ lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
  * With BMGS-(I)CWY, lsba_arnoldi_begin also runs Alg 6's first loop iteration, and step k
  * (its iteration k+1) completes Hessenberg column k and forms V_{k+1}. */
 lsba_status lsba_set_skeleton(lsba_ctx ctx, lsba_skel skel);
+/* ---------------------------------------------------------------- ILU(0) left preconditioning
+ * SURVEY.md 8(f) f4; PAPER.md:485 ("an incomplete LU (ILU) preconditioner with no fill");
+ * SPEC.md:512-528 (IKJ ILU(0) restricted to pattern(A); LEFT preconditioning, every residual
+ * and tolerance in the preconditioned norm — DESIGN.md reading R28).
+ *
+ * lsba_ilu0_setup(ctx, 1): on first use factors the context's matrix on the device (host level
+ * analysis, one launch per level of L); from then on every operator application of the
+ * Arnoldi process and the solvers is M^{-1} A (SpMM followed by two sync-free triangular
+ * solves), the solvers target M^{-1} A X = M^{-1} B and report true_relres =
+ * ||M^{-1}(B - A X)||_F / ||M^{-1} B||_F.  enable = 0 restores the plain operator (factors kept).
+ * With P > 1 each rank factors its local diagonal block (block-Jacobi ILU(0); ghost columns
+ * dropped) — identical to ILU(0) of A on one rank.  lsba_spmm stays the plain A V.
+ * Errors: LSBA_E_NUMERIC on a zero or structurally missing pivot (message names the row). */
+lsba_status lsba_ilu0_setup(lsba_ctx ctx, int32_t enable);
+/* Y = M^{-1} X = U^{-1} L^{-1} X for device n_local x s row-major blocks (X == Y allowed).
+ * LSBA_E_STATE before lsba_ilu0_setup. */
+lsba_status lsba_ilu0_apply(lsba_ctx ctx, const double* X_dev, double* Y_dev);
+/* Copy the factor values (nnz_local doubles in the CSR order of the matrix: strictly-lower
+ * entries are L with unit diagonal implied, the rest U) to lu_host, and the level counts of L
+ * and U to levels_host[2] (either pointer may be NULL). */
+lsba_status lsba_copy_ilu0_factors(lsba_ctx ctx, double* lu_host, int32_t* levels_host);
+
 /* Kernel implementation choice: 0 = default (streaming tensor-core v7 Gram / streaming global
  * Gram, DMMA projection for s in {8, 16}, DFMA otherwise, small step fused into the Gram on one
  * rank), 1 = plain DFMA Gram and projection kernels (for parity tests of both paths). */
@@ -199,7 +222,8 @@ lsba_status lsba_set_kernel_variant(lsba_ctx ctx, int32_t variant);
 enum {
   LSBA_K_SPMM = 0, LSBA_K_GRAM = 1, LSBA_K_GRAM_FINALIZE = 2, LSBA_K_SMALL_STEP = 3,
   LSBA_K_PROJECT = 4, LSBA_K_CYCLE_SOLVE = 5, LSBA_K_COMBINE = 6, LSBA_K_RESIDUAL = 7,
-  LSBA_K_HALO_PACK = 8, LSBA_K_MISC = 9, LSBA_K_STEP_UPDATE = 10, LSBA_K_COUNT = 11
+  LSBA_K_HALO_PACK = 8, LSBA_K_MISC = 9, LSBA_K_STEP_UPDATE = 10, LSBA_K_ILU_SOLVE = 11,
+  LSBA_K_COUNT = 12
 };
 /* enable != 0 starts recording events around every launch (resets the records). */
 lsba_status lsba_profile_enable(lsba_ctx ctx, int32_t enable);

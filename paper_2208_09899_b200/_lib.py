@@ -18,14 +18,14 @@ if not os.path.exists(library_path):
                       "(paper_2208_09899_b200/build.sh). There is no CPU fallback.")
 lib = C.CDLL(library_path)
 
-LSBA_OK, LSBA_E_ARG, LSBA_E_CUDA, LSBA_E_NCCL, LSBA_E_OOM, LSBA_E_STATE = range(6)
+LSBA_OK, LSBA_E_ARG, LSBA_E_CUDA, LSBA_E_NCCL, LSBA_E_OOM, LSBA_E_STATE, LSBA_E_NUMERIC = range(7)
 LSBA_IP_CLASSICAL, LSBA_IP_GLOBAL = 0, 1
 (LSBA_SKEL_BCGS_PIP, LSBA_SKEL_BMGS_CWY, LSBA_SKEL_BMGS_ICWY, LSBA_SKEL_BMGS, LSBA_SKEL_BCGS_PIO,
  LSBA_SKEL_BCGS_IROLS) = 0, 1, 2, 3, 4, 5
 _SKEL = {"pip": 0, "cwy": 1, "icwy": 2, "bmgs": 3, "pio": 4, "irols": 5, 0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5}
 LSBA_CONVERGED, LSBA_MAX_RESTARTS, LSBA_DEAD = 0, 1, 2
 KERNEL_IDS = dict(spmm=0, gram=1, gram_finalize=2, small_step=3, project=4, cycle_solve=5,
-                  combine=6, residual=7, halo_pack=8, misc=9, step_update=10)
+                  combine=6, residual=7, halo_pack=8, misc=9, step_update=10, ilu_solve=11)
 _IP = {"cl": LSBA_IP_CLASSICAL, "gl": LSBA_IP_GLOBAL, 0: 0, 1: 1}
 
 
@@ -75,6 +75,9 @@ _sigs = {
     "lsba_workspace_bytes": [_vp, C.POINTER(_i64)],
     "lsba_ghost_plan": [_i64, _i64, _vp, _i64, _vp, _i32, _vp, _vp, C.POINTER(_i64), _vp],
     "lsba_csr_validate": [_i64, _i64, _vp, _vp, C.POINTER(C.c_char_p)],
+    "lsba_ilu0_setup": [_vp, _i32],
+    "lsba_ilu0_apply": [_vp, _vp, _vp],
+    "lsba_copy_ilu0_factors": [_vp, _vp, _vp],
     "lsba_status_str": [C.c_int],
     "lsba_last_error": [_vp],
 }
@@ -228,6 +231,22 @@ def lsba_block_inner_product(ctx, V, nblocks, Y, ip="cl", s=None):
     return G.reshape(nblocks * s, s) if _IP[ip] == LSBA_IP_CLASSICAL else G
 
 
+def lsba_ilu0_setup(ctx, enable=True):
+    _check(lib.lsba_ilu0_setup(ctx, 1 if enable else 0), ctx)
+
+
+def lsba_ilu0_apply(ctx, X, Y):
+    _check(lib.lsba_ilu0_apply(ctx, _dptr(X, "X"), _dptr(Y, "Y")), ctx)
+    return Y
+
+
+def lsba_copy_ilu0_factors(ctx, nnz):
+    lu = np.zeros(max(int(nnz), 1))
+    lev = np.zeros(2, dtype=np.int32)
+    _check(lib.lsba_copy_ilu0_factors(ctx, _hptr(lu), _hptr(lev)), ctx)
+    return lu[:nnz], (int(lev[0]), int(lev[1]))
+
+
 def lsba_set_force_flag(ctx, k):
     _check(lib.lsba_set_force_flag(ctx, int(k)), ctx)
 
@@ -354,6 +373,16 @@ class Context:
         W = torch.empty_like(V)
         return lsba_spmm(self.ctx, V, W)
 
-    def solve(self, B, X, m, tol, max_restarts, ip="cl", mod="gmres", cond_threshold=float("inf"), skel="pip"):
+    def solve(self, B, X, m, tol, max_restarts, ip="cl", mod="gmres", cond_threshold=float("inf"), skel="pip",
+              prec=None):
+        """prec=None: the plain operator; prec="ilu0": left ILU(0) (factored on first use)."""
+        if prec not in (None, "ilu0"):
+            raise ValueError(f"unknown preconditioner {prec!r}")
+        lsba_ilu0_setup(self.ctx, prec == "ilu0")
         fn = lsba_bgmres_solve if mod == "gmres" else lsba_bfom_solve
         return fn(self.ctx, B, X, m, tol, max_restarts, ip, cond_threshold, skel)
+
+    def ilu0_apply(self, X):
+        import torch
+        Y = torch.empty_like(X)
+        return lsba_ilu0_apply(self.ctx, X, Y)

@@ -1,0 +1,141 @@
+// ilu.cuh — ILU(0) left preconditioning on the device ("an
+// incomplete LU (ILU) preconditioner with no fill"; left side, IKJ variant).
+//
+//   k_ilu0_level   one level of the IKJ factorisation, a warp per row (setup, once per matrix)
+//   k_ilu_trsv     sync-free sparse triangular solve Y <- L^{-1} Y or U^{-1} Y in place, one
+//                  thread per row (all s columns), rows in level order, per-row ready flags
+//
+// Factor storage: lu[p] for CSR position p of the local matrix (row_ptr / col_idx of A):
+// strictly-lower entries are L (unit diagonal implied), the rest U.  Columns >= n_local
+// (ghost rows of other ranks) are not part of the factor: with P > 1 this is block-Jacobi
+// ILU(0) of the local diagonal block, equal to ILU(0) of A on one rank.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lsba {
+
+// One level of Saad's IKJ ILU(0) (Iterative Methods, Alg 10.4), a warp per row i of the level:
+//   for k < i in row i (ascending):  l = a_ik / a_kk;  a_ik = l;
+//                                    a_ij -= l a_kj  for j > k in row i with (k, j) in pattern
+// Rows of earlier levels (every k above) are final.  Lane 0 owns a_ik, lanes stride the j's.
+// Zero / non-finite pivot -> *bad = 1 (the factor is then unusable; the host reports it).
+__global__ void __launch_bounds__(256)
+k_ilu0_level(int cnt, const int* __restrict__ rows, const int* __restrict__ rp,
+             const int* __restrict__ ci, const int* __restrict__ diag, int n_local, double* lu,
+             int* bad) {
+  const int w = (int)((blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= cnt) return;
+  const int i = rows[w];
+  const int p0 = rp[i], p1 = rp[i + 1];
+  for (int p = p0; p < p1; ++p) {
+    const int k = ci[p];
+    if (k >= n_local || k >= i) continue;          // ghost column, or not in the L part
+    const double piv = lu[diag[k]];
+    if (!(piv != 0.0) || !isfinite(piv)) {
+      if (lane == 0) *bad = 1;
+      return;
+    }
+    const double l = lu[p] / piv;
+    __syncwarp();
+    if (lane == 0) lu[p] = l;
+    const int k0 = rp[k], k1 = rp[k + 1];
+    for (int q = p + 1 + lane; q < p1; q += 32) {
+      const int j = ci[q];
+      if (j >= n_local) continue;
+      for (int r = k0; r < k1; ++r)                 // a_kj (row k is short: linear scan)
+        if (ci[r] == j) {
+          lu[q] = fma(-l, lu[r], lu[q]);
+          break;
+        }
+    }
+    __syncwarp();                                   // a_ij updates visible to lane 0's next a_ik
+  }
+  if (lane == 0) {
+    const double d = lu[diag[i]];
+    if (!(d != 0.0) || !isfinite(d)) *bad = 1;
+  }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// Sync-free triangular solve, in place on Y (n_local x S, row-major):
+//   LOWER:  y_i = x_i - sum_{k<i} l_ik y_k          (unit diagonal)
+//   UPPER:  y_i = (x_i - sum_{j>i} u_ij y_j) / u_ii
+// each sum in CSR order (the oracle's order).  Thread t handles row order[t] (rows sorted by
+// level, so every dependency has a smaller position); CTAs take their row ranges in the order
+// they START (atomic ticket), so a CTA's dependencies belong to CTAs already running or done —
+// spinning cannot deadlock.  A row publishes ready[i] = gen (release) after its store; readers
+// acquire ready[k] == gen before loading y_k.  gen is unique per launch (no flag reset).
+template <int S, bool LOWER>
+__global__ void __launch_bounds__(256)
+k_ilu_trsv(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
+           const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
+           int n_local, double* Y, unsigned* ready, unsigned gen, unsigned* ticket,
+           const int* __restrict__ active) {
+  __shared__ int blk;
+  if (threadIdx.x == 0) {
+    const unsigned w = atomicAdd(ticket, 1u);
+    if (w == gridDim.x - 1) *ticket = 0u;          // every CTA has claimed: reset for the next launch
+    blk = (int)w;
+  }
+  __syncthreads();
+  if (active && *active == 0) return;
+  const int t = blk * blockDim.x + threadIdx.x;
+  if (t >= nrows) return;
+  const int i = order[t];
+  const int p0 = rp[i], p1 = rp[i + 1];
+  double acc[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) acc[c] = 0.0;
+  for (int p = p0; p < p1; ++p) {
+    const int k = ci[p];
+    if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
+    if (ld_acquire_u32(ready + k) != gen) {
+      while (ld_acquire_u32(ready + k) != gen) __nanosleep(32);
+    }
+    const double a = lu[p];
+    const double* yk = Y + (size_t)k * S;
+#pragma unroll
+    for (int c = 0; c < S; ++c) acc[c] = fma(a, __ldcg(yk + c), acc[c]);
+  }
+  double* yi = Y + (size_t)i * S;
+  const double dinv = LOWER ? 1.0 : lu[diag[i]];
+#pragma unroll
+  for (int c = 0; c < S; ++c) {
+    const double r = __ldcg(yi + c) - acc[c];
+    __stcg(yi + c, LOWER ? r : r / dinv);
+  }
+  __threadfence();
+  st_release_u32(ready + i, gen);
+}
+
+// per-CTA partial sums of squares of x[0..count) (grid-stride; fixed order per CTA)
+__global__ void __launch_bounds__(256)
+k_sq_partials(long count, const double* __restrict__ x, double* __restrict__ part) {
+  __shared__ double red[8];
+  double t = 0.0;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x) {
+    const double v = x[e];
+    t = fma(v, v, t);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) u += red[w];
+    part[blockIdx.x] = u;
+  }
+}
+
+}  // namespace lsba

@@ -25,6 +25,7 @@
 #include "small.cuh"  // SmallState2 / StepStatus layouts (kernels are in small_inst.cu)
 #include "dmma.cuh"
 #include "gram7.cuh"
+#include "ilu.cuh"
 #include "launch_small.h"
 
 using namespace lsba;
@@ -110,6 +111,17 @@ struct lsba_ctx_ {
   bool forced_done = false;
   int variant = 0;
   bool no_fuse = false;          // diagnostics: LSBA_NO_FUSE=1 keeps the small step a separate launch
+  // ILU(0) left preconditioning (ilu.cuh; lsba_ilu0_setup)
+  bool prec = false;             // operator is M^{-1} A (every spmm / residual)
+  bool ilu_ready = false;
+  double* d_lu = nullptr;        // factor values in the CSR pattern of A
+  int* d_diag = nullptr;         // CSR position of a_ii
+  int* d_ordL = nullptr;         // rows by level of L (ascending dependencies)
+  int* d_ordU = nullptr;         // rows by level of U
+  unsigned* d_ready = nullptr;   // per-row ready flags of the sync-free solves
+  unsigned* d_ticket = nullptr;  // CTA start tickets (2: L and U solves)
+  unsigned ilu_gen = 0;          // launch generation (ready[i] == gen: row i solved)
+  int ilu_levels[2] = {0, 0};
   int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
@@ -250,6 +262,32 @@ static lsba_status halo_t(lsba_ctx c, const double* V) {
   return LSBA_OK;
 }
 
+// ---------------------------------------------------------------- f4: ILU(0) apply
+// Y <- U^{-1} L^{-1} Y in place (two sync-free triangular solves; ilu.cuh)
+template <int S>
+static lsba_status ilu_apply_t(lsba_ctx c, double* Y, const int* active) {
+  if (!c->ilu_ready) return fail(c, LSBA_E_STATE, "ILU(0) preconditioner not set up");
+  if (c->n == 0) return LSBA_OK;
+  const int nblk = cdiv(c->n, kThreads);
+  // algorithmic bytes per solve: the factor half (~12 B per stored entry + row pointers and
+  // the row order) and Y read + written once
+  const double by = 6.0 * c->nnz + 8.0 * (c->n + 1) + 16.0 * c->n * S;
+  {
+    LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+    k_ilu_trsv<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci, c->d_lu,
+        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket, active);
+    CKL();
+  }
+  {
+    LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+    k_ilu_trsv<S, false><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci, c->d_lu,
+        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 1, active);
+    CKL();
+  }
+  return LSBA_OK;
+}
+static lsba_status ilu_apply(lsba_ctx c, double* Y, const int* active = nullptr);
+
 // ---------------------------------------------------------------- a1: SpMM / residual
 template <int S>
 static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* active) {
@@ -266,6 +304,7 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
         c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
   }
   CKL();
+  if (c->prec) TRY(ilu_apply_t<S>(c, W, active));
   return LSBA_OK;
 }
 
@@ -288,6 +327,12 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
       k_spmm_odd<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
                                                               c->d_ghost, Bm, out, c->d_sq, nullptr);
     }
+    CKL();
+  }
+  if (c->prec && c->n > 0) {   // preconditioned residual M^{-1}(B - A X) and its norm (R28)
+    TRY(ilu_apply_t<S>(c, out, nullptr));
+    LaunchScope Ls(c, LSBA_K_MISC, 8.0 * c->n * S);
+    k_sq_partials<<<nblk, kThreads, 0, c->stream>>>((long)c->n * S, out, c->d_sq);
     CKL();
   }
   {
@@ -496,6 +541,9 @@ static lsba_status spmm(lsba_ctx c, const double* V, double* W, const int* activ
 }
 static lsba_status residual(lsba_ctx c, const double* Bm, const double* X, double* out) {
   LSBA_DISPATCH_S(c->s, residual_t, c, Bm, X, out);
+}
+static lsba_status ilu_apply(lsba_ctx c, double* Y, const int* active) {
+  LSBA_DISPATCH_S(c->s, ilu_apply_t, c, Y, active);
 }
 static lsba_status gram(lsba_ctx c, const double* X, size_t xstride, int J, double* Y, int ip,
                         const double* Vk = nullptr, const int* active = nullptr, int coef_k = -1,
@@ -910,8 +958,18 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     info->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   };
 
-  // ||B||_F^2 = s * <B,B>_gl  (R18: tolerance relative to ||B||_F)
-  TRY(gram(c, B, 0, 1, const_cast<double*>(B), LSBA_IP_GLOBAL));
+  // ||B||_F^2 = s * <B,B>_gl  (R18: tolerance relative to ||B||_F); preconditioned (R28):
+  // the method runs on M^{-1} A X = M^{-1} B, so the reference norm is ||M^{-1} B||_F and
+  // slot 0 keeps M^{-1} B (= U when X0 = 0)
+  if (c->prec) {
+    if (c->n > 0) {
+      CK(cudaMemcpyAsync(slotp(c, 0), B, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+      TRY(ilu_apply(c, slotp(c, 0)));
+    }
+    TRY(gram(c, slotp(c, 0), 0, 1, slotp(c, 0), LSBA_IP_GLOBAL));
+  } else {
+    TRY(gram(c, B, 0, 1, const_cast<double*>(B), LSBA_IP_GLOBAL));
+  }
   CK(cudaMemcpyAsync(c->h_scalar, c->d_G, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const double normB = std::sqrt(std::max(0.0, *c->h_scalar * c->s));
@@ -947,7 +1005,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     CK(cudaStreamSynchronize(c->stream));
     if (c->h_info[0]) {
       TRY(residual(c, B, X, slotp(c, 0)));
-    } else if (c->n > 0) {
+    } else if (c->n > 0 && !c->prec) {       // (preconditioned: slot 0 already holds M^{-1} B)
       CK(cudaMemcpyAsync(slotp(c, 0), B, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
     }
   }
@@ -1162,6 +1220,7 @@ extern "C" const char* lsba_status_str(lsba_status st) {
     case LSBA_E_NCCL: return "LSBA_E_NCCL";
     case LSBA_E_OOM: return "LSBA_E_OOM";
     case LSBA_E_STATE: return "LSBA_E_STATE";
+    case LSBA_E_NUMERIC: return "LSBA_E_NUMERIC";
   }
   return "LSBA_E_UNKNOWN";
 }
@@ -1192,7 +1251,8 @@ static void release(lsba_ctx c) {
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
-                  c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb};
+                  c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL,
+                  c->d_ordU, c->d_ready, c->d_ticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1604,8 +1664,122 @@ extern "C" lsba_status lsba_spmm(lsba_ctx c, const double* V_dev, double* W_dev)
   if (c->n > 0 && (!V_dev || !W_dev || V_dev == W_dev)) return fail(c, LSBA_E_ARG, "V/W NULL or aliased");
   if (((uintptr_t)V_dev | (uintptr_t)W_dev) & 15) return fail(c, LSBA_E_ARG, "V/W not 16-byte aligned");
   CK(cudaSetDevice(c->device));
-  if (c->n > 0) TRY(spmm(c, V_dev, W_dev));
+  const bool prec = c->prec;   // lsba_spmm is the plain operator A V (a1), never M^{-1} A V
+  c->prec = false;
+  const lsba_status st = (c->n > 0) ? spmm(c, V_dev, W_dev) : LSBA_OK;
+  c->prec = prec;
+  TRY(st);
   CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+// ---------------------------------------------------------------- f4: ILU(0) setup / apply
+static lsba_status ilu0_factor(lsba_ctx c) {
+  const int n = c->n;
+  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(c->nnz, 1));
+  CK(cudaMemcpy(rp.data(), c->d_rp, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost));
+  if (c->nnz) CK(cudaMemcpy(ci.data(), c->d_ci, sizeof(int32_t) * c->nnz, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> diag(std::max(n, 1), -1), levL(std::max(n, 1), 0), levU(std::max(n, 1), 0);
+  for (int i = 0; i < n; ++i)
+    for (int p = rp[i]; p < rp[i + 1]; ++p)
+      if (ci[p] == i) diag[i] = p;
+  for (int i = 0; i < n; ++i)
+    if (diag[i] < 0) return fail(c, LSBA_E_NUMERIC, "ILU(0): structurally missing diagonal in local row %d", i);
+  // level sets (host graph analysis): L row i after every k < i of its row, U row i after j > i
+  int nlL = 0, nlU = 0;
+  for (int i = 0; i < n; ++i) {
+    int l = 0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p)
+      if (ci[p] < i) l = std::max(l, levL[ci[p]] + 1);
+    levL[i] = l;
+    nlL = std::max(nlL, l + 1);
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    int l = 0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p)
+      if (ci[p] > i && ci[p] < n) l = std::max(l, levU[ci[p]] + 1);
+    levU[i] = l;
+    nlU = std::max(nlU, l + 1);
+  }
+  auto order_by = [&](const std::vector<int32_t>& lev, int nl, std::vector<int32_t>& ord, std::vector<int32_t>& ptr) {
+    ptr.assign(nl + 1, 0);
+    for (int i = 0; i < n; ++i) ptr[lev[i] + 1]++;
+    for (int l = 0; l < nl; ++l) ptr[l + 1] += ptr[l];
+    std::vector<int32_t> pos(ptr.begin(), ptr.end() - 1);
+    ord.assign(std::max(n, 1), 0);
+    for (int i = 0; i < n; ++i) ord[pos[lev[i]]++] = i;     // ascending rows within a level
+  };
+  std::vector<int32_t> ordL, ptrL, ordU, ptrU;
+  order_by(levL, nlL, ordL, ptrL);
+  order_by(levU, nlU, ordU, ptrU);
+  if (!c->d_lu) {
+    TRY(dalloc(c, &c->d_lu, c->nnz));
+    TRY(dalloc(c, &c->d_diag, n));
+    TRY(dalloc(c, &c->d_ordL, n));
+    TRY(dalloc(c, &c->d_ordU, n));
+    TRY(dalloc(c, &c->d_ready, n));
+    TRY(dalloc(c, &c->d_ticket, 2));
+  }
+  CK(cudaMemcpy(c->d_diag, diag.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_ordL, ordL.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_ordU, ordU.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemset(c->d_ready, 0, sizeof(unsigned) * n));
+  CK(cudaMemset(c->d_ticket, 0, sizeof(unsigned) * 2));
+  c->ilu_gen = 0;
+  if (c->nnz) CK(cudaMemcpy(c->d_lu, c->d_va, sizeof(double) * c->nnz, cudaMemcpyDeviceToDevice));
+  CK(cudaMemsetAsync(c->d_info, 0, sizeof(int), c->stream));
+  for (int l = 0; l < nlL; ++l) {          // one launch per level of L (setup only)
+    const int cnt = ptrL[l + 1] - ptrL[l];
+    LaunchScope Ls(c, LSBA_K_MISC, 0.0);
+    k_ilu0_level<<<cdiv((long)cnt * 32, kThreads), kThreads, 0, c->stream>>>(
+        cnt, c->d_ordL + ptrL[l], c->d_rp, c->d_ci, c->d_diag, n, c->d_lu, c->d_info);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->h_info[0]) return fail(c, LSBA_E_NUMERIC, "ILU(0): zero pivot");
+  c->ilu_levels[0] = nlL;
+  c->ilu_levels[1] = nlU;
+  c->ilu_ready = true;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_ilu0_setup(lsba_ctx c, int32_t enable) {
+  if (!c) return LSBA_E_ARG;
+  CK(cudaSetDevice(c->device));
+  if (!enable) {
+    c->prec = false;
+    return LSBA_OK;
+  }
+  if (!c->ilu_ready && c->n > 0) TRY(ilu0_factor(c));
+  if (c->n == 0) c->ilu_ready = true;
+  c->prec = true;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_ilu0_apply(lsba_ctx c, const double* X_dev, double* Y_dev) {
+  if (!c) return LSBA_E_ARG;
+  if (!c->ilu_ready) return fail(c, LSBA_E_STATE, "ILU(0) not set up (lsba_ilu0_setup)");
+  if (c->n > 0 && (!X_dev || !Y_dev)) return fail(c, LSBA_E_ARG, "X/Y NULL");
+  CK(cudaSetDevice(c->device));
+  if (c->n == 0) return LSBA_OK;
+  if (X_dev != Y_dev)
+    CK(cudaMemcpyAsync(Y_dev, X_dev, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+  TRY(ilu_apply(c, Y_dev));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_copy_ilu0_factors(lsba_ctx c, double* lu_host, int32_t* levels_host) {
+  if (!c) return LSBA_E_ARG;
+  if (!c->ilu_ready) return fail(c, LSBA_E_STATE, "ILU(0) not set up (lsba_ilu0_setup)");
+  CK(cudaSetDevice(c->device));
+  if (lu_host && c->nnz)
+    CK(cudaMemcpy(lu_host, c->d_lu, sizeof(double) * c->nnz, cudaMemcpyDeviceToHost));
+  if (levels_host) {
+    levels_host[0] = c->ilu_levels[0];
+    levels_host[1] = c->ilu_levels[1];
+  }
   return LSBA_OK;
 }
 
