@@ -47,6 +47,13 @@ def roof_cycle_extra(n, s, k_used):
     return 8.0 * n * s * (k_used + 7)
 
 
+def ilu_bytes(nnz, n, s, iters):
+    """ILU(0) left preconditioning (--prec ilu0): per operator application two triangular
+    solves, each ~12 B per stored factor entry of its half (6 nnz in total), row pointers and
+    the level order (8 B per row) and the block read + written once (16 ns)."""
+    return iters * 2.0 * (6.0 * nnz + 8.0 * (n + 1) + 16.0 * n * s)
+
+
 def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks, skel="pip"):
     """sum_steps ROOF(k) + per-cycle bytes, from the solver's counters (gram_blocks = sum over
     accepted steps of k+1).  BCGS-PIP: ROOF(k) = A + 8ns(2k+3), + 8ns(k_used+7) per cycle.
@@ -224,6 +231,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
+    ap.add_argument("--prec", default="none", choices=["none", "ilu0"],
+                    help="left ILU(0) preconditioning (SURVEY 8(f) f4); factored before the timed region")
     ap.add_argument("--skel", default="pip", choices=["pip", "cwy", "icwy", "irols", "bmgs", "pio"],
                     help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3), BMGS-CWY / -ICWY (Alg 6), BCGS-IRO-LS "
                          "(Alg 7), or the comparison baselines BMGS (Alg 2) and BCGS-PIO (Alg 4)")
@@ -257,6 +266,8 @@ def main():
                     stream=stream.cuda_stream)
     L.lsba_set_kernel_variant(ctx.ctx, args.variant)
     L.lsba_set_skeleton(ctx.ctx, args.skel)
+    if args.prec == "ilu0":
+        L.lsba_ilu0_setup(ctx.ctx, True)
     B = torch.from_numpy(wl["B"]).cuda()
     X = torch.zeros_like(B)
     m, tol, s = wl["m"], wl["tol"], wl["s"]
@@ -320,6 +331,8 @@ def main():
     # whole-job algorithmic bytes (global problem): sum over accepted steps of ROOF(k) =
     # iters (A + 8ns) + 16ns sum(k+1), plus 8ns(k_used + 7) per cycle
     total_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, iters, cycles, timed_cycles.gram_blocks, args.skel)
+    if args.prec == "ilu0":
+        total_bytes += ilu_bytes(wl["nnz"], n_glob, s, iters)
     gbs = total_bytes / (ms / 1e3) / 1e9
     steps_per_s = iters / (ms / 1e3)
     peak, peak_kind = measured_peaks()
@@ -360,6 +373,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, e2e_iters, e2e_cycles, e2e_gb, args.skel)
+        if args.prec == "ilu0":
+            e2e_bytes += ilu_bytes(wl["nnz"], n_glob, s, e2e_iters)
         e2e = {"value": e2e_bytes / dt / 1e9, "unit": "GB/s", "block_steps_per_s": e2e_iters / dt,
                "h2d_bytes_per_step": 2 * n_loc * s * 8 * world, "d2h_bytes_per_step": n_loc * s * 8 * world,
                "api": "lsba_solve_host (" + ("one full solve per step, X0 = 0" if full_solve
@@ -386,12 +401,16 @@ def main():
                        "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY",
                                                           "irols": "BCGS-IRO-LS", "bmgs": "BMGS",
                                                           "pio": "BCGS-PIO"}[args.skel]
-                                 + " skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO"),
+                                 + " skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO")
+                                 + (", left ILU(0)" if args.prec == "ilu0" else ""),
                        "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
                                       f"{iters / args.steps:.1f} block steps)") if full_solve
                                      else f"restart cycle = IO + {m} block steps + cycle end",
                        "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": dom,
+                         **({"note": "level-scheduled triangular solves: latency-bound (one dependency "
+                                     "level after another), reported against the HBM roof"}
+                            if dom == "ilu_solve" else {}), "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "launches": dn, "kernel_share_of_step": dms / tot_ms if tot_ms else None,
                          "measured_in": "instrumented re-run of the same K cycles (per-launch CUDA events "

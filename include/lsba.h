@@ -209,9 +209,10 @@ lsba_status lsba_ilu0_setup(lsba_ctx ctx, int32_t enable);
  * LSBA_E_STATE before lsba_ilu0_setup. */
 lsba_status lsba_ilu0_apply(lsba_ctx ctx, const double* X_dev, double* Y_dev);
 /* Copy the factor values (nnz_local doubles in the CSR order of the matrix: strictly-lower
- * entries are L with unit diagonal implied, the rest U) to lu_host, and the level counts of L
- * and U to levels_host[2] (either pointer may be NULL). */
-lsba_status lsba_copy_ilu0_factors(lsba_ctx ctx, double* lu_host, int32_t* levels_host);
+ * entries are L with unit diagonal implied, the rest U) to lu_host (capacity doubles;
+ * LSBA_E_ARG if capacity < nnz_local), and the level counts of L and U to levels_host[2]
+ * (either pointer may be NULL). */
+lsba_status lsba_copy_ilu0_factors(lsba_ctx ctx, double* lu_host, int64_t capacity, int32_t* levels_host);
 
 /* Kernel implementation choice: 0 = default (streaming tensor-core v7 Gram / streaming global
  * Gram, DMMA projection for s in {8, 16}, DFMA otherwise, small step fused into the Gram on one

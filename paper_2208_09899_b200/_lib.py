@@ -77,7 +77,7 @@ _sigs = {
     "lsba_csr_validate": [_i64, _i64, _vp, _vp, C.POINTER(C.c_char_p)],
     "lsba_ilu0_setup": [_vp, _i32],
     "lsba_ilu0_apply": [_vp, _vp, _vp],
-    "lsba_copy_ilu0_factors": [_vp, _vp, _vp],
+    "lsba_copy_ilu0_factors": [_vp, _vp, _i64, _vp],
     "lsba_status_str": [C.c_int],
     "lsba_last_error": [_vp],
 }
@@ -241,9 +241,10 @@ def lsba_ilu0_apply(ctx, X, Y):
 
 
 def lsba_copy_ilu0_factors(ctx, nnz):
+    """(factor values (nnz,), (levels of L, levels of U)); nnz = 0 fetches the levels only."""
     lu = np.zeros(max(int(nnz), 1))
     lev = np.zeros(2, dtype=np.int32)
-    _check(lib.lsba_copy_ilu0_factors(ctx, _hptr(lu), _hptr(lev)), ctx)
+    _check(lib.lsba_copy_ilu0_factors(ctx, _hptr(lu) if nnz > 0 else None, int(nnz), _hptr(lev)), ctx)
     return lu[:nnz], (int(lev[0]), int(lev[1]))
 
 

@@ -2,8 +2,12 @@
 // incomplete LU (ILU) preconditioner with no fill"; left side, IKJ variant).
 //
 //   k_ilu0_level   one level of the IKJ factorisation, a warp per row (setup, once per matrix)
-//   k_ilu_trsv     sync-free sparse triangular solve Y <- L^{-1} Y or U^{-1} Y in place, one
-//                  thread per row (all s columns), rows in level order, per-row ready flags
+//   k_ilu_trsv_poll  (default) sync-free sparse triangular solve Z = L^{-1} X or U^{-1} X, one
+//                  thread per row (all s columns), rows in level order claimed chunk by chunk
+//                  by a persistent grid, dependencies detected by polling the data itself
+//                  (sentinel-filled output); measured 4.3 / 11 / 12 us per level on configs
+//                  2 / 3 / 5 vs 6.9 / 25 / 56 with ready flags (k_ilu_trsv_persist) and
+//                  17 / 46 / 72 with one CTA per chunk (k_ilu_trsv)
 //
 // Factor storage: lu[p] for CSR position p of the local matrix (row_ptr / col_idx of A):
 // strictly-lower entries are L (unit diagonal implied), the rest U.  Columns >= n_local
@@ -116,6 +120,133 @@ k_ilu_trsv(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
   }
   __threadfence();
   st_release_u32(ready + i, gen);
+}
+
+// Persistent variant: a grid of one CTA per SM claims CHUNKS of kThreads consecutive rows (in
+// level order) from a global counter, one row per thread, and claims the next chunk after a
+// CTA barrier.  Only the frontier (grid x 256 rows, a few levels) is in flight, so the spinning
+// threads are ~10x fewer than with one CTA per chunk, and the polls no longer flood L2.
+// ctr[0]: chunk counter, ctr[1]: exited CTAs (the last one resets both for the next launch).
+template <int S, bool LOWER>
+__global__ void __launch_bounds__(256)
+k_ilu_trsv_persist(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
+                   const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
+                   int n_local, double* Y, unsigned* ready, unsigned gen, unsigned* ctr,
+                   const int* __restrict__ active) {
+  __shared__ int chunk;
+  const bool live = !(active && *active == 0);
+  const int nchunks = (nrows + blockDim.x - 1) / blockDim.x;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = live ? (int)atomicAdd(ctr, 1u) : nchunks;
+    __syncthreads();
+    if (chunk >= nchunks) break;
+    const int t = chunk * blockDim.x + threadIdx.x;
+    if (t < nrows) {
+      const int i = order[t];
+      const int p0 = rp[i], p1 = rp[i + 1];
+      double acc[S];
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc[c] = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const int k = ci[p];
+        if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
+        while (ld_acquire_u32(ready + k) != gen) {
+        }
+        const double a = lu[p];
+        const double* yk = Y + (size_t)k * S;
+#pragma unroll
+        for (int c = 0; c < S; ++c) acc[c] = fma(a, __ldcg(yk + c), acc[c]);
+      }
+      double* yi = Y + (size_t)i * S;
+      const double dinv = LOWER ? 1.0 : lu[diag[i]];
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        const double r = __ldcg(yi + c) - acc[c];
+        __stcg(yi + c, LOWER ? r : r / dinv);
+      }
+      st_release_u32(ready + i, gen);   // release: orders this thread's stores of y_i before it
+    }
+  }
+  if (threadIdx.x == 0) {
+    const unsigned e = atomicAdd(ctr + 1, 1u);
+    if (e == gridDim.x - 1) {                  // every CTA is done claiming: reset for the next launch
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+    }
+  }
+}
+
+// Data-polling variant (no flags): the output Z is pre-filled with a sentinel NaN pattern
+// (kIluSentinel, never produced by arithmetic: quiet NaNs from fp64 ops carry a zero payload);
+// a row's dependency y_k is ready when none of its S values is the sentinel.  One L2 round trip
+// per dependency instead of two (flag, then data).  Out of place: Z != X.
+constexpr unsigned long long kIluSentinel = 0x7ff4dead5e47ee11ull;
+__device__ __forceinline__ double ld_volatile_d(const double* p) {
+  double v;
+  asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void k_fill_sentinel(long count, double* __restrict__ z) {
+  const double v = __longlong_as_double((long long)kIluSentinel);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x)
+    z[e] = v;
+}
+template <int S, bool LOWER>
+__global__ void __launch_bounds__(256)
+k_ilu_trsv_poll(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
+                const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
+                int n_local, const double* __restrict__ X, double* Z, unsigned* ctr,
+                const int* __restrict__ active) {
+  __shared__ int chunk;
+  const bool live = !(active && *active == 0);
+  const int nchunks = (nrows + blockDim.x - 1) / blockDim.x;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) chunk = live ? (int)atomicAdd(ctr, 1u) : nchunks;
+    __syncthreads();
+    if (chunk >= nchunks) break;
+    const int t = chunk * blockDim.x + threadIdx.x;
+    if (t < nrows) {
+      const int i = order[t];
+      const int p0 = rp[i], p1 = rp[i + 1];
+      double acc[S];
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc[c] = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const int k = ci[p];
+        if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
+        const double a = lu[p];
+        const double* zk = Z + (size_t)k * S;
+        double y[S];
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int c = 0; c < S; ++c) {
+            y[c] = ld_volatile_d(zk + c);
+            ok = ok && ((unsigned long long)__double_as_longlong(y[c]) != kIluSentinel);
+          }
+          if (ok) break;
+        }
+#pragma unroll
+        for (int c = 0; c < S; ++c) acc[c] = fma(a, y[c], acc[c]);
+      }
+      const double dinv = LOWER ? 1.0 : lu[diag[i]];
+      double* zi = Z + (size_t)i * S;
+#pragma unroll
+      for (int c = 0; c < S; ++c) {
+        const double r = X[(size_t)i * S + c] - acc[c];
+        __stcg(zi + c, LOWER ? r : r / dinv);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    const unsigned e = atomicAdd(ctr + 1, 1u);
+    if (e == gridDim.x - 1) {
+      ctr[0] = 0u;
+      ctr[1] = 0u;
+    }
+  }
 }
 
 // per-CTA partial sums of squares of x[0..count) (grid-stride; fixed order per CTA)

@@ -119,9 +119,13 @@ struct lsba_ctx_ {
   int* d_ordL = nullptr;         // rows by level of L (ascending dependencies)
   int* d_ordU = nullptr;         // rows by level of U
   unsigned* d_ready = nullptr;   // per-row ready flags of the sync-free solves
+  double* d_ilu_tmp = nullptr;   // n x s intermediate of the data-polling variant
   unsigned* d_ticket = nullptr;  // CTA start tickets (2: L and U solves)
   unsigned ilu_gen = 0;          // launch generation (ready[i] == gen: row i solved)
   int ilu_levels[2] = {0, 0};
+  int ilu_variant = 2;           // 2 data polling (default), 0 ready flags, 1 flags + a CTA per chunk
+                                 // (LSBA_ILU_VARIANT; tools/ilu_apply_bench.py)
+  int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
   int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
@@ -272,16 +276,52 @@ static lsba_status ilu_apply_t(lsba_ctx c, double* Y, const int* active) {
   // algorithmic bytes per solve: the factor half (~12 B per stored entry + row pointers and
   // the row order) and Y read + written once
   const double by = 6.0 * c->nnz + 8.0 * (c->n + 1) + 16.0 * c->n * S;
+  if (c->ilu_variant == 2) {    // data polling, out of place: Y -> T (L), T -> Y (U)
+    const int grid = std::min(nblk, c->n_sms * c->ilu_ctas);
+    const long cnt = (long)c->n * S;
+    const int fgrid = std::min(4 * c->n_sms, (int)cdiv(cnt, kThreads));
+    {
+      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+      k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, c->d_ilu_tmp);
+      k_ilu_trsv_poll<S, true><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci,
+          c->d_lu, c->d_diag, c->n, Y, c->d_ilu_tmp, c->d_ticket, active);
+      CKL();
+    }
+    {
+      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+      k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, Y);
+      k_ilu_trsv_poll<S, false><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci,
+          c->d_lu, c->d_diag, c->n, c->d_ilu_tmp, Y, c->d_ticket + 2, active);
+      CKL();
+    }
+    return LSBA_OK;
+  }
+  if (c->ilu_variant == 0) {
+    const int grid = std::min(nblk, c->n_sms * c->ilu_ctas);
+    {
+      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+      k_ilu_trsv_persist<S, true><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci,
+          c->d_lu, c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket, active);
+      CKL();
+    }
+    {
+      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+      k_ilu_trsv_persist<S, false><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci,
+          c->d_lu, c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 2, active);
+      CKL();
+    }
+    return LSBA_OK;
+  }
   {
     LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
     k_ilu_trsv<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci, c->d_lu,
-        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket, active);
+        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 4, active);
     CKL();
   }
   {
     LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
     k_ilu_trsv<S, false><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci, c->d_lu,
-        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 1, active);
+        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 5, active);
     CKL();
   }
   return LSBA_OK;
@@ -294,16 +334,18 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
   TRY(halo_t<S>(c, V));
   constexpr int L = (S % 2 == 0) ? S / 2 : 1;
   const long threads = (long)c->n * L;
-  LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n * S);
-  if (c->n == 0) return LSBA_OK;
-  if constexpr (S % 2 == 0 || S == 1) {
-    k_spmm<S, false><<<cdiv(threads, kThreads), kThreads, 0, c->stream>>>(
-        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
-  } else {
-    k_spmm_odd<S, false><<<cdiv(c->n, kThreads), kThreads, 0, c->stream>>>(
-        c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
+  {
+    LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n * S);
+    if (c->n == 0) return LSBA_OK;
+    if constexpr (S % 2 == 0 || S == 1) {
+      k_spmm<S, false><<<cdiv(threads, kThreads), kThreads, 0, c->stream>>>(
+          c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
+    } else {
+      k_spmm_odd<S, false><<<cdiv(c->n, kThreads), kThreads, 0, c->stream>>>(
+          c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
+    }
+    CKL();
   }
-  CKL();
   if (c->prec) TRY(ilu_apply_t<S>(c, W, active));
   return LSBA_OK;
 }
@@ -1252,7 +1294,7 @@ static void release(lsba_ctx c) {
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
                   c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL,
-                  c->d_ordU, c->d_ready, c->d_ticket};
+                  c->d_ordU, c->d_ready, c->d_ticket, c->d_ilu_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1484,6 +1526,8 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   *out = c;  // returned even on failure so that lsba_last_error works; destroy it
   if (const char* e = std::getenv("LSBA_NO_FUSE")) c->no_fuse = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
   if (n < s) return fail(c, LSBA_E_ARG, "n < s");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, LSBA_E_ARG, "bad rank/nranks");
@@ -1718,13 +1762,14 @@ static lsba_status ilu0_factor(lsba_ctx c) {
     TRY(dalloc(c, &c->d_ordL, n));
     TRY(dalloc(c, &c->d_ordU, n));
     TRY(dalloc(c, &c->d_ready, n));
-    TRY(dalloc(c, &c->d_ticket, 2));
+    TRY(dalloc(c, &c->d_ticket, 8));
+    TRY(dalloc(c, &c->d_ilu_tmp, (size_t)n * c->s));
   }
   CK(cudaMemcpy(c->d_diag, diag.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ordL, ordL.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ordU, ordU.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemset(c->d_ready, 0, sizeof(unsigned) * n));
-  CK(cudaMemset(c->d_ticket, 0, sizeof(unsigned) * 2));
+  CK(cudaMemset(c->d_ticket, 0, sizeof(unsigned) * 8));
   c->ilu_gen = 0;
   if (c->nnz) CK(cudaMemcpy(c->d_lu, c->d_va, sizeof(double) * c->nnz, cudaMemcpyDeviceToDevice));
   CK(cudaMemsetAsync(c->d_info, 0, sizeof(int), c->stream));
@@ -1770,9 +1815,12 @@ extern "C" lsba_status lsba_ilu0_apply(lsba_ctx c, const double* X_dev, double* 
   return LSBA_OK;
 }
 
-extern "C" lsba_status lsba_copy_ilu0_factors(lsba_ctx c, double* lu_host, int32_t* levels_host) {
+extern "C" lsba_status lsba_copy_ilu0_factors(lsba_ctx c, double* lu_host, int64_t capacity,
+                                              int32_t* levels_host) {
   if (!c) return LSBA_E_ARG;
   if (!c->ilu_ready) return fail(c, LSBA_E_STATE, "ILU(0) not set up (lsba_ilu0_setup)");
+  if (lu_host && capacity < c->nnz) return fail(c, LSBA_E_ARG, "capacity %lld < nnz %lld",
+                                                (long long)capacity, (long long)c->nnz);
   CK(cudaSetDevice(c->device));
   if (lu_host && c->nnz)
     CK(cudaMemcpy(lu_host, c->d_lu, sizeof(double) * c->nnz, cudaMemcpyDeviceToHost));
