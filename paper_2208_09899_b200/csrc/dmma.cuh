@@ -53,6 +53,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
                const double* base0, double* out0, int J1, const double* __restrict__ C1, double* out1,
                const int* __restrict__ flag_ptr) {
   static_assert(S == 4 || S == 8 || S == 16, "DMMA projection for s in {4,8,16}");
+  pdl_begin();
   if (flag_ptr && *flag_ptr) return;
   constexpr int KC = S / 4;                 // K chunks
   constexpr int NT = S >= 8 ? S / 8 : 1;    // N tiles

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(256, MINB)
 k_gram_v7(GramArgs g, GramFuse f) {
   using C = G7Cfg<S, GMAX, U, MINB, NY>;
   static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v7 Gram: s in {2,4,8,16}");
+  pdl_begin();
   if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
     if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
     return;
@@ -295,6 +296,7 @@ template <int S, int NY = 1>
 __global__ void __launch_bounds__(256, 3)
 k_gram_gl2(GramArgs g, GramFuse f) {
   static_assert(S % 2 == 0, "gl2: even s");
+  pdl_begin();
   if (g.active && *g.active == 0) {
     if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;
     return;

@@ -33,6 +33,16 @@ constexpr int kThreads = 256;
 // +8%, config 5 +1.5%, configs 3/4 neutral; tools/l2exp.sh); LSBA_L2HINT overrides per context.
 // ------------------------------------------------------------------------------------------
 static __constant__ int c_l2hint = 14;
+
+// Programmatic dependent launch (PDL): the hot kernels of a step (SpMM, Gram, projection) may
+// be launched with programmatic stream serialisation, so the next kernel's CTAs are scheduled
+// while this one drains.  Every such kernel first lets its dependents launch, then WAITS for
+// its predecessor grid (completion + memory flush) before touching any input — and before any
+// early exit, so completion stays transitive along the stream.  No-ops without PDL.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t l2pol(bool hint, bool last) {
   uint64_t p;
   if (!hint) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -144,6 +154,7 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ va, const double* __restrict__ V,
        const double* __restrict__ Vghost, const double* __restrict__ Bm,
        double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr) {
+  pdl_begin();
   if (active && *active == 0) return;
   constexpr int L = (S >= 2) ? S / 2 : 1;
   constexpr int C = (S >= 2) ? 2 : 1;  // columns per lane
@@ -407,6 +418,7 @@ __global__ void __launch_bounds__(kThreads)
 k_project(int n, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
           const double* base0, double* out0, int J1, const double* __restrict__ C1,
           double* out1, const int* __restrict__ flag_ptr) {
+  pdl_begin();
   if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   constexpr int CB = GLOBAL ? 1 : S * S;   // coefficients per block

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "kernels.cuh"
@@ -126,6 +127,7 @@ struct lsba_ctx_ {
   int ilu_variant = 2;           // 2 data polling (default), 0 ready flags, 1 flags + a CTA per chunk
                                  // (LSBA_ILU_VARIANT; tools/ilu_apply_bench.py)
   int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
+  bool pdl = true;               // programmatic dependent launch of SpMM / Gram / projection (LSBA_PDL)
   int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
@@ -266,6 +268,23 @@ static lsba_status halo_t(lsba_ctx c, const double* V) {
   return LSBA_OK;
 }
 
+// Launch with programmatic stream serialisation (PDL) when enabled: the kernel may be scheduled
+// while its predecessor drains; it waits for it in-kernel (pdl_begin, kernels.cuh).
+template <typename... P, typename... A>
+static cudaError_t launch_k(lsba_ctx c, void (*kern)(P...), dim3 grid, dim3 block, size_t smem, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+
 // ---------------------------------------------------------------- f4: ILU(0) apply
 // Y <- U^{-1} L^{-1} Y in place (two sync-free triangular solves; ilu.cuh)
 template <int S>
@@ -338,8 +357,9 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
     LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n * S);
     if (c->n == 0) return LSBA_OK;
     if constexpr (S % 2 == 0 || S == 1) {
-      k_spmm<S, false><<<cdiv(threads, kThreads), kThreads, 0, c->stream>>>(
-          c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
+      CK(launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, (int)c->n,
+                  (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
+                  (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active));
     } else {
       k_spmm_odd<S, false><<<cdiv(c->n, kThreads), kThreads, 0, c->stream>>>(
           c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
@@ -407,8 +427,7 @@ static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse&
   if ((size_t)geo.grid * a.J * S * S * NY > c->part_cap || geo.passes > kMaxGramPasses)
     return fail(c, LSBA_E_STATE, "v7 Gram workspace too small (J=%d)", a.J);
   if (geo.smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
-  fn<<<geo.grid, 256, geo.smem, c->stream>>>(a, f);
-  CKL();
+  CK(launch_k(c, fn, dim3(geo.grid), dim3(256), geo.smem, a, f));
   return LSBA_OK;
 }
 
@@ -557,8 +576,8 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
       const int rows_per_warp = (S >= 16 ? 16 : 32);
       const int grid = std::max(1, std::min(cdiv(cdiv(c->n, rows_per_warp), 8), occ * c->n_sms));
-      fn<<<grid, 256, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr);
-      CKL();
+      CK(launch_k(c, fn, dim3(grid), dim3(256), smem, (int)c->n, X, xstride, J0, C0, base0, out0, J1, C1,
+                  out1, flag_ptr));
       return LSBA_OK;
     }
   }
@@ -570,8 +589,8 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
   } else {
     auto fn = k_project<S, false>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<cdiv(c->n, kThreads), kThreads, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0,
-                                                             J1, C1, out1, flag_ptr);
+    CK(launch_k(c, fn, dim3(cdiv(c->n, kThreads)), dim3(kThreads), smem, (int)c->n, X, xstride, J0, C0,
+                base0, out0, J1, C1, out1, flag_ptr));
   }
   CKL();
   return LSBA_OK;
@@ -1526,6 +1545,7 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   *out = c;  // returned even on failure so that lsba_last_error works; destroy it
   if (const char* e = std::getenv("LSBA_NO_FUSE")) c->no_fuse = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_PDL")) c->pdl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
