@@ -32,8 +32,8 @@ constexpr int kMaxGramPasses = 64;  // ticket sets allocated per context (one pe
 // raise the register demand (and spills) of the streaming loop above it.
 template <int B>
 __device__ __noinline__ void step_coef_noinline(const SmallState2& st, const double* G, double* Gs, int k,
-                                                const CycleParams& prm) {
-  step_coef_body<B>(st, G, Gs, k, prm, 1.0);
+                                                const CycleParams& prm, bool g_ready) {
+  step_coef_body<B>(st, G, Gs, k, prm, 1.0, g_ready);
 }
 
 struct GramFuse {
@@ -259,25 +259,31 @@ k_gram_v7(GramArgs g, GramFuse f) {
   __syncthreads();
   if (ticket7 != (unsigned)(ngroups - 1)) return;
   __threadfence();
+  // one pass (and a fused small step): the final sums also go straight into shared memory,
+  // where the small step reads G (no global round trip)
+  const bool g_smem = f.on && passes == 1 && NY == 1;
   for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
     double s2 = 0.0;
     for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * E + e);
     g.G[e] = s2;
+    if (g_smem) sm7[e] = s2;
   }
   if (tid == 0) tk[ngroups] = 0u;
   if (!f.on) return;
   // ---- fused small step, run by the CTA that completes the last pass
-  __threadfence();
-  __syncthreads();
-  unsigned* tpass = g.tickets + (size_t)kMaxGramPasses * (ngroups + 1);
-  if (tid == 0) ticket7 = atomicAdd(tpass, 1u);
-  __syncthreads();
-  if (ticket7 != (unsigned)(passes - 1)) return;
-  __threadfence();
-  if (tid == 0) *tpass = 0u;
+  if (passes > 1) {
+    __threadfence();
+    __syncthreads();
+    unsigned* tpass = g.tickets + (size_t)kMaxGramPasses * (ngroups + 1);
+    if (tid == 0) ticket7 = atomicAdd(tpass, 1u);
+    __syncthreads();
+    if (ticket7 != (unsigned)(passes - 1)) return;
+    __threadfence();
+    if (tid == 0) *tpass = 0u;
+  }
   if constexpr (NY == 1) {
-    if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm);
-    else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0);
+    if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm, g_smem);
+    else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0, g_smem);
   }
 }
 

@@ -177,7 +177,7 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
 // the Gram kernel (gram7.cuh) on a single rank.
 template <int B>
 __device__ __forceinline__ void step_coef_body(const SmallState2& st, const double* G, double* Gs, int k,
-                                               const CycleParams& prm, double rfac) {
+                                               const CycleParams& prm, double rfac, bool g_ready = false) {
   __shared__ double Ss[B * B], Rs[B * B], Ris[B * B];
   __shared__ double red[32];
   __shared__ int flag_s;
@@ -189,7 +189,8 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
     return;
   }
   const int force_flag = (k > 0 && k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
-  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = __ldcg(G + e);
+  if (!g_ready)                          // (fused into a one-pass Gram: Gs already holds G)
+    for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = __ldcg(G + e);
   __syncthreads();
   if (k > 0)
     for (int e = tid; e < kb * B; e += nt) {
