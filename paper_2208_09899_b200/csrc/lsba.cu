@@ -127,6 +127,7 @@ struct lsba_ctx_ {
   int ilu_variant = 2;           // 2 data polling (default), 0 ready flags, 1 flags + a CTA per chunk
                                  // (LSBA_ILU_VARIANT; tools/ilu_apply_bench.py)
   int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
+  int g7force = 0;               // diagnostics: LSBA_G7 forces a v7 Gram configuration (s = 4, 8)
   bool pdl = true;               // programmatic dependent launch of SpMM / Gram / projection (LSBA_PDL)
   int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
@@ -433,12 +434,30 @@ static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse&
 
 template <int S>
 static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
+  if constexpr (S == 4 || S == 8) {         // diagnostics: LSBA_G7=1..4 forces one configuration
+    switch (c->g7force) {
+      case 1: return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+      case 2: return gram_v7_launch<S, 2, 4, 3>(c, a, f);
+      case 3: return gram_v7_launch<S, 3, 6, 2>(c, a, f);
+      case 4: return gram_v7_launch<S, 2, 4, 2>(c, a, f);
+      default: break;
+    }
+  }
+  // (GMAX, U, MINB) per J from in-situ per-launch timings of every configuration on configs
+  // 2, 3 and 5 (tools/g7sweep.py over LSBA_G7-forced timelines; profiles/r01_g7_insitu.md):
+  // the best choice alternates with the number of groups per pass
   if constexpr (S == 2 || S == 4) {
-    if (a.J <= 4) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
-    if (a.J <= 8) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
+    const int J = a.J;
+    if (J == 1) return gram_v7_launch<S, 3, 6, 2>(c, a, f);
+    if (J <= 5) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    if (J <= 9 || (J >= 14 && J <= 17)) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2>(c, a, f);
   } else if constexpr (S == 8) {
-    if (a.J <= 4) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    const int J = a.J;
+    if (J == 1) return gram_v7_launch<S, 3, 6, 2>(c, a, f);
+    if (J <= 3) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    if ((J >= 4 && J <= 5) || (J >= 8 && J <= 9) || (J >= 14 && J <= 17) || (J >= 26 && J <= 33))
+      return gram_v7_launch<S, 2, 4, 3>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2>(c, a, f);
   } else if constexpr (S == 16) {
     if (a.J <= 4) return gram_v7_launch<S, 3, 6, 2, false>(c, a, f);
@@ -1546,6 +1565,7 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_NO_FUSE")) c->no_fuse = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
   if (const char* e = std::getenv("LSBA_PDL")) c->pdl = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_G7")) c->g7force = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
