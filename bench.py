@@ -339,7 +339,9 @@ def main():
 
     # dominant kernel roofline (local rank's launches; per-launch averages)
     tot_ms = sum(v[1] for v in prof.values())
-    dom = max(prof, key=lambda k: prof[k][1])
+    # dominant kernel: the largest summed time among the kernels that move the step's bytes
+    # (the 1-CTA update kernel runs concurrently on stream 2, off the critical path)
+    dom = max((k for k in prof if prof[k][2] > 0), key=lambda k: prof[k][1])
     dn, dms, dbytes = prof[dom]
     achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     traffic = None
