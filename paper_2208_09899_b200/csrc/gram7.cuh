@@ -32,8 +32,48 @@ constexpr int kMaxGramPasses = 64;  // ticket sets allocated per context (one pe
 // raise the register demand (and spills) of the streaming loop above it.
 template <int B>
 __device__ __noinline__ void step_coef_noinline(const SmallState2& st, const double* G, double* Gs, int k,
-                                                const CycleParams& prm, bool g_ready) {
-  step_coef_body<B>(st, G, Gs, k, prm, 1.0, g_ready);
+                                                const CycleParams& prm, bool g_ready, int pre_force) {
+  step_coef_body<B>(st, G, Gs, k, prm, 1.0, g_ready, pre_force);
+}
+
+#ifdef LSBA_TAIL_TRACE
+// diagnostics build only (LSBA_NVCC_EXTRA=-DLSBA_TAIL_TRACE): globaltimer stamps of the Gram's
+// tail, printed by the CTA that runs the fused small step
+__device__ unsigned long long g7_t0 = ~0ull;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define G7T(i) do { if (tid == 0) tt[i] = gtimer(); } while (0)
+#else
+#define G7T(i) do { } while (0)
+#endif
+
+// Ordered sum over c < cnt of p[c * stride] (c ascending, the same rounding as a plain loop);
+// the loads are issued 16 at a time so the sum costs a few L2 round trips, not cnt of them.
+__device__ __forceinline__ double ordered_partial_sum(const double* p, size_t stride, int cnt) {
+  double s = 0.0;
+  for (int c0 = 0; c0 < cnt; c0 += 16) {
+    double v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = (c0 + c < cnt) ? __ldcg(p + (size_t)(c0 + c) * stride) : 0.0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c0 + c < cnt) s += v[c];
+  }
+  return s;
+}
+
+// Ticket increment with acquire-release semantics at GPU scope, by one thread after a CTA
+// barrier: the release half publishes every write the CTA made before the barrier (barrier
+// cumulativity), the acquire half (for the CTA that draws the last ticket) makes the other
+// CTAs' published partials visible to this CTA after the next barrier.  Replaces a full
+// __threadfence in every thread on both sides (the cooperative-groups grid-sync pattern).
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* p) {
+  unsigned r;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(r) : "l"(p) : "memory");
+  return r;
 }
 
 struct GramFuse {
@@ -82,8 +122,14 @@ k_gram_v7(GramArgs g, GramFuse f) {
     if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
     return;
   }
+  // the fused small step's fault-injection state, read now (off the tail's critical path)
+  const int pre_force = (f.on && f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
   extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef LSBA_TAIL_TRACE
+  unsigned long long tt[8] = {};
+  if (tid == 0) atomicMin(&g7_t0, gtimer());
+#endif
   const uint64_t xpol = l2pol(c_l2hint & 2, false);
   const int J = g.J, E = J * S * C::NCOL;
   const int NG = g7_groups<S>(J);
@@ -240,31 +286,26 @@ k_gram_v7(GramArgs g, GramFuse f) {
     g.part[(size_t)chunk * E + e0 + e] = t;
   }
   // ---- deterministic two-level reduction across the row chunks of this pass
-  __threadfence();
+  G7T(0);
   __syncthreads();
   __shared__ unsigned ticket7;
-  if (tid == 0) ticket7 = atomicAdd(&tk[grpi], 1u);
+  if (tid == 0) ticket7 = ticket_acq_rel(&tk[grpi]);
   __syncthreads();
   if (ticket7 != (unsigned)(gsize - 1)) return;
-  __threadfence();
-  for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
-    double s2 = 0.0;
-    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * E + e);
-    g.gpart[(size_t)grpi * E + e] = s2;
-  }
+  G7T(1);
+  for (int e = e0 + tid; e < e0 + EP; e += C::NTHR)
+    g.gpart[(size_t)grpi * E + e] = ordered_partial_sum(g.part + (size_t)grpi * kGramGroup * E + e, E, gsize);
   if (tid == 0) tk[grpi] = 0u;
-  __threadfence();
   __syncthreads();
-  if (tid == 0) ticket7 = atomicAdd(&tk[ngroups], 1u);
+  if (tid == 0) ticket7 = ticket_acq_rel(&tk[ngroups]);
   __syncthreads();
   if (ticket7 != (unsigned)(ngroups - 1)) return;
-  __threadfence();
+  G7T(2);
   // one pass (and a fused small step): the final sums also go straight into shared memory,
   // where the small step reads G (no global round trip)
   const bool g_smem = f.on && passes == 1 && NY == 1;
   for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
-    double s2 = 0.0;
-    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * E + e);
+    const double s2 = ordered_partial_sum(g.gpart + e, E, ngroups);
     g.G[e] = s2;
     if (g_smem) sm7[e] = s2;
   }
@@ -272,19 +313,28 @@ k_gram_v7(GramArgs g, GramFuse f) {
   if (!f.on) return;
   // ---- fused small step, run by the CTA that completes the last pass
   if (passes > 1) {
-    __threadfence();
     __syncthreads();
     unsigned* tpass = g.tickets + (size_t)kMaxGramPasses * (ngroups + 1);
-    if (tid == 0) ticket7 = atomicAdd(tpass, 1u);
+    if (tid == 0) ticket7 = ticket_acq_rel(tpass);
     __syncthreads();
     if (ticket7 != (unsigned)(passes - 1)) return;
-    __threadfence();
     if (tid == 0) *tpass = 0u;
   }
+  G7T(3);
   if constexpr (NY == 1) {
-    if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm, g_smem);
-    else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0, g_smem);
+    if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm, g_smem, pre_force);
+    else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0, g_smem, pre_force);
   }
+#ifdef LSBA_TAIL_TRACE
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long t4 = gtimer(), t0 = g7_t0;
+    printf("G7TAIL S=%d J=%d k=%d passes=%d grid=%d ngroups=%d | loop_end %llu grp_last %llu final %llu "
+           "small_start %llu end %llu (ns from first CTA start)\n", S, J, f.k, passes, (int)gridDim.x, ngroups,
+           tt[0] - t0, tt[1] - t0, tt[2] - t0, tt[3] - t0, t4 - t0);
+    g7_t0 = ~0ull;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------------------------
@@ -361,34 +411,23 @@ k_gram_gl2(GramArgs g, GramFuse f) {
     }
     __syncthreads();
   }
-  __threadfence();
   __syncthreads();
-  if (tid == 0) ticket = atomicAdd(&g.tickets[grpi], 1u);
+  if (tid == 0) ticket = ticket_acq_rel(&g.tickets[grpi]);
   __syncthreads();
   if (ticket != (unsigned)(gsize - 1)) return;
-  __threadfence();
-  for (int e = tid; e < E; e += blockDim.x) {
-    double s2 = 0.0;
-    for (int c = 0; c < gsize; ++c) s2 += __ldcg(g.part + (size_t)(grpi * kGramGroup + c) * E + e);
-    g.gpart[(size_t)grpi * E + e] = s2;
-  }
+  for (int e = tid; e < E; e += blockDim.x)
+    g.gpart[(size_t)grpi * E + e] = ordered_partial_sum(g.part + (size_t)grpi * kGramGroup * E + e, E, gsize);
   if (tid == 0) g.tickets[grpi] = 0u;
-  __threadfence();
   __syncthreads();
-  if (tid == 0) ticket = atomicAdd(&g.tickets[ngroups], 1u);
+  if (tid == 0) ticket = ticket_acq_rel(&g.tickets[ngroups]);
   __syncthreads();
   if (ticket != (unsigned)(ngroups - 1)) return;
-  __threadfence();
-  for (int e = tid; e < E; e += blockDim.x) {
-    double s2 = 0.0;
-    for (int c = 0; c < ngroups; ++c) s2 += __ldcg(g.gpart + (size_t)c * E + e);
-    g.G[e] = s2 * (1.0 / S);                          // Table 1: (1/s) tr(X^T Y)
-  }
+  for (int e = tid; e < E; e += blockDim.x)
+    g.G[e] = ordered_partial_sum(g.gpart + e, E, ngroups) * (1.0 / S);   // Table 1: (1/s) tr(X^T Y)
   if (tid == 0) g.tickets[ngroups] = 0u;
   (void)gsm;
   if (NY != 1 || !f.on) return;
-  __threadfence();
-  __syncthreads();
+  __syncthreads();                                    // (G written by this CTA: visible after the barrier)
   extern __shared__ double gl2_dyn[];                 // (k+1) doubles for the small step
   step_coef_body<1>(f.st, g.G, gl2_dyn, f.k, f.prm, sqrt((double)S));
 }

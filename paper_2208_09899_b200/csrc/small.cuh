@@ -177,18 +177,21 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
 // the Gram kernel (gram7.cuh) on a single rank.
 template <int B>
 __device__ __forceinline__ void step_coef_body(const SmallState2& st, const double* G, double* Gs, int k,
-                                               const CycleParams& prm, double rfac, bool g_ready = false) {
+                                               const CycleParams& prm, double rfac, bool g_ready = false,
+                                               int pre_force = -1) {
   __shared__ double Ss[B * B], Rs[B * B], Ris[B * B];
   __shared__ double red[32];
   __shared__ int flag_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
   const int ldH = st.ldH, kb = k * B;
   CycleCtl* ctl = st.ctl;
-  if (k > 0 && ctl->active == 0) {      // speculative launch after the cycle ended: no-op
+  // pre_force >= 0: fused into a Gram that already checked ctl->active at its start (nothing
+  // changes the control block while it runs) and read the fault-injection state then
+  if (pre_force < 0 && k > 0 && ctl->active == 0) {      // speculative launch after the cycle ended
     if (tid == 0) *st.flag_dev = 1;
     return;
   }
-  const int force_flag = (k > 0 && k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
+  const int force_flag = pre_force >= 0 ? pre_force : (k > 0 && k == ctl->force_k && !ctl->forced_done) ? 1 : 0;
   if (!g_ready)                          // (fused into a one-pass Gram: Gs already holds G)
     for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = __ldcg(G + e);
   __syncthreads();
