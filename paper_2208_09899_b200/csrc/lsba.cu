@@ -471,10 +471,23 @@ static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
 template <int S>
 static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
   const GramFuse f{};
+  if constexpr (S == 4 || S == 8) {         // diagnostics: LSBA_G7=1..4 forces one configuration
+    switch (c->g7force) {
+      case 1: return gram_v7_launch<S, 1, 8, 4, true, 2>(c, a, f);
+      case 2: return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
+      case 3: return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
+      case 4: return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
+      default: break;
+    }
+  }
+  // per J from the in-situ sweep (profiles/r01_g7_insitu.md, BMGS-CWY rows)
   if constexpr (S == 2 || S == 4) {
-    if (a.J <= 8) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
+    const int J = a.J;
+    if (J <= 4) return gram_v7_launch<S, 1, 8, 4, true, 2>(c, a, f);
+    if (J <= 9 || (J >= 13 && J <= 17)) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
   } else if constexpr (S == 8) {
+    if (a.J <= 2) return gram_v7_launch<S, 1, 8, 4, true, 2>(c, a, f);
     return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
   } else if constexpr (S == 16) {
     return gram_v7_launch<S, 1, 4, 2, false, 2>(c, a, f);

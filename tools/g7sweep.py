@@ -13,8 +13,15 @@ for f in sys.argv[1:]:
     grams = [float(re.search(r"dur\s+([\d.]+)", ln).group(1)) for ln in lines if re.match(r"gram\s+start", ln)]
     # launch 0 is IO (J = 1); then steps k = 1.. have J = k + 1, repeating per cycle
     m = int(re.search(r"_m(\d+)_", f).group(1)) if re.search(r"_m(\d+)_", f) else 20
+    cwy = "_cwy" in f          # Alg 6: IO, iteration 1, then the two-block Grams J = 2..m+1
     for i, d in enumerate(grams):
-        J = 1 + (i % (m + 1))
+        if cwy:
+            r = i % (m + 2)
+            J = (1, 1)[r] if r < 2 else r
+            if r < 2:
+                continue
+        else:
+            J = 1 + (i % (m + 1))
         best[J].setdefault(tag, []).append(d)
 for J in sorted(best):
     row = {t: sum(v) / len(v) for t, v in best[J].items()}

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--cold", action="store_true", help="profile a full solve from X0 = 0")
     ap.add_argument("--ip", default="cl")
+    ap.add_argument("--skel", default="pip")
     args = ap.parse_args()
     import torch
     import paper_2208_09899_b200 as L
@@ -32,12 +33,13 @@ def main():
     L.lsba_set_kernel_variant(ctx.ctx, args.variant)
     B = torch.from_numpy(wl["B"]).cuda()
     X = torch.zeros_like(B)
-    L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 0, ip=args.ip)
+    L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 0, ip=args.ip, skel=args.skel)
     torch.cuda.synchronize()
     if args.cold:
         X.zero_()
     L.lsba_profile_enable(ctx.ctx, True)
-    info = L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 200 if args.cold else args.cycles - 1, ip=args.ip)
+    info = L.lsba_bgmres_solve(ctx.ctx, B, X, wl["m"], wl["tol"], 200 if args.cold else args.cycles - 1, ip=args.ip,
+                               skel=args.skel)
     print("solve:", info.as_dict())
     tl = L.lsba_profile_timeline(ctx.ctx)
     L.lsba_profile_enable(ctx.ctx, False)
