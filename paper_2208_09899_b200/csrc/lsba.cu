@@ -127,6 +127,20 @@ struct lsba_ctx_ {
   int ilu_variant = 2;           // 2 data polling (default), 0 ready flags, 1 flags + a CTA per chunk
                                  // (LSBA_ILU_VARIANT; tools/ilu_apply_bench.py)
   int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
+  // overlapped projection -> next SpMM (one rank, BCGS-PIP): the projection of step k runs in
+  // row pieces on the main stream, the SpMM of step k+1 in row pieces on stream3, each piece
+  // after the projection pieces covering the V rows it reads (ovl_need, from the CSR)
+  int ovl_pieces = 0;            // 0: off (LSBA_OVL=P)
+  std::vector<int> ovl_prow;     // projection piece row starts (P + 1)
+  std::vector<int> ovl_srow;     // SpMM piece row starts (P + 1)
+  std::vector<int> ovl_need;     // SpMM piece i needs projection pieces 0..ovl_need[i]
+  std::vector<int64_t> ovl_snnz; // stored entries per SpMM piece
+  int64_t rw_nnz = 0;            // stored entries of the current row window
+  cudaStream_t stream3 = nullptr;
+  cudaEvent_t ev_proj[8] = {}, ev_spmm = nullptr;
+  int spmm_ahead = -1;           // step whose SpMM was already issued by the previous step
+  int rw0 = 0, rwn = -1;         // row window of project_t / spmm_t (rwn < 0: all rows)
+  cudaStream_t kstream = nullptr;  // stream override of spmm_t
   int g7force = 0;               // diagnostics: LSBA_G7 forces a v7 Gram configuration (s = 4, 8)
   bool pdl = true;               // programmatic dependent launch of SpMM / Gram / projection (LSBA_PDL)
   int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
@@ -277,12 +291,12 @@ static cudaError_t launch_k(lsba_ctx c, void (*kern)(P...), dim3 grid, dim3 bloc
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = c->stream;
+  cfg.stream = c->kstream ? c->kstream : c->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = c->pdl ? 1 : 0;
+  cfg.numAttrs = (c->pdl && !c->kstream) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
@@ -351,23 +365,34 @@ static lsba_status ilu_apply(lsba_ctx c, double* Y, const int* active = nullptr)
 // ---------------------------------------------------------------- a1: SpMM / residual
 template <int S>
 static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* active) {
-  TRY(halo_t<S>(c, V));
+  // row window [rw0, rw0 + rwn) (overlapped pipeline, one rank): the row pointers and W shift,
+  // V and the column indices stay global
+  const bool win = c->rwn >= 0;
+  const int n = win ? c->rwn : c->n;
+  const int* rp = c->d_rp + (win ? c->rw0 : 0);
+  if (win) W += (size_t)c->rw0 * S;
+  else TRY(halo_t<S>(c, V));
   constexpr int L = (S % 2 == 0) ? S / 2 : 1;
-  const long threads = (long)c->n * L;
+  const long threads = (long)n * L;
+  // the kernel treats columns >= its row count as ghosts at Vghost + (col - n) s: in a window
+  // (one rank, no ghosts) that must again be V + col s
+  const double* vg = win ? V + (size_t)n * S : c->d_ghost;
   {
-    LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n * S);
-    if (c->n == 0) return LSBA_OK;
+    const double nnzw = win ? (double)c->rw_nnz : (double)c->nnz;
+    LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * nnzw + 4.0 * (n + 1) + 16.0 * n * S,
+                   c->kstream ? c->kstream : c->stream);
+    if (n == 0) return LSBA_OK;
     if constexpr (S % 2 == 0 || S == 1) {
-      CK(launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, (int)c->n,
-                  (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
-                  (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active));
+      CK(launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, n,
+                  rp, (const int*)c->d_ci, (const double*)c->d_va, V,
+                  vg, (const double*)nullptr, W, (double*)nullptr, active));
     } else {
-      k_spmm_odd<S, false><<<cdiv(c->n, kThreads), kThreads, 0, c->stream>>>(
-          c->n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
+      k_spmm_odd<S, false><<<cdiv(n, kThreads), kThreads, 0, c->kstream ? c->kstream : c->stream>>>(
+          n, rp, c->d_ci, c->d_va, V, vg, nullptr, W, nullptr, active);
     }
     CKL();
   }
-  if (c->prec) TRY(ilu_apply_t<S>(c, W, active));
+  if (c->prec && !win) TRY(ilu_apply_t<S>(c, W, active));
   return LSBA_OK;
 }
 
@@ -595,9 +620,17 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
     return project_t<S>(c, X, xstride, 0, nullptr, nullptr, nullptr, J1, C1, out1, flag_ptr, kid);
   }
   const int Jmax = std::max(J0, J1);
-  const double bytes = 8.0 * c->n * S * (Jmax + (J0 > 0) + (J1 > 0) + (base0 ? 1 : 0));
+  const int n = c->rwn >= 0 ? c->rwn : c->n;   // row window (overlapped pipeline)
+  if (c->rwn >= 0) {
+    const size_t off = (size_t)c->rw0 * S;
+    X += off;
+    if (base0) base0 += off;
+    if (out0) out0 += off;
+    if (out1) out1 += off;
+  }
+  const double bytes = 8.0 * n * S * (Jmax + (J0 > 0) + (J1 > 0) + (base0 ? 1 : 0));
   LaunchScope Ls(c, kid, bytes);
-  if (c->n == 0) return LSBA_OK;
+  if (n == 0) return LSBA_OK;
   // s = 4: the DFMA kernel streams faster than the DMMA one (5.8 vs 5.0 TB/s on config 2,
   // profiles/r01_variants.md); s = 8, 16: DMMA (6.65 TB/s on configs 3 and 5)
   if constexpr (S == 8 || S == 16) {
@@ -607,8 +640,8 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
       int occ = 1;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
       const int rows_per_warp = (S >= 16 ? 16 : 32);
-      const int grid = std::max(1, std::min(cdiv(cdiv(c->n, rows_per_warp), 8), occ * c->n_sms));
-      CK(launch_k(c, fn, dim3(grid), dim3(256), smem, (int)c->n, X, xstride, J0, C0, base0, out0, J1, C1,
+      const int grid = std::max(1, std::min(cdiv(cdiv(n, rows_per_warp), 8), occ * c->n_sms));
+      CK(launch_k(c, fn, dim3(grid), dim3(256), smem, n, X, xstride, J0, C0, base0, out0, J1, C1,
                   out1, flag_ptr));
       return LSBA_OK;
     }
@@ -616,12 +649,12 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
   if (gl) {
     auto fn = k_project<S, true>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<cdiv(c->n, kThreads), kThreads, smem, c->stream>>>(c->n, X, xstride, J0, C0, base0, out0,
+    fn<<<cdiv(n, kThreads), kThreads, smem, c->stream>>>(n, X, xstride, J0, C0, base0, out0,
                                                              J1, C1, out1, flag_ptr);
   } else {
     auto fn = k_project<S, false>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(launch_k(c, fn, dim3(cdiv(c->n, kThreads)), dim3(kThreads), smem, (int)c->n, X, xstride, J0, C0,
+    CK(launch_k(c, fn, dim3(cdiv(n, kThreads)), dim3(kThreads), smem, n, X, xstride, J0, C0,
                 base0, out0, J1, C1, out1, flag_ptr));
   }
   CKL();
@@ -796,6 +829,10 @@ static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
 // IO(U) with U in slot 0: Gram (1 sync), chol, scale in place (Alg 3 line 1).  Resets the
 // device cycle control with this cycle's parameters.  Asynchronous.
 static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
+  if (c->spmm_ahead >= 0) {     // a speculative next-step SpMM of the last cycle may still run
+    CK(cudaStreamWaitEvent(c->stream, c->ev_spmm, 0));
+    c->spmm_ahead = -1;
+  }
   bool fused = false;
   TRY(gram(c, slotp(c, 0), c->slot_stride, 1, slotp(c, 0), c->ip, nullptr, nullptr, 0, &prm, &fused));
   if (!fused) TRY(small_step(c, 0, prm));
@@ -814,7 +851,10 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
   c->pending_upd = (k > 1);
   bool fused = false;
-  TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
+  const bool ahead = (c->spmm_ahead == k);   // W = A V_k already computed by the step k-1 pipeline
+  if (ahead) CK(cudaStreamWaitEvent(c->stream, c->ev_spmm, 0));
+  c->spmm_ahead = -1;
+  TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, ahead ? nullptr : slotp(c, k - 1),
            &c->d_ctl->active, k, &none, &fused));                                // lines 3-4 (+5)
   TRY(wait_update(c));
   if (!fused) TRY(small_step(c, k, none));                                       // line 5
@@ -823,8 +863,43 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
   TRY(step_update(c, k, c->d_G));
   CK(cudaEventRecord(c->ev_upd, c->stream2));
-  TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
-              nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
+  if (!(c->ovl_pieces > 0 && c->nranks == 1 && !c->prec && c->variant == 0)) {
+    TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
+                nullptr, c->st.flag_dev, LSBA_K_PROJECT));                       // line 6
+    return LSBA_OK;
+  }
+  // line 6 in row pieces, and the next step's line 3 (W = A V_{k+1} -> slot k+1) in row pieces
+  // on stream 3, each after the projection pieces holding the V_{k+1} rows it reads: the
+  // latency-bound SpMM overlaps the bandwidth-bound projection (speculative like every step)
+  const int P = c->ovl_pieces;
+  for (int p = 0; p < P; ++p) {
+    c->rw0 = c->ovl_prow[p];
+    c->rwn = c->ovl_prow[p + 1] - c->ovl_prow[p];
+    const lsba_status st = project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0,
+                                   nullptr, nullptr, c->st.flag_dev, LSBA_K_PROJECT);
+    c->rwn = -1;
+    c->rw0 = 0;
+    TRY(st);
+    CK(cudaEventRecord(c->ev_proj[p], c->stream));
+  }
+  c->kstream = c->stream3;
+  lsba_status st = LSBA_OK;
+  for (int i = 0; i < P && st == LSBA_OK; ++i) {
+    if (cudaStreamWaitEvent(c->stream3, c->ev_proj[c->ovl_need[i]], 0) != cudaSuccess) {
+      st = fail(c, LSBA_E_CUDA, "stream wait failed");
+      break;
+    }
+    c->rw0 = c->ovl_srow[i];
+    c->rwn = c->ovl_srow[i + 1] - c->ovl_srow[i];
+    c->rw_nnz = c->ovl_snnz[i];
+    st = spmm(c, slotp(c, k), slotp(c, k + 1), &c->d_ctl->active);
+  }
+  c->kstream = nullptr;
+  c->rwn = -1;
+  c->rw0 = 0;
+  TRY(st);
+  CK(cudaEventRecord(c->ev_spmm, c->stream3));
+  c->spmm_ahead = k + 1;
   return LSBA_OK;
 }
 
@@ -947,6 +1022,7 @@ static lsba_status step_async(lsba_ctx c, int k, bool last) {
 // join stream 2 (the last step's update) into the main stream
 static lsba_status join_update(lsba_ctx c) {
   CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
+  if (c->spmm_ahead >= 0) CK(cudaStreamWaitEvent(c->stream, c->ev_spmm, 0));
   return LSBA_OK;
 }
 
@@ -1356,6 +1432,10 @@ static void release(lsba_ctx c) {
   if (c->ev_coef) cudaEventDestroy(c->ev_coef);
   if (c->ev_upd) cudaEventDestroy(c->ev_upd);
   if (c->stream2) cudaStreamDestroy(c->stream2);
+  if (c->stream3) cudaStreamDestroy(c->stream3);
+  for (auto e : c->ev_proj)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_spmm) cudaEventDestroy(c->ev_spmm);
   for (int k = 0; k < LSBA_K_COUNT; ++k)
     for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1553,6 +1633,34 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   }
   CK(cudaEventCreateWithFlags(&c->ev_coef, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking));
+  for (auto& e : c->ev_proj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_spmm, cudaEventDisableTiming));
+  if (c->ovl_pieces > 0 && c->nranks == 1 && n_local > 0) {
+    // piece plan: P equal projection pieces; SpMM piece i = rows whose columns all lie in
+    // projection pieces 0..i (prefix maximum of the column index), the rest in the last piece
+    const int P = std::min(c->ovl_pieces, 8);
+    c->ovl_pieces = P;
+    c->ovl_prow.assign(P + 1, 0);
+    for (int p = 0; p <= P; ++p) c->ovl_prow[p] = (int)((int64_t)n_local * p / P);
+    c->ovl_srow.assign(P + 1, 0);
+    c->ovl_need.assign(P, 0);
+    int64_t pmax = -1;
+    int piece = 0;
+    for (int64_t r = 0; r < n_local && piece < P - 1; ++r) {
+      for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) pmax = std::max<int64_t>(pmax, col_local[q]);
+      while (piece < P - 1 && pmax >= c->ovl_prow[piece + 1]) c->ovl_srow[++piece] = (int)r;
+    }
+    while (piece < P - 1) c->ovl_srow[++piece] = (int)n_local;
+    c->ovl_srow[P] = (int)n_local;
+    c->ovl_snnz.assign(P, 0);
+    for (int i = 0; i < P; ++i) {
+      c->ovl_need[i] = i;
+      c->ovl_snnz[i] = row_ptr[c->ovl_srow[i + 1]] - row_ptr[c->ovl_srow[i]];
+    }
+  } else {
+    c->ovl_pieces = 0;
+  }
   TRY(dalloc(c, &c->st.status, 1));
   TRY(dalloc(c, &c->st.flag_dev, 1));
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
@@ -1579,6 +1687,7 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
   if (const char* e = std::getenv("LSBA_PDL")) c->pdl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_G7")) c->g7force = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_OVL")) c->ovl_pieces = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
