@@ -233,9 +233,11 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
       }
       __syncwarp();
     }
-    if (!f)
-      for (int e = 0; e < B * B; ++e)
-        if (!isfinite(Rs[e])) f = true;
+    if (!f) {                                       // every entry finite (lanes in parallel)
+      bool bad = false;
+      for (int e = lane; e < B * B; e += 32) bad = bad || !isfinite(Rs[e]);
+      f = __any_sync(0xffffffffu, bad);
+    }
     if (force_flag) f = true;
     if (lane == 0) {
       flag_s = f ? 1 : 0;
@@ -273,13 +275,17 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
     __syncwarp();
     if (!f && lane < B) {   // R^{-1}, column `lane` by back substitution
       const int c = lane;
+      // reciprocal diagonal: lane r's 1/R_rr, shared by shuffles (one division per lane
+      // instead of B sequential ones)
+      const double dinv_mine = 1.0 / Rs[lane + lane * B];
       double x[B];
 #pragma unroll
       for (int r = B - 1; r >= 0; --r) {
         double t = (r == c) ? 1.0 : 0.0;
 #pragma unroll
         for (int q = r + 1; q < B; ++q) t -= Rs[r + q * B] * x[q];
-        x[r] = (r <= c) ? t / Rs[r + r * B] : 0.0;
+        const double dinv = __shfl_sync((1u << B) - 1u, dinv_mine, r);
+        x[r] = (r <= c) ? t * dinv : 0.0;
       }
 #pragma unroll
       for (int r = 0; r < B; ++r) Ris[r + c * B] = (r <= c) ? x[r] : 0.0;
@@ -638,9 +644,11 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
       }
       __syncwarp();
     }
-    if (!f)
-      for (int e = 0; e < B * B; ++e)
-        if (!isfinite(Rs[e])) f = true;
+    if (!f) {                                       // every entry finite (lanes in parallel)
+      bool bad = false;
+      for (int e = lane; e < B * B; e += 32) bad = bad || !isfinite(Rs[e]);
+      f = __any_sync(0xffffffffu, bad);
+    }
     if (force_flag) f = true;
     if (lane == 0) {
       flag_s = f ? 1 : 0;
