@@ -141,6 +141,9 @@ struct lsba_ctx_ {
   int spmm_ahead = -1;           // step whose SpMM was already issued by the previous step
   int rw0 = 0, rwn = -1;         // row window of project_t / spmm_t (rwn < 0: all rows)
   cudaStream_t kstream = nullptr;  // stream override of spmm_t
+  bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
+  bool pdl_proj = true;          // PDL for the projection too (LSBA_PDL_PROJ)
+  bool in_proj = false;
   int g7force = 0;               // diagnostics: LSBA_G7 forces a v7 Gram configuration (s = 4, 8)
   bool pdl = true;               // programmatic dependent launch of SpMM / Gram / projection (LSBA_PDL)
   int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
@@ -296,7 +299,7 @@ static cudaError_t launch_k(lsba_ctx c, void (*kern)(P...), dim3 grid, dim3 bloc
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (c->pdl && !c->kstream) ? 1 : 0;
+  cfg.numAttrs = (c->pdl && !c->kstream && (c->pdl_proj || !c->in_proj)) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
@@ -737,10 +740,19 @@ static lsba_status gram2(lsba_ctx c, const double* X, size_t xstride, int J, con
   LSBA_DISPATCH_S(c->s, gram2_t, c, X, xstride, J, Y, Y2, ip, active);
 }
 
+template <int S>
+static lsba_status project_tp(lsba_ctx c, const double* X, size_t xstride, int J0, const double* C0,
+                              const double* base0, double* out0, int J1, const double* C1, double* out1,
+                              const int* flag_ptr, int kid) {
+  c->in_proj = true;
+  const lsba_status st = project_t<S>(c, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr, kid);
+  c->in_proj = false;
+  return st;
+}
 static lsba_status project(lsba_ctx c, const double* X, size_t xstride, int J0, const double* C0,
                            const double* base0, double* out0, int J1, const double* C1, double* out1,
                            const int* flag_ptr, int kid) {
-  LSBA_DISPATCH_S(c->s, project_t, c, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr, kid);
+  LSBA_DISPATCH_S(c->s, project_tp, c, X, xstride, J0, C0, base0, out0, J1, C1, out1, flag_ptr, kid);
 }
 
 
@@ -757,9 +769,11 @@ static lsba_status small_step(lsba_ctx c, int k, const CycleParams& prm) {
 
 template <int B>
 static lsba_status step_update_t(lsba_ctx c, int k, const double* G) {
-  LaunchScope Ls(c, LSBA_K_STEP_UPDATE, 0.0, c->stream2);
+  // (diagnostics: LSBA_UPD_MAIN=1 serialises it on the main stream to time it alone)
+  cudaStream_t st = c->upd_main ? c->stream : c->stream2;
+  LaunchScope Ls(c, LSBA_K_STEP_UPDATE, 0.0, st);
   const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
-  CK(launch_step_update<B>(c->st, G, k, rfac, c->stream2));
+  CK(launch_step_update<B>(c->st, G, k, rfac, st));
   return LSBA_OK;
 }
 static lsba_status step_update(lsba_ctx c, int k, const double* G) {
@@ -1687,6 +1701,8 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
   if (const char* e = std::getenv("LSBA_PDL")) c->pdl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_G7")) c->g7force = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_UPD_MAIN")) c->upd_main = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_PDL_PROJ")) c->pdl_proj = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_OVL")) c->ovl_pieces = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));

@@ -361,10 +361,12 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
   const int ldH = st.ldH, kb = k * B;
   CycleCtl* ctl = st.ctl;
   if (ctl->active == 0) return;          // speculative launch after the cycle ended
-  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = G[e];
+#pragma unroll 4
+  for (int e = tid; e < (kb + B) * B; e += nt) Gs[e] = __ldcg(G + e);
   double* Vs = Gs + (kb + B) * B;
   double* Ts = Vs + (size_t)(k > 1 ? k - 1 : 0) * B * 2 * B;
   if (k > 1) {
+#pragma unroll 4
     for (int e = tid; e < (k - 1) * B * 2 * B; e += nt) {
       const int jset = e / (B * 2 * B), rem = e % (B * 2 * B);
       const int q = rem / (2 * B), r = rem % (2 * B);
@@ -509,10 +511,17 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
 #pragma unroll
       for (int c = 0; c < B; ++c) acc[c] = 0.0;
       const double* Rr = st.Rinv + (size_t)r * ldH;
-      for (int q = r + lane; q < kb; q += 32) {
-        const double a = Rr[q];
+      // 8 independent loads per lane in flight: this kernel shares its SM with the streaming
+      // projection, where a dependent load chain costs microseconds per link
+      for (int q = r + lane; q < kb; q += 8 * 32) {
+        double a[8];
 #pragma unroll
-        for (int c = 0; c < B; ++c) acc[c] += a * Gs[q * B + c];
+        for (int u = 0; u < 8; ++u) a[u] = (q + u * 32 < kb) ? __ldcg(Rr + q + u * 32) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q + u * 32 < kb)
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc[c] += a[u] * Gs[(q + u * 32) * B + c];
       }
 #pragma unroll
       for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
