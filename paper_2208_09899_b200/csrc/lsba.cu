@@ -470,6 +470,14 @@ static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
       case 4: return gram_v7_launch<S, 2, 4, 2>(c, a, f);
       default: break;
     }
+  } else if constexpr (S == 16) {
+    switch (c->g7force) {
+      case 1: return gram_v7_launch<S, 1, 4, 4, false>(c, a, f);
+      case 2: return gram_v7_launch<S, 2, 4, 3, false>(c, a, f);
+      case 3: return gram_v7_launch<S, 3, 6, 2, false>(c, a, f);
+      case 4: return gram_v7_launch<S, 2, 4, 2, false>(c, a, f);
+      default: break;
+    }
   }
   // (GMAX, U, MINB) per J from in-situ per-launch timings of every configuration on configs
   // 2, 3 and 5 (tools/g7sweep.py over LSBA_G7-forced timelines; profiles/r01_g7_insitu.md):
@@ -487,9 +495,12 @@ static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
     if ((J >= 4 && J <= 5) || (J >= 8 && J <= 9) || (J >= 14 && J <= 17) || (J >= 26 && J <= 33))
       return gram_v7_launch<S, 2, 4, 3>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2>(c, a, f);
-  } else if constexpr (S == 16) {
-    if (a.J <= 4) return gram_v7_launch<S, 3, 6, 2, false>(c, a, f);
-    return gram_v7_launch<S, 2, 4, 3, false>(c, a, f);
+  } else if constexpr (S == 16) {            // (config 4, cold full solves, per J)
+    const int J = a.J;
+    if (J == 2) return gram_v7_launch<S, 1, 4, 4, false>(c, a, f);
+    if (J == 3 || J == 5) return gram_v7_launch<S, 2, 4, 3, false>(c, a, f);
+    if ((J >= 8 && J <= 9) || (J >= 14 && J <= 17)) return gram_v7_launch<S, 2, 4, 2, false>(c, a, f);
+    return gram_v7_launch<S, 3, 6, 2, false>(c, a, f);
   } else {
     return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
   }
