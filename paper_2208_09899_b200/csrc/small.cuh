@@ -17,6 +17,7 @@
 //   Y = Xi C_acc, Z = [M; -H_{k+1,k}], C_acc <- cos C_acc.
 #pragma once
 #include "kernels.cuh"
+#include <cstdio>
 
 namespace lsba {
 
@@ -611,6 +612,13 @@ template <int B>
 __global__ void __launch_bounds__(256)
 k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
   extern __shared__ double cw[];
+#ifdef LSBA_TAIL_TRACE
+  unsigned long long tt[8] = {};
+#define CWT(n) do { if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[n])); } while (0)
+#else
+#define CWT(n) do { } while (0)
+#endif
+  CWT(0);
   __shared__ double Rs[B * B], Ris[B * B], Ps[B * B];
   __shared__ int flag_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -631,6 +639,7 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     st.gpip[e] = st.Hbar[r + (size_t)((k - 1) * B + c) * ldH];
   }
   __syncthreads();
+  CWT(1);
   if (warp == 0) {
     // R = chol(sym(Omega)) (R2), column-major upper
     for (int e = lane; e < B * B; e += 32) {
@@ -692,6 +701,7 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     }
     return;
   }
+  CWT(2);
   // P = R^{-T} Pt  (P[x][y] = sum_q (R^{-1})[q][x] Pt[q][y])
   for (int e = tid; e < B * B; e += nt) {
     const int x = e % B, y = e / B;
@@ -710,6 +720,7 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     ZP[r + (size_t)c * kb] = t;          // (scratch: YR, column-major kb x B)
   }
   __syncthreads();
+  CWT(3);
   double* TmT = st.TmT;
   const int nw = nt >> 5;
   if (inverse) {
@@ -725,10 +736,18 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
       double acc[B];
 #pragma unroll
       for (int c = 0; c < B; ++c) acc[c] = 0.0;
-      for (int q = (r - r % B) + lane; q < kb; q += 32) {   // T block upper triangular
-        const double t = TmT[q + (size_t)r * ldH];
+      // T block upper triangular; 8 independent row loads per lane in flight (this kernel sits
+      // on the critical path between the Gram and the projection)
+      const double* Tr = TmT + (size_t)r * ldH;
+      for (int q = (r - r % B) + lane; q < kb; q += 8 * 32) {
+        double t[8];
 #pragma unroll
-        for (int c = 0; c < B; ++c) acc[c] += t * ZP[q + (size_t)c * kb];
+        for (int u = 0; u < 8; ++u) t[u] = (q + u * 32 < kb) ? __ldcg(Tr + q + u * 32) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q + u * 32 < kb)
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc[c] += t[u] * ZP[q + u * 32 + (size_t)c * kb];
       }
 #pragma unroll
       for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
@@ -745,6 +764,7 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     TmT[(Tcol + y) + (size_t)(kb + x) * ldH] = (x == y) ? 1.0 : 0.0;
   }
   __syncthreads();
+  CWT(4);
   // ZP = [Z; P] R^{-1}  (column-major k1b x B)
   for (int e = tid; e < k1b * B; e += nt) {
     const int r = e % k1b, c = e / k1b;
@@ -756,6 +776,7 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     ZP[r + (size_t)c * k1b] = t;
   }
   __syncthreads();
+  CWT(5);
   if (!inverse) {
     // Hn = T^T ZP: Hn[r][c] = sum_q T[q][r] ZP[q][c] (column r of T, contiguous in Tm), one warp
     // per r, lanes over q; T[q][r] nonzero for q < (r/B + 1) B
@@ -764,10 +785,16 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
 #pragma unroll
       for (int c = 0; c < B; ++c) acc[c] = 0.0;
       const int qend = (r / B + 1) * B;
-      for (int q = lane; q < qend; q += 32) {
-        const double t = Tm[q + (size_t)r * ldH];
+      const double* Tc = Tm + (size_t)r * ldH;
+      for (int q = lane; q < qend; q += 8 * 32) {
+        double t[8];
 #pragma unroll
-        for (int c = 0; c < B; ++c) acc[c] += t * ZP[q + (size_t)c * k1b];
+        for (int u = 0; u < 8; ++u) t[u] = (q + u * 32 < qend) ? __ldcg(Tc + q + u * 32) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q + u * 32 < qend)
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc[c] += t[u] * ZP[q + u * 32 + (size_t)c * k1b];
       }
 #pragma unroll
       for (int c = 0; c < B; ++c) acc[c] = warp_sum(acc[c]);
@@ -779,13 +806,15 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
       for (int e = tid; e < B * B; e += nt) {
         const int rl = e % B, c = e / B, r = i * B + rl;
         double t = ZP[r + (size_t)c * k1b];
-        for (int q = 0; q < i * B; ++q) t -= Tm[q + (size_t)r * ldH] * Hn[q + (size_t)c * k1b];
+#pragma unroll 8
+        for (int q = 0; q < i * B; ++q) t -= __ldcg(Tm + q + (size_t)r * ldH) * Hn[q + (size_t)c * k1b];
         Hn[r + (size_t)c * k1b] = t;
       }
       __syncthreads();
     }
   }
   __syncthreads();
+  CWT(6);
   // Hbar: subdiagonal of column k = R; top of column k+1 = Hn (if it exists)
   for (int e = tid; e < B * B; e += nt) {
     const int x = e % B, y = e / B;
@@ -818,6 +847,14 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
     }
     C1[e] = t;
   }
+#ifdef LSBA_TAIL_TRACE
+  __syncthreads();
+  CWT(7);
+  if (threadIdx.x == 0 && (k == 10 || k == 20 || k == 30))
+    printf("CWYCOEF k=%d inv=%d | load %llu chol %llu P,YR %llu Tcol %llu ZP %llu Hn %llu out %llu ns\n", k, inverse,
+           tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5], tt[7] - tt[6]);
+#endif
+#undef CWT
 }
 
 // ---------------------------------------------------------------------------- BMGS / BCGS-PIO
