@@ -612,6 +612,7 @@ template <int B>
 __global__ void __launch_bounds__(256)
 k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
   extern __shared__ double cw[];
+  __shared__ double part4[4 * B * B];    // ICWY forward substitution partial sums
 #ifdef LSBA_TAIL_TRACE
   unsigned long long tt[8] = {};
 #define CWT(n) do { if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[n])); } while (0)
@@ -801,14 +802,62 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
       if (lane < B) Hn[r + (size_t)lane * k1b] = sel<B>(acc, lane);
     }
   } else {
-    // Hn = T^{-T} ZP: forward substitution over block rows (T^T lower, unit diagonal blocks)
+    // Hn = T^{-T} ZP: forward substitution over block rows (T^T lower, unit diagonal blocks).
+    // Block column i of T (rows 0..iB) is staged in shared memory (G's copy is dead here) by
+    // all threads in one coalesced pass, so each block row costs one global round trip
+    // Double-buffered: block column i+1 is fetched into registers while block row i is solved
+    // (Gs holds 2 k1b B >= 2 kb B doubles: two staging buffers).
+    constexpr int kPf = 16;                 // prefetch registers per thread (kb B <= 16 x 256)
+    double pf[kPf];
+    auto fetch = [&](int i) {
+      const int ib = i * B;
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        const int e = tid + u * nt;
+        pf[u] = 0.0;
+        if (e < ib * B) {
+          const int q = e % ib, rl = e / ib;
+          pf[u] = __ldcg(Tm + q + (size_t)(ib + rl) * ldH);
+        }
+      }
+    };
+    auto stash = [&](int i, double* Tb) {
+      const int ib = i * B;
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        const int e = tid + u * nt;
+        if (e < ib * B) Tb[(e % ib) + (size_t)(e / ib) * ib] = pf[u];
+      }
+    };
+    const bool pf_ok = (size_t)kb * B <= (size_t)kPf * nt;
+    if (pf_ok) fetch(0);
     for (int i = 0; i <= k; ++i) {
-      for (int e = tid; e < B * B; e += nt) {
-        const int rl = e % B, c = e / B, r = i * B + rl;
-        double t = ZP[r + (size_t)c * k1b];
-#pragma unroll 8
-        for (int q = 0; q < i * B; ++q) t -= __ldcg(Tm + q + (size_t)r * ldH) * Hn[q + (size_t)c * k1b];
-        Hn[r + (size_t)c * k1b] = t;
+      const int ib = i * B;
+      double* Tb = Gs + (size_t)(i & 1) * kb * B;
+      if (pf_ok) {
+        stash(i, Tb);
+        if (i < k) fetch(i + 1);            // in flight during this block row's arithmetic
+      } else {
+        for (int e = tid; e < ib * B; e += nt) {
+          const int q = e % ib, rl = e / ib;
+          Tb[q + (size_t)rl * ib] = __ldcg(Tm + q + (size_t)(ib + rl) * ldH);
+        }
+      }
+      __syncthreads();
+      // each of the B x B sums split into 4 quarter-range partials (4x shorter chains), added in
+      // a fixed order
+      for (int e = tid; e < 4 * B * B; e += nt) {
+        const int part = e / (B * B), o = e % (B * B), rl = o % B, c = o / B;
+        const int q0 = (ib * part) / 4, q1 = (ib * (part + 1)) / 4;
+        double t = 0.0;
+        for (int q = q0; q < q1; ++q) t += Tb[q + (size_t)rl * ib] * Hn[q + (size_t)c * k1b];
+        part4[e] = t;
+      }
+      __syncthreads();
+      for (int o = tid; o < B * B; o += nt) {
+        const int rl = o % B, c = o / B, r = ib + rl;
+        const double t = (part4[o] + part4[B * B + o]) + (part4[2 * B * B + o] + part4[3 * B * B + o]);
+        Hn[r + (size_t)c * k1b] = ZP[r + (size_t)c * k1b] - t;
       }
       __syncthreads();
     }
