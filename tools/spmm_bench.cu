@@ -188,6 +188,81 @@ k_spmm_batch(int n, const int* __restrict__ rp, const int* __restrict__ ci, cons
   reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
 }
 
+// P: persistent CTAs with a cp.async double-buffered shared-memory ring of the CSR slices
+// (row pointers, column indices, values of one chunk of RPC rows) — the CSR stream runs ahead
+// asynchronously; the compute warps read indices from shared memory and issue all of a row's
+// gathers at once (up to NB per batch).  Chunks whose slice exceeds MAXE entries fall back to
+// global index loads.
+__device__ __forceinline__ void cpa4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+template <int S, int MAXPR, int NB, int CPS>
+__global__ void __launch_bounds__(256, CPS)
+k_spmm_pipe(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+            const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 2, RPC = 256 / L, MAXE = MAXPR * RPC;
+  __shared__ int srp[2][RPC + 1];
+  __shared__ int sci[2][MAXE];
+  __shared__ double sva[2][MAXE];
+  const int nchunks = (n + RPC - 1) / RPC;
+  const int tid = threadIdx.x;
+  auto stage = [&](int chunk, int buf) {
+    const int r0 = chunk * RPC, r1 = min(n, r0 + RPC);
+    for (int e = tid; e <= r1 - r0; e += 256) cpa4(&srp[buf][e], rp + r0 + e);
+    const int p0 = __ldg(rp + r0), p1 = __ldg(rp + r1);
+    if (p1 - p0 <= MAXE) {
+      for (int e = tid; e < p1 - p0; e += 256) {
+        cpa4(&sci[buf][e], ci + p0 + e);
+        cpa8(&sva[buf][e], va + p0 + e);
+      }
+    }
+    cpa_commit();
+  };
+  int chunk = blockIdx.x;
+  if (chunk < nchunks) stage(chunk, 0);
+  for (int it = 0; chunk < nchunks; ++it, chunk += gridDim.x) {
+    const int buf = it & 1;
+    const int nxt = chunk + gridDim.x;
+    if (nxt < nchunks) stage(nxt, buf ^ 1); else cpa_commit();
+    cpa_wait<1>();
+    __syncthreads();
+    const int r0 = chunk * RPC;
+    const int lr = tid / L, lane = tid % L;
+    const int row = r0 + lr;
+    if (row < n) {
+      const int pb = srp[buf][0];
+      const int q0 = srp[buf][lr] - pb, q1 = srp[buf][lr + 1] - pb;
+      const bool in_smem = (srp[buf][min(RPC, n - r0)] - pb) <= MAXE;
+      double a0 = 0, a1 = 0;
+      for (int q = q0; q < q1; q += NB) {
+        int c[NB]; double a[NB]; double2 v[NB];
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+          const bool ok = q + t < q1;
+          c[t] = ok ? (in_smem ? sci[buf][q + t] : __ldg(ci + pb + q + t)) : row;
+          a[t] = ok ? (in_smem ? sva[buf][q + t] : __ldg(va + pb + q + t)) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < NB; ++t) v[t] = __ldg(reinterpret_cast<const double2*>(V + (size_t)c[t] * S) + lane);
+#pragma unroll
+        for (int t = 0; t < NB; ++t) { a0 = fma(a[t], v[t].x, a0); a1 = fma(a[t], v[t].y, a1); }
+      }
+      reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
+    }
+    __syncthreads();
+  }
+  cpa_wait<0>();
+}
+
 template <typename F>
 static double time_it(F launch) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -201,6 +276,8 @@ static double time_it(F launch) {
 
 template <int S>
 static void run(int dims, int N) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   long n = 1; for (int d = 0; d < dims; ++d) n *= N;
   std::vector<int> rp(n + 1), ci; std::vector<double> va;
   ci.reserve(n * (2 * dims + 1)); va.reserve(n * (2 * dims + 1));
@@ -248,8 +325,12 @@ static void run(int dims, int N) {
 #define HB(NB, MINB, NA) \
   us = time_it([&] { k_spmm_batch<S, NB, MINB, NA><<<gA, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
   check("b" #NB "m" #MINB #NA, us);
-  HB(4, 8, false) HB(4, 4, false) HB(8, 4, false) HB(8, 3, false) HB(4, 8, true) HB(8, 4, true)
 #undef HB
+#define HP(MAXPR, NB, CPS, G) \
+  us = time_it([&] { k_spmm_pipe<S, MAXPR, NB, CPS><<<sms * G, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
+  check("pipe" #MAXPR "_" #NB "_" #CPS "x" #G, us);
+  HP(8, 4, 2, 2) HP(8, 8, 2, 2) HP(8, 4, 3, 3) HP(8, 8, 3, 3) HP(8, 4, 4, 4) HP(8, 8, 4, 4) HP(8, 4, 4, 8)
+#undef HP
   cudaFree(drp); cudaFree(dci); cudaFree(dva); cudaFree(dV); cudaFree(dW); cudaFree(dW2);
 }
 
