@@ -142,6 +142,11 @@ struct lsba_ctx_ {
   int rw0 = 0, rwn = -1;         // row window of project_t / spmm_t (rwn < 0: all rows)
   cudaStream_t kstream = nullptr;  // stream override of spmm_t
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
+  size_t csr_bytes = 0;          // joint col_idx + vals allocation (d_va points into it)
+  int l2persist = -1;            // SpMM CSR window persisting in L2: -1 auto, 0 off, 1 on (LSBA_L2PERSIST)
+  size_t l2win = 0;
+  float l2hit = 0.f;
+  bool in_spmm = false;
   bool pdl_proj = true;          // PDL for the projection too (LSBA_PDL_PROJ)
   bool in_proj = false;
   int g7force = 0;               // diagnostics: LSBA_G7 forces a v7 Gram configuration (s = 4, 8)
@@ -295,11 +300,24 @@ static cudaError_t launch_k(lsba_ctx c, void (*kern)(P...), dim3 grid, dim3 bloc
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->kstream ? c->kstream : c->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (c->pdl && !c->kstream && (c->pdl_proj || !c->in_proj)) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (c->in_spmm && c->l2win > 0) {   // CSR arrays persisting in the L2 set-aside
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow.base_ptr = (void*)c->d_ci;
+    attr[na].val.accessPolicyWindow.num_bytes = c->l2win;
+    attr[na].val.accessPolicyWindow.hitRatio = c->l2hit;
+    attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (c->pdl && !c->kstream && (c->pdl_proj || !c->in_proj)) ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
@@ -386,9 +404,12 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
                    c->kstream ? c->kstream : c->stream);
     if (n == 0) return LSBA_OK;
     if constexpr (S % 2 == 0 || S == 1) {
-      CK(launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, n,
+      c->in_spmm = true;
+      const cudaError_t le = launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, n,
                   rp, (const int*)c->d_ci, (const double*)c->d_va, V,
-                  vg, (const double*)nullptr, W, (double*)nullptr, active));
+                  vg, (const double*)nullptr, W, (double*)nullptr, active);
+      c->in_spmm = false;
+      CK(le);
     } else {
       k_spmm_odd<S, false><<<cdiv(n, kThreads), kThreads, 0, c->kstream ? c->kstream : c->stream>>>(
           n, rp, c->d_ci, c->d_va, V, vg, nullptr, W, nullptr, active);
@@ -1441,7 +1462,11 @@ static lsba_status dalloc(lsba_ctx c, T** p, size_t count) {
 static void release(lsba_ctx c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->d_rp, c->d_ci, c->d_va, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
+  if (c->l2win > 0) {                  // give the L2 set-aside back
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
+  void* ptrs[] = {c->d_rp, c->d_ci, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
@@ -1560,12 +1585,46 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   std::vector<int32_t> rp32(n_local + 1);
   for (int64_t i = 0; i <= n_local; ++i) rp32[i] = (int32_t)row_ptr[i];
   TRY(dalloc(c, &c->d_rp, n_local + 1));
-  TRY(dalloc(c, &c->d_ci, c->nnz));
-  TRY(dalloc(c, &c->d_va, c->nnz));
+  {  // column indices and values in one allocation: one L2 access-policy window covers both
+    const size_t ci_bytes = ((std::max<int64_t>(c->nnz, 1) * sizeof(int32_t)) + 255) / 256 * 256;
+    const size_t bytes = ci_bytes + std::max<int64_t>(c->nnz, 1) * sizeof(double);
+    char* base = nullptr;
+    CK(cudaMalloc((void**)&base, bytes));
+    c->ws_bytes += (int64_t)bytes;
+    c->d_ci = reinterpret_cast<int*>(base);
+    c->d_va = reinterpret_cast<double*>(base + ci_bytes);
+    c->csr_bytes = bytes;
+  }
   CK(cudaMemcpy(c->d_rp, rp32.data(), sizeof(int32_t) * (n_local + 1), cudaMemcpyHostToDevice));
   if (c->nnz) {
     CK(cudaMemcpy(c->d_ci, col_local.data(), sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_va, vals, sizeof(double) * c->nnz, cudaMemcpyHostToDevice));
+  }
+  if (c->l2persist != 0 && c->nnz > 0 && c->nranks == 1) {
+    // The SpMM's column indices and values (constant across the solve) are kept in an L2
+    // set-aside when they fit: config 2 (63 MB) +4%; a CSR larger than the set-aside (config 3,
+    // 175 MB) lost 3.5% (tools/l2persist_exp.sh), so "auto" requires it to fit in the set-aside
+    // and in half of L2.
+    int max_win = 0, max_persist = 0, l2 = 0;
+    CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
+    CK(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
+    const bool fits = c->csr_bytes <= (size_t)max_win && c->csr_bytes <= (size_t)max_persist &&
+                      c->csr_bytes <= (size_t)l2 / 2;
+    if (c->l2persist < 0 && !fits) c->l2persist = 0;
+  }
+  if (c->l2persist != 0 && c->nnz > 0 && c->nranks == 1) {
+    int max_win = 0, max_persist = 0;
+    CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
+    c->l2win = std::min<size_t>(c->csr_bytes, (size_t)max_win);
+    const size_t aside = std::min<size_t>(c->l2win, (size_t)max_persist);
+    if (aside > 0) {
+      CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside));
+      c->l2hit = (float)std::min(1.0, (double)aside / (double)c->l2win);
+    } else {
+      c->l2win = 0;
+    }
   }
   if (c->nranks > 1) {
     TRY(dalloc(c, &c->d_ghost, (size_t)c->n_ghost * s));
@@ -1714,6 +1773,7 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_G7")) c->g7force = std::atoi(e);
   if (const char* e = std::getenv("LSBA_UPD_MAIN")) c->upd_main = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_PDL_PROJ")) c->pdl_proj = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_L2PERSIST")) c->l2persist = std::atoi(e);
   if (const char* e = std::getenv("LSBA_OVL")) c->ovl_pieces = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
