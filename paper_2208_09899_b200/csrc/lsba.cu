@@ -1617,7 +1617,9 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     int max_win = 0, max_persist = 0;
     CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
     CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
-    c->l2win = std::min<size_t>(c->csr_bytes, (size_t)max_win);
+    // (LSBA_L2PERSIST=2: the column indices only)
+    const size_t want = (c->l2persist == 2) ? (size_t)((char*)c->d_va - (char*)c->d_ci) : c->csr_bytes;
+    c->l2win = std::min<size_t>(want, (size_t)max_win);
     const size_t aside = std::min<size_t>(c->l2win, (size_t)max_persist);
     if (aside > 0) {
       CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside));
