@@ -503,24 +503,23 @@ static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   // (GMAX, U, MINB) per J from in-situ per-launch timings of every configuration on configs
   // 2, 3 and 5 (tools/g7sweep.py over LSBA_G7-forced timelines; profiles/r01_g7_insitu.md):
   // the best choice alternates with the number of groups per pass
+  // (the best choice follows the number of groups per pass: NG = ceil(J / (16 / s)))
   if constexpr (S == 2 || S == 4) {
     const int J = a.J;
-    if (J == 1) return gram_v7_launch<S, 3, 6, 2>(c, a, f);
-    if (J <= 5) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
-    if (J <= 9 || (J >= 14 && J <= 17)) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
+    if (J <= 4) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    if (J <= 8 || (J >= 13 && J <= 16)) return gram_v7_launch<S, 2, 4, 3>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2>(c, a, f);
   } else if constexpr (S == 8) {
     const int J = a.J;
-    if (J == 1) return gram_v7_launch<S, 3, 6, 2>(c, a, f);
-    if (J <= 3) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
-    if ((J >= 4 && J <= 5) || (J >= 8 && J <= 9) || (J >= 14 && J <= 17) || (J >= 26 && J <= 33))
+    if (J <= 2) return gram_v7_launch<S, 1, 8, 4>(c, a, f);
+    if ((J >= 3 && J <= 4) || (J >= 7 && J <= 8) || (J >= 13 && J <= 16) || (J >= 25 && J <= 32))
       return gram_v7_launch<S, 2, 4, 3>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2>(c, a, f);
   } else if constexpr (S == 16) {            // (config 4, cold full solves, per J)
     const int J = a.J;
-    if (J == 2) return gram_v7_launch<S, 1, 4, 4, false>(c, a, f);
-    if (J == 3 || J == 5) return gram_v7_launch<S, 2, 4, 3, false>(c, a, f);
-    if ((J >= 8 && J <= 9) || (J >= 14 && J <= 17)) return gram_v7_launch<S, 2, 4, 2, false>(c, a, f);
+    if (J == 1) return gram_v7_launch<S, 1, 4, 4, false>(c, a, f);
+    if (J == 2 || J == 4) return gram_v7_launch<S, 2, 4, 3, false>(c, a, f);
+    if ((J >= 7 && J <= 8) || (J >= 13 && J <= 16)) return gram_v7_launch<S, 2, 4, 2, false>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2, false>(c, a, f);
   } else {
     return fail(c, LSBA_E_STATE, "v7 Gram: s=%d unsupported", S);
@@ -543,11 +542,10 @@ static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
   // per J from the in-situ sweep (profiles/r01_g7_insitu.md, BMGS-CWY rows)
   if constexpr (S == 2 || S == 4) {
     const int J = a.J;
-    if (J <= 4) return gram_v7_launch<S, 1, 8, 4, true, 2>(c, a, f);
-    if (J <= 9 || (J >= 13 && J <= 17)) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
+    if (J <= 3) return gram_v7_launch<S, 1, 8, 4, true, 2>(c, a, f);
+    if (J <= 8 || (J >= 12 && J <= 16)) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
   } else if constexpr (S == 8) {
-    if (a.J <= 2) return gram_v7_launch<S, 1, 8, 4, true, 2>(c, a, f);
     return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
   } else if constexpr (S == 16) {
     return gram_v7_launch<S, 1, 4, 2, false, 2>(c, a, f);

@@ -11,15 +11,16 @@ for f in sys.argv[1:]:
     tag = re.search(r"_(g\d)\.txt$", f).group(1)
     lines = open(f).read().split("\n")
     grams = [float(re.search(r"dur\s+([\d.]+)", ln).group(1)) for ln in lines if re.match(r"gram\s+start", ln)]
+    grams = grams[1:]          # launch 0 is the ||B||_F Gram of the solve call, not a step
     # launch 0 is IO (J = 1); then steps k = 1.. have J = k + 1, repeating per cycle
     m = int(re.search(r"_m(\d+)_", f).group(1)) if re.search(r"_m(\d+)_", f) else 20
     cwy = "_cwy" in f          # Alg 6: IO, iteration 1, then the two-block Grams J = 2..m+1
     for i, d in enumerate(grams):
-        if cwy:
+        if cwy:                # per cycle: IO, iteration 1, then steps k = 1..m with J = k + 1
             r = i % (m + 2)
-            J = (1, 1)[r] if r < 2 else r
             if r < 2:
                 continue
+            J = r
         else:
             J = 1 + (i % (m + 1))
         best[J].setdefault(tag, []).append(d)
