@@ -10,7 +10,8 @@ and checks it against the single-rank oracle:
   * the allreduced partial Gram equals the global Gram to rounding;
   * K distributed BCGS-PIP steps (one halo + one allreduce each) reproduce the single-rank
     H and basis, with exactly K + 1 Gram allreduces (IO + K steps);
-  * the same for K BMGS-CWY steps (Alg 6): loop iteration 1 + K steps, K + 1 allreduces.
+  * the same for K BMGS-CWY steps (Alg 6): loop iteration 1 + K steps, K + 1 allreduces;
+  * and for K BCGS-IRO-LS steps (Alg 7): K + 1 allreduces, H and basis equal to the oracle's.
 """
 import os
 import socket
@@ -154,7 +155,34 @@ def _worker(rank, world, port, kind, K, out):
                 Hc[:(k + 1) * s, k * s:(k + 1) * s] = Hn
             U = W @ Ri - np.concatenate(Vc, axis=1) @ Hn
         assert n_allreduce[0] == K + 1
-        out[rank] = dict(H=Hbar, beta=beta, V=np.stack(Vs), rows=(r0, r1), Hc=Hc, Vc=np.stack(Vc))
+
+        # (5) BCGS-IRO-LS (Alg 7, block DCGS2): the same lagged loop, still ONE allreduce of the
+        # two-block Gram per step; Omega = Omega~ - Y^T Y, column k = J + Y, P = R^{-T}(P~ - Y^T Z),
+        # J = ([Z; P] - H_{1:k+1,1:k} Y) R^{-1}
+        n_allreduce[0] = 0
+        Vi = [Vs[0]]
+        W = spmm_dist(Vi[0])
+        J = allreduce(O.ip_cl([Vi[0]], W))                             # iteration 1
+        U = W - Vi[0] @ J
+        Hi = np.zeros(((K + 1) * s, K * s))
+        for k in range(1, K + 1):
+            W = spmm_dist(U)
+            Gk = allreduce(O.ip_cl(Vi + [U], np.concatenate([U, W], axis=1)))   # the single sync
+            Y, Z, Omt, Pt = Gk[:k * s, :s], Gk[:k * s, s:], Gk[k * s:, :s], Gk[k * s:, s:]
+            R, flag = O.chol_flag(Omt - Y.T @ Y)
+            assert not flag
+            Hi[:k * s, (k - 1) * s:k * s] = J + Y
+            Hi[k * s:(k + 1) * s, (k - 1) * s:k * s] = R
+            Ri = O.right_trsm_upper(np.eye(s), R)
+            P = np.linalg.solve(R.T, Pt - Y.T @ Z)
+            ZP = np.vstack([Z, P])
+            J = (ZP - Hi[:(k + 1) * s, :k * s] @ Y) @ Ri
+            Vn = (U - np.concatenate(Vi, axis=1) @ Y) @ Ri
+            Vi.append(Vn)
+            U = (W - np.concatenate(Vi, axis=1) @ ZP) @ Ri
+        assert n_allreduce[0] == K + 1
+        out[rank] = dict(H=Hbar, beta=beta, V=np.stack(Vs), rows=(r0, r1), Hc=Hc, Vc=np.stack(Vc),
+                         Hi=Hi, Vi=np.stack(Vi))
     finally:
         dist.destroy_process_group()
 
@@ -194,9 +222,17 @@ def test_distributed_pip_steps_match_single_rank(world, kind):
     assert not cwy.begin(B)
     for _ in range(K):
         assert not cwy.step().flag
+    iro = O.IrolsArnoldi(A, "cl", K, s)
+    assert not iro.begin(B)
+    for _ in range(K):
+        assert not iro.step().flag
     for r in range(world):
         d = res[r]
-        assert np.array_equal(d["Hc"], res[0]["Hc"])
+        assert np.array_equal(d["Hc"], res[0]["Hc"]) and np.array_equal(d["Hi"], res[0]["Hi"])
+        np.testing.assert_allclose(d["Hi"], iro.Hbar, rtol=0, atol=1e-11 * np.abs(iro.Hbar).max())
+        for j in range(K + 1):
+            r0, r1 = d["rows"]
+            assert np.linalg.norm(d["Vi"][j] - iro.V[j][r0:r1]) <= 1e-11 * np.linalg.norm(iro.V[j])
         np.testing.assert_allclose(d["Hc"], cwy.Hbar, rtol=0, atol=1e-11 * np.abs(cwy.Hbar).max())
         for j in range(K + 1):
             r0, r1 = d["rows"]
