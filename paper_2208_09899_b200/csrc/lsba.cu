@@ -1174,18 +1174,29 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   // ||B||_F^2 = s * <B,B>_gl  (R18: tolerance relative to ||B||_F); preconditioned (R28):
   // the method runs on M^{-1} A X = M^{-1} B, so the reference norm is ||M^{-1} B||_F and
   // slot 0 keeps M^{-1} B (= U when X0 = 0)
-  if (c->prec) {
-    if (c->n > 0) {
-      CK(cudaMemcpyAsync(slotp(c, 0), B, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
-      TRY(ilu_apply(c, slotp(c, 0)));
-    }
-    TRY(gram(c, slotp(c, 0), 0, 1, slotp(c, 0), LSBA_IP_GLOBAL));
-  } else {
-    TRY(gram(c, B, 0, 1, const_cast<double*>(B), LSBA_IP_GLOBAL));
+  if (c->prec && c->n > 0) {
+    CK(cudaMemcpyAsync(slotp(c, 0), B, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(ilu_apply(c, slotp(c, 0)));
   }
-  CK(cudaMemcpyAsync(c->h_scalar, c->d_G, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  {  // sum of squares: per-CTA partials in a fixed order, then one fixed-order sum (+ allreduce)
+    const double* Bn = c->prec ? slotp(c, 0) : B;
+    const long cnt = (long)c->n * c->s;
+    const int nblk = std::max(1, std::min<int>(c->sq_cap, std::min<long>(4L * c->n_sms, cdiv(cnt, kThreads))));
+    LaunchScope Ls(c, LSBA_K_MISC, 8.0 * cnt);
+    if (c->n > 0) {
+      k_sq_partials<<<nblk, kThreads, 0, c->stream>>>(cnt, Bn, c->d_sq);
+      CKL();
+      k_sum_partials<<<1, kThreads, 0, c->stream>>>(nblk, c->d_sq, c->d_scalar);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(c->d_scalar, 0, sizeof(double), c->stream));
+    }
+  }
+  if (c->nranks > 1)
+    CKN(ncclAllReduce(c->d_scalar, c->d_scalar, 1, ncclDouble, ncclSum, c->comm, c->stream));
+  CK(cudaMemcpyAsync(c->h_scalar, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  const double normB = std::sqrt(std::max(0.0, *c->h_scalar * c->s));
+  const double normB = std::sqrt(std::max(0.0, *c->h_scalar));
   if (normB == 0.0) {  // B = 0: X = 0 exactly
     if (c->n > 0) CK(cudaMemsetAsync(X, 0, sizeof(double) * c->slot, c->stream));
     CK(cudaStreamSynchronize(c->stream));
