@@ -176,11 +176,22 @@ __device__ double warp_norm_prod(const double (&colv)[B], const double* Cacc, co
 // step_coef_body: the whole block runs it (any blockDim multiple of 32, >= 64); Gs is a
 // shared buffer of (k+1) B B doubles.  Called by k_step_coef and, fused, by the last CTA of
 // the Gram kernel (gram7.cuh) on a single rank.
+constexpr int kSpParts = 16;   // max partial row ranges per S entry in step_coef_body
+// quiet NaN as a compile-time constant (device nan("") is a library call parsing its string)
+#define kQNaN __longlong_as_double(0x7ff8000000000000LL)
+
 template <int B>
 __device__ __forceinline__ void step_coef_body(const SmallState2& st, const double* G, double* Gs, int k,
                                                const CycleParams& prm, double rfac, bool g_ready = false,
                                                int pre_force = -1) {
   __shared__ double Ss[B * B], Rs[B * B], Ris[B * B];
+#ifdef LSBA_TAIL_TRACE
+  unsigned long long tq[8] = {};
+#define SCT(n) do { if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq[n])); } while (0)
+#else
+#define SCT(n) do { } while (0)
+#endif
+  SCT(0);
   __shared__ double red[32];
   __shared__ int flag_s;
   const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -201,17 +212,29 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
       const int r = e / B, c = e % B;
       st.Hbar[r + (size_t)((k - 1) * B + c) * ldH] = Gs[e];
     }
-  {  // S = Omega - Hcol^T Hcol: one output per warp at a time, lanes split the kb-long sum
-    const int nw = nt >> 5;
-    for (int e = warp; e < B * B; e += nw) {
-      const int x = e % B, y = e / B;
+  SCT(1);
+  {  // S = Omega - Hcol^T Hcol: every thread owns one (entry, row range) pair — P = nt / B^2
+     // contiguous row ranges per entry — and the P partials are added in range order
+    constexpr int BB = B * B;
+    constexpr int kParts = (256 / BB) < 1 ? 1 : ((256 / BB) > kSpParts ? kSpParts : (256 / BB));
+    __shared__ double sp[kParts * BB];                            // <= 2 KB
+    const int P = (nt / BB) < 1 ? 1 : ((nt / BB) < kParts ? (nt / BB) : kParts);
+    for (int e = tid; e < P * BB; e += nt) {
+      const int o = e % BB, part = e / BB, x = o % B, y = o / B;
+      const int r0 = (kb * part) / P, r1 = (kb * (part + 1)) / P;
       double t = 0.0;
-      for (int r = lane; r < kb; r += 32) t += Gs[r * B + x] * Gs[r * B + y];
-      t = warp_sum(t);
-      if (lane == 0) Ss[x + y * B] = Gs[(kb + x) * B + y] - t;
+      for (int r = r0; r < r1; ++r) t += Gs[r * B + x] * Gs[r * B + y];
+      sp[e] = t;
+    }
+    __syncthreads();
+    for (int o = tid; o < BB; o += nt) {
+      double t = 0.0;
+      for (int part = 0; part < P; ++part) t += sp[part * BB + o];
+      Ss[o] = Gs[(kb + o % B) * B + o / B] - t;
     }
   }
   __syncthreads();
+  SCT(2);
   if (warp == 0) {
     // symmetrise (R2) then right-looking Cholesky with NaN-flag; R^{-1}
     for (int e = lane; e < B * B; e += 32) {
@@ -259,14 +282,14 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
         ctl->tol_abs = prm.tol_abs;
         ctl->tau = prm.tau;
         ctl->need_kappa = prm.need_kappa;
-        ctl->res_est = nan("");
-        ctl->kappa = nan("");
+        ctl->res_est = kQNaN;
+        ctl->kappa = kQNaN;
         publish_progress(st, 0, f ? 0 : 1);
       }
       st.status->k = k;
       st.status->flag = flag_s;
       st.status->proj_singular = 0;
-      st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
+      st.status->res_gmres = st.status->res_fom = st.status->kappa_F = kQNaN;
       if (k == 0) {
         double tr = 0.0;
         for (int x = 0; x < B; ++x) tr += Gs[x * B + x];
@@ -293,6 +316,7 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
     }
   }
   __syncthreads();
+  SCT(3);
   if (flag_s) {
     if (k > 0)
       for (int e = tid; e < B * B; e += nt) {
@@ -340,6 +364,14 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
     const int x = e % B, y = e / B;
     st.Hbar[(kb + x) + (size_t)((k - 1) * B + y) * ldH] = Rs[e];
   }
+#ifdef LSBA_TAIL_TRACE
+  __syncthreads();
+  SCT(4);
+  if (threadIdx.x == 0 && (k == 5 || k == 15))
+    printf("STEPCOEF B=%d k=%d | entry->G %llu S %llu chol+Rinv %llu coef+stores %llu ns\n", B, k,
+           tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2], tq[4] - tq[3]);
+#endif
+#undef SCT
 }
 
 // k_step_coef: blockDim 128; dyn smem (k+1) B B doubles.
@@ -436,7 +468,7 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
     for (int r = 0; r < B; ++r)
       colv[r] = (lane < B) ? Ht[r + lane * B] : ((lane < 2 * B) ? Gh[r + (lane - B) * B] : 0.0);
     const bool sing = warp_gesv<B>(colv);
-    double rf = nan("");
+    double rf = kQNaN;
     if (!sing) rf = warp_norm_prod<B>(colv, st.Cacc, Rs) * rfac;
     if (lane == 0) {
       st.status->proj_singular = sing ? 1 : 0;
@@ -503,7 +535,7 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
   // kappa_F (reading R8): T = R_k^{-1} Hcol (kb x B); X = -T R^{-1} -> Rinv[:, kb..kb+B).
   // Rinv is row-major: one warp per row, lanes over the contiguous row.  Skipped unless
   // needed (no condition threshold in a solve: the decision does not use it).
-  double kap = nan("");
+  double kap = kQNaN;
   if (need_kappa) {
     double part_r = 0.0, part_i = 0.0;
     const int nw = nt >> 5;
@@ -677,7 +709,7 @@ k_cwy_coef(SmallState2 st, const double* __restrict__ G, int k, int inverse) {
       st.status->k = k;
       st.status->flag = flag_s;
       st.status->proj_singular = 0;
-      st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
+      st.status->res_gmres = st.status->res_fom = st.status->kappa_F = kQNaN;
     }
     __syncwarp();
     if (!f && lane < B) {               // R^{-1}, column `lane`
@@ -961,7 +993,7 @@ __device__ __forceinline__ void close_status(const SmallState2& st, int k, int f
   st.status->k = k;
   st.status->flag = flag;
   st.status->proj_singular = 0;
-  st.status->res_gmres = st.status->res_fom = st.status->kappa_F = nan("");
+  st.status->res_gmres = st.status->res_fom = st.status->kappa_F = kQNaN;
 }
 
 // BMGS-Arnoldi (Alg 2), inner step j of step k: H_{j,k} = G (B x B, row-major),
