@@ -483,12 +483,16 @@ static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse&
 
 template <int S>
 static lsba_status gram_v7(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
-  if constexpr (S == 4 || S == 8) {         // diagnostics: LSBA_G7=1..4 forces one configuration
+  if constexpr (S == 4 || S == 8) {         // diagnostics: LSBA_G7=1..8 forces one configuration
     switch (c->g7force) {
       case 1: return gram_v7_launch<S, 1, 8, 4>(c, a, f);
       case 2: return gram_v7_launch<S, 2, 4, 3>(c, a, f);
       case 3: return gram_v7_launch<S, 3, 6, 2>(c, a, f);
       case 4: return gram_v7_launch<S, 2, 4, 2>(c, a, f);
+      case 5: return gram_v7_launch<S, 1, 4, 3>(c, a, f);
+      case 6: return gram_v7_launch<S, 1, 8, 2>(c, a, f);
+      case 7: return gram_v7_launch<S, 3, 4, 2>(c, a, f);
+      case 8: return gram_v7_launch<S, 3, 6, 1>(c, a, f);
       default: break;
     }
   } else if constexpr (S == 16) {
@@ -536,6 +540,10 @@ static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
       case 2: return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
       case 3: return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
       case 4: return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
+      case 5: return gram_v7_launch<S, 1, 4, 3, true, 2>(c, a, f);
+      case 6: return gram_v7_launch<S, 1, 8, 2, true, 2>(c, a, f);
+      case 7: return gram_v7_launch<S, 2, 2, 2, true, 2>(c, a, f);
+      case 8: return gram_v7_launch<S, 2, 4, 1, true, 2>(c, a, f);
       default: break;
     }
   }
@@ -546,6 +554,8 @@ static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
     if (J <= 8 || (J >= 12 && J <= 16)) return gram_v7_launch<S, 2, 4, 3, true, 2>(c, a, f);
     return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
   } else if constexpr (S == 8) {
+    const int J = a.J;
+    if ((J >= 17 && J <= 19) || J >= 32) return gram_v7_launch<S, 1, 8, 2, true, 2>(c, a, f);
     return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
   } else if constexpr (S == 16) {
     return gram_v7_launch<S, 1, 4, 2, false, 2>(c, a, f);
