@@ -555,7 +555,7 @@ static lsba_status gram2_v7(lsba_ctx c, const GramArgs& a) {
     return gram_v7_launch<S, 3, 6, 2, true, 2>(c, a, f);
   } else if constexpr (S == 8) {
     const int J = a.J;
-    if ((J >= 17 && J <= 19) || J >= 32) return gram_v7_launch<S, 1, 8, 2, true, 2>(c, a, f);
+    if ((J >= 18 && J <= 20) || J >= 33) return gram_v7_launch<S, 1, 8, 2, true, 2>(c, a, f);
     return gram_v7_launch<S, 2, 4, 2, true, 2>(c, a, f);
   } else if constexpr (S == 16) {
     return gram_v7_launch<S, 1, 4, 2, false, 2>(c, a, f);

@@ -11,7 +11,10 @@ for f in sys.argv[1:]:
     tag = re.search(r"_(g\d)\.txt$", f).group(1)
     lines = open(f).read().split("\n")
     grams = [float(re.search(r"dur\s+([\d.]+)", ln).group(1)) for ln in lines if re.match(r"gram\s+start", ln)]
-    grams = grams[1:]          # launch 0 is the ||B||_F Gram of the solve call, not a step
+    # older timelines start with the solve call's ||B||_F Gram (a fallback Gram + finalize);
+    # newer ones compute ||B||_F with a sum-of-squares kernel, so launch 0 is already IO
+    if any(re.match(r"gram_finalize\s+start", ln) for ln in lines):
+        grams = grams[1:]
     # launch 0 is IO (J = 1); then steps k = 1.. have J = k + 1, repeating per cycle
     m = int(re.search(r"_m(\d+)_", f).group(1)) if re.search(r"_m(\d+)_", f) else 20
     cwy = "_cwy" in f          # Alg 6: IO, iteration 1, then the two-block Grams J = 2..m+1
