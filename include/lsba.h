@@ -113,6 +113,10 @@ lsba_status lsba_get_unique_id(uint8_t id[128]);
  * The CSR is validated and copied; the caller keeps its arrays.
  * s in [1,16]; m_max >= 1 (basis of m_max+1 blocks is allocated: 8 n_local s (m_max+1) bytes).
  * nccl_id may be NULL iff nranks == 1.  cuda_stream is a cudaStream_t (NULL = legacy stream).
+ * Device-wide side effect: on one rank, when the column indices and values fit in the device's
+ * persisting-L2 set-aside (and in half of L2), the context sets cudaLimitPersistingL2CacheSize
+ * to their size and marks them persisting on its SpMM launches; lsba_destroy resets the limit
+ * to 0 (LSBA_L2PERSIST=0 in the environment disables this).
  * Errors: LSBA_E_ARG on invalid sizes or CSR; LSBA_E_OOM; LSBA_E_CUDA; LSBA_E_NCCL. */
 lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
                         const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
