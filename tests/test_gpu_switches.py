@@ -1,0 +1,70 @@
+"""The diagnostic environment switches of DESIGN.md 6.5 change only how the step is scheduled or
+cached, never what it computes: with each non-default setting a restarted solve still matches
+the oracle (true residual <= tol checked with the oracle's SpMM, cycles within one), and the
+first Arnoldi steps match the default run to rounding.  The switches are read at lsba_create."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SWITCHES = [
+    {"LSBA_PDL": "0"},
+    {"LSBA_PDL_PROJ": "0"},
+    {"LSBA_L2PERSIST": "0"},
+    {"LSBA_L2PERSIST": "1"},
+    {"LSBA_L2HINT": "0"},
+    {"LSBA_NO_FUSE": "1"},
+    {"LSBA_OVL": "3"},
+    {"LSBA_UPD_MAIN": "1"},
+    {"LSBA_G7": "2"},
+]
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2208_09899_b200 as L
+    return L
+
+
+def _run(L, env, p, skel="pip"):
+    import torch
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        with L.Context(p.n, p.s, p.m, p.row_ptr, p.col_idx, p.vals) as ctx:
+            B = torch.from_numpy(p.B).cuda()
+            X = torch.zeros_like(B)
+            info = ctx.solve(B, X, p.m, p.tol, 2000, skel=skel)
+            L.lsba_set_skeleton(ctx.ctx, skel)
+            assert ctx.begin(B, "cl") == 0
+            for _ in range(4):
+                ctx.step()
+            H = ctx.hessenberg(4, p.s)
+            return X.cpu().numpy(), info, H
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("env", SWITCHES, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_switch_keeps_results(L, env):
+    from lsba_inputs import make_twin
+    from oracle import lsba_oracle as O
+    p = make_twin(2)                                   # 2D Laplacian 64^2, s = 4
+    X0, i0, H0 = _run(L, {}, p)
+    X1, i1, H1 = _run(L, env, p)
+    A = (p.row_ptr, p.col_idx, p.vals)
+    for X, info in ((X0, i0), (X1, i1)):
+        assert info.outcome == L.LSBA_CONVERGED
+        rel = np.linalg.norm(p.B - O.spmm(*A, X)) / np.linalg.norm(p.B)
+        assert rel <= p.tol * (1 + 1e-6)
+    assert abs(i1.cycles - i0.cycles) <= 1
+    assert np.linalg.norm(H1 - H0) <= 1e-12 * np.linalg.norm(H0)
