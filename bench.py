@@ -54,6 +54,21 @@ def ilu_bytes(nnz, n, s, iters):
     return iters * 2.0 * (6.0 * nnz + 8.0 * (n + 1) + 16.0 * n * s)
 
 
+def l2_resident_csr(nnz, world):
+    """Whether liblsba keeps this CSR in the persisting L2 set-aside (its rule: one rank, and
+    col_idx + vals fit in the set-aside and in half of L2; LSBA_L2PERSIST=0 disables)."""
+    if world != 1 or os.environ.get("LSBA_L2PERSIST") == "0":
+        return False
+    try:
+        from cuda.bindings import runtime as rt
+        _, maxp = rt.cudaDeviceGetAttribute(rt.cudaDeviceAttr.cudaDevAttrMaxPersistingL2CacheSize, 0)
+        _, l2 = rt.cudaDeviceGetAttribute(rt.cudaDeviceAttr.cudaDevAttrL2CacheSize, 0)
+    except Exception:
+        return False
+    csr = 12 * nnz + 256
+    return csr <= maxp and csr <= l2 // 2
+
+
 def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks, skel="pip"):
     """sum_steps ROOF(k) + per-cycle bytes, from the solver's counters (gram_blocks = sum over
     accepted steps of k+1).  BCGS-PIP: ROOF(k) = A + 8ns(2k+3), + 8ns(k_used+7) per cycle.
@@ -414,7 +429,9 @@ def main():
                        "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
                                       f"{iters / args.steps:.1f} block steps)") if full_solve
                                      else f"restart cycle = IO + {m} block steps + cycle end",
-                       "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"},
+                       "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"
+                             + (f"; the CSR ({12 * wl['nnz'] / 1e6:.0f} MB) is kept in the persisting L2 set-aside"
+                                if l2_resident_csr(wl["nnz"], world) else "")},
             "roofline": {"bound": "hbm", "kernel": dom,
                          **({"note": "level-scheduled triangular solves: latency-bound (one dependency "
                                      "level after another), reported against the HBM roof"}
