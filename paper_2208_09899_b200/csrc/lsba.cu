@@ -137,11 +137,12 @@ struct lsba_ctx_ {
   std::vector<int64_t> ovl_snnz; // stored entries per SpMM piece
   int64_t rw_nnz = 0;            // stored entries of the current row window
   cudaStream_t stream3 = nullptr;
-  cudaEvent_t ev_proj[8] = {}, ev_spmm = nullptr;
+  cudaEvent_t ev_proj[8] = {}, ev_spmm = nullptr, ev_status = nullptr;
   int spmm_ahead = -1;           // step whose SpMM was already issued by the previous step
   int rw0 = 0, rwn = -1;         // row window of project_t / spmm_t (rwn < 0: all rows)
   cudaStream_t kstream = nullptr;  // stream override of spmm_t
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
+  bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
   size_t csr_bytes = 0;          // joint col_idx + vals allocation (d_va points into it)
   int l2persist = -1;            // SpMM CSR window persisting in L2: -1 auto, 0 off, 1 on (LSBA_L2PERSIST)
   size_t l2win = 0;
@@ -873,7 +874,7 @@ static lsba_status pio_coef(lsba_ctx c, const double* G1, const double* G2, int 
 static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
   CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, 7 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (out) *out = *c->h_status;
   if (ctl) *ctl = *c->h_ctl;
@@ -1106,6 +1107,19 @@ static lsba_status cycle_solve_async(lsba_ctx c, int k, int gmres) {
   }
 }
 
+// The speculative cycle end (one rank): enqueued with k = m before the host reads the cycle's
+// status; runs only if the cycle ended at k = m (k_cycle_end's guard).  Ping-pong flag slots
+// per cycle parity: d_info[4 + par] = singular / combine guard, d_info[6 + par] = skipped.
+static lsba_status cycle_solve_spec(lsba_ctx c, int k, int gmres, int par) {
+  switch (c->b) {
+#define CASE(B) case B: return cycle_end_t<B>(c, k, gmres, 0, 2, c->d_info + 4 + par);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
+#undef CASE
+    default: return LSBA_E_ARG;
+  }
+}
+
 static lsba_status cycle_solve(lsba_ctx c, int k, int gmres, int happy, int* singular, int upd = 1) {
   lsba_status st;
   switch (c->b) {
@@ -1246,6 +1260,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   TRY(set_identity(c));                   // C_acc = I
   int m_cur = m;
   bool sing_pending = false;   // a guarded combine was enqueued; its flag is read later
+  int sing_slot = 1;           // ... in d_info[sing_slot]
   CycleCtl cc;
   info->outcome = LSBA_MAX_RESTARTS;
   bool finished = false;
@@ -1273,8 +1288,27 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       TRY(step_async(c, k, k == m_cur));
     }
     TRY(join_update(c));
-    TRY(read_status(c, nullptr, &cc));
-    if (sing_pending && c->h_info[1]) {                     // last cycle end was singular:
+    // speculative cycle end for the common case (the cycle runs to m): enqueued before the
+    // status read, so the GPU solves the projected problem and combines while the host wakes
+    // up; it no-ops on the device for any other ending, which the host then handles below
+    const int par = cycle & 1;
+    const bool spec = c->spec_end && c->nranks == 1 && m_cur >= 1;
+    if (spec) {
+      // the status is copied (and waited for) BEFORE the speculative kernels, so the host
+      // decides while the GPU solves and combines, and enqueues the next cycle behind them
+      CK(cudaMemcpyAsync(c->h_status, c->st.status, sizeof(StepStatus), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, 7 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaEventRecord(c->ev_status, c->stream));
+      TRY(cycle_solve_spec(c, m_cur, gmres, par));
+      TRY(project(c, slotp(c, 0), c->slot_stride, m_cur, c->d_Y, X, X, m_cur + 1, c->d_Z, slotp(c, 0),
+                  c->d_info + 4 + par, LSBA_K_COMBINE));
+      CK(cudaEventSynchronize(c->ev_status));
+      cc = *c->h_ctl;
+    } else {
+      TRY(read_status(c, nullptr, &cc));
+    }
+    if (sing_pending && c->h_info[sing_slot]) {             // last cycle end was singular:
       fail(c, LSBA_OK, "projected system singular at cycle end");   // its combine no-op'd,
       info->cycles = cycle - 1;                             // this cycle ran on stale data
       info->outcome = LSBA_DEAD;
@@ -1315,6 +1349,11 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       info->cond_restarts++;
     }
     if (k_used == 0) { info->outcome = LSBA_DEAD; break; }
+    if (spec && cc.why == 4 && k_used == m_cur) {   // the speculative cycle end ran (its guard)
+      sing_pending = true;
+      sing_slot = 4 + par;
+      continue;
+    }
     if (cc.why != 2) {
       // X += V_k Xi C_acc ;  U = V_{k+1} [M; -H_{k+1,k}] -> slot 0,
       // enqueued behind the projected solve without a host round trip (guarded by its flag)
@@ -1322,6 +1361,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       TRY(project(c, slotp(c, 0), c->slot_stride, k_used, c->d_Y, X, X, k_used + 1, c->d_Z, slotp(c, 0),
                   c->d_info + 1, LSBA_K_COMBINE));
       sing_pending = true;
+      sing_slot = 1;
       continue;
     }
     int sing = 0;
@@ -1349,9 +1389,10 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     }
   }
   if (sing_pending) {                                        // the last cycle's combine
-    CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_info + sing_slot, c->d_info + sing_slot, sizeof(int), cudaMemcpyDeviceToHost,
+                       c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (c->h_info[1]) {
+    if (c->h_info[sing_slot]) {
       fail(c, LSBA_OK, "projected system singular at cycle end");
       info->outcome = LSBA_DEAD;
     }
@@ -1505,6 +1546,7 @@ static void release(lsba_ctx c) {
   for (auto e : c->ev_proj)
     if (e) cudaEventDestroy(e);
   if (c->ev_spmm) cudaEventDestroy(c->ev_spmm);
+  if (c->ev_status) cudaEventDestroy(c->ev_status);
   for (int k = 0; k < LSBA_K_COUNT; ++k)
     for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1741,6 +1783,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   CK(cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking));
   for (auto& e : c->ev_proj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_spmm, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_status, cudaEventDisableTiming));
   if (c->ovl_pieces > 0 && c->nranks == 1 && n_local > 0) {
     // piece plan: P equal projection pieces; SpMM piece i = rows whose columns all lie in
     // projection pieces 0..i (prefix maximum of the column index), the rest in the last piece
@@ -1771,9 +1814,9 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
   TRY(dalloc(c, &c->d_Y, (size_t)(m_max + 1) * s * s));
   TRY(dalloc(c, &c->d_Z, (size_t)(m_max + 1) * s * s));
-  TRY(dalloc(c, &c->d_info, 4));
+  TRY(dalloc(c, &c->d_info, 8));
   CK(cudaMallocHost((void**)&c->h_status, sizeof(StepStatus)));
-  CK(cudaMallocHost((void**)&c->h_info, sizeof(int) * 4));
+  CK(cudaMallocHost((void**)&c->h_info, sizeof(int) * 8));
   CK(cudaMallocHost((void**)&c->h_scalar, sizeof(double) * 4));
   set_ip(c, LSBA_IP_CLASSICAL);
   return LSBA_OK;
@@ -1795,6 +1838,7 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_UPD_MAIN")) c->upd_main = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_PDL_PROJ")) c->pdl_proj = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2PERSIST")) c->l2persist = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_SPEC_END")) c->spec_end = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_OVL")) c->ovl_pieces = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));

@@ -1307,6 +1307,19 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
   const int ldH = st.ldH, kb = k * B;
   const bool use_fom = happy || !gmres;
   if (tid == 0) sing_s = 0;
+  if (update_cacc == 2) {
+    // speculative cycle end, enqueued before the host has read the cycle's status: it runs
+    // only if the cycle ended at k = m (why 4) with k accepted steps; otherwise it marks itself
+    // skipped (info[2]) and raises the guard (info[0]) so that its combine no-ops
+    __shared__ int skip_s;
+    if (tid == 0) {
+      skip_s = (st.ctl->why == 4 && st.ctl->k_used == k) ? 0 : 1;
+      info[2] = skip_s;
+      if (skip_s) info[0] = 1;
+    }
+    __syncthreads();
+    if (skip_s) return;
+  }
   // the R factor of Hbar: staged into shared memory when the launcher gave room for it (one
   // coalesced pass instead of two dependent global round trips per block row below)
   const double* Rm = st.Rfac;

@@ -19,6 +19,7 @@ SWITCHES = [
     {"LSBA_OVL": "3"},
     {"LSBA_UPD_MAIN": "1"},
     {"LSBA_G7": "2"},
+    {"LSBA_SPEC_END": "0"},
 ]
 
 
