@@ -2,27 +2,33 @@
 """Benchmark: restarted cl-BGMRES with BCGS-PIP block Arnoldi on B200 (BASELINE.json metric
 "block Arnoldi steps/s and fp64 HBM GB/s (% roofline) at 1/2/4/8 B200").
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
+* Workload: BASELINE.json configs[4] = config 5, the 3D 7-point Laplacian on a 256^3 grid
+  (n = 16,777,216, s = 8, m = 40, tau = 1e8), the largest configuration and the one BASELINE
+  quotes at 1/2/4/8 GPUs.  --config 2/3/4 bench the other BASELINE configs.
 * A bench "step" is one restart cycle of the solver: IO(U) + m block Arnoldi steps (SpMM,
-  fused single-sync Gram, Cholesky, projection) + the cycle-end projected solve and the
-  X/U update, i.e. every row of SURVEY.md 8(a).  K cycles run inside ONE lsba_bgmres_solve
-  call (max_restarts = K-1) at the real tol 1e-8 (config 2 needs ~4400 cycles, so none of
-  the timed cycles converges).
-* value = whole-job algorithmic fp64 HBM GB/s: sum over steps of ROOF(k) = 12 nnz + 4(n+1)
-  + 8 n s (2k+3) plus 8 n s (k+7) per cycle, all ranks,
-  divided by the max-over-ranks device time.  block_steps_per_s is reported beside it.
-* N > 1: weak scaling, one 1024 x 1024 y-slab of a 1024 x (1024 N) 2D Laplacian per GPU,
-  row-partitioned, halo send/recv + exactly one Gram allreduce per block step.
-* --impl reference: the oracle (oracle/, NumPy fp64) on this box's host cores on the same
-  workload, a bounded sample per step.
+  fused single-sync Gram, Cholesky, projection, estimates) + the cycle-end projected solve and
+  the X/U update, i.e. every row of SURVEY.md 8(a).  K cycles run inside ONE
+  lsba_bgmres_solve call (max_restarts = K-1) from X0 = 0 at the real tol 1e-8 (config 5 needs
+  ~88 cycles, so none of the timed cycles converges).  Configs 1
+  and 4 converge in a few cycles: there a step is one full solve.
+* value = whole-job algorithmic fp64 GB/s: sum over steps of ROOF(k) = 12 nnz + 4(n+1)
+  + 8 n s (2k+3) plus 8 n s (k+7) per cycle, divided by the max-over-ranks
+  device time.  block_steps_per_s is reported beside it.
+* N > 1: STRONG scaling of the same global problem: contiguous row ranges (whole z-planes for
+  the stencils), each rank holding its rows of A, B and the basis; per block step one halo
+  exchange and exactly one Gram allreduce.
+* --impl reference: the oracle (oracle/, NumPy fp64, as it stands) on this box's host cores,
+  on a bounded sample of the same workload per step (no reference implementation exists:
+  /root/reference holds only the paper's text).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -35,6 +41,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "block Arnoldi steps/s and fp64 HBM GB/s (% roofline) at 1/2/4/8 B200"
+SAMPLE_ROWS = 1 << 20      # oracle samples: the leading 2^20 rows (16 planes of 256^2 for config 5)
 
 
 def roof_step(nnz, n, s, k):
@@ -86,16 +93,29 @@ def algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks, skel="pip"):
     return iters * (A + 6 * blk) + 2 * blk * gram_blocks + blk * (iters + 14 * cycles)
 
 
-def cycle_bytes(nnz, n, s, m):
-    return sum(roof_step(nnz, n, s, k) for k in range(1, m + 1)) + roof_cycle_extra(n, s, m)
-
-
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
         return float(d.get("hbm_gbs", 6650.0)), "measured"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # --------------------------------------------------------------------------- clocks sampler
@@ -144,90 +164,151 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload
-def build_workload(config, rank, world):
-    """Returns dict(name, n_global, row_begin, row_end, A_local, B_local, s, m, tol, nnz_global)."""
-    from lsba_inputs import CONFIGS, rhs, stencil, random_sparse
+def partition(n_global, world, rank, unit=1):
+    """Contiguous row range of `rank`: whole units (z-planes for the stencils) split as evenly
+    as possible, the first (units % world) ranks taking one more."""
+    units = n_global // unit
+    q, r = divmod(units, world)
+    u0 = rank * q + min(rank, r)
+    u1 = u0 + q + (1 if rank < r else 0)
+    return u0 * unit, u1 * unit
+
+
+def build_workload(config, rank, world, need_sha=True):
+    """The GLOBAL problem of BASELINE config `config` (strong scaling: the same A and B at
+    every N), and this rank's rows of it."""
+    from lsba_inputs import CONFIGS, csr_sha256, random_sparse, rhs, stencil
     spec = dict(CONFIGS[config])
     s, m = spec["s"], spec["m"]
+    sha = None
     if spec["kind"] == "stencil":
         dims, N = spec["dims"], spec["N"]
-        if world > 1:   # weak scaling: stack world slabs along the slowest dimension
-            shape = [N] * dims
-            shape[-1] = N * world
-        else:
-            shape = [N] * dims
-        n = int(np.prod(shape))
-        per = n // world
-        r0, r1 = rank * per, (rank + 1) * per if rank < world - 1 else n
-        A = stencil(dims, N, spec["v"], shape=shape, rows=(r0, r1))
-        # nnz of the global operator (closed form for the stencil)
-        nnz = n * (2 * dims + 1) - 2 * sum(n // shape[d] for d in range(dims))
-        name = spec["name"] + (f" x{world} (weak, slab per GPU)" if world > 1 else "")
+        n = N ** dims
+        plane = N ** (dims - 1)                # rows of one slowest-dimension plane
+        r0, r1 = partition(n, world, rank, plane)
+        A = stencil(dims, N, spec["v"], rows=(r0, r1))
+        nnz = n * (2 * dims + 1) - 2 * dims * (n // N)      # closed form (SURVEY.md App. B)
     else:
-        n = spec["n"] * world
-        per = n // world
-        r0, r1 = rank * per, (rank + 1) * per
-        rp, ci, va = random_sparse(n)   # every rank builds the same matrix (seeded)
-        A = (rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]], va[rp[r0]:rp[r1]])
+        n = spec["n"]
+        r0, r1 = partition(n, world, rank)
+        rp, ci, va = random_sparse(n)        # every rank builds the same matrix (seeded)
         nnz = int(rp[-1])
-        name = spec["name"] + (f" x{world}" if world > 1 else "")
-    Bfull_rows = rhs(n, s) if world == 1 else None
-    if world == 1:
-        B = Bfull_rows
-    else:
-        B = np.random.default_rng(rank).standard_normal((r1 - r0, s))
-    return dict(name=name, n_global=n, row_begin=r0, row_end=r1, A=A, B=np.ascontiguousarray(B), s=s, m=m,
-                tol=spec["tol"], nnz=nnz, spec=spec)
+        A = (rp[r0:r1 + 1] - rp[r0], ci[rp[r0]:rp[r1]], va[rp[r0]:rp[r1]])
+    if need_sha:
+        sha = csr_sha256(*A)                 # = the global CSR's at N = 1
+    B = np.ascontiguousarray(rhs(n, s)[r0:r1])   # this rank's rows of the global B
+    return dict(name=spec["name"], n_global=n, row_begin=r0, row_end=r1, A=A, B=B, s=s, m=m,
+                tol=spec["tol"], tau=spec["tau"], nnz=nnz, spec=spec, sha=sha)
 
 
 # --------------------------------------------------------------------------- oracle timing
-def oracle_sample(wl, budget_s):
-    """Time the oracle (as it stands) on a bounded sample of the same workload: the first
-    block steps of one cycle on the full matrix, until ~budget_s of CPU work."""
+def oracle_sample_problem(wl):
+    """The bounded CPU sample: the leading principal submatrix of A on the first SAMPLE_ROWS
+    rows (whole z-planes of the stencils: the same operator on a thinner slab) and those rows of
+    B.  Returns (A_sample, B_sample, n_sample, nnz_sample, description)."""
+    rp, ci, va = wl["A"]
+    n = wl["B"].shape[0]
+    ns = min(n, SAMPLE_ROWS)
+    if ns == n:
+        return (rp, ci, va), wl["B"], n, int(rp[-1]), f"all {n} rows"
+    p1 = int(rp[ns])
+    keep = ci[:p1] < ns
+    rows = np.repeat(np.arange(ns), np.diff(rp[:ns + 1]))
+    counts = np.bincount(rows[keep], minlength=ns)
+    rps = np.zeros(ns + 1, dtype=np.int64)
+    np.cumsum(counts, out=rps[1:])
+    A = (rps, ci[:p1][keep], va[:p1][keep])
+    return A, np.ascontiguousarray(wl["B"][:ns]), ns, int(rps[-1]), \
+        f"leading principal {ns} x {ns} submatrix ({ns / n:.4g} of the rows) and those rows of B"
+
+
+def oracle_sample(A, B, nnz, m, budget_s, plain_gram=False):
+    """Time the oracle (as it stands) on a bounded sample: IO(B) and the first block steps of one
+    cycle until ~budget_s.  plain_gram: the same oracle with its near-exactly rounded Gram
+    replaced by one BLAS X^T Y (the fair CPU speed variant of BASELINE.md 3)."""
     from oracle import lsba_oracle as O
-    A = wl["A"]
-    B = wl["B"]
     n, s = B.shape
-    arn = O.PipArnoldi(A, "cl", wl["m"], s)
-    t0 = time.perf_counter()
-    arn.begin(B)
-    steps, byts = 0, roof_cycle_extra(n, s, 0)
-    while steps < wl["m"]:
-        arn.step()
-        steps += 1
-        byts += roof_step(wl["nnz"], n, s, steps)
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
+    g0 = O.gram
+    if plain_gram:
+        O.gram = lambda X, Y, chunk_rows=0: np.asarray(X, dtype=np.float64).T @ np.asarray(Y, dtype=np.float64)
+    try:
+        arn = O.PipArnoldi(A, "cl", m, s)
+        t0 = time.perf_counter()
+        arn.begin(B)
+        steps, byts = 0, roof_cycle_extra(n, s, 0)
+        while steps < m:
+            arn.step()
+            steps += 1
+            byts += roof_step(nnz, n, s, steps)
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+    finally:
+        O.gram = g0
     return dict(seconds=dt, steps=steps, bytes=byts)
+
+
+def cpu_baseline_legs(wl, budget_s=6.0):
+    """the oracle on this host with BLAS threads = all cores and = 1, with the
+    accurate (parity) Gram and the plain-BLAS Gram, plus the full tiny-config solve."""
+    from threadpoolctl import threadpool_limits
+    from lsba_inputs import make_twin
+    from oracle import lsba_oracle as O
+    A, B, ns, nnz_s, desc = oracle_sample_problem(wl)
+    cores = host_cores()
+    legs = {}
+    for gram_kind in ("plain", "accurate"):
+        for thr in (cores, 1):
+            with threadpool_limits(thr):
+                r = oracle_sample(A, B, nnz_s, wl["m"], budget_s, plain_gram=(gram_kind == "plain"))
+            legs[f"{gram_kind}_gram_{'all' if thr == cores else 1}_threads"] = {
+                "GBps": r["bytes"] / r["seconds"] / 1e9, "block_steps_per_s": r["steps"] / r["seconds"],
+                "s_per_block_step": r["seconds"] / max(1, r["steps"]), "threads": thr,
+                "seconds": round(r["seconds"], 2), "steps": r["steps"]}
+    p = make_twin(1)
+    t0 = time.perf_counter()
+    _, io = O.solve((p.row_ptr, p.col_idx, p.vals), p.B, m=p.m, tol=p.tol, max_restarts=p.max_restarts,
+                    ip="cl", mod="gmres")
+    tiny = {"seconds": time.perf_counter() - t0, "cycles": io.cycles, "iterations": io.iterations,
+            "workload": p.name, "outcome": int(io.outcome)}
+    # the fair CPU speed baseline: the plain-BLAS Gram, at the faster of its two thread counts
+    fair_name = max(("plain_gram_all_threads", "plain_gram_1_threads"), key=lambda k: legs[k]["GBps"])
+    fair = legs[fair_name]
+    return {"value": fair["GBps"], "unit": "GB/s", "cores": fair["threads"], "kind": "oracle",
+            "host_cores": cores, "fair_leg": fair_name,
+            "block_steps_per_s": fair["block_steps_per_s"], "cpu_model": cpu_model(),
+            "sample": f"oracle IO + first block steps of one cycle (~{budget_s:.0f} s per leg) on the {desc} "
+                      f"of {wl['name']}; GB/s with the same ROOF(k) numerator at the sample's n, nnz",
+            "legs": legs, "tiny_full_solve": tiny}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    from threadpoolctl import threadpool_limits
-    wl = build_workload(args.config, 0, 1)
+    wl = build_workload(args.config, 0, 1, need_sha=False)
+    A, B, ns, nnz_s, desc = oracle_sample_problem(wl)
     per_step_budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     tot_s, tot_b, tot_steps = 0.0, 0.0, 0
-    with threadpool_limits(1):              # the oracle as it stands, on one host core
-        for _ in range(args.warmup):
-            oracle_sample(wl, per_step_budget / 4)
-        for _ in range(args.steps):
-            r = oracle_sample(wl, per_step_budget)
-            tot_s += r["seconds"]
-            tot_b += r["bytes"]
-            tot_steps += r["steps"]
+    for _ in range(args.warmup):
+        oracle_sample(A, B, nnz_s, wl["m"], per_step_budget / 4)
+    for _ in range(args.steps):                 # the oracle as it stands, default BLAS threads
+        r = oracle_sample(A, B, nnz_s, wl["m"], per_step_budget)
+        tot_s += r["seconds"]
+        tot_b += r["bytes"]
+        tot_steps += r["steps"]
     gbs = tot_b / tot_s / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "block_steps_per_s": tot_steps / tot_s,
         "config": {"workload": wl["name"], "n": wl["n_global"], "s": wl["s"], "m": wl["m"],
-                   "method": "cl-BCGS-PIP block Arnoldi (oracle, NumPy fp64)",
-                   "timed_unit": "bounded sample: the first block steps of one cycle"},
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{tot_steps} block steps over {args.steps} samples of config {args.config}"},
+                   "method": "cl-BCGS-PIP block Arnoldi (oracle, NumPy fp64, accurate Gram)",
+                   "timed_unit": f"bounded sample: IO + the first block steps of one cycle on the {desc}"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": host_cores(), "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"{tot_steps} block steps over {args.steps} samples of config {args.config} "
+                                   f"({desc})"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -240,11 +321,14 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--repeats", type=int, default=5, help="timed regions of K steps (PAPER.md:424: mean of 5)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the fixed-k step sweep")
+    ap.add_argument("--no-tts", action="store_true", help="skip the full time-to-solution run")
     ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
     ap.add_argument("--prec", default="none", choices=["none", "ilu0"],
                     help="left ILU(0) preconditioning (SURVEY 8(f) f4); factored before the timed region")
@@ -252,7 +336,7 @@ def main():
                     help="Gram-Schmidt skeleton: BCGS-PIP (Alg 3), BMGS-CWY / -ICWY (Alg 6), BCGS-IRO-LS "
                          "(Alg 7), or the comparison baselines BMGS (Alg 2) and BCGS-PIO (Alg 4)")
     args = ap.parse_args()
-    assert args.warmup >= 0 and args.steps >= 1
+    assert args.warmup >= 0 and args.steps >= 1 and args.repeats >= 1
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -285,7 +369,7 @@ def main():
         L.lsba_ilu0_setup(ctx.ctx, True)
     B = torch.from_numpy(wl["B"]).cuda()
     X = torch.zeros_like(B)
-    m, tol, s = wl["m"], wl["tol"], wl["s"]
+    m, tol, s, tau = wl["m"], wl["tol"], wl["s"], wl["tau"]
     n_loc, n_glob = wl["row_end"] - wl["row_begin"], wl["n_global"]
 
     def barrier():
@@ -294,27 +378,39 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def solve(max_restarts):
+        return L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, max_restarts, ip=args.ip, cond_threshold=tau,
+                                   skel=args.skel)
+
     # warm-up: W cycles (one solve call), not timed
     if args.warmup:
-        L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, args.warmup - 1, ip=args.ip, skel=args.skel)
+        X.zero_()
+        solve(args.warmup - 1)
     barrier()
 
     # configs 1 and 4 converge in a few cycles: a bench step is then one full solve from X0 = 0
     full_solve = wl["spec"].get("max_restarts", 0) <= 50 or args.config == 4
 
     def timed_cycles(profile):
-        """K cycles in one solve call (or K full solves), CUDA events on the library's stream,
-        max over ranks.  Returns (iterations, cycles, ms, per-kernel profile, last info)."""
+        """K cycles in one solve call from X0 = 0 (or K full solves), CUDA events on the
+        library's stream, max over ranks.  Returns (iterations, cycles, ms, profile, info)."""
         L.lsba_profile_enable(ctx.ctx, profile)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        X.zero_()
         barrier()
         e0.record(stream)
         it = cy = nl = gb = 0
-        for _ in range(args.steps if full_solve else 1):
-            if full_solve:
+        for i in range(args.steps if full_solve else 1):
+            if full_solve and i:
                 X.zero_()
-            inf = L.lsba_bgmres_solve(ctx.ctx, B, X, m, tol, 200 if full_solve else args.steps - 1,
-                                      ip=args.ip, skel=args.skel)
+            inf = solve(200 if full_solve else args.steps - 1)
             it += inf.iterations
             cy += inf.cycles
             nl += inf.kernel_launches
@@ -323,32 +419,36 @@ def main():
         timed_cycles.gram_blocks = gb
         e1.record(stream)
         torch.cuda.synchronize()
-        t_ms = e0.elapsed_time(e1)
+        t_ms = max_over_ranks(e0.elapsed_time(e1))
         pr = {k: L.lsba_profile_read(ctx.ctx, k) for k in L.KERNEL_IDS} if profile else None
         L.lsba_profile_enable(ctx.ctx, False)
-        if dist is not None:
-            t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_ms = float(t.item())
         return it, cy, t_ms, pr, inf
 
-    # headline: un-instrumented (a CUDA event around every launch costs ~2 us of GPU idle each,
-    # ~8% of a config-2 step); then the same K cycles again with per-launch events for the
-    # per-kernel times behind `roofline`
+    def region_bytes(iters, cycles, gram_blocks):
+        b = algorithmic_bytes(wl["nnz"], n_glob, s, iters, cycles, gram_blocks, args.skel)
+        if args.prec == "ilu0":
+            b += ilu_bytes(wl["nnz"], n_glob, s, iters)
+        return b
+
+    # headline: un-instrumented (a CUDA event around every launch costs ~2 us of GPU idle each);
+    # then args.repeats - 1 more identical regions (mean / min); then the same K
+    # cycles once more with per-launch events for the per-kernel times behind `roofline`
     clocks = ClockSampler(local)
     clocks.start()
     iters, cycles, ms, _, info = timed_cycles(False)
     launches = timed_cycles.launches
+    total_bytes = region_bytes(iters, cycles, timed_cycles.gram_blocks)
+    reps = [total_bytes / (ms / 1e3) / 1e9]
+    reps_ms = [ms]
+    for _ in range(args.repeats - 1):
+        it_r, cy_r, ms_r, _, _ = timed_cycles(False)
+        reps.append(region_bytes(it_r, cy_r, timed_cycles.gram_blocks) / (ms_r / 1e3) / 1e9)
+        reps_ms.append(ms_r)
     clk = clocks.stop()
     _, _, ms_prof, prof, _ = timed_cycles(True)
     if not full_solve:
         assert cycles == args.steps, f"expected {args.steps} cycles, ran {cycles} (outcome {info.outcome})"
-    # whole-job algorithmic bytes (global problem): sum over accepted steps of ROOF(k) =
-    # iters (A + 8ns) + 16ns sum(k+1), plus 8ns(k_used + 7) per cycle
-    total_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, iters, cycles, timed_cycles.gram_blocks, args.skel)
-    if args.prec == "ilu0":
-        total_bytes += ilu_bytes(wl["nnz"], n_glob, s, iters)
-    gbs = total_bytes / (ms / 1e3) / 1e9
+    gbs = reps[0]
     steps_per_s = iters / (ms / 1e3)
     peak, peak_kind = measured_peaks()
 
@@ -367,60 +467,98 @@ def main():
         except Exception:
             traffic = None
 
+    # fixed-k step sweep: one Arnoldi cycle through the step API (one
+    # lsba_block_arnoldi_step call per step, each reading its status word), CUDA events around
+    # every step; ROOF(k) / time at k = 1, m/2, m
+    sweep = None
+    if not args.no_sweep and args.skel == "pip" and args.prec == "none":
+        L.lsba_set_skeleton(ctx.ctx, "pip")
+        X.zero_()
+        barrier()
+        ctx.begin(B, args.ip)
+        per_k = {}
+        for k in range(1, m + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            si = ctx.step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if si.chol_flag:
+                break
+            per_k[k] = max_over_ranks(e0.elapsed_time(e1))
+        sweep = {}
+        for k in sorted({1, max(1, m // 2), m}):
+            if k in per_k:
+                t = per_k[k]
+                sweep[f"k={k}"] = {"ms": round(t, 4), "GBps": roof_step(wl["nnz"], n_glob, s, k) / (t / 1e3) / 1e9,
+                                   "roof_bytes": roof_step(wl["nnz"], n_glob, s, k)}
+        sweep["note"] = ("one step of the step API per k (its status read after each step adds "
+                         "~10 us of launch latency per step); ROOF(k) / step time")
+
     # e2e through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
         Bh = torch.from_numpy(wl["B"]).pin_memory().numpy()
         Xh = torch.zeros(B.shape, dtype=torch.float64).pin_memory().numpy()
         # untimed warm-up call: allocates the library's device staging buffers once
-        L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 0, ip=args.ip)
+        L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 0, ip=args.ip, cond_threshold=tau)
         Xh[:] = 0.0
         barrier()
         t0 = time.perf_counter()
-        e2e_iters = 0
-        e2e_cycles = e2e_gb = 0
+        e2e_iters = e2e_cycles = e2e_gb = 0
         e2e_calls = []
         for _ in range(args.steps):
             if full_solve:
                 Xh[:] = 0.0
-            ih = L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 200 if full_solve else 0, ip=args.ip)
+            ih = L.lsba_solve_host(ctx.ctx, Bh, Xh, m, tol, 200 if full_solve else 0, ip=args.ip,
+                                   cond_threshold=tau)
             e2e_calls.append(ih.seconds)
             e2e_iters += ih.iterations
             e2e_cycles += ih.cycles
             e2e_gb += ih.gram_blocks
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        e2e_bytes = algorithmic_bytes(wl["nnz"], n_glob, s, e2e_iters, e2e_cycles, e2e_gb, args.skel)
-        if args.prec == "ilu0":
-            e2e_bytes += ilu_bytes(wl["nnz"], n_glob, s, e2e_iters)
-        e2e = {"value": e2e_bytes / dt / 1e9, "unit": "GB/s", "block_steps_per_s": e2e_iters / dt,
-               "h2d_bytes_per_step": 2 * n_loc * s * 8 * world, "d2h_bytes_per_step": n_loc * s * 8 * world,
+        dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": region_bytes(e2e_iters, e2e_cycles, e2e_gb) / dt / 1e9, "unit": "GB/s",
+               "block_steps_per_s": e2e_iters / dt,
+               "h2d_bytes_per_step": 2 * n_glob * s * 8, "d2h_bytes_per_step": n_glob * s * 8,
                "api": "lsba_solve_host (" + ("one full solve per step, X0 = 0" if full_solve
                                              else "1 cycle per call, X0 = previous X") + ")",
                "ms_per_call": [round(1e3 * x, 3) for x in e2e_calls]}
 
+    # time to solution: one full solve from X0 = 0 to tol (SURVEY.md 8(d) "separately, run the
+    # full solve"); at N > 1 its counts must match N = 1's within the R20 rule
+    tts = None
+    if not args.no_tts and not full_solve:
+        X.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        it = solve(wl["spec"]["max_restarts"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = max_over_ranks(e0.elapsed_time(e1)) / 1e3
+        tts = {"seconds": t, "outcome": int(it.outcome), "cycles": it.cycles, "iterations": it.iterations,
+               "nan_flags": it.nan_flags, "cond_restarts": it.cond_restarts, "true_relres": it.true_relres,
+               "block_steps_per_s": it.iterations / t,
+               "GBps": region_bytes(it.iterations, it.cycles, it.gram_blocks) / t / 1e9}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from threadpoolctl import threadpool_limits
-        with threadpool_limits(1):          # the oracle as it stands, on one host core
-            r = oracle_sample(wl, 20.0)
-        cpu = {"value": r["bytes"] / r["seconds"] / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "block_steps_per_s": r["steps"] / r["seconds"],
-               "sample": f"oracle IO + first {r['steps']} block steps of one cycle of {wl['name']} "
-                         f"({r['seconds']:.1f} s, single-threaded NumPy)"}
+        cpu = cpu_baseline_legs(wl)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "block_steps_per_s": steps_per_s, "ms_per_block_step": ms / iters,
             "pct_roofline": {"of_measured_hbm": gbs / (peak * world), "of_8TBps_nominal": gbs / (8000.0 * world)},
+            "repeats": {"n": len(reps), "GBps": [round(x, 1) for x in reps], "mean": statistics.mean(reps),
+                        "min": min(reps), "max": max(reps),
+                        "ms_per_step": [round(x / args.steps, 3) for x in reps_ms]},
             "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
+                       "tau": tau, "csr_sha256": wl["sha"] if world == 1 else None,
+                       "csr_sha256_rank0_rows": wl["sha"] if world > 1 else None,
                        "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY",
                                                           "irols": "BCGS-IRO-LS", "bmgs": "BMGS",
                                                           "pio": "BCGS-PIO"}[args.skel]
@@ -428,8 +566,11 @@ def main():
                                  + (", left ILU(0)" if args.prec == "ilu0" else ""),
                        "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
                                       f"{iters / args.steps:.1f} block steps)") if full_solve
-                                     else f"restart cycle = IO + {m} block steps + cycle end",
-                       "parallelism": f"rows-dp{world}", "l2": f"inputs larger than L2 (basis {8 * n_glob * s * (m + 1) / 1e9:.2f} GB)"
+                                     else f"restart cycle = IO + {m} block steps + cycle end (K cycles from X0 = 0)",
+                       "parallelism": f"rows-dp{world} (strong scaling: the same global problem, "
+                                      f"{'z-plane slabs' if wl['spec']['kind'] == 'stencil' else 'row blocks'})",
+                       "rows_rank0": [wl["row_begin"], wl["row_end"]],
+                       "l2": f"inputs larger than L2 (basis {8 * n_loc * s * (m + 1) / 1e9:.2f} GB per rank)"
                              + (f"; the CSR ({12 * wl['nnz'] / 1e6:.0f} MB) is kept in the persisting L2 set-aside"
                                 if l2_resident_csr(wl["nnz"], world) else "")},
             "roofline": {"bound": "hbm", "kernel": dom,
@@ -442,10 +583,12 @@ def main():
                                         f"on the launching streams; {ms_prof / args.steps:.3f} ms per cycle)"},
             "kernel_times_ms": {k: round(v[1], 3) for k, v in prof.items() if v[0]},
             "kernel_gbs": {k: round(v[2] / (v[1] / 1e3) / 1e9, 1) for k, v in prof.items() if v[1] > 0 and v[2] > 0},
+            "step_sweep": sweep,
             "gpu_launches": int(launches),
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "time_to_solution": tts,
             "solver": {"cycles": cycles, "iterations": iters, "nan_flags": info.nan_flags,
                        "res_est_rel": info.res_est, "true_relres": info.true_relres},
         }

@@ -190,6 +190,10 @@ lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t 
 
 /* Fault injection: make the Cholesky of step k_flag report a NaN-flag once (0 = off). */
 lsba_status lsba_set_force_flag(lsba_ctx ctx, int32_t k_flag);
+/* Fault injection: make the cycle-end projected solve of solve cycle `cycle` report singular
+ * (its combine then no-ops and the solve ends DEAD with the previous cycle's X; 0 = off).
+ * Covers the guard chain between a singular cycle end and the next cycle's speculative end. */
+lsba_status lsba_set_force_singular(lsba_ctx ctx, int32_t cycle);
 /* Skeleton of the step API (lsba_arnoldi_begin / lsba_block_arnoldi_step) and of
  * lsba_solve_host (default BCGS-PIP); the *_solve calls take theirs as an argument.
  * With BMGS-(I)CWY, lsba_arnoldi_begin also runs Alg 6's first loop iteration, and step k

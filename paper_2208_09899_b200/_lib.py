@@ -66,6 +66,7 @@ _sigs = {
     "lsba_spmm": [_vp, _vp, _vp],
     "lsba_block_inner_product": [_vp, _vp, _i32, _vp, C.c_int, _vp],
     "lsba_set_force_flag": [_vp, _i32],
+    "lsba_set_force_singular": [_vp, _i32],
     "lsba_set_kernel_variant": [_vp, _i32],
     "lsba_set_skeleton": [_vp, C.c_int],
     "lsba_profile_enable": [_vp, _i32],
@@ -250,6 +251,10 @@ def lsba_copy_ilu0_factors(ctx, nnz):
 
 def lsba_set_force_flag(ctx, k):
     _check(lib.lsba_set_force_flag(ctx, int(k)), ctx)
+
+
+def lsba_set_force_singular(ctx, cycle):
+    _check(lib.lsba_set_force_singular(ctx, int(cycle)), ctx)
 
 
 def lsba_set_kernel_variant(ctx, variant):

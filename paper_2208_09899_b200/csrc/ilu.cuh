@@ -6,8 +6,8 @@
 //                  thread per row (all s columns), rows in level order claimed chunk by chunk
 //                  by a persistent grid, dependencies detected by polling the data itself
 //                  (sentinel-filled output); measured 4.3 / 11 / 12 us per level on configs
-//                  2 / 3 / 5 vs 6.9 / 25 / 56 with ready flags (k_ilu_trsv_persist) and
-//                  17 / 46 / 72 with one CTA per chunk (k_ilu_trsv)
+//                  2 / 3 / 5 vs 6.9 / 25 / 56 with per-row ready flags and 17 / 46 / 72 with
+//                  one CTA per chunk (round-1 variants, removed; profiles/r01_ilu_apply.txt)
 //
 // Factor storage: lu[p] for CSR position p of the local matrix (row_ptr / col_idx of A):
 // strictly-lower entries are L (unit diagonal implied), the rest U.  Columns >= n_local
@@ -59,121 +59,6 @@ k_ilu0_level(int cnt, const int* __restrict__ rows, const int* __restrict__ rp,
   if (lane == 0) {
     const double d = lu[diag[i]];
     if (!(d != 0.0) || !isfinite(d)) *bad = 1;
-  }
-}
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
-}
-
-// Sync-free triangular solve, in place on Y (n_local x S, row-major):
-//   LOWER:  y_i = x_i - sum_{k<i} l_ik y_k          (unit diagonal)
-//   UPPER:  y_i = (x_i - sum_{j>i} u_ij y_j) / u_ii
-// each sum in CSR order (the oracle's order).  Thread t handles row order[t] (rows sorted by
-// level, so every dependency has a smaller position); CTAs take their row ranges in the order
-// they START (atomic ticket), so a CTA's dependencies belong to CTAs already running or done —
-// spinning cannot deadlock.  A row publishes ready[i] = gen (release) after its store; readers
-// acquire ready[k] == gen before loading y_k.  gen is unique per launch (no flag reset).
-template <int S, bool LOWER>
-__global__ void __launch_bounds__(256)
-k_ilu_trsv(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
-           const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
-           int n_local, double* Y, unsigned* ready, unsigned gen, unsigned* ticket,
-           const int* __restrict__ active) {
-  __shared__ int blk;
-  if (threadIdx.x == 0) {
-    const unsigned w = atomicAdd(ticket, 1u);
-    if (w == gridDim.x - 1) *ticket = 0u;          // every CTA has claimed: reset for the next launch
-    blk = (int)w;
-  }
-  __syncthreads();
-  if (active && *active == 0) return;
-  const int t = blk * blockDim.x + threadIdx.x;
-  if (t >= nrows) return;
-  const int i = order[t];
-  const int p0 = rp[i], p1 = rp[i + 1];
-  double acc[S];
-#pragma unroll
-  for (int c = 0; c < S; ++c) acc[c] = 0.0;
-  for (int p = p0; p < p1; ++p) {
-    const int k = ci[p];
-    if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
-    if (ld_acquire_u32(ready + k) != gen) {
-      while (ld_acquire_u32(ready + k) != gen) __nanosleep(32);
-    }
-    const double a = lu[p];
-    const double* yk = Y + (size_t)k * S;
-#pragma unroll
-    for (int c = 0; c < S; ++c) acc[c] = fma(a, __ldcg(yk + c), acc[c]);
-  }
-  double* yi = Y + (size_t)i * S;
-  const double dinv = LOWER ? 1.0 : lu[diag[i]];
-#pragma unroll
-  for (int c = 0; c < S; ++c) {
-    const double r = __ldcg(yi + c) - acc[c];
-    __stcg(yi + c, LOWER ? r : r / dinv);
-  }
-  __threadfence();
-  st_release_u32(ready + i, gen);
-}
-
-// Persistent variant: a grid of one CTA per SM claims CHUNKS of kThreads consecutive rows (in
-// level order) from a global counter, one row per thread, and claims the next chunk after a
-// CTA barrier.  Only the frontier (grid x 256 rows, a few levels) is in flight, so the spinning
-// threads are ~10x fewer than with one CTA per chunk, and the polls no longer flood L2.
-// ctr[0]: chunk counter, ctr[1]: exited CTAs (the last one resets both for the next launch).
-template <int S, bool LOWER>
-__global__ void __launch_bounds__(256)
-k_ilu_trsv_persist(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
-                   const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
-                   int n_local, double* Y, unsigned* ready, unsigned gen, unsigned* ctr,
-                   const int* __restrict__ active) {
-  __shared__ int chunk;
-  const bool live = !(active && *active == 0);
-  const int nchunks = (nrows + blockDim.x - 1) / blockDim.x;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) chunk = live ? (int)atomicAdd(ctr, 1u) : nchunks;
-    __syncthreads();
-    if (chunk >= nchunks) break;
-    const int t = chunk * blockDim.x + threadIdx.x;
-    if (t < nrows) {
-      const int i = order[t];
-      const int p0 = rp[i], p1 = rp[i + 1];
-      double acc[S];
-#pragma unroll
-      for (int c = 0; c < S; ++c) acc[c] = 0.0;
-      for (int p = p0; p < p1; ++p) {
-        const int k = ci[p];
-        if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
-        while (ld_acquire_u32(ready + k) != gen) {
-        }
-        const double a = lu[p];
-        const double* yk = Y + (size_t)k * S;
-#pragma unroll
-        for (int c = 0; c < S; ++c) acc[c] = fma(a, __ldcg(yk + c), acc[c]);
-      }
-      double* yi = Y + (size_t)i * S;
-      const double dinv = LOWER ? 1.0 : lu[diag[i]];
-#pragma unroll
-      for (int c = 0; c < S; ++c) {
-        const double r = __ldcg(yi + c) - acc[c];
-        __stcg(yi + c, LOWER ? r : r / dinv);
-      }
-      st_release_u32(ready + i, gen);   // release: orders this thread's stores of y_i before it
-    }
-  }
-  if (threadIdx.x == 0) {
-    const unsigned e = atomicAdd(ctr + 1, 1u);
-    if (e == gridDim.x - 1) {                  // every CTA is done claiming: reset for the next launch
-      ctr[0] = 0u;
-      ctr[1] = 0u;
-    }
   }
 }
 

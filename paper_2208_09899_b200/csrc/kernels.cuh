@@ -29,10 +29,11 @@ constexpr int kThreads = 256;
 // 1 = the SpMM's CSR streams (row_ptr, col_idx, vals) evict_last, so A can stay L2-resident
 // across the step while the basis streams through; 2 = the Gram's basis reads evict_first;
 // 4 = the projection's basis reads evict_first; 8 = the SpMM output W and the projection output
-// V_{k+1} stored evict_last (the next kernel re-reads them).  Default 14 (measured: config 2
-// +8%, config 5 +1.5%, configs 3/4 neutral; tools/l2exp.sh); LSBA_L2HINT overrides per context.
+// V_{k+1} stored evict_last (the next kernel re-reads them).  The product uses 14 (measured in
+// round 1: config 2 +8%, config 5 +1.5%, configs 3/4 neutral; bit 1 lost); a compile-time
+// constant so that no module-wide state is shared between contexts.
 // ------------------------------------------------------------------------------------------
-static __constant__ int c_l2hint = 14;
+constexpr int c_l2hint = 14;
 
 // Programmatic dependent launch (PDL): the hot kernels of a step (SpMM, Gram, projection) may
 // be launched with programmatic stream serialisation, so the next kernel's CTAs are scheduled

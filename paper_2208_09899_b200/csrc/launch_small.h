@@ -16,7 +16,7 @@ cudaError_t launch_step_update(const SmallState2& st, const double* G, int k, do
                                cudaStream_t stream);
 template <int B>
 cudaError_t launch_cycle_end(const SmallState2& st, int k, int gmres, int happy, int upd, double* Y,
-                             double* Z, int* info, cudaStream_t stream);
+                             double* Z, int* info, const int* prior, int force_sing, cudaStream_t stream);
 
 template <int B>
 cudaError_t launch_cwy_iter1(const SmallState2& st, const double* G, cudaStream_t stream);
@@ -39,7 +39,7 @@ cudaError_t launch_pio_coef(const SmallState2& st, const double* G1, const doubl
   cudaError_t launch_step_update<B>(const SmallState2&, const double*, int, double, cudaStream_t);     \
   template <>                                                                                           \
   cudaError_t launch_cycle_end<B>(const SmallState2&, int, int, int, int, double*, double*, int*,     \
-                                  cudaStream_t);                                                        \
+                                  const int*, int, cudaStream_t);                                       \
   template <>                                                                                           \
   cudaError_t launch_cwy_iter1<B>(const SmallState2&, const double*, cudaStream_t);                    \
   template <>                                                                                           \

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -119,30 +120,15 @@ struct lsba_ctx_ {
   int* d_diag = nullptr;         // CSR position of a_ii
   int* d_ordL = nullptr;         // rows by level of L (ascending dependencies)
   int* d_ordU = nullptr;         // rows by level of U
-  unsigned* d_ready = nullptr;   // per-row ready flags of the sync-free solves
   double* d_ilu_tmp = nullptr;   // n x s intermediate of the data-polling variant
   unsigned* d_ticket = nullptr;  // CTA start tickets (2: L and U solves)
-  unsigned ilu_gen = 0;          // launch generation (ready[i] == gen: row i solved)
   int ilu_levels[2] = {0, 0};
-  int ilu_variant = 2;           // 2 data polling (default), 0 ready flags, 1 flags + a CTA per chunk
-                                 // (LSBA_ILU_VARIANT; tools/ilu_apply_bench.py)
   int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
-  // overlapped projection -> next SpMM (one rank, BCGS-PIP): the projection of step k runs in
-  // row pieces on the main stream, the SpMM of step k+1 in row pieces on stream3, each piece
-  // after the projection pieces covering the V rows it reads (ovl_need, from the CSR)
-  int ovl_pieces = 0;            // 0: off (LSBA_OVL=P)
-  std::vector<int> ovl_prow;     // projection piece row starts (P + 1)
-  std::vector<int> ovl_srow;     // SpMM piece row starts (P + 1)
-  std::vector<int> ovl_need;     // SpMM piece i needs projection pieces 0..ovl_need[i]
-  std::vector<int64_t> ovl_snnz; // stored entries per SpMM piece
-  int64_t rw_nnz = 0;            // stored entries of the current row window
-  cudaStream_t stream3 = nullptr;
-  cudaEvent_t ev_proj[8] = {}, ev_spmm = nullptr, ev_status = nullptr;
-  int spmm_ahead = -1;           // step whose SpMM was already issued by the previous step
-  int rw0 = 0, rwn = -1;         // row window of project_t / spmm_t (rwn < 0: all rows)
-  cudaStream_t kstream = nullptr;  // stream override of spmm_t
+  cudaEvent_t ev_status = nullptr;
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
   bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
+  int force_sing_cycle = 0;      // test hook: the cycle end of this cycle reports singular
+  int cur_cycle = 0;
   size_t csr_bytes = 0;          // joint col_idx + vals allocation (d_va points into it)
   int l2persist = -1;            // SpMM CSR window persisting in L2: -1 auto, 0 off, 1 on (LSBA_L2PERSIST)
   size_t l2win = 0;
@@ -152,7 +138,6 @@ struct lsba_ctx_ {
   bool in_proj = false;
   int g7force = 0;               // diagnostics: LSBA_G7 forces a v7 Gram configuration (s = 4, 8)
   bool pdl = true;               // programmatic dependent launch of SpMM / Gram / projection (LSBA_PDL)
-  int l2hint = 14;               // L2 eviction-priority hints (kernels.cuh c_l2hint; LSBA_L2HINT)
   bool pending_upd = false;   // the main stream must join ev_upd before the next Gram
   int skel = LSBA_SKEL_BCGS_PIP;          // skeleton of the running solve / Arnoldi process
   int skel_default = LSBA_SKEL_BCGS_PIP;  // lsba_set_skeleton: step API and lsba_solve_host
@@ -300,10 +285,10 @@ static cudaError_t launch_k(lsba_ctx c, void (*kern)(P...), dim3 grid, dim3 bloc
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = c->kstream ? c->kstream : c->stream;
+  cfg.stream = c->stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (c->pdl && !c->kstream && (c->pdl_proj || !c->in_proj)) {
+  if (c->pdl && (c->pdl_proj || !c->in_proj)) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
@@ -332,52 +317,22 @@ static lsba_status ilu_apply_t(lsba_ctx c, double* Y, const int* active) {
   // algorithmic bytes per solve: the factor half (~12 B per stored entry + row pointers and
   // the row order) and Y read + written once
   const double by = 6.0 * c->nnz + 8.0 * (c->n + 1) + 16.0 * c->n * S;
-  if (c->ilu_variant == 2) {    // data polling, out of place: Y -> T (L), T -> Y (U)
-    const int grid = std::min(nblk, c->n_sms * c->ilu_ctas);
-    const long cnt = (long)c->n * S;
-    const int fgrid = std::min(4 * c->n_sms, (int)cdiv(cnt, kThreads));
-    {
-      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
-      k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, c->d_ilu_tmp);
-      k_ilu_trsv_poll<S, true><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci,
-          c->d_lu, c->d_diag, c->n, Y, c->d_ilu_tmp, c->d_ticket, active);
-      CKL();
-    }
-    {
-      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
-      k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, Y);
-      k_ilu_trsv_poll<S, false><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci,
-          c->d_lu, c->d_diag, c->n, c->d_ilu_tmp, Y, c->d_ticket + 2, active);
-      CKL();
-    }
-    return LSBA_OK;
-  }
-  if (c->ilu_variant == 0) {
-    const int grid = std::min(nblk, c->n_sms * c->ilu_ctas);
-    {
-      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
-      k_ilu_trsv_persist<S, true><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci,
-          c->d_lu, c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket, active);
-      CKL();
-    }
-    {
-      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
-      k_ilu_trsv_persist<S, false><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci,
-          c->d_lu, c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 2, active);
-      CKL();
-    }
-    return LSBA_OK;
-  }
+  // data polling, out of place: Y -> T (L), T -> Y (U)
+  const int grid = std::min(nblk, c->n_sms * c->ilu_ctas);
+  const long cnt = (long)c->n * S;
+  const int fgrid = std::min(4 * c->n_sms, (int)cdiv(cnt, kThreads));
   {
     LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
-    k_ilu_trsv<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci, c->d_lu,
-        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 4, active);
+    k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, c->d_ilu_tmp);
+    k_ilu_trsv_poll<S, true><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci,
+        c->d_lu, c->d_diag, c->n, Y, c->d_ilu_tmp, c->d_ticket, active);
     CKL();
   }
   {
     LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
-    k_ilu_trsv<S, false><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci, c->d_lu,
-        c->d_diag, c->n, Y, c->d_ready, ++c->ilu_gen, c->d_ticket + 5, active);
+    k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, Y);
+    k_ilu_trsv_poll<S, false><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci,
+        c->d_lu, c->d_diag, c->n, c->d_ilu_tmp, Y, c->d_ticket + 2, active);
     CKL();
   }
   return LSBA_OK;
@@ -387,37 +342,27 @@ static lsba_status ilu_apply(lsba_ctx c, double* Y, const int* active = nullptr)
 // ---------------------------------------------------------------- a1: SpMM / residual
 template <int S>
 static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* active) {
-  // row window [rw0, rw0 + rwn) (overlapped pipeline, one rank): the row pointers and W shift,
-  // V and the column indices stay global
-  const bool win = c->rwn >= 0;
-  const int n = win ? c->rwn : c->n;
-  const int* rp = c->d_rp + (win ? c->rw0 : 0);
-  if (win) W += (size_t)c->rw0 * S;
-  else TRY(halo_t<S>(c, V));
+  const int n = c->n;
+  TRY(halo_t<S>(c, V));
   constexpr int L = (S % 2 == 0) ? S / 2 : 1;
   const long threads = (long)n * L;
-  // the kernel treats columns >= its row count as ghosts at Vghost + (col - n) s: in a window
-  // (one rank, no ghosts) that must again be V + col s
-  const double* vg = win ? V + (size_t)n * S : c->d_ghost;
   {
-    const double nnzw = win ? (double)c->rw_nnz : (double)c->nnz;
-    LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * nnzw + 4.0 * (n + 1) + 16.0 * n * S,
-                   c->kstream ? c->kstream : c->stream);
+    LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (n + 1) + 16.0 * n * S);
     if (n == 0) return LSBA_OK;
     if constexpr (S % 2 == 0 || S == 1) {
       c->in_spmm = true;
       const cudaError_t le = launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, n,
-                  rp, (const int*)c->d_ci, (const double*)c->d_va, V,
-                  vg, (const double*)nullptr, W, (double*)nullptr, active);
+                  (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
+                  (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active);
       c->in_spmm = false;
       CK(le);
     } else {
-      k_spmm_odd<S, false><<<cdiv(n, kThreads), kThreads, 0, c->kstream ? c->kstream : c->stream>>>(
-          n, rp, c->d_ci, c->d_va, V, vg, nullptr, W, nullptr, active);
+      k_spmm_odd<S, false><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(
+          n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
     }
     CKL();
   }
-  if (c->prec && !win) TRY(ilu_apply_t<S>(c, W, active));
+  if (c->prec) TRY(ilu_apply_t<S>(c, W, active));
   return LSBA_OK;
 }
 
@@ -664,14 +609,7 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
     return project_t<S>(c, X, xstride, 0, nullptr, nullptr, nullptr, J1, C1, out1, flag_ptr, kid);
   }
   const int Jmax = std::max(J0, J1);
-  const int n = c->rwn >= 0 ? c->rwn : c->n;   // row window (overlapped pipeline)
-  if (c->rwn >= 0) {
-    const size_t off = (size_t)c->rw0 * S;
-    X += off;
-    if (base0) base0 += off;
-    if (out0) out0 += off;
-    if (out1) out1 += off;
-  }
+  const int n = c->n;
   const double bytes = 8.0 * n * S * (Jmax + (J0 > 0) + (J1 > 0) + (base0 ? 1 : 0));
   LaunchScope Ls(c, kid, bytes);
   if (n == 0) return LSBA_OK;
@@ -884,10 +822,6 @@ static lsba_status read_status(lsba_ctx c, StepStatus* out, CycleCtl* ctl) {
 // IO(U) with U in slot 0: Gram (1 sync), chol, scale in place (Alg 3 line 1).  Resets the
 // device cycle control with this cycle's parameters.  Asynchronous.
 static lsba_status io_begin_async(lsba_ctx c, const CycleParams& prm) {
-  if (c->spmm_ahead >= 0) {     // a speculative next-step SpMM of the last cycle may still run
-    CK(cudaStreamWaitEvent(c->stream, c->ev_spmm, 0));
-    c->spmm_ahead = -1;
-  }
   bool fused = false;
   TRY(gram(c, slotp(c, 0), c->slot_stride, 1, slotp(c, 0), c->ip, nullptr, nullptr, 0, &prm, &fused));
   if (!fused) TRY(small_step(c, 0, prm));
@@ -906,10 +840,7 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
   c->pending_upd = (k > 1);
   bool fused = false;
-  const bool ahead = (c->spmm_ahead == k);   // W = A V_k already computed by the step k-1 pipeline
-  if (ahead) CK(cudaStreamWaitEvent(c->stream, c->ev_spmm, 0));
-  c->spmm_ahead = -1;
-  TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, ahead ? nullptr : slotp(c, k - 1),
+  TRY(gram(c, slotp(c, 0), c->slot_stride, k + 1, slotp(c, k), c->ip, slotp(c, k - 1),
            &c->d_ctl->active, k, &none, &fused));                                // lines 3-4 (+5)
   TRY(wait_update(c));
   if (!fused) TRY(small_step(c, k, none));                                       // line 5
@@ -918,43 +849,8 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   CK(cudaStreamWaitEvent(c->stream2, c->ev_coef, 0));
   TRY(step_update(c, k, c->d_G));
   CK(cudaEventRecord(c->ev_upd, c->stream2));
-  if (!(c->ovl_pieces > 0 && c->nranks == 1 && !c->prec && c->variant == 0)) {
-    TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
-                nullptr, c->st.flag_dev, LSBA_K_PROJECT));                       // line 6
-    return LSBA_OK;
-  }
-  // line 6 in row pieces, and the next step's line 3 (W = A V_{k+1} -> slot k+1) in row pieces
-  // on stream 3, each after the projection pieces holding the V_{k+1} rows it reads: the
-  // latency-bound SpMM overlaps the bandwidth-bound projection (speculative like every step)
-  const int P = c->ovl_pieces;
-  for (int p = 0; p < P; ++p) {
-    c->rw0 = c->ovl_prow[p];
-    c->rwn = c->ovl_prow[p + 1] - c->ovl_prow[p];
-    const lsba_status st = project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0,
-                                   nullptr, nullptr, c->st.flag_dev, LSBA_K_PROJECT);
-    c->rwn = -1;
-    c->rw0 = 0;
-    TRY(st);
-    CK(cudaEventRecord(c->ev_proj[p], c->stream));
-  }
-  c->kstream = c->stream3;
-  lsba_status st = LSBA_OK;
-  for (int i = 0; i < P && st == LSBA_OK; ++i) {
-    if (cudaStreamWaitEvent(c->stream3, c->ev_proj[c->ovl_need[i]], 0) != cudaSuccess) {
-      st = fail(c, LSBA_E_CUDA, "stream wait failed");
-      break;
-    }
-    c->rw0 = c->ovl_srow[i];
-    c->rwn = c->ovl_srow[i + 1] - c->ovl_srow[i];
-    c->rw_nnz = c->ovl_snnz[i];
-    st = spmm(c, slotp(c, k), slotp(c, k + 1), &c->d_ctl->active);
-  }
-  c->kstream = nullptr;
-  c->rwn = -1;
-  c->rw0 = 0;
-  TRY(st);
-  CK(cudaEventRecord(c->ev_spmm, c->stream3));
-  c->spmm_ahead = k + 1;
+  TRY(project(c, slotp(c, 0), c->slot_stride, k + 1, c->st.coef, nullptr, slotp(c, k), 0, nullptr,
+              nullptr, c->st.flag_dev, LSBA_K_PROJECT));                         // line 6
   return LSBA_OK;
 }
 
@@ -1077,7 +973,6 @@ static lsba_status step_async(lsba_ctx c, int k, bool last) {
 // join stream 2 (the last step's update) into the main stream
 static lsba_status join_update(lsba_ctx c) {
   CK(cudaStreamWaitEvent(c->stream, c->ev_upd, 0));
-  if (c->spmm_ahead >= 0) CK(cudaStreamWaitEvent(c->stream, c->ev_spmm, 0));
   return LSBA_OK;
 }
 
@@ -1089,47 +984,34 @@ static lsba_status set_identity(lsba_ctx c) {
 }
 
 template <int B>
-static lsba_status cycle_end_t(lsba_ctx c, int k, int gmres, int happy, int upd, int* info) {
+static lsba_status cycle_end_t(lsba_ctx c, int k, int gmres, int happy, int upd, int* info,
+                               const int* prior) {
   LaunchScope Ls(c, LSBA_K_CYCLE_SOLVE, 0.0);
-  CK(launch_cycle_end<B>(c->st, k, gmres, happy, upd, c->d_Y, c->d_Z, info, c->stream));
+  const int force = (!happy && c->force_sing_cycle > 0 && c->cur_cycle == c->force_sing_cycle) ? 1 : 0;
+  CK(launch_cycle_end<B>(c->st, k, gmres, happy, upd, c->d_Y, c->d_Z, info, prior, force, c->stream));
   return LSBA_OK;
+}
+static lsba_status cycle_end(lsba_ctx c, int k, int gmres, int happy, int upd, int* info,
+                             const int* prior = nullptr) {
+  LSBA_DISPATCH_S(c->b, cycle_end_t, c, k, gmres, happy, upd, info, prior);
 }
 
 // Enqueue the cycle-end projected solve; its singular flag goes to d_info[1] and guards the
 // combine that follows (no host round trip; the flag is read with the next cycle's status).
 static lsba_status cycle_solve_async(lsba_ctx c, int k, int gmres) {
-  switch (c->b) {
-#define CASE(B) case B: return cycle_end_t<B>(c, k, gmres, 0, 1, c->d_info + 1);
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-    default: return LSBA_E_ARG;
-  }
+  return cycle_end(c, k, gmres, 0, 1, c->d_info + 1);
 }
 
 // The speculative cycle end (one rank): enqueued with k = m before the host reads the cycle's
-// status; runs only if the cycle ended at k = m (k_cycle_end's guard).  Ping-pong flag slots
-// per cycle parity: d_info[4 + par] = singular / combine guard, d_info[6 + par] = skipped.
-static lsba_status cycle_solve_spec(lsba_ctx c, int k, int gmres, int par) {
-  switch (c->b) {
-#define CASE(B) case B: return cycle_end_t<B>(c, k, gmres, 0, 2, c->d_info + 4 + par);
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-    default: return LSBA_E_ARG;
-  }
+// status; runs only if the cycle ended at k = m and the previous cycle end (guard `prior`, if
+// one is pending) was not singular (k_cycle_end's guard).  Ping-pong flag slots per cycle
+// parity: d_info[4 + par] = singular / combine guard, d_info[6 + par] = skipped.
+static lsba_status cycle_solve_spec(lsba_ctx c, int k, int gmres, int par, const int* prior) {
+  return cycle_end(c, k, gmres, 0, 2, c->d_info + 4 + par, prior);
 }
 
 static lsba_status cycle_solve(lsba_ctx c, int k, int gmres, int happy, int* singular, int upd = 1) {
-  lsba_status st;
-  switch (c->b) {
-#define CASE(B) case B: st = cycle_end_t<B>(c, k, gmres, happy, upd, c->d_info); break;
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
-    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15) CASE(16)
-#undef CASE
-    default: return LSBA_E_ARG;
-  }
-  TRY(st);
+  TRY(cycle_end(c, k, gmres, happy, upd, c->d_info));
   CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   *singular = c->h_info[0];
@@ -1266,6 +1148,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
   bool finished = false;
   for (int cycle = 1; cycle <= max_restarts + 1 && !finished; ++cycle) {
     info->cycles = cycle;
+    c->cur_cycle = cycle;
     // enqueue IO(U) and all m_cur steps of the cycle; the step kernels take the
     // continue/restart decision on the device and later launches no-op (one host sync)
     CycleParams prm;
@@ -1300,11 +1183,16 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(CycleCtl), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(c->h_info + 1, c->d_info + 1, 7 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaEventRecord(c->ev_status, c->stream));
-      TRY(cycle_solve_spec(c, m_cur, gmres, par));
+      TRY(cycle_solve_spec(c, m_cur, gmres, par, sing_pending ? c->d_info + sing_slot : nullptr));
+      const double comb0 = c->prof.bytes[LSBA_K_COMBINE];
       TRY(project(c, slotp(c, 0), c->slot_stride, m_cur, c->d_Y, X, X, m_cur + 1, c->d_Z, slotp(c, 0),
                   c->d_info + 4 + par, LSBA_K_COMBINE));
       CK(cudaEventSynchronize(c->ev_status));
       cc = *c->h_ctl;
+      // the speculative combine moves its bytes only if it ran (k = m ending, no pending
+      // singular guard); otherwise it no-op'd on the device: take its bytes back out
+      if (!(cc.why == 4 && cc.k_used == m_cur && !(sing_pending && c->h_info[sing_slot])))
+        c->prof.bytes[LSBA_K_COMBINE] = comb0;
     } else {
       TRY(read_status(c, nullptr, &cc));
     }
@@ -1519,19 +1407,48 @@ static lsba_status dalloc(lsba_ctx c, T** p, size_t count) {
   return LSBA_OK;
 }
 
+// The persisting-L2 limit is device state shared by every context on the device: reference-
+// count it per device, raise it to the largest set-aside any live context asked for, and
+// restore the limit found by the first user when the last one releases it.
+static std::mutex g_l2_mu;
+static int g_l2_users[64];
+static size_t g_l2_prev[64], g_l2_cur[64];
+static cudaError_t l2_setaside_acquire(int dev, size_t aside) {
+  std::lock_guard<std::mutex> lk(g_l2_mu);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (g_l2_users[dev] == 0) {
+    cudaError_t e = cudaDeviceGetLimit(&g_l2_prev[dev], cudaLimitPersistingL2CacheSize);
+    if (e != cudaSuccess) return e;
+    g_l2_cur[dev] = g_l2_prev[dev];
+  }
+  if (aside > g_l2_cur[dev]) {
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside);
+    if (e != cudaSuccess) return e;
+    g_l2_cur[dev] = aside;
+  }
+  ++g_l2_users[dev];
+  return cudaSuccess;
+}
+static void l2_setaside_release(int dev) {
+  std::lock_guard<std::mutex> lk(g_l2_mu);
+  if (dev < 0 || dev >= 64 || g_l2_users[dev] == 0) return;
+  if (--g_l2_users[dev] == 0) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_prev[dev]);
+    g_l2_cur[dev] = g_l2_prev[dev];
+  }
+}
+
 static void release(lsba_ctx c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->l2win > 0) {                  // give the L2 set-aside back
-    cudaCtxResetPersistingL2Cache();
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
-  }
+  if (c->l2win > 0) l2_setaside_release(c->device);   // give the L2 set-aside back
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
                   c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL,
-                  c->d_ordU, c->d_ready, c->d_ticket, c->d_ilu_tmp};
+                  c->d_ordU, c->d_ticket, c->d_ilu_tmp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1542,10 +1459,6 @@ static void release(lsba_ctx c) {
   if (c->ev_coef) cudaEventDestroy(c->ev_coef);
   if (c->ev_upd) cudaEventDestroy(c->ev_upd);
   if (c->stream2) cudaStreamDestroy(c->stream2);
-  if (c->stream3) cudaStreamDestroy(c->stream3);
-  for (auto e : c->ev_proj)
-    if (e) cudaEventDestroy(e);
-  if (c->ev_spmm) cudaEventDestroy(c->ev_spmm);
   if (c->ev_status) cudaEventDestroy(c->ev_status);
   for (int k = 0; k < LSBA_K_COUNT; ++k)
     for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -1641,7 +1554,6 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
       if (send_idx[i] < 0 || send_idx[i] >= n_local) return fail(c, LSBA_E_ARG, "peer requested a row this rank does not own");
     }
   }
-  CK(cudaMemcpyToSymbol(c_l2hint, &c->l2hint, sizeof(int)));
   // ---- device CSR
   std::vector<int32_t> rp32(n_local + 1);
   for (int64_t i = 0; i <= n_local; ++i) rp32[i] = (int32_t)row_ptr[i];
@@ -1683,7 +1595,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     c->l2win = std::min<size_t>(want, (size_t)max_win);
     const size_t aside = std::min<size_t>(c->l2win, (size_t)max_persist);
     if (aside > 0) {
-      CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, aside));
+      CK(l2_setaside_acquire(c->device, aside));
       c->l2hit = (float)std::min(1.0, (double)aside / (double)c->l2win);
     } else {
       c->l2win = 0;
@@ -1780,35 +1692,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   }
   CK(cudaEventCreateWithFlags(&c->ev_coef, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming));
-  CK(cudaStreamCreateWithFlags(&c->stream3, cudaStreamNonBlocking));
-  for (auto& e : c->ev_proj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->ev_spmm, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_status, cudaEventDisableTiming));
-  if (c->ovl_pieces > 0 && c->nranks == 1 && n_local > 0) {
-    // piece plan: P equal projection pieces; SpMM piece i = rows whose columns all lie in
-    // projection pieces 0..i (prefix maximum of the column index), the rest in the last piece
-    const int P = std::min(c->ovl_pieces, 8);
-    c->ovl_pieces = P;
-    c->ovl_prow.assign(P + 1, 0);
-    for (int p = 0; p <= P; ++p) c->ovl_prow[p] = (int)((int64_t)n_local * p / P);
-    c->ovl_srow.assign(P + 1, 0);
-    c->ovl_need.assign(P, 0);
-    int64_t pmax = -1;
-    int piece = 0;
-    for (int64_t r = 0; r < n_local && piece < P - 1; ++r) {
-      for (int64_t q = row_ptr[r]; q < row_ptr[r + 1]; ++q) pmax = std::max<int64_t>(pmax, col_local[q]);
-      while (piece < P - 1 && pmax >= c->ovl_prow[piece + 1]) c->ovl_srow[++piece] = (int)r;
-    }
-    while (piece < P - 1) c->ovl_srow[++piece] = (int)n_local;
-    c->ovl_srow[P] = (int)n_local;
-    c->ovl_snnz.assign(P, 0);
-    for (int i = 0; i < P; ++i) {
-      c->ovl_need[i] = i;
-      c->ovl_snnz[i] = row_ptr[c->ovl_srow[i + 1]] - row_ptr[c->ovl_srow[i]];
-    }
-  } else {
-    c->ovl_pieces = 0;
-  }
   TRY(dalloc(c, &c->st.status, 1));
   TRY(dalloc(c, &c->st.flag_dev, 1));
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
@@ -1832,15 +1716,12 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (!c) return LSBA_E_OOM;
   *out = c;  // returned even on failure so that lsba_last_error works; destroy it
   if (const char* e = std::getenv("LSBA_NO_FUSE")) c->no_fuse = (e[0] == '1');
-  if (const char* e = std::getenv("LSBA_L2HINT")) c->l2hint = std::atoi(e);
   if (const char* e = std::getenv("LSBA_PDL")) c->pdl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_G7")) c->g7force = std::atoi(e);
   if (const char* e = std::getenv("LSBA_UPD_MAIN")) c->upd_main = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_PDL_PROJ")) c->pdl_proj = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2PERSIST")) c->l2persist = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPEC_END")) c->spec_end = (e[0] == '1');
-  if (const char* e = std::getenv("LSBA_OVL")) c->ovl_pieces = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("LSBA_ILU_VARIANT")) c->ilu_variant = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
   if (n < s) return fail(c, LSBA_E_ARG, "n < s");
@@ -2075,16 +1956,13 @@ static lsba_status ilu0_factor(lsba_ctx c) {
     TRY(dalloc(c, &c->d_diag, n));
     TRY(dalloc(c, &c->d_ordL, n));
     TRY(dalloc(c, &c->d_ordU, n));
-    TRY(dalloc(c, &c->d_ready, n));
     TRY(dalloc(c, &c->d_ticket, 8));
     TRY(dalloc(c, &c->d_ilu_tmp, (size_t)n * c->s));
   }
   CK(cudaMemcpy(c->d_diag, diag.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ordL, ordL.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ordU, ordU.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
-  CK(cudaMemset(c->d_ready, 0, sizeof(unsigned) * n));
   CK(cudaMemset(c->d_ticket, 0, sizeof(unsigned) * 8));
-  c->ilu_gen = 0;
   if (c->nnz) CK(cudaMemcpy(c->d_lu, c->d_va, sizeof(double) * c->nnz, cudaMemcpyDeviceToDevice));
   CK(cudaMemsetAsync(c->d_info, 0, sizeof(int), c->stream));
   for (int l = 0; l < nlL; ++l) {          // one launch per level of L (setup only)
@@ -2164,6 +2042,13 @@ extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
   if (k_flag < 0) return fail(c, LSBA_E_ARG, "k_flag < 0");
   c->force_flag_k = k_flag;
   c->forced_done = false;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_set_force_singular(lsba_ctx c, int32_t cycle) {
+  if (!c) return LSBA_E_ARG;
+  if (cycle < 0) return fail(c, LSBA_E_ARG, "cycle < 0");
+  c->force_sing_cycle = cycle;
   return LSBA_OK;
 }
 

@@ -1299,7 +1299,8 @@ k_irols_coef(SmallState2 st, const double* __restrict__ G, int k) {
 template <int B>
 __global__ void __launch_bounds__(512)
 k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double* __restrict__ Y,
-            double* __restrict__ Z, int* __restrict__ info, int stage_r) {
+            double* __restrict__ Z, int* __restrict__ info, int stage_r,
+            const int* __restrict__ prior, int force_sing) {
   extern __shared__ double Xi[];             // kb x B, column-major (ld kb) [+ kb x kb R copy]
   __shared__ double Tb[B * B], HtH[B * B], cosC[B * B];
   __shared__ int sing_s;
@@ -1309,11 +1310,13 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
   if (tid == 0) sing_s = 0;
   if (update_cacc == 2) {
     // speculative cycle end, enqueued before the host has read the cycle's status: it runs
-    // only if the cycle ended at k = m (why 4) with k accepted steps; otherwise it marks itself
-    // skipped (info[2]) and raises the guard (info[0]) so that its combine no-ops
+    // only if the cycle ended at k = m (why 4) with k accepted steps and the previous cycle
+    // end was not singular (prior guard: that combine no-op'd, so this cycle ran on stale
+    // data and the host will end the solve as DEAD); otherwise it marks itself skipped
+    // (info[2]) and raises the guard (info[0]) so that its combine no-ops
     __shared__ int skip_s;
     if (tid == 0) {
-      skip_s = (st.ctl->why == 4 && st.ctl->k_used == k) ? 0 : 1;
+      skip_s = (st.ctl->why == 4 && st.ctl->k_used == k && !(prior && *prior)) ? 0 : 1;
       info[2] = skip_s;
       if (skip_s) info[0] = 1;
     }
@@ -1491,8 +1494,9 @@ k_cycle_end(SmallState2 st, int k, int gmres, int happy, int update_cacc, double
     for (int q = 0; q < B; ++q) t += Xi[(kb - B + x) + (size_t)q * kb] * st.Cacc[q + y * B];
     cosC[e] = t;
   }
+  if (tid == 0 && force_sing) sing_s = 1;     // test hook (lsba_set_force_singular)
   __syncthreads();
-  if (update_cacc)
+  if (update_cacc && !sing_s)                 // a singular cycle end leaves C_acc as it was
     for (int e = tid; e < B * B; e += nt) st.Cacc[e] = cosC[e];
   if (tid == 0) info[0] = sing_s;
 }

@@ -39,7 +39,8 @@ cudaError_t launch_step_update<LSBA_B>(const SmallState2& st, const double* G, i
 
 template <>
 cudaError_t launch_cycle_end<LSBA_B>(const SmallState2& st, int k, int gmres, int happy, int upd,
-                                     double* Y, double* Z, int* info, cudaStream_t stream) {
+                                     double* Y, double* Z, int* info, const int* prior, int force_sing,
+                                     cudaStream_t stream) {
   constexpr int B = LSBA_B;
   const size_t kb = (size_t)k * B;
   size_t smem = sizeof(double) * kb * B;
@@ -50,7 +51,8 @@ cudaError_t launch_cycle_end<LSBA_B>(const SmallState2& st, int k, int gmres, in
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  fn<<<1, 32 * (B > 8 ? B : 8), smem, stream>>>(st, k, gmres, happy, upd, Y, Z, info, stage_r);
+  fn<<<1, 32 * (B > 8 ? B : 8), smem, stream>>>(st, k, gmres, happy, upd, Y, Z, info, stage_r, prior,
+                                                 force_sing);
   return cudaGetLastError();
 }
 

@@ -14,9 +14,7 @@ SWITCHES = [
     {"LSBA_PDL_PROJ": "0"},
     {"LSBA_L2PERSIST": "0"},
     {"LSBA_L2PERSIST": "1"},
-    {"LSBA_L2HINT": "0"},
     {"LSBA_NO_FUSE": "1"},
-    {"LSBA_OVL": "3"},
     {"LSBA_UPD_MAIN": "1"},
     {"LSBA_G7": "2"},
     {"LSBA_SPEC_END": "0"},
@@ -69,3 +67,40 @@ def test_switch_keeps_results(L, env):
         assert rel <= p.tol * (1 + 1e-6)
     assert abs(i1.cycles - i0.cycles) <= 1
     assert np.linalg.norm(H1 - H0) <= 1e-12 * np.linalg.norm(H0)
+
+
+def _run_forced(L, env, p, max_restarts, sing_cycle):
+    import torch
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        with L.Context(p.n, p.s, p.m, p.row_ptr, p.col_idx, p.vals) as ctx:
+            L.lsba_set_force_singular(ctx.ctx, sing_cycle)
+            B = torch.from_numpy(p.B).cuda()
+            X = torch.zeros_like(B)
+            info = ctx.solve(B, X, p.m, p.tol, max_restarts)
+            return X.cpu().numpy(), info
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("spec", ["0", "1"])
+@pytest.mark.parametrize("sing_cycle,max_restarts", [(2, 50), (2, 1), (3, 50)])
+def test_singular_cycle_end_keeps_last_good_x(L, spec, sing_cycle, max_restarts):
+    """A singular cycle-end projected solve (forced) ends the solve DEAD with the X of the
+    cycle before it, whether or not the next cycle's end was enqueued speculatively
+    (LSBA_SPEC_END): the speculative end checks the pending guard and no-ops."""
+    from lsba_inputs import make_twin
+    p = make_twin(2)                          # 2D Laplacian 64^2, s = 4, m = 20: ~33 cycles to m
+    Xref, iref = _run_forced(L, {"LSBA_SPEC_END": spec}, p, sing_cycle - 2, 0)   # cycles 1..c-1
+    assert iref.outcome == L.LSBA_MAX_RESTARTS and iref.cycles == sing_cycle - 1
+    X, info = _run_forced(L, {"LSBA_SPEC_END": spec}, p, max_restarts, sing_cycle)
+    assert info.outcome == L.LSBA_DEAD
+    assert info.cycles == sing_cycle - 1
+    assert np.all(np.isfinite(X))
+    assert np.array_equal(X, Xref)            # bitwise: the same deterministic kernels
+    assert info.true_relres == pytest.approx(iref.true_relres, rel=1e-12)

@@ -36,7 +36,7 @@ def main():
             us = 1e3 * e0.elapsed_time(e1) / args.reps
             print(f"config {cfg} ({p.name}, n={p.n}, s={p.s}): levels L {nlL} U {nlU}: "
                   f"{us:.0f} us per apply, {us / (nlL + nlU):.2f} us per level "
-                  f"(env LSBA_ILU_VARIANT={os.environ.get('LSBA_ILU_VARIANT', 'default')}, "
+                  f"("
                   f"LSBA_ILU_CTAS={os.environ.get('LSBA_ILU_CTAS', '1')})", flush=True)
         torch.cuda.empty_cache()
 
