@@ -185,6 +185,19 @@ lsba_status lsba_spmm(lsba_ctx ctx, const double* V_dev, double* W_dev);
  * includes the allreduce.  G_host receives the result. */
 lsba_status lsba_block_inner_product(lsba_ctx ctx, const double* V_dev, int32_t nblocks,
                                      const double* Y_dev, lsba_ip ip, double* G_host);
+/* Basis-slot access for kernel-level parity of the shipped streaming Gram (Alg 3 line 4,
+ * PAPER.md:268-269; Alg 6 line 10).  The basis owns m_max + 2 slots V_1..V_{m_max+2}
+ * (1-based as in lsba_copy_basis_block).
+ * lsba_set_basis_block: copy a caller device block (n_local x s, row-major) into slot V_j; it
+ *   invalidates the step API's Arnoldi state (the next step needs lsba_arnoldi_begin).
+ * lsba_basis_inner_product: G = <[V_{j0} .. V_{j0+nblocks-1}], Y> over slots with the kernels
+ *   the solver runs (k_gram_v7 / k_gram_gl2; no small step fused), including the allreduce.
+ *   Y = V_{y}; if y2 > 0, Y = [V_y V_{y2}] (the two-block Gram of BMGS-(I)CWY).  Classical:
+ *   (nblocks s) x (s or 2s) row-major; global: nblocks scalars (1/s) tr(V^T Y) (or nblocks
+ *   pairs).  LSBA_E_ARG for slots outside [1, m_max + 2] or j0 + nblocks - 1 > m_max + 2. */
+lsba_status lsba_set_basis_block(lsba_ctx ctx, int32_t j, const double* src_dev);
+lsba_status lsba_basis_inner_product(lsba_ctx ctx, int32_t j0, int32_t nblocks, int32_t y, int32_t y2,
+                                     lsba_ip ip, double* G_host);
 
 /* ---------------------------------------------------------------- debug / measurement */
 

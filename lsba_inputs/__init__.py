@@ -13,6 +13,8 @@ from .generators import (  # noqa: F401
     make_twin,
     random_sparse,
     rhs,
+    sample_rows,
+    sketch_chunks,
     stencil,
     tridiag,
     tridiag_rhs,

@@ -195,6 +195,23 @@ def rhs(n: int, s: int, seed: int = 0):
     return np.random.default_rng(seed).standard_normal((n, s))
 
 
+def sketch_chunks(n: int, width: int = 8, seed: int = 11, chunk: int = 1 << 20):
+    """Seeded Gaussian test matrix R (n x width, N(0,1) entries), yielded in row chunks
+    (r0, r1, R[r0:r1]) so that it is never held whole at n = 2^24.  Chunk c is drawn from
+    default_rng([seed, c]).  (A random input for full-size checks: E||R^T D||_F^2 =
+    width ||D||_F^2 for any n x s matrix D.)"""
+    for c, r0 in enumerate(range(0, n, chunk)):
+        r1 = min(n, r0 + chunk)
+        yield r0, r1, np.random.default_rng([seed, c]).standard_normal((r1 - r0, width))
+
+
+def sample_rows(n: int, count: int = 1024, seed: int = 5) -> np.ndarray:
+    """Seeded sorted sample of distinct row indices, always including the first and last row."""
+    rng = np.random.default_rng(seed)
+    rows = rng.choice(n, size=min(count, n), replace=False) if n > count else np.arange(n)
+    return np.unique(np.concatenate([[0, n - 1], rows])).astype(np.int64)
+
+
 def csr_sha256(row_ptr, col_idx, vals) -> str:
     h = hashlib.sha256()
     for a in (row_ptr, col_idx, vals):

@@ -67,6 +67,8 @@ _sigs = {
     "lsba_block_inner_product": [_vp, _vp, _i32, _vp, C.c_int, _vp],
     "lsba_set_force_flag": [_vp, _i32],
     "lsba_set_force_singular": [_vp, _i32],
+    "lsba_set_basis_block": [_vp, _i32, _vp],
+    "lsba_basis_inner_product": [_vp, _i32, _i32, _i32, _i32, _i32, _vp],
     "lsba_set_kernel_variant": [_vp, _i32],
     "lsba_set_skeleton": [_vp, C.c_int],
     "lsba_profile_enable": [_vp, _i32],
@@ -251,6 +253,25 @@ def lsba_copy_ilu0_factors(ctx, nnz):
 
 def lsba_set_force_flag(ctx, k):
     _check(lib.lsba_set_force_flag(ctx, int(k)), ctx)
+
+
+def lsba_set_basis_block(ctx, j, src):
+    _check(lib.lsba_set_basis_block(ctx, int(j), _dptr(src, "src")), ctx)
+
+
+def lsba_basis_inner_product(ctx, j0, nblocks, y, y2=0, ip="cl", s=None):
+    """<[V_j0 .. V_{j0+nblocks-1}], V_y (, V_y2)> over basis slots by the shipped Gram kernels.
+    Classical: (nblocks s) x (s or 2s); global: (nblocks,) or (nblocks, 2)."""
+    ipc = _IP[ip]
+    if s is None:
+        raise ValueError("s is required")
+    w = 2 if y2 else 1
+    E = nblocks * (1 if ipc == LSBA_IP_GLOBAL else s * s) * w
+    G = np.zeros(E)
+    _check(lib.lsba_basis_inner_product(ctx, int(j0), int(nblocks), int(y), int(y2), ipc, _hptr(G)), ctx)
+    if ipc == LSBA_IP_GLOBAL:
+        return G.reshape(nblocks, w) if w == 2 else G
+    return G.reshape(nblocks * s, w * s)
 
 
 def lsba_set_force_singular(ctx, cycle):

@@ -2037,6 +2037,38 @@ extern "C" lsba_status lsba_block_inner_product(lsba_ctx c, const double* V_dev,
   return LSBA_OK;
 }
 
+extern "C" lsba_status lsba_set_basis_block(lsba_ctx c, int32_t j, const double* src_dev) {
+  if (!c) return LSBA_E_ARG;
+  if (j < 1 || j > c->m_max + 2) return fail(c, LSBA_E_ARG, "j outside [1, m_max+2]");
+  if ((uintptr_t)src_dev & 15) return fail(c, LSBA_E_ARG, "not 16-byte aligned");
+  c->k = -1;                          // the step API's Arnoldi process is no longer valid
+  if (c->n == 0) return LSBA_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(slotp(c, j - 1), src_dev, sizeof(double) * c->slot, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_basis_inner_product(lsba_ctx c, int32_t j0, int32_t nblocks, int32_t y,
+                                                int32_t y2, lsba_ip ip, double* G_host) {
+  if (!c || !G_host) return LSBA_E_ARG;
+  const int top = c->m_max + 2;
+  if (nblocks < 1 || j0 < 1 || j0 + nblocks - 1 > top || y < 1 || y > top || y2 < 0 || y2 > top)
+    return fail(c, LSBA_E_ARG, "basis slots outside [1, m_max+2]");
+  if (ip != LSBA_IP_CLASSICAL && ip != LSBA_IP_GLOBAL) return fail(c, LSBA_E_ARG, "bad inner product");
+  CK(cudaSetDevice(c->device));
+  set_ip(c, ip);
+  c->k = -1;
+  c->d_G = c->d_Gbase;
+  const double* X = slotp(c, j0 - 1);
+  if (y2 > 0) TRY(gram2(c, X, c->slot_stride, nblocks, slotp(c, y - 1), slotp(c, y2 - 1), ip, nullptr));
+  else TRY(gram(c, X, c->slot_stride, nblocks, slotp(c, y - 1), ip));
+  const size_t E = ((ip == LSBA_IP_GLOBAL) ? (size_t)nblocks : (size_t)nblocks * c->s * c->s) * (y2 > 0 ? 2 : 1);
+  CK(cudaMemcpyAsync(G_host, c->d_G, sizeof(double) * E, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LSBA_OK;
+}
+
 extern "C" lsba_status lsba_set_force_flag(lsba_ctx c, int32_t k_flag) {
   if (!c) return LSBA_E_ARG;
   if (k_flag < 0) return fail(c, LSBA_E_ARG, "k_flag < 0");

@@ -178,3 +178,29 @@ def test_intra_ortho_scaling_quotient(ip):
         assert math.isclose(beta, np.linalg.norm(X) / math.sqrt(5), rel_tol=1e-15)
         assert math.isclose(O.ip_gl([Q], Q)[0], 1.0, rel_tol=1e-14)
     assert O.io_cl(np.zeros((10, 2)))[2] and O.io_gl(np.zeros((10, 2)))[2]
+
+
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+@pytest.mark.parametrize("c", [0.0, 1e-9, 0.3, -0.45, 0.9])
+def test_loss_of_orthogonality_closed_form(ip, c):
+    """Eq loo, ||I - <Q,Q>||_2, on bases with a prescribed Gram matrix.
+    (a) two blocks V_1 (orthonormal) and V_2 = V_1 cos(t) + P sin(t), P orthonormal and
+        orthogonal to V_1: <Q,Q> = [[I, c I], [c I, I]], so LOO = |c|, c = cos(t);
+    (b) three blocks with pairwise block inner product c I: <Q,Q> = ((1-c) I + c 1 1^T) (x) I_s,
+        I - <Q,Q> = -c (1 1^T - I) (x) I_s with eigenvalues -2c and c: LOO = 2|c|;
+    (c) one block scaled by a: LOO = |1 - a^2|.
+    Both inner products give the same value (global: (1/s) tr of each s x s block)."""
+    n, s = 400, 3
+    rng = np.random.default_rng(17)
+    U, _ = np.linalg.qr(rng.standard_normal((n, 4 * s)))
+    blk = [U[:, i * s:(i + 1) * s] for i in range(4)]
+    t = math.acos(c)
+    V2 = blk[0] * c + blk[1] * math.sin(t)
+    assert math.isclose(O.loss_of_orthogonality([blk[0], V2], ip), abs(c), rel_tol=1e-10, abs_tol=1e-14)
+    Gt = (1 - c) * np.eye(3) + c * np.ones((3, 3))
+    Lc = np.linalg.cholesky(Gt)                         # Gt = Lc Lc^T
+    Vs = [sum(blk[q] * Lc[i, q] for q in range(3)) for i in range(3)]   # <V_i, V_j> = Gt_ij I
+    assert math.isclose(O.loss_of_orthogonality(Vs, ip), 2 * abs(c), rel_tol=1e-10, abs_tol=1e-14)
+    a = 1.0 + c / 3
+    assert math.isclose(O.loss_of_orthogonality([a * blk[2]], ip), abs(1 - a * a), rel_tol=1e-10,
+                        abs_tol=1e-14)
