@@ -148,31 +148,59 @@ __device__ __forceinline__ double warp_sum(double x) {
 // a1: SpMM  W = A V   (and the residual variant R = B - A X with ||R||^2 partials)
 // L lanes per row; lane l owns columns {2l, 2l+1} (S >= 2) -> coalesced 16-byte accesses.
 // Summation over a row's nonzeros runs in CSR order (same order as the oracle).
+//
+// The kernel is latency-bound (one dependent index -> gather -> FMA chain per entry, few bytes
+// in flight per warp), so thread 0 of every CTA issues bulk L2 prefetches
+// (cp.async.bulk.prefetch.L2) for the CTA launched pf_dist CTAs later: its column indices and
+// values, its own V rows (pf_v) and, one distance further, its row pointers.  When that CTA
+// runs, its matrix stream comes from L2 (standalone, config 5: 884 -> 687 us, config 3: 117 ->
+// 93 us; tools/spmm_tile_bench.cu, profiles/r02_spmm_prefetch_raw.txt).
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, long bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  for (uintptr_t q = a; q < e; q += 65536) {
+    const unsigned sz = (unsigned)((e - q) < 65536 ? (e - q) : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(q), "r"(sz) : "memory");
+  }
+}
+
 template <int S, bool RESID>
 __global__ void __launch_bounds__(kThreads)
 k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ va, const double* __restrict__ V,
        const double* __restrict__ Vghost, const double* __restrict__ Bm,
-       double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr) {
+       double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr,
+       int pf_dist = 0, int pf_v = 0) {
   pdl_begin();
   if (active && *active == 0) return;
   constexpr int L = (S >= 2) ? S / 2 : 1;
   constexpr int C = (S >= 2) ? 2 : 1;  // columns per lane
+  constexpr int RPC = kThreads / L;    // rows per CTA
+  if (pf_dist > 0 && threadIdx.x == 0) {
+    const long r0 = (long)(blockIdx.x + pf_dist) * RPC;
+    if (r0 < n) {
+      const long r1 = r0 + RPC < n ? r0 + RPC : n;
+      const int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
+      bulk_prefetch_l2(ci + q0, 4L * (q1 - q0));
+      bulk_prefetch_l2(va + q0, 8L * (q1 - q0));
+      if (pf_v) bulk_prefetch_l2(V + r0 * S, 8L * S * (r1 - r0));
+      const long r2 = (long)(blockIdx.x + 2L * pf_dist) * RPC;
+      if (r2 < n) bulk_prefetch_l2(rp + r2, 4L * ((r2 + RPC < n ? r2 + RPC : n) - r2 + 1));
+    }
+  }
   const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / L);
   const int lane = (int)(gt % L);
   double sq = 0.0;
-  const uint64_t apol = l2pol(c_l2hint & 1, true);
   // row pointers: for L >= 2 one coalesced load of the warp's 32/L + 1 pointers, then shuffles
-  // (instead of 2 L redundant dependent loads per row; +4-7% on the stencil configs,
-  // tools/spmm_bench.cu)
+  // (instead of 2 L redundant dependent loads per row; +4-7% on the stencil configs)
   int p0, p1;
   if constexpr (L >= 2) {
     const int lane32 = threadIdx.x & 31;
     const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
     const int rr = row_w + lane32;
-    const int pv = (lane32 <= 32 / L && rr <= n) ? ldh(rp + rr, apol) : 0;
+    const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
     p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
     p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
   } else {
@@ -182,8 +210,8 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   if (row < n) {
     double a0 = 0.0, a1 = 0.0;
     for (int p = p0; p < p1; ++p) {
-      const int c = ldh(ci + p, apol);
-      const double a = ldh(va + p, apol);
+      const int c = __ldg(ci + p);
+      const double a = __ldg(va + p);
       const double* src = (c < n) ? (V + (size_t)c * S) : (Vghost + (size_t)(c - n) * S);
       if constexpr (C == 2) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(src) + lane);

@@ -127,6 +127,8 @@ struct lsba_ctx_ {
   cudaEvent_t ev_status = nullptr;
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
   bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
+  int spmm_pf = -1;              // SpMM L2 prefetch distance in CTAs (-1: 4 x SMs; LSBA_SPMM_PF)
+  int spmm_pfv = 1;              // ... and of the CTA's V rows (LSBA_SPMM_PFV)
   int force_sing_cycle = 0;      // test hook: the cycle end of this cycle reports singular
   int cur_cycle = 0;
   size_t csr_bytes = 0;          // joint col_idx + vals allocation (d_va points into it)
@@ -353,7 +355,8 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
       c->in_spmm = true;
       const cudaError_t le = launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, n,
                   (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
-                  (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active);
+                  (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active,
+                  c->spmm_pf, c->spmm_pfv);
       c->in_spmm = false;
       CK(le);
     } else {
@@ -380,7 +383,8 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
       CK(cudaMemsetAsync(c->d_sq, 0, sizeof(double), c->stream));
     } else if constexpr (S % 2 == 0 || S == 1) {
       k_spmm<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
-                                                          c->d_ghost, Bm, out, c->d_sq, nullptr);
+                                                          c->d_ghost, Bm, out, c->d_sq, nullptr,
+                                                          c->spmm_pf, c->spmm_pfv);
     } else {
       k_spmm_odd<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
                                                               c->d_ghost, Bm, out, c->d_sq, nullptr);
@@ -1624,6 +1628,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess && sms > 0)
       c->n_sms = sms;
   }
+  if (c->spmm_pf < 0) c->spmm_pf = 4 * c->n_sms;
   // DMMA Gram: persistent grid of 2 CTAs per SM; partials [cta][E] and [group][E]
   c->gram_grid = 4 * c->n_sms;
   const size_t Emax = 2 * (size_t)(m_max + 2) * s * s;      // (k+1)s x 2s for BMGS-(I)CWY
@@ -1722,6 +1727,8 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_PDL_PROJ")) c->pdl_proj = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2PERSIST")) c->l2persist = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPEC_END")) c->spec_end = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_SPMM_PF")) c->spmm_pf = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_SPMM_PFV")) c->spmm_pfv = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
   if (n < s) return fail(c, LSBA_E_ARG, "n < s");

@@ -1,0 +1,327 @@
+// spmm_tile_bench.cu — standalone timing of warp-tiled SpMM candidates against the shipped
+// row-lane CSR kernel (dev tool; stencil shapes of configs 2, 3, 5 and the random config 4).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o build_tools/spmm_tile_bench tools/spmm_tile_bench.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+#include <random>
+#include <algorithm>
+#include "../paper_2208_09899_b200/csrc/kernels.cuh"
+
+using namespace lsba;
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1); } } while (0)
+
+// T: persistent warps walk tiles of RW = 32/L consecutive rows.  The tile's CSR segment (row
+// pointers, column indices, values) is loaded with coalesced loads into registers one tile
+// AHEAD (its DRAM latency overlaps the current tile's gathers), parked in a per-warp shared
+// buffer, and each lane group then issues up to RB gathers of its row at once; FMAs in CSR order.
+template <int S, int NE, int RB, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_spmm_tile(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+            const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 2, RW = 32 / L, CAP = 32 * NE;
+  __shared__ int s_ci[8][CAP];
+  __shared__ double s_va[8][CAP];
+  const int lane32 = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int grp = lane32 / L, lane = lane32 % L;
+  const int ntiles = (n + RW - 1) / RW;
+  const int gw = blockIdx.x * 8 + wib, nw = gridDim.x * 8;
+  int cr[NE];
+  double vr[NE];
+  int pv = 0, seg0 = 0, seg1 = 0;
+  auto fetch = [&](int tile) {
+    const int r0 = tile * RW;
+    const int rr = r0 + lane32;
+    pv = (lane32 <= RW) ? __ldg(rp + min(rr, n)) : 0;
+    seg0 = __shfl_sync(0xffffffffu, pv, 0);
+    seg1 = __shfl_sync(0xffffffffu, pv, RW);
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      const int e = seg0 + q * 32 + lane32;
+      const bool ok = e < seg1;
+      cr[q] = ok ? __ldg(ci + e) : 0;
+      vr[q] = ok ? __ldg(va + e) : 0.0;
+    }
+  };
+  int tile = gw;
+  if (tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += nw) {
+    // park the current tile, start the next one's loads
+    const int cpv = pv, cs0 = seg0, cs1 = seg1;
+#pragma unroll
+    for (int q = 0; q < NE; ++q) { s_ci[wib][q * 32 + lane32] = cr[q]; s_va[wib][q * 32 + lane32] = vr[q]; }
+    __syncwarp();
+    if (tile + nw < ntiles) fetch(tile + nw);
+    const int row = tile * RW + grp;
+    const int p0 = __shfl_sync(0xffffffffu, cpv, grp), p1 = __shfl_sync(0xffffffffu, cpv, grp + 1);
+    if (row < n) {
+      double a0 = 0, a1 = 0;
+      const bool fits = (cs1 - cs0) <= CAP;
+      for (int p = p0; p < p1; p += RB) {
+        int c[RB]; double a[RB]; double2 v[RB];
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+          const bool ok = p + t < p1;
+          const int e = p + t - cs0;
+          c[t] = ok ? (fits ? s_ci[wib][e] : __ldg(ci + p + t)) : row;
+          a[t] = ok ? (fits ? s_va[wib][e] : __ldg(va + p + t)) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < RB; ++t) v[t] = __ldg(reinterpret_cast<const double2*>(V + (size_t)c[t] * S) + lane);
+#pragma unroll
+        for (int t = 0; t < RB; ++t) { a0 = fma(a[t], v[t].x, a0); a1 = fma(a[t], v[t].y, a1); }
+      }
+      reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
+    }
+    __syncwarp();
+  }
+}
+
+// R: non-persistent variant of T (one tile per warp, no lookahead): coalesced segment loads,
+// per-warp shared buffer, batched gathers.
+template <int S, int NE, int RB>
+__global__ void __launch_bounds__(256)
+k_spmm_tile1(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+             const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 2, RW = 32 / L, CAP = 32 * NE;
+  __shared__ int s_ci[8][CAP];
+  __shared__ double s_va[8][CAP];
+  const int lane32 = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int grp = lane32 / L, lane = lane32 % L;
+  const int tile = blockIdx.x * 8 + wib;
+  const int r0 = tile * RW;
+  if (r0 >= n) return;
+  const int pv = (lane32 <= RW) ? __ldg(rp + min(r0 + lane32, n)) : 0;
+  const int s0 = __shfl_sync(0xffffffffu, pv, 0), s1 = __shfl_sync(0xffffffffu, pv, RW);
+  const bool fits = (s1 - s0) <= CAP;
+  if (fits) {
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+      const int e = s0 + q * 32 + lane32;
+      if (e < s1) { s_ci[wib][q * 32 + lane32] = __ldg(ci + e); s_va[wib][q * 32 + lane32] = __ldg(va + e); }
+    }
+  }
+  __syncwarp();
+  const int row = r0 + grp;
+  const int p0 = __shfl_sync(0xffffffffu, pv, grp), p1 = __shfl_sync(0xffffffffu, pv, grp + 1);
+  if (row >= n) return;
+  double a0 = 0, a1 = 0;
+  for (int p = p0; p < p1; p += RB) {
+    int c[RB]; double a[RB]; double2 v[RB];
+#pragma unroll
+    for (int t = 0; t < RB; ++t) {
+      const bool ok = p + t < p1;
+      const int e = p + t - s0;
+      c[t] = ok ? (fits ? s_ci[wib][e] : __ldg(ci + p + t)) : row;
+      a[t] = ok ? (fits ? s_va[wib][e] : __ldg(va + p + t)) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < RB; ++t) v[t] = __ldg(reinterpret_cast<const double2*>(V + (size_t)c[t] * S) + lane);
+#pragma unroll
+    for (int t = 0; t < RB; ++t) { a0 = fma(a[t], v[t].x, a0); a1 = fma(a[t], v[t].y, a1); }
+  }
+  reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
+}
+
+// X: lane-split row: the L lanes of a row group split the row's CSR loads (lane l loads entries
+// l, l + L, ...) and exchange them by width-L shuffles; then all gathers of the batch at once.
+template <int S, int RB>
+__global__ void __launch_bounds__(256)
+k_spmm_split(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+             const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 2, PL = (RB + L - 1) / L;
+  const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / L), lane = (int)(gt % L);
+  const int lane32 = threadIdx.x & 31;
+  const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
+  const int rr = row_w + lane32;
+  const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+  const int me = lane32 / L;
+  int p0 = __shfl_sync(0xffffffffu, pv, me), p1 = __shfl_sync(0xffffffffu, pv, me + 1);
+  if (row >= n) { p0 = p1 = 0; }
+  // uniform trip count over the warp (shuffles need every lane)
+  int len = p1 - p0, mx = len;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double a0 = 0, a1 = 0;
+  for (int t0 = 0; t0 < mx; t0 += RB) {
+    int cm[PL]; double am[PL];
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int t = t0 + q * L + lane;
+      const bool ok = t < len;
+      cm[q] = ok ? __ldg(ci + p0 + t) : 0;
+      am[q] = ok ? __ldg(va + p0 + t) : 0.0;
+    }
+    int c[RB]; double a[RB]; double2 v[RB];
+#pragma unroll
+    for (int t = 0; t < RB; ++t) {
+      c[t] = __shfl_sync(0xffffffffu, cm[t / L], t % L, L);
+      a[t] = __shfl_sync(0xffffffffu, am[t / L], t % L, L);
+    }
+#pragma unroll
+    for (int t = 0; t < RB; ++t) {
+      const bool ok = t0 + t < len;
+      v[t] = ok ? __ldg(reinterpret_cast<const double2*>(V + (size_t)c[t] * S) + lane) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int t = 0; t < RB; ++t) { a0 = fma(a[t], v[t].x, a0); a1 = fma(a[t], v[t].y, a1); }
+  }
+  if (row < n) reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
+}
+
+// P: the shipped row-lane kernel plus an L2 bulk prefetch AHEAD: thread 0 of each CTA issues
+// cp.async.bulk.prefetch.L2 for the CSR segment (column indices and values) of CTA blockIdx + D
+// (PFV: and its V rows), so that the CTA resident D launches later finds its matrix in L2.
+__device__ __forceinline__ void bulk_pf(const void* p, long bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  for (uintptr_t q = a; q < e; q += 65536) {
+    const unsigned sz = (unsigned)min((uintptr_t)65536, e - q);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(q), "r"(sz) : "memory");
+  }
+}
+__device__ __forceinline__ int ld256_i(const int* p) {
+  int v; asm volatile("ld.global.nc.L2::256B.b32 %0, [%1];" : "=r"(v) : "l"(p)); return v;
+}
+__device__ __forceinline__ double ld256_d(const double* p) {
+  double v; asm volatile("ld.global.nc.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p)); return v;
+}
+template <int S, bool PFV, bool P256>
+__global__ void __launch_bounds__(256)
+k_spmm_pfa(int n, int D, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+           const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 2, RPC = 256 / L;
+  if (threadIdx.x == 0 && D > 0) {
+    const long r0 = (long)(blockIdx.x + D) * RPC;
+    if (r0 < n) {
+      const long r1 = min((long)n, r0 + RPC);
+      const int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
+      bulk_pf(ci + q0, 4L * (q1 - q0));
+      bulk_pf(va + q0, 8L * (q1 - q0));
+      if (PFV) bulk_pf(V + r0 * S, 8L * S * (r1 - r0));
+      const long r2 = (long)(blockIdx.x + 2 * D) * RPC;     // the row pointers one distance further
+      if (r2 < n) bulk_pf(rp + r2, 4L * (min((long)n, r2 + RPC) - r2 + 1));
+    }
+  }
+  const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / L), lane = (int)(gt % L);
+  const int lane32 = threadIdx.x & 31;
+  const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
+  const int rr = row_w + lane32;
+  const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+  const int me = lane32 / L;
+  const int p0 = __shfl_sync(0xffffffffu, pv, me), p1 = __shfl_sync(0xffffffffu, pv, me + 1);
+  if (row >= n) return;
+  double a0 = 0, a1 = 0;
+  for (int p = p0; p < p1; ++p) {
+    const int c = P256 ? ld256_i(ci + p) : __ldg(ci + p);
+    const double a = P256 ? ld256_d(va + p) : __ldg(va + p);
+    const double2 v = __ldg(reinterpret_cast<const double2*>(V + (size_t)c * S) + lane);
+    a0 = fma(a, v.x, a0); a1 = fma(a, v.y, a1);
+  }
+  reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
+}
+
+template <typename F>
+static double time_it(F launch) {
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  launch(); CK(cudaDeviceSynchronize());
+  cudaEventRecord(a);
+  for (int r = 0; r < 20; ++r) launch();
+  cudaEventRecord(b); CK(cudaEventSynchronize(b));
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  return 1e3 * ms / 20;
+}
+
+template <int S>
+static void run(int dims, int N, bool random_cfg4 = false) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  long n = 1;
+  std::vector<int> rp, ci; std::vector<double> va;
+  if (!random_cfg4) {
+    for (int d = 0; d < dims; ++d) n *= N;
+    rp.resize(n + 1);
+    ci.reserve(n * (2 * dims + 1)); va.reserve(n * (2 * dims + 1));
+    long stride[3] = {1, N, (long)N * N};
+    for (long i = 0; i < n; ++i) {
+      rp[i] = (int)ci.size();
+      long coord[3] = {i % N, (i / N) % N, i / ((long)N * N)};
+      for (int d = dims - 1; d >= 0; --d) if (coord[d] > 0) { ci.push_back((int)(i - stride[d])); va.push_back(-1.0); }
+      ci.push_back((int)i); va.push_back(2.0 * dims);
+      for (int d = 0; d < dims; ++d) if (coord[d] < N - 1) { ci.push_back((int)(i + stride[d])); va.push_back(-1.0); }
+    }
+    rp[n] = (int)ci.size();
+  } else {      // config-4 shape: 16 per row, 8 in a +-64 band, 8 uniform (a quick stand-in)
+    n = 1L << 22;
+    rp.resize(n + 1);
+    std::mt19937_64 g(1);
+    for (long i = 0; i < n; ++i) {
+      rp[i] = (int)ci.size();
+      std::vector<int> c;
+      c.push_back((int)i);
+      while (c.size() < 8) { long j = (long)i + (long)(g() % 129) - 64; if (j >= 0 && j < n && std::find(c.begin(), c.end(), (int)j) == c.end()) c.push_back((int)j); }
+      while (c.size() < 16) { int j = (int)(g() % n); if (std::find(c.begin(), c.end(), j) == c.end()) c.push_back(j); }
+      std::sort(c.begin(), c.end());
+      for (int j : c) { ci.push_back(j); va.push_back(j == i ? 10.0 : 0.5); }
+    }
+    rp[n] = (int)ci.size();
+  }
+  const long nnz = ci.size();
+  int *drp, *dci; double *dva, *dV, *dW, *dW2;
+  CK(cudaMalloc(&drp, 4 * (n + 1))); CK(cudaMalloc(&dci, 4 * nnz)); CK(cudaMalloc(&dva, 8 * nnz));
+  CK(cudaMalloc(&dV, 8 * n * S)); CK(cudaMalloc(&dW, 8 * n * S)); CK(cudaMalloc(&dW2, 8 * n * S));
+  CK(cudaMemcpy(drp, rp.data(), 4 * (n + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dci, ci.data(), 4 * nnz, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dva, va.data(), 8 * nnz, cudaMemcpyHostToDevice));
+  std::vector<double> hv(n * S); for (long i = 0; i < n * S; ++i) hv[i] = std::sin(0.001 * i);
+  CK(cudaMemcpy(dV, hv.data(), 8 * n * S, cudaMemcpyHostToDevice));
+  const double bytes = 12.0 * nnz + 4.0 * (n + 1) + 16.0 * n * S;
+  constexpr int L = S / 2;
+  auto check = [&](const char* name, double us) {
+    std::vector<double> a(n * S), b(n * S);
+    CK(cudaMemcpy(a.data(), dW, 8 * n * S, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), dW2, 8 * n * S, cudaMemcpyDeviceToHost));
+    double md = 0; for (long i = 0; i < n * S; ++i) md = std::max(md, std::fabs(a[i] - b[i]));
+    printf("  %-16s %8.1f us %7.0f GB/s  maxdiff %.1e\n", name, us, bytes / us / 1e3, md);
+    CK(cudaMemset(dW, 0, 8 * n * S));
+  };
+  printf("%s n %ld s %d nnz %ld (%.0f MB)\n", random_cfg4 ? "random" : (dims == 2 ? "2D" : "3D"), n, S, nnz, bytes / 1e6);
+  const int gA = (int)((n * L + 255) / 256);
+  double us = time_it([&] { k_spmm<S, false><<<gA, 256>>>((int)n, drp, dci, dva, dV, nullptr, nullptr, dW, nullptr, nullptr); });
+  CK(cudaMemcpy(dW2, dW, 8 * n * S, cudaMemcpyDeviceToDevice));
+  check("current", us);
+  const int RW = 32 / L;
+  const int gT1 = (int)((n + RW * 8 - 1) / (RW * 8));
+#define T1(NE, RB) \
+  us = time_it([&] { k_spmm_tile1<S, NE, RB><<<gT1, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
+  check("tile1_" #NE "_" #RB, us);
+#define TP(NE, RB, MINB, G) \
+  us = time_it([&] { k_spmm_tile<S, NE, RB, MINB><<<sms * G, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
+  check("tileP_" #NE "_" #RB "_" #MINB "x" #G, us);
+#define SP(RB) \
+  us = time_it([&] { k_spmm_split<S, RB><<<gA, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
+  check("split_" #RB, us);
+#define PA(PFV, P256, DD) \
+  us = time_it([&] { k_spmm_pfa<S, PFV, P256><<<gA, 256>>>((int)n, DD, drp, dci, dva, dV, dW); }); \
+  check("pfa_" #PFV "_" #P256 "_" #DD, us);
+  PA(false, false, 0) PA(false, true, 0) PA(false, false, 600) PA(false, false, 1200) PA(false, false, 2400)
+  PA(false, false, 4800) PA(true, false, 1200) PA(true, false, 2400) PA(false, true, 1200) PA(false, true, 2400)
+  PA(true, true, 2400)
+  T1(2, 4) TP(2, 8, 4, 4)
+#undef T1
+#undef TP
+#undef SP
+#undef PA
+  cudaFree(drp); cudaFree(dci); cudaFree(dva); cudaFree(dV); cudaFree(dW); cudaFree(dW2);
+}
+
+int main() {
+  run<4>(2, 1024);
+  run<8>(3, 128);
+  run<8>(3, 256);
+  run<16>(0, 0, true);
+  return 0;
+}
