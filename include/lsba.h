@@ -115,14 +115,35 @@ lsba_status lsba_get_unique_id(uint8_t id[128]);
  * nccl_id may be NULL iff nranks == 1.  cuda_stream is a cudaStream_t (NULL = legacy stream).
  * Device-wide side effect: on one rank, when the column indices and values fit in the device's
  * persisting-L2 set-aside (and in half of L2), the context sets cudaLimitPersistingL2CacheSize
- * to their size and marks them persisting on its SpMM launches; lsba_destroy resets the limit
- * to 0 (LSBA_L2PERSIST=0 in the environment disables this).
+ * to (at least) their size and marks them persisting on its SpMM launches; the limit is
+ * reference-counted per device and restored when the last such context is destroyed
+ * (LSBA_L2PERSIST=0 in the environment disables this).
  * Errors: LSBA_E_ARG on invalid sizes or CSR; LSBA_E_OOM; LSBA_E_CUDA; LSBA_E_NCCL. */
 lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
                         const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
                         int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
                         const uint8_t* nccl_id, int32_t device, void* cuda_stream);
 lsba_status lsba_destroy(lsba_ctx ctx);
+
+/* Distributed code path on ONE rank: with LSBA_FORCE_COMM=1 in the environment, lsba_create on
+ * nranks == 1 builds a one-rank NCCL communicator and runs exactly the P > 1 code path (every
+ * Gram through ncclAllReduce, the small step as its own launch, no speculative cycle end);
+ * results match the default path to rounding. */
+
+/* Loopback group (testing the multi-rank path on one device): P contexts, each driven by its
+ * own host thread, whose collectives (the Gram / norm allreduces, the halo send/recv and the
+ * create-time ghost-plan exchange) rendezvous on the host and move data with stream-ordered
+ * device copies and one rank-ordered reduction kernel — no kernel waits on another rank's
+ * kernel.  Not a performance path.  lsba_create_loopback is lsba_create with the group in place
+ * of the NCCL id; the group must outlive its contexts; every rank must make the same sequence
+ * of calls (as with NCCL).  nranks in [1, 16]. */
+typedef struct lsba_loopback_* lsba_loopback;
+lsba_status lsba_loopback_create(int32_t nranks, lsba_loopback* out);
+lsba_status lsba_loopback_destroy(lsba_loopback group);
+lsba_status lsba_create_loopback(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                                 const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                                 int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                                 lsba_loopback group, int32_t device, void* cuda_stream);
 
 const char* lsba_status_str(lsba_status st);
 const char* lsba_last_error(lsba_ctx ctx);   /* never NULL; "" if no error */

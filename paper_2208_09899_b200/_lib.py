@@ -54,6 +54,9 @@ _sigs = {
     "lsba_get_unique_id": [_vp],
     "lsba_create": [C.POINTER(_vp), _i64, _i32, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _i32, _vp],
     "lsba_destroy": [_vp],
+    "lsba_loopback_create": [_i32, C.POINTER(_vp)],
+    "lsba_loopback_destroy": [_vp],
+    "lsba_create_loopback": [C.POINTER(_vp), _i64, _i32, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _i32, _vp],
     "lsba_arnoldi_begin": [_vp, _vp, C.c_int, C.POINTER(_i32)],
     "lsba_block_arnoldi_step": [_vp, C.POINTER(StepInfo)],
     "lsba_copy_hessenberg": [_vp, _vp, _i32],
@@ -130,9 +133,27 @@ def lsba_get_unique_id() -> bytes:
     return bytes(buf)
 
 
+def lsba_loopback_create(nranks):
+    """A loopback group (P ranks as host threads on one device; testing only)."""
+    g = C.c_void_p()
+    _check(lib.lsba_loopback_create(int(nranks), C.byref(g)))
+    return g
+
+
+def lsba_loopback_destroy(group):
+    _check(lib.lsba_loopback_destroy(group))
+
+
+def lsba_create_loopback(n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks, group,
+                         device=0, stream=None):
+    return lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks,
+                       device=device, stream=stream, loopback=group)
+
+
 def lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin=0, row_end=None, rank=0, nranks=1,
-                nccl_id=None, device=0, stream=None):
-    """row_ptr/col_idx/vals: host numpy (int64 / int32 global cols / float64) for the local rows."""
+                nccl_id=None, device=0, stream=None, loopback=None):
+    """row_ptr/col_idx/vals: host numpy (int64 / int32 global cols / float64) for the local rows.
+    loopback: a group from lsba_loopback_create (then nccl_id is not used)."""
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
     col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
     vals = np.ascontiguousarray(vals, dtype=np.float64)
@@ -142,9 +163,14 @@ def lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin=0, row_end=None, 
     idbuf = None
     if nccl_id is not None:
         idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-    st = lib.lsba_create(C.byref(ctx), int(n), int(s), int(m_max), _hptr(row_ptr), _hptr(col_idx),
-                         _hptr(vals), int(row_begin), int(row_end), int(rank), int(nranks), idbuf,
-                         int(device), C.c_void_p(stream or 0))
+    if loopback is not None:
+        st = lib.lsba_create_loopback(C.byref(ctx), int(n), int(s), int(m_max), _hptr(row_ptr), _hptr(col_idx),
+                                      _hptr(vals), int(row_begin), int(row_end), int(rank), int(nranks),
+                                      loopback, int(device), C.c_void_p(stream or 0))
+    else:
+        st = lib.lsba_create(C.byref(ctx), int(n), int(s), int(m_max), _hptr(row_ptr), _hptr(col_idx),
+                             _hptr(vals), int(row_begin), int(row_end), int(rank), int(nranks), idbuf,
+                             int(device), C.c_void_p(stream or 0))
     if st != LSBA_OK:
         msg = lsba_last_error(ctx) if ctx else ""
         if ctx:
@@ -345,7 +371,7 @@ class Context:
     """RAII wrapper: one context (one rank's rows) on one device."""
 
     def __init__(self, n, s, m_max, row_ptr, col_idx, vals, row_begin=0, row_end=None, rank=0,
-                 nranks=1, nccl_id=None, device=None, stream=None):
+                 nranks=1, nccl_id=None, device=None, stream=None, loopback=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2208_09899_b200 needs a CUDA device (no CPU fallback)")
@@ -358,7 +384,7 @@ class Context:
         self.n_local = self.row_end - self.row_begin
         self.device = device
         self.ctx = lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin, self.row_end, rank,
-                               nranks, nccl_id, device, stream)
+                               nranks, nccl_id, device, stream, loopback)
 
     def close(self):
         if getattr(self, "ctx", None):

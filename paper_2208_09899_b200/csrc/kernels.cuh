@@ -165,32 +165,35 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, long bytes) {
   }
 }
 
+// Rows [row0, row1) of the n local rows (the halo overlap runs the interior rows while the
+// ghost rows are in flight, then the boundary rows); columns >= n address Vghost.
 template <int S, bool RESID>
 __global__ void __launch_bounds__(kThreads)
 k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ va, const double* __restrict__ V,
        const double* __restrict__ Vghost, const double* __restrict__ Bm,
        double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr,
-       int pf_dist = 0, int pf_v = 0) {
+       int pf_dist = 0, int pf_v = 0, int row0 = 0, int row1 = -1) {
   pdl_begin();
   if (active && *active == 0) return;
   constexpr int L = (S >= 2) ? S / 2 : 1;
   constexpr int C = (S >= 2) ? 2 : 1;  // columns per lane
   constexpr int RPC = kThreads / L;    // rows per CTA
+  if (row1 < 0) row1 = n;
   if (pf_dist > 0 && threadIdx.x == 0) {
-    const long r0 = (long)(blockIdx.x + pf_dist) * RPC;
-    if (r0 < n) {
-      const long r1 = r0 + RPC < n ? r0 + RPC : n;
+    const long r0 = row0 + (long)(blockIdx.x + pf_dist) * RPC;
+    if (r0 < row1) {
+      const long r1 = r0 + RPC < row1 ? r0 + RPC : row1;
       const int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
       bulk_prefetch_l2(ci + q0, 4L * (q1 - q0));
       bulk_prefetch_l2(va + q0, 8L * (q1 - q0));
       if (pf_v) bulk_prefetch_l2(V + r0 * S, 8L * S * (r1 - r0));
-      const long r2 = (long)(blockIdx.x + 2L * pf_dist) * RPC;
-      if (r2 < n) bulk_prefetch_l2(rp + r2, 4L * ((r2 + RPC < n ? r2 + RPC : n) - r2 + 1));
+      const long r2 = row0 + (long)(blockIdx.x + 2L * pf_dist) * RPC;
+      if (r2 < row1) bulk_prefetch_l2(rp + r2, 4L * ((r2 + RPC < row1 ? r2 + RPC : row1) - r2 + 1));
     }
   }
   const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = (int)(gt / L);
+  const int row = row0 + (int)(gt / L);
   const int lane = (int)(gt % L);
   double sq = 0.0;
   // row pointers: for L >= 2 one coalesced load of the warp's 32/L + 1 pointers, then shuffles
@@ -198,16 +201,16 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   int p0, p1;
   if constexpr (L >= 2) {
     const int lane32 = threadIdx.x & 31;
-    const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
+    const int row_w = row0 + (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
     const int rr = row_w + lane32;
-    const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+    const int pv = (lane32 <= 32 / L && rr <= row1) ? __ldg(rp + rr) : 0;
     p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
     p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
   } else {
-    p0 = (row < n) ? rp[row] : 0;
-    p1 = (row < n) ? rp[row + 1] : 0;
+    p0 = (row < row1) ? rp[row] : 0;
+    p1 = (row < row1) ? rp[row + 1] : 0;
   }
-  if (row < n) {
+  if (row < row1) {
     double a0 = 0.0, a1 = 0.0;
     for (int p = p0; p < p1; ++p) {
       const int c = __ldg(ci + p);
@@ -256,11 +259,13 @@ __global__ void __launch_bounds__(kThreads)
 k_spmm_odd(int n, const int* __restrict__ rp, const int* __restrict__ ci,
            const double* __restrict__ va, const double* __restrict__ V,
            const double* __restrict__ Vghost, const double* __restrict__ Bm,
-           double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr) {
+           double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr,
+           int row0 = 0, int row1 = -1) {
   if (active && *active == 0) return;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row1 < 0) row1 = n;
+  const int row = row0 + blockIdx.x * blockDim.x + threadIdx.x;
   double sq = 0.0;
-  if (row < n) {
+  if (row < row1) {
     double acc[S];
 #pragma unroll
     for (int t = 0; t < S; ++t) acc[t] = 0.0;

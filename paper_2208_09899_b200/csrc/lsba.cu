@@ -29,6 +29,7 @@
 #include "gram7.cuh"
 #include "ilu.cuh"
 #include "launch_small.h"
+#include "comm.h"
 
 using namespace lsba;
 
@@ -72,7 +73,7 @@ struct lsba_ctx_ {
   int* d_send_idx = nullptr;
   double* d_sendbuf = nullptr;
   int64_t n_send = 0;
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;            // collectives (NCCL, or the loopback test group); null on one rank
   // Gram
   double* d_part = nullptr;
   size_t part_cap = 0;
@@ -87,7 +88,7 @@ struct lsba_ctx_ {
   cudaStream_t stream2 = nullptr;  // update kernels run here, concurrent with the projection
   cudaEvent_t ev_coef = nullptr, ev_upd = nullptr;
   CycleCtl* h_ctl = nullptr;      // pinned copy
-  volatile int* h_prog = nullptr; // mapped pinned {k_done, active} (see publish_progress)
+  volatile int* h_prog = nullptr; // mapped pinned 2 k_done + active (see publish_progress)
   int n_sms = 148;
   // small state
   SmallState2 st{};
@@ -125,10 +126,15 @@ struct lsba_ctx_ {
   int ilu_levels[2] = {0, 0};
   int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
   cudaEvent_t ev_status = nullptr;
+  cudaStream_t cstream = nullptr;  // P > 1: halo exchange stream (overlaps the interior SpMM)
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+  int int0 = 0, int1 = 0;          // contiguous interior rows (no ghost columns); int1 > int0: overlap
+  bool halo_ovl = true;            // LSBA_HALO_OVERLAP
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
   bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
   int spmm_pf = -1;              // SpMM L2 prefetch distance in CTAs (-1: 4 x SMs; LSBA_SPMM_PF)
   int spmm_pfv = 1;              // ... and of the CTA's V rows (LSBA_SPMM_PFV)
+  bool force_comm = false;       // LSBA_FORCE_COMM=1: one rank through the distributed code path
   int force_sing_cycle = 0;      // test hook: the cycle end of this cycle reports singular
   int cur_cycle = 0;
   size_t csr_bytes = 0;          // joint col_idx + vals allocation (d_va points into it)
@@ -184,6 +190,12 @@ static lsba_status fail(lsba_ctx c, lsba_status st, const char* fmt, ...) {
     if (r_ != ncclSuccess)                                                                \
       return fail(c, LSBA_E_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,              \
                   ncclGetErrorString(r_));                                                \
+  } while (0)
+
+#define TRYC(call)                                                                        \
+  do {                                                                                    \
+    const int e_ = (call);                                                                \
+    if (e_) return fail(c, e_ == 2 ? LSBA_E_NCCL : LSBA_E_CUDA, "%s", c->comm->err.c_str()); \
   } while (0)
 
 #define TRY(x)                        \
@@ -255,9 +267,12 @@ static inline bool in_basis(lsba_ctx c, const double* p) {
 }
 
 // ---------------------------------------------------------------- halo exchange (P > 1)
+// Pack the rows peers need (main stream), then the grouped send/recv: on the main stream, or
+// on the comm stream when the SpMM overlaps it (ovl: the interior rows run meanwhile; the
+// caller joins ev_halo before the boundary rows).
 template <int S>
-static lsba_status halo_t(lsba_ctx c, const double* V) {
-  if (c->nranks == 1) return LSBA_OK;
+static lsba_status halo_t(lsba_ctx c, const double* V, bool ovl = false) {
+  if (!c->comm) return LSBA_OK;
   if (c->n_send > 0) {
     LaunchScope L(c, LSBA_K_HALO_PACK, 16.0 * c->n_send * S + 4.0 * c->n_send);
     const long tot = c->n_send * S;
@@ -265,17 +280,20 @@ static lsba_status halo_t(lsba_ctx c, const double* V) {
                                                                      c->d_sendbuf);
     CKL();
   }
-  CKN(ncclGroupStart());
+  std::vector<P2POp> ops;
   for (int r = 0; r < c->nranks; ++r) {
-    if (r == c->rank) continue;
-    if (c->send_cnt[r] > 0)
-      CKN(ncclSend(c->d_sendbuf + c->send_off[r] * S, (size_t)c->send_cnt[r] * S, ncclDouble, r,
-                   c->comm, c->stream));
-    if (c->recv_cnt[r] > 0)
-      CKN(ncclRecv(c->d_ghost + c->recv_off[r] * S, (size_t)c->recv_cnt[r] * S, ncclDouble, r,
-                   c->comm, c->stream));
+    if (r == c->rank || (c->send_cnt[r] == 0 && c->recv_cnt[r] == 0)) continue;
+    ops.push_back({r, c->d_sendbuf + c->send_off[r] * S, sizeof(double) * (size_t)c->send_cnt[r] * S,
+                   c->d_ghost + c->recv_off[r] * S, sizeof(double) * (size_t)c->recv_cnt[r] * S});
   }
-  CKN(ncclGroupEnd());
+  if (!ovl) {
+    TRYC(c->comm->exchange(ops, c->stream));
+    return LSBA_OK;
+  }
+  CK(cudaEventRecord(c->ev_pack, c->stream));
+  CK(cudaStreamWaitEvent(c->cstream, c->ev_pack, 0));
+  TRYC(c->comm->exchange(ops, c->cstream));
+  CK(cudaEventRecord(c->ev_halo, c->cstream));
   return LSBA_OK;
 }
 
@@ -345,25 +363,43 @@ static lsba_status ilu_apply(lsba_ctx c, double* Y, const int* active = nullptr)
 template <int S>
 static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* active) {
   const int n = c->n;
-  TRY(halo_t<S>(c, V));
+  // P > 1 with a contiguous interior block [int0, int1) (rows without ghost columns, e.g. all
+  // but the boundary planes of a z-slab): the halo moves on the comm stream while the interior
+  // rows compute; the boundary rows follow once it has arrived
+  const bool ovl = c->comm && c->halo_ovl && c->int1 > c->int0;
+  TRY(halo_t<S>(c, V, ovl));
   constexpr int L = (S % 2 == 0) ? S / 2 : 1;
-  const long threads = (long)n * L;
   {
     LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (n + 1) + 16.0 * n * S);
-    if (n == 0) return LSBA_OK;
-    if constexpr (S % 2 == 0 || S == 1) {
-      c->in_spmm = true;
-      const cudaError_t le = launch_k(c, k_spmm<S, false>, dim3(cdiv(threads, kThreads)), dim3(kThreads), 0, n,
-                  (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
-                  (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active,
-                  c->spmm_pf, c->spmm_pfv);
-      c->in_spmm = false;
-      CK(le);
-    } else {
-      k_spmm_odd<S, false><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(
-          n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active);
+    if (n == 0) {
+      if (ovl) CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+      return LSBA_OK;
     }
-    CKL();
+    auto rows = [&](int r0, int r1) -> lsba_status {
+      if (r1 <= r0) return LSBA_OK;
+      if constexpr (S % 2 == 0 || S == 1) {
+        c->in_spmm = true;
+        const cudaError_t le = launch_k(c, k_spmm<S, false>, dim3(cdiv((long)(r1 - r0) * L, kThreads)),
+                    dim3(kThreads), 0, n, (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
+                    (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active,
+                    c->spmm_pf, c->spmm_pfv, r0, r1);
+        c->in_spmm = false;
+        CK(le);
+      } else {
+        k_spmm_odd<S, false><<<cdiv(r1 - r0, kThreads), kThreads, 0, c->stream>>>(
+            n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active, r0, r1);
+      }
+      CKL();
+      return LSBA_OK;
+    };
+    if (!ovl) {
+      TRY(rows(0, n));
+    } else {
+      TRY(rows(c->int0, c->int1));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+      TRY(rows(0, c->int0));
+      TRY(rows(c->int1, n));
+    }
   }
   if (c->prec) TRY(ilu_apply_t<S>(c, W, active));
   return LSBA_OK;
@@ -402,8 +438,7 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
     k_sum_partials<<<1, kThreads, 0, c->stream>>>(c->n == 0 ? 1 : nblk, c->d_sq, c->d_scalar);
     CKL();
   }
-  if (c->nranks > 1)
-    CKN(ncclAllReduce(c->d_scalar, c->d_scalar, 1, ncclDouble, ncclSum, c->comm, c->stream));
+  if (c->comm) TRYC(c->comm->allreduce_sum_f64(c->d_scalar, 1, c->stream));
   return LSBA_OK;
 }
 
@@ -552,7 +587,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       GramFuse f{};
       // fuse the small step into the Gram tail on one rank (no allreduce in between) while its
       // Gram copy fits next to the partials (<= 64 KB of shared memory)
-      if (coef_k >= 0 && coef_fused && c->nranks == 1 && !c->no_fuse && E * sizeof(double) <= 64 * 1024) {
+      if (coef_k >= 0 && coef_fused && !c->comm && !c->no_fuse && E * sizeof(double) <= 64 * 1024) {
         f.on = 1;
         f.st = c->st;
         f.k = coef_k;
@@ -594,8 +629,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       CKL();
     }
   }
-  if (c->nranks > 1)
-    CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+  if (c->comm) TRYC(c->comm->allreduce_sum_f64(c->d_G, E, c->stream));
   return LSBA_OK;
 }
 
@@ -697,7 +731,7 @@ static lsba_status gram2_t(lsba_ctx c, const double* X, size_t xstride, int J, c
     }
   }
   if (done) {
-    if (c->nranks > 1) CKN(ncclAllReduce(c->d_G, c->d_G, E, ncclDouble, ncclSum, c->comm, c->stream));
+    if (c->comm) TRYC(c->comm->allreduce_sum_f64(c->d_G, E, c->stream));
     return LSBA_OK;
   }
   // fallback (odd s, DFMA variant, non-slot inputs): two block inner products (two syncs on
@@ -859,20 +893,22 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
 }
 
 // Host-side lookahead bound for the speculative enqueue of a cycle: step k is enqueued once
-// the device has decided step k - kLookahead (polling the mapped progress word).  Returns
-// false if the device already ended the cycle.
+// the device has decided step k - kLookahead (polling the mapped progress word 2 k + active).
+// Returns false once no more steps of this cycle are to be enqueued.
+//  * One rank: stop as soon as the device has ended the cycle (flag, convergence, kappa).
+//  * P > 1 ranks: every step carries a halo exchange and the Gram allreduce, so all ranks must
+//    enqueue the same steps.  The end step k_end is a replicated device decision (bitwise-equal
+//    allreduce results), and no host is ever more than kLookahead steps past the decided step,
+//    so every rank enqueues exactly steps 1 .. min(m, k_end + kLookahead) and stops there.
 constexpr int kLookahead = 3;
-// With P > 1 ranks every speculative step still contains its allreduce and halo exchange, and
-// the count of collectives must match across ranks, so there the host only paces (it never
-// stops early: which step a rank's host is at when its device ends the cycle is timing).
 static bool throttle(lsba_ctx c, int k) {
-  const bool may_stop = (c->nranks == 1);
-  if (k <= kLookahead) return !may_stop || c->h_prog[1] != 0 || c->h_prog[0] < 0;
+  const bool single = !c->comm;
   for (;;) {
-    const int done = c->h_prog[0], act = c->h_prog[1];
-    if (done >= 0 && act == 0) return !may_stop;
-    if (done >= k - kLookahead) return true;
-    if (cudaStreamQuery(c->stream) == cudaSuccess) return true;   // (device drained: no stall)
+    const int v = c->h_prog[0];
+    const int done = v < 0 ? -1 : (v >> 1), act = v < 0 ? 1 : (v & 1);
+    if (done >= 0 && act == 0) return single ? false : (k <= done + kLookahead);
+    if (k <= kLookahead || done >= k - kLookahead) return true;
+    if (single && cudaStreamQuery(c->stream) == cudaSuccess) return true;   // (device drained: no stall)
   }
 }
 
@@ -1102,8 +1138,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
       CK(cudaMemsetAsync(c->d_scalar, 0, sizeof(double), c->stream));
     }
   }
-  if (c->nranks > 1)
-    CKN(ncclAllReduce(c->d_scalar, c->d_scalar, 1, ncclDouble, ncclSum, c->comm, c->stream));
+  if (c->comm) TRYC(c->comm->allreduce_sum_f64(c->d_scalar, 1, c->stream));
   CK(cudaMemcpyAsync(c->h_scalar, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const double normB = std::sqrt(std::max(0.0, *c->h_scalar));
@@ -1134,7 +1169,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
           (long)c->slot, X, c->d_info);
       CKL();
     }
-    if (c->nranks > 1) CKN(ncclAllReduce(c->d_info, c->d_info, 1, ncclInt, ncclMax, c->comm, c->stream));
+    if (c->comm) TRYC(c->comm->allreduce_max_i32(c->d_info, 1, c->stream));
     CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (c->h_info[0]) {
@@ -1164,7 +1199,6 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     prm.tau = tau;                                           // R8
     prm.need_kappa = std::isfinite(tau) ? 1 : 0;
     c->h_prog[0] = -1;                                       // (device idle: cycle boundary)
-    c->h_prog[1] = 1;
     TRY(io_begin_async(c, prm));                             // [V_1, beta] = IO(U)
     if (lagged(c->skel))
       TRY(cwy_iter1_async(c));                               // Alg 6 iteration 1
@@ -1179,7 +1213,7 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     // status read, so the GPU solves the projected problem and combines while the host wakes
     // up; it no-ops on the device for any other ending, which the host then handles below
     const int par = cycle & 1;
-    const bool spec = c->spec_end && c->nranks == 1 && m_cur >= 1;
+    const bool spec = c->spec_end && !c->comm && m_cur >= 1;
     if (spec) {
       // the status is copied (and waited for) BEFORE the speculative kernels, so the host
       // decides while the GPU solves and combines, and enqueues the next cycle behind them
@@ -1464,13 +1498,17 @@ static void release(lsba_ctx c) {
   if (c->ev_upd) cudaEventDestroy(c->ev_upd);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->ev_status) cudaEventDestroy(c->ev_status);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
   for (int k = 0; k < LSBA_K_COUNT; ++k)
     for (auto& e : c->prof.ev[k]) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
-  if (c->comm) ncclCommDestroy(c->comm);
+  delete c->comm;
 }
 
 static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, const int64_t* row_ptr,
-                               const int32_t* col_idx, const double* vals, const uint8_t* nccl_id) {
+                               const int32_t* col_idx, const double* vals, const uint8_t* nccl_id,
+                               LoopGroup* loop) {
   const int64_t n_local = c->row_end - c->row_begin;
   if (n_local > INT32_MAX / 16) return fail(c, LSBA_E_ARG, "n_local too large");
   const char* msg = nullptr;
@@ -1480,7 +1518,23 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   if (c->nnz > INT32_MAX) return fail(c, LSBA_E_ARG, "local nnz exceeds int32");
   if (vals == nullptr && c->nnz > 0) return fail(c, LSBA_E_ARG, "vals is NULL");
   CK(cudaSetDevice(c->device));
-  // ---- NCCL communicator and ghost plan
+  // ---- communicator (NCCL across processes, the loopback test group, or a one-rank NCCL
+  // communicator when LSBA_FORCE_COMM=1 runs the distributed code path on one rank)
+  if (loop) {
+    auto* lc = new (std::nothrow) LoopComm(loop, c->rank);
+    if (!lc) return fail(c, LSBA_E_OOM, "comm");
+    c->comm = lc;
+    TRYC(lc->init());
+  } else if (c->nranks > 1 || c->force_comm) {
+    auto* nc = new (std::nothrow) NcclComm();
+    if (!nc) return fail(c, LSBA_E_OOM, "comm");
+    c->comm = nc;
+    ncclUniqueId uid;
+    if (nccl_id) std::memcpy(&uid, nccl_id, 128);
+    else CKN(ncclGetUniqueId(&uid));
+    TRYC(nc->init(uid, c->nranks, c->rank));
+  }
+  // ---- ghost plan
   std::vector<int32_t> col_local(c->nnz);
   std::vector<int64_t> ghost_global;
   c->send_cnt.assign(c->nranks, 0);
@@ -1491,15 +1545,12 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   if (c->nranks == 1) {
     for (int64_t p = 0; p < c->nnz; ++p) col_local[p] = col_idx[p];
   } else {
-    ncclUniqueId uid;
-    std::memcpy(&uid, nccl_id, 128);
-    CKN(ncclCommInitRank(&c->comm, c->nranks, uid, c->rank));
     // partition starts
     int64_t* d_tmp = nullptr;
     CK(cudaMalloc((void**)&d_tmp, sizeof(int64_t) * (2 * c->nranks + 2 * (size_t)c->nranks * c->nranks + 2)));
     int64_t mine[2] = {c->row_begin, c->row_end};
     CK(cudaMemcpy(d_tmp, mine, sizeof mine, cudaMemcpyHostToDevice));
-    CKN(ncclAllGather(d_tmp, d_tmp + 2, 2, ncclInt64, c->comm, c->stream));
+    TRYC(c->comm->allgather_i64(d_tmp, d_tmp + 2, 2, c->stream));
     std::vector<int64_t> rr(2 * c->nranks);
     CK(cudaMemcpyAsync(rr.data(), d_tmp + 2, sizeof(int64_t) * 2 * c->nranks, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1522,7 +1573,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     // everyone's recv counts -> my send counts
     int64_t* d_cnt = d_tmp + 2 * c->nranks + 2;
     CK(cudaMemcpy(d_cnt, c->recv_cnt.data(), sizeof(int64_t) * c->nranks, cudaMemcpyHostToDevice));
-    CKN(ncclAllGather(d_cnt, d_cnt + c->nranks, c->nranks, ncclInt64, c->comm, c->stream));
+    TRYC(c->comm->allgather_i64(d_cnt, d_cnt + c->nranks, c->nranks, c->stream));
     std::vector<int64_t> allc((size_t)c->nranks * c->nranks);
     CK(cudaMemcpyAsync(allc.data(), d_cnt + c->nranks, sizeof(int64_t) * allc.size(), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1541,13 +1592,13 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     CK(cudaMalloc((void**)&d_req, sizeof(int64_t) * std::max<int64_t>(ng, 1)));
     CK(cudaMalloc((void**)&d_want, sizeof(int64_t) * std::max<int64_t>(so, 1)));
     if (ng) CK(cudaMemcpy(d_req, ghost_global.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice));
-    CKN(ncclGroupStart());
+    std::vector<P2POp> ops;
     for (int r = 0; r < c->nranks; ++r) {
-      if (r == c->rank) continue;
-      if (c->recv_cnt[r] > 0) CKN(ncclSend(d_req + c->recv_off[r], c->recv_cnt[r], ncclInt64, r, c->comm, c->stream));
-      if (c->send_cnt[r] > 0) CKN(ncclRecv(d_want + c->send_off[r], c->send_cnt[r], ncclInt64, r, c->comm, c->stream));
+      if (r == c->rank || (c->recv_cnt[r] == 0 && c->send_cnt[r] == 0)) continue;
+      ops.push_back({r, d_req + c->recv_off[r], sizeof(int64_t) * (size_t)c->recv_cnt[r],
+                     d_want + c->send_off[r], sizeof(int64_t) * (size_t)c->send_cnt[r]});
     }
-    CKN(ncclGroupEnd());
+    TRYC(c->comm->exchange(ops, c->stream));
     send_idx.resize(std::max<int64_t>(so, 1));
     CK(cudaMemcpyAsync(send_idx.data(), d_want, sizeof(int64_t) * std::max<int64_t>(so, 1), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1557,6 +1608,19 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
       send_idx[i] -= c->row_begin;
       if (send_idx[i] < 0 || send_idx[i] >= n_local) return fail(c, LSBA_E_ARG, "peer requested a row this rank does not own");
     }
+    // the interior block: first and last row without ghost columns; used only if every row
+    // between them is ghost-free too (z-slabs of a stencil: all but the boundary planes)
+    auto ghost_row = [&](int64_t r) {
+      for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; ++p)
+        if (col_local[p] >= n_local) return true;
+      return false;
+    };
+    int64_t b0 = 0, b1 = n_local;
+    while (b0 < n_local && ghost_row(b0)) ++b0;
+    while (b1 > b0 && ghost_row(b1 - 1)) --b1;
+    bool clean = b1 - b0 >= 256;
+    for (int64_t r = b0; clean && r < b1; ++r) clean = !ghost_row(r);
+    if (clean) { c->int0 = (int)b0; c->int1 = (int)b1; }
   }
   // ---- device CSR
   std::vector<int32_t> rp32(n_local + 1);
@@ -1577,7 +1641,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     CK(cudaMemcpy(c->d_ci, col_local.data(), sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_va, vals, sizeof(double) * c->nnz, cudaMemcpyHostToDevice));
   }
-  if (c->l2persist != 0 && c->nnz > 0 && c->nranks == 1) {
+  if (c->l2persist != 0 && c->nnz > 0 && !c->comm) {
     // The SpMM's column indices and values (constant across the solve) are kept in an L2
     // set-aside when they fit: config 2 (63 MB) +4%; a CSR larger than the set-aside (config 3,
     // 175 MB) lost 3.5% (tools/l2persist_exp.sh), so "auto" requires it to fit in the set-aside
@@ -1590,7 +1654,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
                       c->csr_bytes <= (size_t)l2 / 2;
     if (c->l2persist < 0 && !fits) c->l2persist = 0;
   }
-  if (c->l2persist != 0 && c->nnz > 0 && c->nranks == 1) {
+  if (c->l2persist != 0 && c->nnz > 0 && !c->comm) {
     int max_win = 0, max_persist = 0;
     CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device));
     CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device));
@@ -1683,7 +1747,6 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   {  // progress word in mapped pinned host memory (written by the device, polled by the host)
     CK(cudaHostAlloc((void**)&c->h_prog, 2 * sizeof(int), cudaHostAllocMapped));
     c->h_prog[0] = -1;
-    c->h_prog[1] = 0;
     int* dp = nullptr;
     CK(cudaHostGetDevicePointer((void**)&dp, (void*)c->h_prog, 0));
     c->st.prog = dp;
@@ -1698,6 +1761,11 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   CK(cudaEventCreateWithFlags(&c->ev_coef, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_status, cudaEventDisableTiming));
+  if (c->comm) {
+    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+  }
   TRY(dalloc(c, &c->st.status, 1));
   TRY(dalloc(c, &c->st.flag_dev, 1));
   CK(cudaMemset(c->st.flag_dev, 0, sizeof(int)));
@@ -1711,10 +1779,10 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   return LSBA_OK;
 }
 
-extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
-                                   const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
-                                   int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
-                                   const uint8_t* nccl_id, int32_t device, void* cuda_stream) {
+static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                              const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                              int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                              const uint8_t* nccl_id, LoopGroup* loop, int32_t device, void* cuda_stream) {
   if (!out) return LSBA_E_ARG;
   *out = nullptr;
   lsba_ctx c = new (std::nothrow) lsba_ctx_();
@@ -1730,12 +1798,15 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   if (const char* e = std::getenv("LSBA_SPMM_PF")) c->spmm_pf = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPMM_PFV")) c->spmm_pfv = std::atoi(e);
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_HALO_OVERLAP")) c->halo_ovl = (e[0] == '1');
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
   if (n < s) return fail(c, LSBA_E_ARG, "n < s");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, LSBA_E_ARG, "bad rank/nranks");
   if (row_begin < 0 || row_end < row_begin || row_end > n) return fail(c, LSBA_E_ARG, "bad row range");
   if (nranks == 1 && (row_begin != 0 || row_end != n)) return fail(c, LSBA_E_ARG, "nranks == 1 needs rows [0, n)");
-  if (nranks > 1 && !nccl_id) return fail(c, LSBA_E_ARG, "nccl_id required when nranks > 1");
+  if (nranks > 1 && !nccl_id && !loop) return fail(c, LSBA_E_ARG, "nccl_id required when nranks > 1");
+  if (loop && loop->P != nranks) return fail(c, LSBA_E_ARG, "loopback group size != nranks");
   if (!row_ptr || (!col_idx && row_end > row_begin)) return fail(c, LSBA_E_ARG, "CSR arrays NULL");
   c->device = device;
   c->stream = (cudaStream_t)cuda_stream;
@@ -1747,7 +1818,40 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
   c->m_max = m_max;
   c->rank = rank;
   c->nranks = nranks;
-  return create_impl(c, n, s, m_max, row_ptr, col_idx, vals, nccl_id);
+  return create_impl(c, n, s, m_max, row_ptr, col_idx, vals, nccl_id, loop);
+}
+
+extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                                   const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                                   int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                                   const uint8_t* nccl_id, int32_t device, void* cuda_stream) {
+  return create_any(out, n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks, nccl_id,
+                    nullptr, device, cuda_stream);
+}
+
+struct lsba_loopback_ {
+  LoopGroup g;
+  explicit lsba_loopback_(int P) : g(P) {}
+};
+
+extern "C" lsba_status lsba_loopback_create(int32_t nranks, lsba_loopback* out) {
+  if (!out || nranks < 1 || nranks > kLoopMaxRanks) return LSBA_E_ARG;
+  *out = new (std::nothrow) lsba_loopback_(nranks);
+  return *out ? LSBA_OK : LSBA_E_OOM;
+}
+
+extern "C" lsba_status lsba_loopback_destroy(lsba_loopback g) {
+  delete g;
+  return LSBA_OK;
+}
+
+extern "C" lsba_status lsba_create_loopback(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                                            const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                                            int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                                            lsba_loopback group, int32_t device, void* cuda_stream) {
+  if (!group) return LSBA_E_ARG;
+  return create_any(out, n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks, nullptr,
+                    &group->g, device, cuda_stream);
 }
 
 extern "C" lsba_status lsba_destroy(lsba_ctx c) {

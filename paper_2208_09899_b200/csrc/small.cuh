@@ -40,7 +40,7 @@ struct SmallState2 {
   double* rscr;    // 2 b b: R and R^{-1} of the current step (coef -> update)
   int* iscr;       // [0] flag, [1] forced
   int ldH, m, bmax;
-  volatile int* prog;   // host-mapped progress word {k_done, active} read by the enqueueing host
+  volatile int* prog;   // host-mapped progress word 2 k_done + active, read by the enqueueing host
   double* Tm;           // BMGS-(I)CWY: T ((m+1)b square, col-major, ld ldH)
   double* TmT;          // and its transpose (T row-major), for row-wise dot products
   double* gpip;         // BMGS-(I)CWY: H_{1:k,k} in the Gram layout the update kernel reads
@@ -49,11 +49,11 @@ struct SmallState2 {
 
 // publish the step just decided to the host (mapped pinned memory; the host bounds how far
 // ahead of the device it enqueues speculative steps)
+// One 32-bit word 2 k + active, so the host never pairs a stale step with a new active flag
+// (on P > 1 ranks every host derives the same end step from it).
 __device__ __forceinline__ void publish_progress(const SmallState2& st, int k, int active) {
   if (st.prog) {
-    st.prog[1] = active;
-    __threadfence_system();
-    st.prog[0] = k;
+    st.prog[0] = 2 * k + (active ? 1 : 0);
     __threadfence_system();
   }
 }
