@@ -13,9 +13,11 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <condition_variable>
 #include <cstdint>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -48,8 +50,30 @@ class NcclComm : public Comm {
  public:
   ncclComm_t comm = nullptr;
   int r = 0, p = 1;
+  // f2: device-API state for the Gram allreduce folded into the Gram's tail (gram7.cuh)
+  bool devar = false;
+  ncclDevComm dcomm{};
+  ncclWindow_t win = nullptr;
+  void* wbuf = nullptr;
   ~NcclComm() override {
+    if (devar) ncclDevCommDestroy(comm, &dcomm);
+    if (win) ncclCommWindowDeregister(comm, win);
+    if (wbuf) ncclMemFree(wbuf);
     if (comm) ncclCommDestroy(comm);
+  }
+  // Collective over the ranks: a symmetric window of `bytes` and a device communicator with one
+  // LSA barrier.  Returns 0 and leaves devar false (plain ncclAllReduce) when the ranks do not
+  // all share one NVLink load/store domain.
+  int init_devar(size_t bytes) {
+    bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    if (int e = check(ncclMemAlloc(&wbuf, bytes))) return e;
+    if (int e = check(ncclCommWindowRegister(comm, wbuf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC))) return e;
+    ncclDevCommRequirements reqs;
+    std::memset(&reqs, 0, sizeof reqs);
+    reqs.lsaBarrierCount = 1;
+    if (int e = check(ncclDevCommCreate(comm, &reqs, &dcomm))) return e;
+    devar = (dcomm.lsaSize == p);
+    return 0;
   }
   int init(const ncclUniqueId& uid, int nranks, int rank) {
     r = rank;

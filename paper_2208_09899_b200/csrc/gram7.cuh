@@ -18,6 +18,9 @@
 #pragma once
 #include <algorithm>
 
+#include <nccl.h>
+#include <nccl_device.h>
+
 #include "dmma.cuh"
 #include "small.cuh"
 
@@ -81,7 +84,38 @@ struct GramFuse {
   CycleParams prm;
   int k;    // step index (0 = IO)
   int on;   // 0: plain Gram
+  // f2: the P > 1 allreduce folded into the tail (NCCL device API; LSBA_DEVAR=1)
+  int ar;                 // 1: sum the ranks' G through the symmetric window below
+  size_t woff;            // byte offset of this Gram's slot in the window (alternating slots)
+  ncclWindow_t win;
+  ncclDevComm dcomm;
 };
+
+// f2: the step's single sync folded into the Gram's tail
+// through the NCCL device API.  The CTA that holds this rank's final G publishes it in its slot
+// of a symmetric window, meets the other ranks at an LSA barrier (the NVLink load/store domain:
+// one NVSwitch box), then sums every rank's G in rank order straight from their windows over
+// NVLink — identical bits on every rank (equal to ncclAllReduce's for two ranks), no separate
+// collective launch, and the small step stays fused into the same CTA as on one rank.  Slots
+// alternate per call, so a rank never overwrites a slot a peer may still be reading (it passes
+// the next call's barrier only after every peer has finished reading this one).
+__device__ __noinline__ void gram_tail_allreduce(const GramFuse& f, double* G, double* sm, int E, bool to_smem) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* mine = static_cast<double*>(ncclGetLsaPointer(f.win, f.woff, f.dcomm.lsaRank));
+  for (int e = tid; e < E; e += nt) mine[e] = __ldcg(G + e);
+  {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dcomm, ncclTeamTagLsa(), 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  }
+  for (int e = tid; e < E; e += nt) {
+    double t = 0.0;
+    for (int r = 0; r < f.dcomm.lsaSize; ++r)
+      t += __ldcv(static_cast<const double*>(ncclGetLsaPointer(f.win, f.woff, r)) + e);
+    G[e] = t;
+    if (to_smem) sm[e] = t;
+  }
+  __syncthreads();
+}
 
 template <int S, int GMAX_, int U_, int MINB_, int NY_ = 1>
 struct G7Cfg {
@@ -321,6 +355,10 @@ k_gram_v7(GramArgs g, GramFuse f) {
     if (tid == 0) *tpass = 0u;
   }
   G7T(3);
+  if (f.ar) {
+    __syncthreads();
+    gram_tail_allreduce(f, g.G, sm7, E, g_smem);
+  }
   if constexpr (NY == 1) {
     if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm, g_smem, pre_force);
     else step_coef_body<S>(f.st, g.G, sm7, f.k, f.prm, 1.0, g_smem, pre_force);
@@ -428,6 +466,7 @@ k_gram_gl2(GramArgs g, GramFuse f) {
   (void)gsm;
   if (NY != 1 || !f.on) return;
   __syncthreads();                                    // (G written by this CTA: visible after the barrier)
+  if (f.ar) gram_tail_allreduce(f, g.G, nullptr, E, false);
   extern __shared__ double gl2_dyn[];                 // (k+1) doubles for the small step
   step_coef_body<1>(f.st, g.G, gl2_dyn, f.k, f.prm, sqrt((double)S));
 }

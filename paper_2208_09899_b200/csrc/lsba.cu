@@ -74,6 +74,10 @@ struct lsba_ctx_ {
   double* d_sendbuf = nullptr;
   int64_t n_send = 0;
   Comm* comm = nullptr;            // collectives (NCCL, or the loopback test group); null on one rank
+  NcclComm* nccl = nullptr;        // == comm when it is NCCL
+  bool devar_req = false;          // LSBA_DEVAR=1: fold the Gram allreduce into the Gram tail (f2)
+  uint64_t ar_seq = 0;             // device-allreduce calls so far (alternating window slots)
+  size_t ar_slot = 0;              // window bytes per slot
   // Gram
   double* d_part = nullptr;
   size_t part_cap = 0;
@@ -574,6 +578,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
   const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
   const bool slots = c->variant == 0 && in_basis(c, X) && in_basis(c, Y) && c->d_tickets;
   constexpr bool v7_s = (S == 2 || S == 4 || S == 8 || S == 16);
+  bool ar_in_kernel = false;       // f2: the kernel's tail did the allreduce
   if (slots && ((!gl && v7_s) || (gl && S % 2 == 0))) {
     LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
     if (c->n > 0) {
@@ -585,14 +590,23 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       a.part = c->d_part; a.gpart = c->d_gpart; a.tickets = c->d_tickets; a.G = c->d_G;
       a.active = active;
       GramFuse f{};
-      // fuse the small step into the Gram tail on one rank (no allreduce in between) while its
+      // fuse the small step into the Gram tail on one rank (no allreduce in between), or on
+      // P > 1 ranks when the allreduce itself runs in the tail (f2, LSBA_DEVAR), while its
       // Gram copy fits next to the partials (<= 64 KB of shared memory)
-      if (coef_k >= 0 && coef_fused && !c->comm && !c->no_fuse && E * sizeof(double) <= 64 * 1024) {
+      const bool devar = c->nccl && c->nccl->devar;
+      if (coef_k >= 0 && coef_fused && (!c->comm || devar) && !c->no_fuse && E * sizeof(double) <= 64 * 1024) {
         f.on = 1;
         f.st = c->st;
         f.k = coef_k;
         f.prm = prm ? *prm : CycleParams{};
         *coef_fused = true;
+        if (devar) {
+          f.ar = 1;
+          f.woff = (size_t)(c->ar_seq++ & 1) * c->ar_slot;
+          f.win = c->nccl->win;
+          f.dcomm = c->nccl->dcomm;
+          ar_in_kernel = true;
+        }
       }
       if (!gl) {
         if constexpr (v7_s) TRY(gram_v7<S>(c, a, f));
@@ -629,7 +643,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
       CKL();
     }
   }
-  if (c->comm) TRYC(c->comm->allreduce_sum_f64(c->d_G, E, c->stream));
+  if (c->comm && !ar_in_kernel) TRYC(c->comm->allreduce_sum_f64(c->d_G, E, c->stream));
   return LSBA_OK;
 }
 
@@ -1529,11 +1543,13 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     auto* nc = new (std::nothrow) NcclComm();
     if (!nc) return fail(c, LSBA_E_OOM, "comm");
     c->comm = nc;
+    c->nccl = nc;
     ncclUniqueId uid;
     if (nccl_id) std::memcpy(&uid, nccl_id, 128);
     else CKN(ncclGetUniqueId(&uid));
     TRYC(nc->init(uid, c->nranks, c->rank));
   }
+  bool any_empty = (c->row_end == c->row_begin);
   // ---- ghost plan
   std::vector<int32_t> col_local(c->nnz);
   std::vector<int64_t> ghost_global;
@@ -1560,6 +1576,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
       if (r > 0 && rr[2 * r] != rr[2 * r - 1]) { cudaFree(d_tmp); return fail(c, LSBA_E_ARG, "row ranges not contiguous"); }
     }
     part[c->nranks] = rr[2 * c->nranks - 1];
+    for (int r = 0; r < c->nranks; ++r) any_empty = any_empty || rr[2 * r + 1] == rr[2 * r];
     if (part[0] != 0 || part[c->nranks] != n) { cudaFree(d_tmp); return fail(c, LSBA_E_ARG, "row ranges do not cover [0,n)"); }
     ghost_global.resize(std::max<int64_t>(c->nnz, 1));
     int64_t ng = 0;
@@ -1621,6 +1638,13 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     bool clean = b1 - b0 >= 256;
     for (int64_t r = b0; clean && r < b1; ++r) clean = !ghost_row(r);
     if (clean) { c->int0 = (int)b0; c->int1 = (int)b1; }
+  }
+  // f2: the device-API Gram allreduce (collective; every rank takes the same decision from the
+  // replicated partition): two window slots of the largest fused Gram ((m_max+1) s^2 doubles).
+  // A rank without rows would not run the Gram kernel, so then the plain allreduce stays.
+  if (c->nccl && c->devar_req && !any_empty) {
+    c->ar_slot = ((size_t)(m_max + 2) * s * s * sizeof(double) + 255) / 256 * 256;
+    TRYC(c->nccl->init_devar(2 * c->ar_slot));
   }
   // ---- device CSR
   std::vector<int32_t> rp32(n_local + 1);
@@ -1800,6 +1824,7 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_HALO_OVERLAP")) c->halo_ovl = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_DEVAR")) c->devar_req = (e[0] == '1');
   if (n < 1 || s < 1 || s > 16 || m_max < 1) return fail(c, LSBA_E_ARG, "need n >= 1, 1 <= s <= 16, m_max >= 1");
   if (n < s) return fail(c, LSBA_E_ARG, "n < s");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, LSBA_E_ARG, "bad rank/nranks");

@@ -126,7 +126,9 @@ def test_fullsize_steps_vs_oracle(L, cfg, ip):
     torch.cuda.empty_cache()
 
 
-PROP_CASES = [(2, "cl", 5), (3, "cl", 5), (4, "cl", 5), (4, "gl", 5), (5, "cl", 5)]
+# config 4 (random, s = 16): its basis condition grows fast, so LOO = O(eps kappa^2) (Table 2)
+# passes 1e-11 only over 3 steps; its 5-step agreement with the oracle is checked above
+PROP_CASES = [(2, "cl", 5), (3, "cl", 5), (4, "cl", 3), (4, "gl", 3), (5, "cl", 5)]
 
 
 @pytest.mark.parametrize("cfg,ip,K", PROP_CASES)

@@ -142,13 +142,16 @@ def test_loopback_steps_match_single_rank(L, twin, ip, P):
     b = p.s if ip == "cl" else 1
     for r in range(1, P):                 # replicated small state: identical on every rank
         assert np.array_equal(out[r][0], out[0][0])
+    # stencils: 1e-12; the random s = 16 twin amplifies the Gram's rounding ~10x per step
+    # through Omega - H^T H (SURVEY.md 8(c) parity note), so the north star's 1e-10 applies
+    tol = 1e-10 if p.meta["kind"] == "random" else 1e-12
     H = out[0][0]
     for k in range(K):
         col, col1 = H[:, k * b:(k + 1) * b], H1[:, k * b:(k + 1) * b]
-        assert np.linalg.norm(col - col1) <= 1e-12 * np.linalg.norm(col1), k
+        assert np.linalg.norm(col - col1) <= tol * np.linalg.norm(col1), k
     for j in range(K + 1):
         Vj = np.concatenate([o[1][j] for o in out])
-        assert np.linalg.norm(Vj - V1[j]) <= 1e-12 * np.linalg.norm(V1[j]), j
+        assert np.linalg.norm(Vj - V1[j]) <= tol * np.linalg.norm(V1[j]), j
 
 
 SOLVES = [(5, "cl", 2, 1e8), (5, "cl", 3, 1e8), (2, "cl", 4, float("inf")), (4, "gl", 2, float("inf")),
@@ -178,9 +181,12 @@ def test_loopback_solve_matches_single_rank(L, twin, ip, P, tau, ovl):
     assert ip_["syncs"] == ip_["iterations"] + ip_["cycles"]
 
 
-@pytest.mark.parametrize("twin,ip", [(2, "cl"), (5, "cl"), (4, "gl")])
-def test_force_comm_one_rank_nccl(L, twin, ip):
-    """LSBA_FORCE_COMM=1: one rank through the distributed path with a real NCCL communicator."""
+@pytest.mark.parametrize("devar", ["0", "1"])
+@pytest.mark.parametrize("twin,ip", [(2, "cl"), (5, "cl"), (4, "gl"), (4, "cl")])
+def test_force_comm_one_rank_nccl(L, twin, ip, devar):
+    """LSBA_FORCE_COMM=1: one rank through the distributed path with a real NCCL communicator;
+    LSBA_DEVAR=1 adds f2: the Gram allreduce in the Gram kernel's tail through the NCCL device
+    API (symmetric window + LSA barrier) with the small step fused again."""
     import torch
     from lsba_inputs import make_twin
     p = make_twin(twin)
@@ -188,11 +194,13 @@ def test_force_comm_one_rank_nccl(L, twin, ip):
     i1, X1 = single(L, p, solve_fn(ip, tau))
     H1, V1 = single(L, p, steps_fn(ip, 5))
     os.environ["LSBA_FORCE_COMM"] = "1"
+    os.environ["LSBA_DEVAR"] = devar
     try:
         i2, X2 = single(L, p, solve_fn(ip, tau))
         H2, V2 = single(L, p, steps_fn(ip, 5))
     finally:
         os.environ.pop("LSBA_FORCE_COMM", None)
+        os.environ.pop("LSBA_DEVAR", None)
     assert i2["outcome"] == L.LSBA_CONVERGED and i2["true_relres"] <= p.tol
     assert abs(i2["cycles"] - i1["cycles"]) <= 1
     if (i2["cycles"], i2["iterations"]) == (i1["cycles"], i1["iterations"]):
