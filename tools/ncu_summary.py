@@ -78,7 +78,8 @@ def dram(src, out, config, traffic_json=None):
         d = json.load(open(traffic_json)) if os.path.exists(traffic_json) else {}
         ent = {}
         for kid, prefixes in KID.items():
-            hits = [a for k, a in agg.items() if any(k.split("::")[-1].startswith(p) for p in prefixes)]
+            hits = [a for k, a in agg.items() if any(k.split("::")[-1].startswith(p) for p in prefixes)
+                    and "true>" not in k]      # (not the residual SpMM variant)
             n = sum(a[0] for a in hits)
             if n:
                 ent[kid] = sum(a[2] + a[3] for a in hits) / n
