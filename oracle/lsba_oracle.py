@@ -993,7 +993,8 @@ def _basis_combine(Vs, Y, b: int) -> np.ndarray:
 
 
 def loss_of_orthogonality(Vs, ip: str) -> float:
-    """||I - <Q,Q>||_2 (Eq loo) — diagnostic, exact SVD norm."""
+    """||I - <Q,Q>||_2 (Eq loo) — diagnostic, exact SVD norm.  Pinned by
+    closed forms in tests/test_oracle_kernels.py::test_loss_of_orthogonality_closed_form."""
     if ip == "cl":
         Q = np.concatenate(Vs, axis=1)
         G = gram(Q, Q)
