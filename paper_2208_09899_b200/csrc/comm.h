@@ -53,9 +53,11 @@ class NcclComm : public Comm {
   // f2: device-API state for the Gram allreduce folded into the Gram's tail (gram7.cuh)
   bool devar = false;
   ncclDevComm dcomm{};
+  ncclDevComm* d_dcomm = nullptr;   // device copy read by the Gram kernel
   ncclWindow_t win = nullptr;
   void* wbuf = nullptr;
   ~NcclComm() override {
+    if (d_dcomm) cudaFree(d_dcomm);
     if (devar) ncclDevCommDestroy(comm, &dcomm);
     if (win) ncclCommWindowDeregister(comm, win);
     if (wbuf) ncclMemFree(wbuf);
@@ -72,6 +74,12 @@ class NcclComm : public Comm {
     std::memset(&reqs, 0, sizeof reqs);
     reqs.lsaBarrierCount = 1;
     if (int e = check(ncclDevCommCreate(comm, &reqs, &dcomm))) return e;
+    if (cudaMalloc((void**)&d_dcomm, sizeof dcomm) != cudaSuccess ||
+        cudaMemcpy(d_dcomm, &dcomm, sizeof dcomm, cudaMemcpyHostToDevice) != cudaSuccess) {
+      err = "CUDA: device communicator copy";
+      ncclDevCommDestroy(comm, &dcomm);
+      return 1;
+    }
     devar = (dcomm.lsaSize == p);
     return 0;
   }

@@ -88,7 +88,8 @@ struct GramFuse {
   int ar;                 // 1: sum the ranks' G through the symmetric window below
   size_t woff;            // byte offset of this Gram's slot in the window (alternating slots)
   ncclWindow_t win;
-  ncclDevComm dcomm;
+  const ncclDevComm* dcomm;   // device copy (a pointer: the kernel parameter block stays small
+                              // and is never addressed, which would copy it to local memory)
 };
 
 // f2: the step's single sync folded into the Gram's tail
@@ -99,18 +100,20 @@ struct GramFuse {
 // collective launch, and the small step stays fused into the same CTA as on one rank.  Slots
 // alternate per call, so a rank never overwrites a slot a peer may still be reading (it passes
 // the next call's barrier only after every peer has finished reading this one).
-__device__ __noinline__ void gram_tail_allreduce(const GramFuse& f, double* G, double* sm, int E, bool to_smem) {
+__device__ __noinline__ void gram_tail_allreduce(const ncclDevComm* dc, ncclWindow_t win, size_t woff, double* G,
+                                                double* sm, int E, bool to_smem) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  double* mine = static_cast<double*>(ncclGetLsaPointer(f.win, f.woff, f.dcomm.lsaRank));
+  double* mine = static_cast<double*>(ncclGetLsaPointer(win, woff, dc->lsaRank));
   for (int e = tid; e < E; e += nt) mine[e] = __ldcg(G + e);
   {
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), f.dcomm, ncclTeamTagLsa(), 0);
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), *dc, ncclTeamTagLsa(), 0);
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   }
+  const int P = dc->lsaSize;
   for (int e = tid; e < E; e += nt) {
     double t = 0.0;
-    for (int r = 0; r < f.dcomm.lsaSize; ++r)
-      t += __ldcv(static_cast<const double*>(ncclGetLsaPointer(f.win, f.woff, r)) + e);
+    for (int r = 0; r < P; ++r)
+      t += __ldcv(static_cast<const double*>(ncclGetLsaPointer(win, woff, r)) + e);
     G[e] = t;
     if (to_smem) sm[e] = t;
   }
@@ -357,7 +360,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
   G7T(3);
   if (f.ar) {
     __syncthreads();
-    gram_tail_allreduce(f, g.G, sm7, E, g_smem);
+    gram_tail_allreduce(f.dcomm, f.win, f.woff, g.G, sm7, E, g_smem);
   }
   if constexpr (NY == 1) {
     if constexpr (S >= 16) step_coef_noinline<S>(f.st, g.G, sm7, f.k, f.prm, g_smem, pre_force);
@@ -466,7 +469,7 @@ k_gram_gl2(GramArgs g, GramFuse f) {
   (void)gsm;
   if (NY != 1 || !f.on) return;
   __syncthreads();                                    // (G written by this CTA: visible after the barrier)
-  if (f.ar) gram_tail_allreduce(f, g.G, nullptr, E, false);
+  if (f.ar) gram_tail_allreduce(f.dcomm, f.win, f.woff, g.G, nullptr, E, false);
   extern __shared__ double gl2_dyn[];                 // (k+1) doubles for the small step
   step_coef_body<1>(f.st, g.G, gl2_dyn, f.k, f.prm, sqrt((double)S));
 }

@@ -165,9 +165,31 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, long bytes) {
   }
 }
 
+// 32-byte vector access (sm_100a LDG.E.256 / STG.E.256)
+__device__ __forceinline__ double4 ld4nc(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4h(double* p, double4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w), "l"(pol) : "memory");
+}
+
+// Columns per lane of the row-lane SpMM: 4 (one 32-byte access) when s % 4 == 0, else 2
+// (16 bytes) for even s, else 1.  Round 2: 32-byte lanes halve the lanes per row and with them
+// the redundant index/value loads per entry (standalone, config 5: 852 -> 606 us = 6.0 TB/s;
+// config 3: 115 -> 79 us; tools/spmm_tile_bench.cu, profiles/r02_spmm_q256_raw.txt).
+template <int S>
+struct SpmmLanes {
+  static constexpr int C = (S % 4 == 0) ? 4 : ((S % 2 == 0) ? 2 : 1);
+  static constexpr int L = S / C;      // lanes per row
+};
+
 // Rows [row0, row1) of the n local rows (the halo overlap runs the interior rows while the
 // ghost rows are in flight, then the boundary rows); columns >= n address Vghost.
-template <int S, bool RESID>
+// CW: columns per lane (SpmmLanes<S>::C; 2 when a caller buffer is only 16-byte aligned)
+template <int S, bool RESID, int CW = SpmmLanes<S>::C>
 __global__ void __launch_bounds__(kThreads)
 k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ va, const double* __restrict__ V,
@@ -176,8 +198,8 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        int pf_dist = 0, int pf_v = 0, int row0 = 0, int row1 = -1) {
   pdl_begin();
   if (active && *active == 0) return;
-  constexpr int L = (S >= 2) ? S / 2 : 1;
-  constexpr int C = (S >= 2) ? 2 : 1;  // columns per lane
+  constexpr int C = CW;                // columns per lane
+  constexpr int L = S / CW;            // lanes per row
   constexpr int RPC = kThreads / L;    // rows per CTA
   if (row1 < 0) row1 = n;
   if (pf_dist > 0 && threadIdx.x == 0) {
@@ -196,49 +218,60 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   const int row = row0 + (int)(gt / L);
   const int lane = (int)(gt % L);
   double sq = 0.0;
-  // row pointers: for L >= 2 one coalesced load of the warp's 32/L + 1 pointers, then shuffles
-  // (instead of 2 L redundant dependent loads per row; +4-7% on the stencil configs)
+  // row pointers: one coalesced load of the warp's 32/L + 1 pointers, then shuffles (instead
+  // of 2 L redundant dependent loads per row)
   int p0, p1;
-  if constexpr (L >= 2) {
+  {
     const int lane32 = threadIdx.x & 31;
     const int row_w = row0 + (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
     const int rr = row_w + lane32;
     const int pv = (lane32 <= 32 / L && rr <= row1) ? __ldg(rp + rr) : 0;
-    p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
-    p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
-  } else {
-    p0 = (row < row1) ? rp[row] : 0;
-    p1 = (row < row1) ? rp[row + 1] : 0;
+    if constexpr (L == 1) {            // 32 rows per warp: the 33rd pointer by a second load
+      const int nx = __shfl_down_sync(0xffffffffu, pv, 1);
+      p0 = pv;
+      p1 = (lane32 < 31) ? nx : ((rr + 1 <= row1) ? __ldg(rp + rr + 1) : 0);
+    } else {
+      p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
+      p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
+    }
   }
   if (row < row1) {
-    double a0 = 0.0, a1 = 0.0;
+    double acc[C];
+#pragma unroll
+    for (int t = 0; t < C; ++t) acc[t] = 0.0;
     for (int p = p0; p < p1; ++p) {
       const int c = __ldg(ci + p);
       const double a = __ldg(va + p);
-      const double* src = (c < n) ? (V + (size_t)c * S) : (Vghost + (size_t)(c - n) * S);
-      if constexpr (C == 2) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(src) + lane);
-        a0 = fma(a, v.x, a0);
-        a1 = fma(a, v.y, a1);
+      const double* src = ((c < n) ? (V + (size_t)c * S) : (Vghost + (size_t)(c - n) * S)) + C * lane;
+      if constexpr (C == 4) {
+        const double4 v = ld4nc(src);
+        acc[0] = fma(a, v.x, acc[0]);
+        acc[1] = fma(a, v.y, acc[1]);
+        acc[2] = fma(a, v.z, acc[2]);
+        acc[3] = fma(a, v.w, acc[3]);
+      } else if constexpr (C == 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(src));
+        acc[0] = fma(a, v.x, acc[0]);
+        acc[1] = fma(a, v.y, acc[1]);
       } else {
-        a0 = fma(a, __ldg(src), a0);
+        acc[0] = fma(a, __ldg(src), acc[0]);
       }
     }
-    double* dst = W + (size_t)row * S;
+    double* dst = W + (size_t)row * S + C * lane;
     if constexpr (RESID) {
-      if constexpr (C == 2) {
-        const double2 b = __ldg(reinterpret_cast<const double2*>(Bm + (size_t)row * S) + lane);
-        a0 = b.x - a0;
-        a1 = b.y - a1;
-      } else {
-        a0 = __ldg(Bm + row) - a0;
+      const double* bsrc = Bm + (size_t)row * S + C * lane;
+#pragma unroll
+      for (int t = 0; t < C; ++t) {
+        acc[t] = __ldg(bsrc + t) - acc[t];
+        sq += acc[t] * acc[t];
       }
-      sq = a0 * a0 + (C == 2 ? a1 * a1 : 0.0);
     }
-    if constexpr (C == 2)
-      sth2(dst + 2 * lane, make_double2(a0, a1), l2pol(c_l2hint & 8, true));
+    if constexpr (C == 4)
+      st4h(dst, make_double4(acc[0], acc[1], acc[2], acc[3]), l2pol(c_l2hint & 8, true));
+    else if constexpr (C == 2)
+      sth2(dst, make_double2(acc[0], acc[1]), l2pol(c_l2hint & 8, true));
     else
-      dst[0] = a0;
+      dst[0] = acc[0];
   }
   if constexpr (RESID) {
     __shared__ double red[kThreads / 32];

@@ -372,7 +372,10 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
   // rows compute; the boundary rows follow once it has arrived
   const bool ovl = c->comm && c->halo_ovl && c->int1 > c->int0;
   TRY(halo_t<S>(c, V, ovl));
-  constexpr int L = (S % 2 == 0) ? S / 2 : 1;
+  // 32-byte lanes need 32-byte aligned rows (basis slots always are; caller buffers of
+  // lsba_spmm / the residual may only be 16-byte aligned: then 16-byte lanes)
+  constexpr int CW = SpmmLanes<S>::C;
+  const bool a32 = CW != 4 || !((((uintptr_t)V) | ((uintptr_t)W) | ((uintptr_t)c->d_ghost)) & 31);
   {
     LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (n + 1) + 16.0 * n * S);
     if (n == 0) {
@@ -382,8 +385,11 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
     auto rows = [&](int r0, int r1) -> lsba_status {
       if (r1 <= r0) return LSBA_OK;
       if constexpr (S % 2 == 0 || S == 1) {
+        constexpr int CW2 = (CW == 4) ? 2 : CW;
+        auto kern = a32 ? k_spmm<S, false, CW> : k_spmm<S, false, CW2>;
+        const int L = S / (a32 ? CW : CW2);
         c->in_spmm = true;
-        const cudaError_t le = launch_k(c, k_spmm<S, false>, dim3(cdiv((long)(r1 - r0) * L, kThreads)),
+        const cudaError_t le = launch_k(c, kern, dim3(cdiv((long)(r1 - r0) * L, kThreads)),
                     dim3(kThreads), 0, n, (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
                     (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active,
                     c->spmm_pf, c->spmm_pfv, r0, r1);
@@ -413,7 +419,9 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
 template <int S>
 static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, double* out) {
   TRY(halo_t<S>(c, X));
-  constexpr int L = (S % 2 == 0) ? S / 2 : 1;
+  constexpr int CW = SpmmLanes<S>::C, CW2 = (CW == 4) ? 2 : CW;
+  const bool a32 = CW != 4 || !((((uintptr_t)X) | ((uintptr_t)out) | ((uintptr_t)c->d_ghost)) & 31);
+  const int L = S / (a32 ? CW : CW2);
   int nblk = (S % 2 == 0 || S == 1) ? cdiv((long)c->n * L, kThreads) : cdiv(c->n, kThreads);
   if (nblk < 1) nblk = 1;
   if (nblk > c->sq_cap) return fail(c, LSBA_E_STATE, "residual partial buffer too small");
@@ -422,9 +430,9 @@ static lsba_status residual_t(lsba_ctx c, const double* Bm, const double* X, dou
     if (c->n == 0) {
       CK(cudaMemsetAsync(c->d_sq, 0, sizeof(double), c->stream));
     } else if constexpr (S % 2 == 0 || S == 1) {
-      k_spmm<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
-                                                          c->d_ghost, Bm, out, c->d_sq, nullptr,
-                                                          c->spmm_pf, c->spmm_pfv);
+      auto kern = a32 ? k_spmm<S, true, CW> : k_spmm<S, true, CW2>;
+      kern<<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X, c->d_ghost, Bm, out,
+                                               c->d_sq, nullptr, c->spmm_pf, c->spmm_pfv, 0, -1);
     } else {
       k_spmm_odd<S, true><<<nblk, kThreads, 0, c->stream>>>(c->n, c->d_rp, c->d_ci, c->d_va, X,
                                                               c->d_ghost, Bm, out, c->d_sq, nullptr);
@@ -604,7 +612,7 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
           f.ar = 1;
           f.woff = (size_t)(c->ar_seq++ & 1) * c->ar_slot;
           f.win = c->nccl->win;
-          f.dcomm = c->nccl->dcomm;
+          f.dcomm = c->nccl->d_dcomm;
           ar_in_kernel = true;
         }
       }
@@ -1716,7 +1724,19 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess && sms > 0)
       c->n_sms = sms;
   }
-  if (c->spmm_pf < 0) c->spmm_pf = 4 * c->n_sms;
+  if (c->spmm_pf < 0) {
+    // the L2 bulk prefetch helps banded / stencil matrices (standalone: configs 2, 3 -8..-10%
+    // time at 2 x #SMs CTAs ahead, config 5 neutral) and hurts matrices whose gathers reach far
+    // (config 4's uniform-random columns: +7..12%): off when > 10% of the entries lie more than
+    // 2^20 rows from the diagonal (profiles/r02_spmm_q256_raw.txt)
+    int64_t far = 0;
+    for (int64_t r = 0; r < n_local; ++r)
+      for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
+        const int64_t d = (int64_t)col_idx[p] - (c->row_begin + r);
+        far += (d > (1 << 20) || d < -(1 << 20)) ? 1 : 0;
+      }
+    c->spmm_pf = (c->nnz > 0 && far * 10 > c->nnz) ? 0 : 2 * c->n_sms;
+  }
   // DMMA Gram: persistent grid of 2 CTAs per SM; partials [cta][E] and [group][E]
   c->gram_grid = 4 * c->n_sms;
   const size_t Emax = 2 * (size_t)(m_max + 2) * s * s;      // (k+1)s x 2s for BMGS-(I)CWY

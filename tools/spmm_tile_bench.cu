@@ -224,6 +224,60 @@ k_spmm_pfa(int n, int D, const int* __restrict__ rp, const int* __restrict__ ci,
   reinterpret_cast<double2*>(W + (size_t)row * S)[lane] = make_double2(a0, a1);
 }
 
+// Q: the row-lane kernel with 32-byte lanes: L = S/4 lanes per row, each owning 4 columns and
+// loading them with one 256-bit LDG (sm_100a LDG.E.256): half the lanes per row of the 16-byte
+// kernel, so half the redundant index/value loads per entry; plus the bulk L2 prefetch ahead.
+__device__ __forceinline__ void ld4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+template <int S, bool PFV>
+__global__ void __launch_bounds__(256)
+k_spmm_q(int n, int D, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
+         const double* __restrict__ V, double* __restrict__ W) {
+  constexpr int L = S / 4, RPC = 256 / L;
+  if (threadIdx.x == 0 && D > 0) {
+    const long r0 = (long)(blockIdx.x + D) * RPC;
+    if (r0 < n) {
+      const long r1 = min((long)n, r0 + RPC);
+      const int q0 = __ldg(rp + r0), q1 = __ldg(rp + r1);
+      bulk_pf(ci + q0, 4L * (q1 - q0));
+      bulk_pf(va + q0, 8L * (q1 - q0));
+      if (PFV) bulk_pf(V + r0 * S, 8L * S * (r1 - r0));
+      const long r2 = (long)(blockIdx.x + 2 * D) * RPC;
+      if (r2 < n) bulk_pf(rp + r2, 4L * (min((long)n, r2 + RPC) - r2 + 1));
+    }
+  }
+  const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / L), lane = (int)(gt % L);
+  const int lane32 = threadIdx.x & 31;
+  int p0, p1;
+  if constexpr (L >= 2) {
+    const int row_w = (int)(((long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / L);
+    const int rr = row_w + lane32;
+    const int pv = (lane32 <= 32 / L && rr <= n) ? __ldg(rp + rr) : 0;
+    p0 = __shfl_sync(0xffffffffu, pv, lane32 / L);
+    p1 = __shfl_sync(0xffffffffu, pv, lane32 / L + 1);
+  } else {
+    const int rr = row;   // one lane per row: a coalesced pair of loads
+    const int a = (rr <= n) ? __ldg(rp + rr) : 0;
+    const int b = __shfl_down_sync(0xffffffffu, a, 1);
+    p0 = a;
+    p1 = (lane32 < 31) ? b : ((rr + 1 <= n) ? __ldg(rp + rr + 1) : 0);
+  }
+  if (row >= n) return;
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (int p = p0; p < p1; ++p) {
+    const int c = __ldg(ci + p); const double a = __ldg(va + p);
+    double v0, v1, v2, v3;
+    ld4(V + (size_t)c * S + 4 * lane, v0, v1, v2, v3);
+    a0 = fma(a, v0, a0); a1 = fma(a, v1, a1); a2 = fma(a, v2, a2); a3 = fma(a, v3, a3);
+  }
+  st4(W + (size_t)row * S + 4 * lane, a0, a1, a2, a3);
+}
+
 template <typename F>
 static double time_it(F launch) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -307,10 +361,14 @@ static void run(int dims, int N, bool random_cfg4 = false) {
 #define PA(PFV, P256, DD) \
   us = time_it([&] { k_spmm_pfa<S, PFV, P256><<<gA, 256>>>((int)n, DD, drp, dci, dva, dV, dW); }); \
   check("pfa_" #PFV "_" #P256 "_" #DD, us);
-  PA(false, false, 0) PA(false, true, 0) PA(false, false, 600) PA(false, false, 1200) PA(false, false, 2400)
-  PA(false, false, 4800) PA(true, false, 1200) PA(true, false, 2400) PA(false, true, 1200) PA(false, true, 2400)
-  PA(true, true, 2400)
-  T1(2, 4) TP(2, 8, 4, 4)
+  PA(false, false, 0) PA(true, false, 600) PA(true, false, 1200)
+  constexpr int LQ = S / 4;
+  const int gQ = (int)((n * LQ + 255) / 256);
+#define QQ(PFV, DD) \
+  us = time_it([&] { k_spmm_q<S, PFV><<<gQ, 256>>>((int)n, DD, drp, dci, dva, dV, dW); }); \
+  check("q256_" #PFV "_" #DD, us);
+  QQ(false, 0) QQ(true, 300) QQ(true, 600) QQ(true, 1200) QQ(false, 600)
+#undef QQ
 #undef T1
 #undef TP
 #undef SP
