@@ -27,7 +27,7 @@ for CFG in ${CFGS:-5 2}; do
   esac
   i=0
   # demangled names read "lsba::k_spmm<(int)8, (bool)0>(...)"
-  for K in "k_spmm<\\(int\\)$S, \\(bool\\)0>" "k_gram_v7<\\(int\\)$S," "$PROJ"; do
+  for K in "k_spmm<\\(int\\)$S, \\(bool\\)0" "k_gram_v7<\\(int\\)$S," "$PROJ"; do
     i=$((i+1))
     timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
       -k regex:"$K" --launch-skip $SKIP -c 1 -o gpurun_out/full_c${CFG}_$i -f $B > gpurun_out/ncu_full_c${CFG}_$i.log 2>&1
