@@ -47,6 +47,24 @@ struct GramArgs {
 // per block j: A = X_j rows (8 x 4 chunks), B = C_j (4 x 8 chunks, shared memory), D in
 // registers.  out0/out1 may alias an input block (each warp reads its rows before writing).
 // ------------------------------------------------------------------------------------------
+// K index of chunk kc, lane k4 (the column of X the lane's A value came from)
+template <int S>
+__device__ __forceinline__ int kmap(int kc, int k4) {
+  return S == 16 ? 4 * k4 + kc : (S == 8 ? 2 * k4 + kc : kc * 4 + k4);
+}
+__device__ __forceinline__ double2 ldh2_rw(const double* p, uint64_t pol) {   // coherent, 16 bytes
+  double2 v;
+  asm("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ double4 ldh4_rw(const double* p, uint64_t pol) {   // coherent, 32 bytes
+  double4 v;
+  asm("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+
 template <int S>
 __global__ void __launch_bounds__(256)
 k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
@@ -83,8 +101,20 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         const int row = (sb * RB + rb) * 8 + r8;
+        if constexpr (S == 16) {
+          // one 32-byte load per lane covers a quarter row: K chunk kc takes column 4 k4 + kc
+          // (the coefficient rows below use the same map), a quarter of the load instructions
+          // of 8-byte loads (round 1: the L1 pipe was the limit at s = 16)
+          const double4 v = (row < n) ? ldh4_rw(Xj + (size_t)row * S + 4 * k4, xpol) : make_double4(0, 0, 0, 0);
+          a[rb][0] = v.x; a[rb][1] = v.y; a[rb][2] = v.z; a[rb][3] = v.w;
+        } else if constexpr (S == 8) {
+          // s = 8: one 16-byte load per lane, K chunk kc takes column 2 k4 + kc
+          const double2 v = (row < n) ? ldh2_rw(Xj + (size_t)row * S + 2 * k4, xpol) : make_double2(0, 0);
+          a[rb][0] = v.x; a[rb][1] = v.y;
+        } else {
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) a[rb][kc] = (row < n) ? ldh_rw(Xj + (size_t)row * S + kc * 4 + k4, xpol) : 0.0;
+          for (int kc = 0; kc < KC; ++kc) a[rb][kc] = (row < n) ? ldh_rw(Xj + (size_t)row * S + kc * 4 + k4, xpol) : 0.0;
+        }
       }
       if (j < J0) {
         const double* cj = c0 + (size_t)j * S * S;
@@ -93,7 +123,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
 #pragma unroll
           for (int tn = 0; tn < NT; ++tn) {
             const int col = tn * 8 + r8;
-            const double b = (col < S) ? cj[(kc * 4 + k4) * S + col] : 0.0;
+            const double b = (col < S) ? cj[kmap<S>(kc, k4) * S + col] : 0.0;
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) dmma(d0[rb][tn][0], d0[rb][tn][1], a[rb][kc], b);
           }
@@ -105,7 +135,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
 #pragma unroll
           for (int tn = 0; tn < NT; ++tn) {
             const int col = tn * 8 + r8;
-            const double b = (col < S) ? cj[(kc * 4 + k4) * S + col] : 0.0;
+            const double b = (col < S) ? cj[kmap<S>(kc, k4) * S + col] : 0.0;
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) dmma(d1[rb][tn][0], d1[rb][tn][1], a[rb][kc], b);
           }

@@ -480,6 +480,58 @@ static __global__ void k_sum_partials(int P, const double* __restrict__ part, do
 // an input block: every thread reads its row of all blocks before writing it.
 // flag_ptr: if non-null and *flag_ptr != 0 the kernel does nothing (NaN-flagged step).
 // ------------------------------------------------------------------------------------------
+// Global inner product (Table 1): the projection coefficients are scalars, so
+// a projection is an elementwise combination of whole blocks.  Flat over the n S doubles of a
+// block (S even: 16-byte vectors, coalesced across the warp), up to 4 blocks in flight per
+// thread, the same j-ascending fma chain as k_project (bitwise the same results).  A thread
+// reads its elements of every block before writing them, so an output may alias an input block.
+__device__ __forceinline__ double2 ldh2_co(const double* p, uint64_t pol) {   // coherent, 16 bytes
+  double2 v;
+  asm("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+static __global__ void __launch_bounds__(kThreads)
+k_project_flat(long cnt2, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
+               const double* base0, double* out0, int J1, const double* __restrict__ C1, double* out1,
+               const int* __restrict__ flag_ptr) {
+  pdl_begin();
+  if (flag_ptr && *flag_ptr) return;
+  extern __shared__ double sm[];
+  double* c0 = sm;
+  double* c1 = sm + J0;
+  for (int e = threadIdx.x; e < J0; e += blockDim.x) c0[e] = C0[e];
+  for (int e = threadIdx.x; e < J1; e += blockDim.x) c1[e] = C1[e];
+  __syncthreads();
+  const int Jmax = max(J0, J1);
+  const uint64_t xpol = l2pol(c_l2hint & 4, false), opol = l2pol(c_l2hint & 8, true);
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < cnt2; e += (long)gridDim.x * blockDim.x) {
+    double2 o0 = make_double2(0.0, 0.0), o1 = make_double2(0.0, 0.0);
+    int j = 0;
+    for (; j + 4 <= Jmax; j += 4) {
+      double2 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = ldh2_co(X + (size_t)(j + u) * xstride + 2 * e, xpol);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j + u < J0) { o0.x = fma(x[u].x, c0[j + u], o0.x); o0.y = fma(x[u].y, c0[j + u], o0.y); }
+        if (j + u < J1) { o1.x = fma(x[u].x, c1[j + u], o1.x); o1.y = fma(x[u].y, c1[j + u], o1.y); }
+      }
+    }
+    for (; j < Jmax; ++j) {
+      const double2 x = ldh2_co(X + (size_t)j * xstride + 2 * e, xpol);
+      if (j < J0) { o0.x = fma(x.x, c0[j], o0.x); o0.y = fma(x.y, c0[j], o0.y); }
+      if (j < J1) { o1.x = fma(x.x, c1[j], o1.x); o1.y = fma(x.y, c1[j], o1.y); }
+    }
+    if (base0) {
+      const double2 b = *reinterpret_cast<const double2*>(base0 + 2 * e);
+      o0.x += b.x;
+      o0.y += b.y;
+    }
+    if (J0 > 0) sth2(out0 + 2 * e, o0, opol);
+    if (J1 > 0) sth2(out1 + 2 * e, o1, opol);
+  }
+}
+
 template <int S, bool GLOBAL>
 __global__ void __launch_bounds__(kThreads)
 k_project(int n, const double* X, size_t xstride, int J0, const double* __restrict__ C0,

@@ -688,6 +688,13 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
       return LSBA_OK;
     }
   }
+  if (gl && S % 2 == 0) {           // flat elementwise combination (scalar coefficients)
+    const long cnt2 = (long)n * S / 2;
+    const int grid = std::max(1, std::min(cdiv(cnt2, kThreads), 8 * c->n_sms));
+    CK(launch_k(c, k_project_flat, dim3(grid), dim3(kThreads), smem, cnt2, X, xstride, J0, C0, base0,
+                out0, J1, C1, out1, flag_ptr));
+    return LSBA_OK;
+  }
   if (gl) {
     auto fn = k_project<S, true>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
