@@ -188,9 +188,12 @@ struct SpmmLanes {
 
 // Rows [row0, row1) of the n local rows (the halo overlap runs the interior rows while the
 // ghost rows are in flight, then the boundary rows); columns >= n address Vghost.
-// CW: columns per lane (SpmmLanes<S>::C; 2 when a caller buffer is only 16-byte aligned)
+// CW: columns per lane (SpmmLanes<S>::C; 2 when a caller buffer is only 16-byte aligned).
+// Register budget for 6 CTAs of 256 per SM (<= 40 registers): the compiler then keeps more
+// entries' loads in flight than at its default 36 (interleaved standalone A/B:
+// profiles/r02_spmm_ab_raw.txt: configs 3 / 5 -5% / -2% time, config 2 -6%)
 template <int S, bool RESID, int CW = SpmmLanes<S>::C>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 6)
 k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ va, const double* __restrict__ V,
        const double* __restrict__ Vghost, const double* __restrict__ Bm,

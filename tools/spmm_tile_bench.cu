@@ -7,6 +7,8 @@
 #include <cmath>
 #include <random>
 #include <algorithm>
+#include <functional>
+#include <utility>
 #include "../paper_2208_09899_b200/csrc/kernels.cuh"
 
 using namespace lsba;
@@ -233,8 +235,8 @@ __device__ __forceinline__ void ld4(const double* p, double& a, double& b, doubl
 __device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" :: "l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
-template <int S, bool PFV>
-__global__ void __launch_bounds__(256)
+template <int S, bool PFV, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 k_spmm_q(int n, int D, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ va,
          const double* __restrict__ V, double* __restrict__ W) {
   constexpr int L = S / 4, RPC = 256 / L;
@@ -347,28 +349,25 @@ static void run(int dims, int N, bool random_cfg4 = false) {
   double us = time_it([&] { k_spmm<S, false><<<gA, 256>>>((int)n, drp, dci, dva, dV, nullptr, nullptr, dW, nullptr, nullptr); });
   CK(cudaMemcpy(dW2, dW, 8 * n * S, cudaMemcpyDeviceToDevice));
   check("current", us);
-  const int RW = 32 / L;
-  const int gT1 = (int)((n + RW * 8 - 1) / (RW * 8));
-#define T1(NE, RB) \
-  us = time_it([&] { k_spmm_tile1<S, NE, RB><<<gT1, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
-  check("tile1_" #NE "_" #RB, us);
-#define TP(NE, RB, MINB, G) \
-  us = time_it([&] { k_spmm_tile<S, NE, RB, MINB><<<sms * G, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
-  check("tileP_" #NE "_" #RB "_" #MINB "x" #G, us);
-#define SP(RB) \
-  us = time_it([&] { k_spmm_split<S, RB><<<gA, 256>>>((int)n, drp, dci, dva, dV, dW); }); \
-  check("split_" #RB, us);
-#define PA(PFV, P256, DD) \
-  us = time_it([&] { k_spmm_pfa<S, PFV, P256><<<gA, 256>>>((int)n, DD, drp, dci, dva, dV, dW); }); \
-  check("pfa_" #PFV "_" #P256 "_" #DD, us);
-  PA(false, false, 0) PA(true, false, 600) PA(true, false, 1200)
+  // interleaved A/B: every candidate timed in each of 4 rounds, the minimum reported (the box's
+  // clock drifts between runs)
   constexpr int LQ = S / 4;
   const int gQ = (int)((n * LQ + 255) / 256);
-#define QQ(PFV, DD) \
-  us = time_it([&] { k_spmm_q<S, PFV><<<gQ, 256>>>((int)n, DD, drp, dci, dva, dV, dW); }); \
-  check("q256_" #PFV "_" #DD, us);
-  QQ(false, 0) QQ(true, 300) QQ(true, 600) QQ(true, 1200) QQ(false, 600)
-#undef QQ
+  std::vector<std::pair<const char*, std::function<void()>>> cand = {
+    {"lib_pf0", [&] { k_spmm<S, false><<<gQ, 256>>>((int)n, drp, dci, dva, dV, nullptr, nullptr, dW, nullptr, nullptr, 0, 0, 0, -1); }},
+    {"lib_pf296", [&] { k_spmm<S, false><<<gQ, 256>>>((int)n, drp, dci, dva, dV, nullptr, nullptr, dW, nullptr, nullptr, 296, 1, 0, -1); }},
+    {"q_minb1_pf0", [&] { k_spmm_q<S, false, 1><<<gQ, 256>>>((int)n, 0, drp, dci, dva, dV, dW); }},
+    {"q_minb1_pf300", [&] { k_spmm_q<S, true, 1><<<gQ, 256>>>((int)n, 300, drp, dci, dva, dV, dW); }},
+    {"q_minb6_pf0", [&] { k_spmm_q<S, false, 6><<<gQ, 256>>>((int)n, 0, drp, dci, dva, dV, dW); }},
+    {"q_minb6_pf300", [&] { k_spmm_q<S, true, 6><<<gQ, 256>>>((int)n, 300, drp, dci, dva, dV, dW); }},
+    {"q_minb8_pf0", [&] { k_spmm_q<S, false, 8><<<gQ, 256>>>((int)n, 0, drp, dci, dva, dV, dW); }},
+    {"q_minb8_pf300", [&] { k_spmm_q<S, true, 8><<<gQ, 256>>>((int)n, 300, drp, dci, dva, dV, dW); }},
+    {"q_minb8_pf600", [&] { k_spmm_q<S, true, 8><<<gQ, 256>>>((int)n, 600, drp, dci, dva, dV, dW); }},
+  };
+  std::vector<double> best(cand.size(), 1e30);
+  for (int round = 0; round < 4; ++round)
+    for (size_t c = 0; c < cand.size(); ++c) best[c] = std::min(best[c], time_it(cand[c].second));
+  for (size_t c = 0; c < cand.size(); ++c) { cand[c].second(); CK(cudaDeviceSynchronize()); check(cand[c].first, best[c]); }
 #undef T1
 #undef TP
 #undef SP
