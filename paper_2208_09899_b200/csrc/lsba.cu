@@ -138,6 +138,7 @@ struct lsba_ctx_ {
   bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
   int spmm_pf = -1;              // SpMM L2 prefetch distance in CTAs (-1: 4 x SMs; LSBA_SPMM_PF)
   int spmm_pfv = 1;              // ... and of the CTA's V rows (LSBA_SPMM_PFV)
+  bool spmm_lanes16 = false;     // diagnostics: LSBA_SPMM_LANES16=1 forces 16-byte SpMM lanes
   bool force_comm = false;       // LSBA_FORCE_COMM=1: one rank through the distributed code path
   int force_sing_cycle = 0;      // test hook: the cycle end of this cycle reports singular
   int cur_cycle = 0;
@@ -375,7 +376,7 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
   // 32-byte lanes need 32-byte aligned rows (basis slots always are; caller buffers of
   // lsba_spmm / the residual may only be 16-byte aligned: then 16-byte lanes)
   constexpr int CW = SpmmLanes<S>::C;
-  const bool a32 = CW != 4 || !((((uintptr_t)V) | ((uintptr_t)W) | ((uintptr_t)c->d_ghost)) & 31);
+  const bool a32 = CW != 4 || (!c->spmm_lanes16 && !((((uintptr_t)V) | ((uintptr_t)W) | ((uintptr_t)c->d_ghost)) & 31));
   {
     LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (n + 1) + 16.0 * n * S);
     if (n == 0) {
@@ -1848,6 +1849,7 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_SPEC_END")) c->spec_end = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_SPMM_PF")) c->spmm_pf = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPMM_PFV")) c->spmm_pfv = std::atoi(e);
+  if (const char* e = std::getenv("LSBA_SPMM_LANES16")) c->spmm_lanes16 = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_HALO_OVERLAP")) c->halo_ovl = (e[0] == '1');

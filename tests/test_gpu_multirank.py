@@ -208,3 +208,55 @@ def test_force_comm_one_rank_nccl(L, twin, ip, devar):
     # one rank: the allreduce is the identity, the fused and unfused small steps agree bitwise
     assert np.linalg.norm(H2 - H1) <= 1e-13 * np.linalg.norm(H1)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("skel", ["cwy", "icwy", "irols", "bmgs", "pio"])
+@pytest.mark.parametrize("ip", ["cl", "gl"])
+def test_loopback_other_skeletons(L, skel, ip):
+    """The comparison / lagged skeletons (Alg 2, 4, 6, 7) through the P > 1 path: the same
+    decisions on every rank, converged, cycles within one of the one-rank run, X within 1e-8
+    when the counts agree."""
+    from lsba_inputs import make_twin
+    p = make_twin(5)
+
+    def fn(ctx, B, X, rank, rows):
+        info = ctx.solve(B, X, ctx.m_max, 1e-8, 2000, ip=ip, cond_threshold=1e8, skel=skel)
+        return info.as_dict(), X.cpu().numpy()
+
+    i1, X1 = single(L, p, fn)
+    out = run_ranks(L, p, 3, fn)
+    infos = [o[0] for o in out]
+    for r in range(1, 3):
+        for key in ("outcome", "cycles", "iterations", "nan_flags", "true_relres", "syncs"):
+            assert infos[r][key] == infos[0][key], key
+    i2 = infos[0]
+    X = np.concatenate([o[1] for o in out])
+    assert i2["outcome"] == L.LSBA_CONVERGED and i2["true_relres"] <= p.tol
+    assert abs(i2["cycles"] - i1["cycles"]) <= 1
+    if (i2["cycles"], i2["iterations"]) == (i1["cycles"], i1["iterations"]):
+        assert np.linalg.norm(X - X1) <= 1e-8 * np.linalg.norm(X1)
+        assert i2["syncs"] == i1["syncs"]          # the paper's counters do not depend on P
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_ilu0_block_jacobi(L, P):
+    """Left ILU(0) at P > 1 is block-Jacobi ILU(0) of the local diagonal blocks (R28): every rank
+    takes the same decisions and the solve converges in the preconditioned norm; the plain
+    residual of X is checked with the oracle's SpMM."""
+    from lsba_inputs import make_twin
+    from oracle import lsba_oracle as O
+    p = make_twin(5)
+
+    def fn(ctx, B, X, rank, rows):
+        info = ctx.solve(B, X, ctx.m_max, 1e-8, 2000, ip="cl", cond_threshold=1e8, prec="ilu0")
+        return info.as_dict(), X.cpu().numpy()
+
+    out = run_ranks(L, p, P, fn)
+    infos = [o[0] for o in out]
+    for r in range(1, P):
+        for key in ("outcome", "cycles", "iterations", "true_relres"):
+            assert infos[r][key] == infos[0][key], key
+    assert infos[0]["outcome"] == L.LSBA_CONVERGED
+    X = np.concatenate([o[1] for o in out])
+    rel = np.linalg.norm(p.B - O.spmm(p.row_ptr, p.col_idx, p.vals, X)) / np.linalg.norm(p.B)
+    assert rel <= 1e-6            # (tol 1e-8 holds in the block-Jacobi-preconditioned norm)
