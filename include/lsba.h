@@ -27,6 +27,7 @@
 #ifndef LSBA_H
 #define LSBA_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -124,6 +125,26 @@ lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
                         int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
                         const uint8_t* nccl_id, int32_t device, void* cuda_stream);
 lsba_status lsba_destroy(lsba_ctx ctx);
+
+/* Caller-owned workspace: the same as lsba_create, but every long-lived device
+ * buffer of the context (CSR, basis slots, Gram partials, small state; lsba_workspace_bytes
+ * reports the total afterwards) is obtained from the caller's allocator — e.g. PyTorch's
+ * caching allocator (the Python binding's Context(..., allocator="torch")).
+ *   alloc(bytes, device, stream, user): device memory, >= 256-byte aligned, NULL on failure
+ *     (-> LSBA_E_OOM); stream is the context's stream;
+ *   free(ptr, device, stream, user): called once per buffer by lsba_destroy, after the
+ *     context's streams have drained.
+ * Transient create-time buffers, pinned host words and NCCL's own memory stay with CUDA/NCCL. */
+typedef struct {
+  void* (*alloc)(size_t bytes, int32_t device, void* stream, void* user);
+  void (*free)(void* ptr, int32_t device, void* stream, void* user);
+  void* user;
+} lsba_allocator;
+lsba_status lsba_create_with_allocator(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                                       const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
+                                       int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
+                                       const uint8_t* nccl_id, int32_t device, void* cuda_stream,
+                                       const lsba_allocator* allocator);
 
 /* Distributed code path on ONE rank: with LSBA_FORCE_COMM=1 in the environment, lsba_create on
  * nranks == 1 builds a one-rank NCCL communicator and runs exactly the P > 1 code path (every

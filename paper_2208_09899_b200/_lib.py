@@ -50,6 +50,32 @@ class SolveInfo(C.Structure):
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+
+# lsba_allocator (include/lsba.h): the caller-owned workspace variant of lsba_create
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("user", C.c_void_p)]
+
+
+def torch_allocator():
+    """An lsba_allocator backed by PyTorch's caching allocator (torch owns the workspace)."""
+    import torch
+
+    def _alloc(nbytes, device, stream, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), int(device), int(stream or 0))
+        except Exception:           # (OOM -> NULL -> LSBA_E_OOM)
+            return None
+
+    def _free(ptr, device, stream, user):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    a = Allocator(_ALLOC_FN(_alloc), _FREE_FN(_free), None)
+    a._keep = (_alloc, _free)      # the Python callables must outlive the context
+    return a
 _sigs = {
     "lsba_get_unique_id": [_vp],
     "lsba_create": [C.POINTER(_vp), _i64, _i32, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _i32, _vp],
@@ -57,6 +83,8 @@ _sigs = {
     "lsba_loopback_create": [_i32, C.POINTER(_vp)],
     "lsba_loopback_destroy": [_vp],
     "lsba_create_loopback": [C.POINTER(_vp), _i64, _i32, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _i32, _vp],
+    "lsba_create_with_allocator": [C.POINTER(_vp), _i64, _i32, _i32, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp,
+                                   _i32, _vp, _vp],
     "lsba_arnoldi_begin": [_vp, _vp, C.c_int, C.POINTER(_i32)],
     "lsba_block_arnoldi_step": [_vp, C.POINTER(StepInfo)],
     "lsba_copy_hessenberg": [_vp, _vp, _i32],
@@ -150,10 +178,17 @@ def lsba_create_loopback(n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end
                        device=device, stream=stream, loopback=group)
 
 
+def lsba_create_with_allocator(n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks,
+                               nccl_id, device, stream, allocator):
+    return lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks, nccl_id,
+                       device, stream, allocator=allocator)
+
+
 def lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin=0, row_end=None, rank=0, nranks=1,
-                nccl_id=None, device=0, stream=None, loopback=None):
+                nccl_id=None, device=0, stream=None, loopback=None, allocator=None):
     """row_ptr/col_idx/vals: host numpy (int64 / int32 global cols / float64) for the local rows.
-    loopback: a group from lsba_loopback_create (then nccl_id is not used)."""
+    loopback: a group from lsba_loopback_create (then nccl_id is not used).
+    allocator: an Allocator (e.g. torch_allocator()) that owns the workspace."""
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
     col_idx = np.ascontiguousarray(col_idx, dtype=np.int32)
     vals = np.ascontiguousarray(vals, dtype=np.float64)
@@ -163,7 +198,11 @@ def lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin=0, row_end=None, 
     idbuf = None
     if nccl_id is not None:
         idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
-    if loopback is not None:
+    if allocator is not None:
+        st = lib.lsba_create_with_allocator(C.byref(ctx), int(n), int(s), int(m_max), _hptr(row_ptr), _hptr(col_idx),
+                                            _hptr(vals), int(row_begin), int(row_end), int(rank), int(nranks), idbuf,
+                                            int(device), C.c_void_p(stream or 0), C.byref(allocator))
+    elif loopback is not None:
         st = lib.lsba_create_loopback(C.byref(ctx), int(n), int(s), int(m_max), _hptr(row_ptr), _hptr(col_idx),
                                       _hptr(vals), int(row_begin), int(row_end), int(rank), int(nranks),
                                       loopback, int(device), C.c_void_p(stream or 0))
@@ -371,7 +410,7 @@ class Context:
     """RAII wrapper: one context (one rank's rows) on one device."""
 
     def __init__(self, n, s, m_max, row_ptr, col_idx, vals, row_begin=0, row_end=None, rank=0,
-                 nranks=1, nccl_id=None, device=None, stream=None, loopback=None):
+                 nranks=1, nccl_id=None, device=None, stream=None, loopback=None, allocator=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2208_09899_b200 needs a CUDA device (no CPU fallback)")
@@ -383,8 +422,10 @@ class Context:
         self.row_end = n if row_end is None else row_end
         self.n_local = self.row_end - self.row_begin
         self.device = device
+        # allocator="torch": PyTorch's caching allocator owns the workspace (lsba_create_with_allocator)
+        self.allocator = torch_allocator() if allocator == "torch" else allocator
         self.ctx = lsba_create(n, s, m_max, row_ptr, col_idx, vals, row_begin, self.row_end, rank,
-                               nranks, nccl_id, device, stream, loopback)
+                               nranks, nccl_id, device, stream, loopback, self.allocator)
 
     def close(self):
         if getattr(self, "ctx", None):

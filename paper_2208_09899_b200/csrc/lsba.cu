@@ -156,6 +156,9 @@ struct lsba_ctx_ {
   int skel_default = LSBA_SKEL_BCGS_PIP;  // lsba_set_skeleton: step API and lsba_solve_host
   int64_t launches = 0;
   int64_t ws_bytes = 0;
+  lsba_allocator alloc{};          // lsba_create_with_allocator: the caller owns the workspace
+  bool has_alloc = false;
+  std::vector<void*> owned;
   std::string err;
   Prof prof;
 };
@@ -1467,12 +1470,23 @@ extern "C" lsba_status lsba_get_unique_id(uint8_t id[128]) {
   return LSBA_OK;
 }
 
-template <typename T>
-static lsba_status dalloc(lsba_ctx c, T** p, size_t count) {
-  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
-  CK(cudaMalloc((void**)p, bytes));
+// Every long-lived device buffer of a context comes from here: cudaMalloc, or the caller's
+// allocator (lsba_create_with_allocator, e.g. PyTorch's caching allocator).
+static lsba_status dalloc_bytes(lsba_ctx c, void** p, size_t bytes) {
+  if (c->has_alloc) {
+    *p = c->alloc.alloc(bytes, c->device, (void*)c->stream, c->alloc.user);
+    if (!*p) return fail(c, LSBA_E_OOM, "caller allocator returned NULL for %zu bytes", bytes);
+    c->owned.push_back(*p);
+    if ((uintptr_t)*p & 255) return fail(c, LSBA_E_ARG, "caller allocator: buffer not 256-byte aligned");
+  } else {
+    CK(cudaMalloc(p, bytes));
+  }
   c->ws_bytes += (int64_t)bytes;
   return LSBA_OK;
+}
+template <typename T>
+static lsba_status dalloc(lsba_ctx c, T** p, size_t count) {
+  return dalloc_bytes(c, (void**)p, std::max<size_t>(count, 1) * sizeof(T));
 }
 
 // The persisting-L2 limit is device state shared by every context on the device: reference-
@@ -1517,8 +1531,16 @@ static void release(lsba_ctx c) {
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
                   c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL,
                   c->d_ordU, c->d_ticket, c->d_ilu_tmp};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  // (the caller's allocator may hand the memory to other work at once: drain our streams first)
+  cudaStreamSynchronize(c->stream);
+  if (c->stream2) cudaStreamSynchronize(c->stream2);
+  if (c->cstream) cudaStreamSynchronize(c->cstream);
+  if (c->has_alloc) {
+    for (void* p : c->owned) c->alloc.free(p, c->device, (void*)c->stream, c->alloc.user);
+  } else {
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_info) cudaFreeHost(c->h_info);
   if (c->h_scalar) cudaFreeHost(c->h_scalar);
@@ -1670,8 +1692,7 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
     const size_t ci_bytes = ((std::max<int64_t>(c->nnz, 1) * sizeof(int32_t)) + 255) / 256 * 256;
     const size_t bytes = ci_bytes + std::max<int64_t>(c->nnz, 1) * sizeof(double);
     char* base = nullptr;
-    CK(cudaMalloc((void**)&base, bytes));
-    c->ws_bytes += (int64_t)bytes;
+    TRY(dalloc_bytes(c, (void**)&base, bytes));
     c->d_ci = reinterpret_cast<int*>(base);
     c->d_va = reinterpret_cast<double*>(base + ci_bytes);
     c->csr_bytes = bytes;
@@ -1834,7 +1855,8 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
 static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
                               const int64_t* row_ptr, const int32_t* col_idx, const double* vals,
                               int64_t row_begin, int64_t row_end, int32_t rank, int32_t nranks,
-                              const uint8_t* nccl_id, LoopGroup* loop, int32_t device, void* cuda_stream) {
+                              const uint8_t* nccl_id, LoopGroup* loop, int32_t device, void* cuda_stream,
+                              const lsba_allocator* allocator = nullptr) {
   if (!out) return LSBA_E_ARG;
   *out = nullptr;
   lsba_ctx c = new (std::nothrow) lsba_ctx_();
@@ -1864,6 +1886,11 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (!row_ptr || (!col_idx && row_end > row_begin)) return fail(c, LSBA_E_ARG, "CSR arrays NULL");
   c->device = device;
   c->stream = (cudaStream_t)cuda_stream;
+  if (allocator) {
+    if (!allocator->alloc || !allocator->free) return fail(c, LSBA_E_ARG, "allocator without alloc/free");
+    c->alloc = *allocator;
+    c->has_alloc = true;
+  }
   c->n_global = n;
   c->row_begin = row_begin;
   c->row_end = row_end;
@@ -1881,6 +1908,17 @@ extern "C" lsba_status lsba_create(lsba_ctx* out, int64_t n, int32_t s, int32_t 
                                    const uint8_t* nccl_id, int32_t device, void* cuda_stream) {
   return create_any(out, n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks, nccl_id,
                     nullptr, device, cuda_stream);
+}
+
+extern "C" lsba_status lsba_create_with_allocator(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max,
+                                                  const int64_t* row_ptr, const int32_t* col_idx,
+                                                  const double* vals, int64_t row_begin, int64_t row_end,
+                                                  int32_t rank, int32_t nranks, const uint8_t* nccl_id,
+                                                  int32_t device, void* cuda_stream,
+                                                  const lsba_allocator* allocator) {
+  if (!allocator) return LSBA_E_ARG;
+  return create_any(out, n, s, m_max, row_ptr, col_idx, vals, row_begin, row_end, rank, nranks, nccl_id,
+                    nullptr, device, cuda_stream, allocator);
 }
 
 struct lsba_loopback_ {

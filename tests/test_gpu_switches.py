@@ -104,3 +104,31 @@ def test_singular_cycle_end_keeps_last_good_x(L, spec, sing_cycle, max_restarts)
     assert np.all(np.isfinite(X))
     assert np.array_equal(X, Xref)            # bitwise: the same deterministic kernels
     assert info.true_relres == pytest.approx(iref.true_relres, rel=1e-12)
+
+
+def test_caller_allocator_owns_workspace(L):
+    """lsba_create_with_allocator (SURVEY.md 8(b)'s caller-owned workspace): with PyTorch's
+    caching allocator the context's device buffers are torch's (memory_allocated grows by the
+    workspace and falls back after destroy), and the solve is bitwise the default one."""
+    import torch
+    from lsba_inputs import make_twin
+    p = make_twin(5)
+    with L.Context(p.n, p.s, p.m, p.row_ptr, p.col_idx, p.vals) as ctx:
+        B = torch.from_numpy(p.B).cuda()
+        X0 = torch.zeros_like(B)
+        i0 = ctx.solve(B, X0, p.m, p.tol, 2000, cond_threshold=1e8)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    ctx = L.Context(p.n, p.s, p.m, p.row_ptr, p.col_idx, p.vals, allocator="torch")
+    try:
+        ws = L.lsba_workspace_bytes(ctx.ctx)
+        grown = torch.cuda.memory_allocated() - before
+        assert grown >= 0.9 * ws and ws > 8 * p.n * p.s * (p.m + 1)
+        X1 = torch.zeros_like(B)
+        i1 = ctx.solve(B, X1, p.m, p.tol, 2000, cond_threshold=1e8)
+        assert (i1.cycles, i1.iterations) == (i0.cycles, i0.iterations)
+        assert torch.equal(X0, X1)
+    finally:
+        ctx.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() - before < 0.1 * ws
