@@ -369,3 +369,25 @@ def test_profile_and_launch_counters(L):
         assert cnt >= info.iterations and ms > 0 and by > 0
         assert L.lsba_launch_count(ctx.ctx) >= info.kernel_launches > 0
         assert L.lsba_workspace_bytes(ctx.ctx) > 11 * n * s * 8
+
+
+def test_solve_count_agreement_rate(L):
+    """How often the GPU and the oracle take the same trajectory (reading R20 allows +-1 cycle
+    when a rounding-sensitive flag moves): over every SOLVE_CASES problem, both inner products
+    and both BGMRES / BFOM where listed, the (cycles, iterations) pairs must agree exactly in at
+    least 80% of the cases, and X within 1e-8 wherever they do (printed for the record)."""
+    from oracle import lsba_oracle as O
+    same, rows = 0, []
+    for name, ip, mod, tau in SOLVE_CASES:
+        A, B, p = get_problem(name)
+        Xo, io = O.solve(A, B, m=p.m, tol=p.tol, max_restarts=2000, ip=ip, mod=mod, cond_threshold=tau)
+        Xg, ig = run_gpu_solve(L, A, B, p.m, p.tol, 2000, ip, mod, tau)
+        agree = (ig.cycles, ig.iterations) == (io.cycles, io.iterations)
+        same += agree
+        rel = np.linalg.norm(Xg - Xo) / np.linalg.norm(Xo)
+        rows.append((name, ip, mod, (ig.cycles, ig.iterations), (io.cycles, io.iterations), rel))
+        if agree:
+            assert rel <= 1e-8, rows[-1]
+    for r in rows:
+        print("solve", r)
+    assert same >= 0.8 * len(SOLVE_CASES), rows
