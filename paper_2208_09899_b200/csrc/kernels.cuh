@@ -289,6 +289,36 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
   }
 }
 
+// P > 1 without a contiguous interior block (config 4's random columns): the SpMM runs on the
+// local-column part of A while the halo is in flight, then this kernel adds the ghost-column
+// part of the rows that have one: W[row] += sum over the row's ghost entries (ghost index c,
+// Vghost rows).  The row's sum is then local entries (CSR order) + ghost entries (CSR order).
+template <int S>
+__global__ void __launch_bounds__(kThreads)
+k_spmm_ghost_acc(int ng, const int* __restrict__ rows, const int* __restrict__ rp, const int* __restrict__ ci,
+                 const double* __restrict__ va, const double* __restrict__ Vghost, double* __restrict__ W,
+                 const int* __restrict__ active) {
+  pdl_begin();
+  if (active && *active == 0) return;
+  constexpr int C = (S % 2 == 0) ? 2 : 1;
+  constexpr int L = S / C;
+  const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (int)(gt / L), lane = (int)(gt % L);
+  if (t >= ng) return;
+  double acc[C];
+#pragma unroll
+  for (int q = 0; q < C; ++q) acc[q] = 0.0;
+  for (int p = rp[t]; p < rp[t + 1]; ++p) {
+    const double a = __ldg(va + p);
+    const double* src = Vghost + (size_t)__ldg(ci + p) * S + C * lane;
+#pragma unroll
+    for (int q = 0; q < C; ++q) acc[q] = fma(a, __ldg(src + q), acc[q]);
+  }
+  double* dst = W + (size_t)rows[t] * S + C * lane;
+#pragma unroll
+  for (int q = 0; q < C; ++q) dst[q] += acc[q];
+}
+
 // odd s: one thread per row, scalar column loads
 template <int S, bool RESID>
 __global__ void __launch_bounds__(kThreads)

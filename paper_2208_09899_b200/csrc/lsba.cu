@@ -133,6 +133,11 @@ struct lsba_ctx_ {
   cudaStream_t cstream = nullptr;  // P > 1: halo exchange stream (overlaps the interior SpMM)
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   int int0 = 0, int1 = 0;          // contiguous interior rows (no ghost columns); int1 > int0: overlap
+  // no interior block (random columns): local/ghost split of A for the overlap (P > 1)
+  bool split = false;
+  int* d_rpL = nullptr; int* d_ciL = nullptr; double* d_vaL = nullptr;   // local columns, all rows
+  int ng_rows = 0;
+  int* d_rowsG = nullptr; int* d_rpG = nullptr; int* d_ciG = nullptr; double* d_vaG = nullptr;
   bool halo_ovl = true;            // LSBA_HALO_OVERLAP
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
   bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
@@ -375,7 +380,8 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
   // but the boundary planes of a z-slab): the halo moves on the comm stream while the interior
   // rows compute; the boundary rows follow once it has arrived
   const bool ovl = c->comm && c->halo_ovl && c->int1 > c->int0;
-  TRY(halo_t<S>(c, V, ovl));
+  const bool split = c->split;
+  TRY(halo_t<S>(c, V, ovl || split));
   // 32-byte lanes need 32-byte aligned rows (basis slots always are; caller buffers of
   // lsba_spmm / the residual may only be 16-byte aligned: then 16-byte lanes)
   constexpr int CW = SpmmLanes<S>::C;
@@ -383,10 +389,10 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
   {
     LaunchScope Ls(c, LSBA_K_SPMM, 12.0 * c->nnz + 4.0 * (n + 1) + 16.0 * n * S);
     if (n == 0) {
-      if (ovl) CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+      if (ovl || split) CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
       return LSBA_OK;
     }
-    auto rows = [&](int r0, int r1) -> lsba_status {
+    auto rows = [&](int r0, int r1, const int* rp, const int* ci, const double* va) -> lsba_status {
       if (r1 <= r0) return LSBA_OK;
       if constexpr (S % 2 == 0 || S == 1) {
         constexpr int CW2 = (CW == 4) ? 2 : CW;
@@ -394,25 +400,37 @@ static lsba_status spmm_t(lsba_ctx c, const double* V, double* W, const int* act
         const int L = S / (a32 ? CW : CW2);
         c->in_spmm = true;
         const cudaError_t le = launch_k(c, kern, dim3(cdiv((long)(r1 - r0) * L, kThreads)),
-                    dim3(kThreads), 0, n, (const int*)c->d_rp, (const int*)c->d_ci, (const double*)c->d_va, V,
+                    dim3(kThreads), 0, n, rp, ci, va, V,
                     (const double*)c->d_ghost, (const double*)nullptr, W, (double*)nullptr, active,
                     c->spmm_pf, c->spmm_pfv, r0, r1);
         c->in_spmm = false;
         CK(le);
       } else {
         k_spmm_odd<S, false><<<cdiv(r1 - r0, kThreads), kThreads, 0, c->stream>>>(
-            n, c->d_rp, c->d_ci, c->d_va, V, c->d_ghost, nullptr, W, nullptr, active, r0, r1);
+            n, rp, ci, va, V, c->d_ghost, nullptr, W, nullptr, active, r0, r1);
       }
       CKL();
       return LSBA_OK;
     };
-    if (!ovl) {
-      TRY(rows(0, n));
-    } else {
-      TRY(rows(c->int0, c->int1));
+    const int* rp = c->d_rp;
+    const int* ci = c->d_ci;
+    const double* va = c->d_va;
+    if (!ovl && !split) {
+      TRY(rows(0, n, rp, ci, va));
+    } else if (ovl) {
+      TRY(rows(c->int0, c->int1, rp, ci, va));
       CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
-      TRY(rows(0, c->int0));
-      TRY(rows(c->int1, n));
+      TRY(rows(0, c->int0, rp, ci, va));
+      TRY(rows(c->int1, n, rp, ci, va));
+    } else {                        // local columns of every row, then the ghost part
+      TRY(rows(0, n, c->d_rpL, c->d_ciL, c->d_vaL));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+      if (c->ng_rows > 0) {
+        constexpr int LG = (S % 2 == 0) ? S / 2 : S;
+        CK(launch_k(c, k_spmm_ghost_acc<S>, dim3(cdiv((long)c->ng_rows * LG, kThreads)), dim3(kThreads), 0,
+                    c->ng_rows, (const int*)c->d_rowsG, (const int*)c->d_rpG, (const int*)c->d_ciG,
+                    (const double*)c->d_vaG, (const double*)c->d_ghost, W, active));
+      }
     }
   }
   if (c->prec) TRY(ilu_apply_t<S>(c, W, active));
@@ -1530,7 +1548,8 @@ static void release(lsba_ctx c) {
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
                   c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL,
-                  c->d_ordU, c->d_ticket, c->d_ilu_tmp};
+                  c->d_ordU, c->d_ticket, c->d_ilu_tmp, c->d_rpL, c->d_ciL, c->d_vaL, c->d_rowsG,
+                  c->d_rpG, c->d_ciG, c->d_vaG};
   // (the caller's allocator may hand the memory to other work at once: drain our streams first)
   cudaStreamSynchronize(c->stream);
   if (c->stream2) cudaStreamSynchronize(c->stream2);
@@ -1701,6 +1720,52 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   if (c->nnz) {
     CK(cudaMemcpy(c->d_ci, col_local.data(), sizeof(int32_t) * c->nnz, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->d_va, vals, sizeof(double) * c->nnz, cudaMemcpyHostToDevice));
+  }
+  if (c->comm && c->halo_ovl && c->int1 <= c->int0 && c->n_ghost > 0) {
+    // local / ghost split of the local rows (overlap config 4's ghost
+    // exchange with the band part of the SpMM)
+    std::vector<int32_t> rpL(n_local + 1, 0), ciL, rowsG, rpG(1, 0), ciG;
+    std::vector<double> vaL, vaG;
+    ciL.reserve(c->nnz);
+    vaL.reserve(c->nnz);
+    for (int64_t r = 0; r < n_local; ++r) {
+      bool has_g = false;
+      for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; ++p) {
+        if (col_local[p] < n_local) {
+          ciL.push_back(col_local[p]);
+          vaL.push_back(vals[p]);
+        } else {
+          ciG.push_back((int32_t)(col_local[p] - n_local));
+          vaG.push_back(vals[p]);
+          has_g = true;
+        }
+      }
+      rpL[r + 1] = (int32_t)ciL.size();
+      if (has_g) {
+        rowsG.push_back((int32_t)r);
+        rpG.push_back((int32_t)ciG.size());
+      }
+    }
+    c->ng_rows = (int)rowsG.size();
+    TRY(dalloc(c, &c->d_rpL, n_local + 1));
+    TRY(dalloc(c, &c->d_ciL, ciL.size()));
+    TRY(dalloc(c, &c->d_vaL, vaL.size()));
+    TRY(dalloc(c, &c->d_rowsG, rowsG.size()));
+    TRY(dalloc(c, &c->d_rpG, rpG.size()));
+    TRY(dalloc(c, &c->d_ciG, ciG.size()));
+    TRY(dalloc(c, &c->d_vaG, vaG.size()));
+    CK(cudaMemcpy(c->d_rpL, rpL.data(), sizeof(int32_t) * rpL.size(), cudaMemcpyHostToDevice));
+    if (!ciL.empty()) {
+      CK(cudaMemcpy(c->d_ciL, ciL.data(), sizeof(int32_t) * ciL.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->d_vaL, vaL.data(), sizeof(double) * vaL.size(), cudaMemcpyHostToDevice));
+    }
+    if (!rowsG.empty()) {
+      CK(cudaMemcpy(c->d_rowsG, rowsG.data(), sizeof(int32_t) * rowsG.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->d_rpG, rpG.data(), sizeof(int32_t) * rpG.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->d_ciG, ciG.data(), sizeof(int32_t) * ciG.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->d_vaG, vaG.data(), sizeof(double) * vaG.size(), cudaMemcpyHostToDevice));
+    }
+    c->split = true;
   }
   if (c->l2persist != 0 && c->nnz > 0 && !c->comm) {
     // The SpMM's column indices and values (constant across the solve) are kept in an L2

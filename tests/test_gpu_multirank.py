@@ -132,13 +132,14 @@ CASES = [(5, "cl", 2), (5, "cl", 3), (5, "cl", 4), (2, "cl", 2), (2, "cl", 4), (
          (3, "cl", 3)]
 
 
+@pytest.mark.parametrize("ovl", ["1", "0"])
 @pytest.mark.parametrize("twin,ip,P", CASES)
-def test_loopback_steps_match_single_rank(L, twin, ip, P):
+def test_loopback_steps_match_single_rank(L, twin, ip, P, ovl):
     from lsba_inputs import make_twin
     p = make_twin(twin)
     K = 5
     H1, V1 = single(L, p, steps_fn(ip, K))
-    out = run_ranks(L, p, P, steps_fn(ip, K))
+    out = run_ranks(L, p, P, steps_fn(ip, K), env={"LSBA_HALO_OVERLAP": ovl})
     b = p.s if ip == "cl" else 1
     for r in range(1, P):                 # replicated small state: identical on every rank
         assert np.array_equal(out[r][0], out[0][0])
@@ -154,6 +155,7 @@ def test_loopback_steps_match_single_rank(L, twin, ip, P):
         assert np.linalg.norm(Vj - V1[j]) <= tol * np.linalg.norm(V1[j]), j
 
 
+# (the random twin has no interior block: with the overlap on it runs the local/ghost split)
 SOLVES = [(5, "cl", 2, 1e8), (5, "cl", 3, 1e8), (2, "cl", 4, float("inf")), (4, "gl", 2, float("inf")),
           (4, "cl", 3, float("inf")), (3, "cl", 2, 1e8)]
 
