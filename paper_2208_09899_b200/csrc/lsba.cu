@@ -959,7 +959,10 @@ static bool throttle(lsba_ctx c, int k) {
     const int done = v < 0 ? -1 : (v >> 1), act = v < 0 ? 1 : (v & 1);
     if (done >= 0 && act == 0) return single ? false : (k <= done + kLookahead);
     if (k <= kLookahead || done >= k - kLookahead) return true;
-    if (single && cudaStreamQuery(c->stream) == cudaSuccess) return true;   // (device drained: no stall)
+    // device drained (no stall possible) or failed (the error surfaces at the next CUDA call):
+    // stop polling.  (On P > 1 a drained stream has decided every enqueued step, so the
+    // conditions above already hold unless the device failed.)
+    if (cudaStreamQuery(c->stream) != cudaErrorNotReady) return true;
   }
 }
 
