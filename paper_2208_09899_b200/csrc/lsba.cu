@@ -144,6 +144,7 @@ struct lsba_ctx_ {
   int spmm_pf = -1;              // SpMM L2 prefetch distance in CTAs (-1: 4 x SMs; LSBA_SPMM_PF)
   int spmm_pfv = 1;              // ... and of the CTA's V rows (LSBA_SPMM_PFV)
   bool spmm_lanes16 = false;     // diagnostics: LSBA_SPMM_LANES16=1 forces 16-byte SpMM lanes
+  bool proj_dfma = false;        // diagnostics: LSBA_PROJ_DFMA=1 uses the DFMA projection at s = 8, 16
   bool force_comm = false;       // LSBA_FORCE_COMM=1: one rank through the distributed code path
   int force_sing_cycle = 0;      // test hook: the cycle end of this cycle reports singular
   int cur_cycle = 0;
@@ -698,7 +699,7 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
   // s = 4: the DFMA kernel streams faster than the DMMA one (5.8 vs 5.0 TB/s on config 2,
   // profiles/r01_variants.md); s = 8, 16: DMMA (6.65 TB/s on configs 3 and 5)
   if constexpr (S == 8 || S == 16) {
-    if (!gl && c->variant == 0) {
+    if (!gl && c->variant == 0 && !c->proj_dfma) {
       auto fn = k_project_dmma<S>;
       if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int occ = 1;
@@ -1940,6 +1941,7 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_SPMM_PF")) c->spmm_pf = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPMM_PFV")) c->spmm_pfv = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPMM_LANES16")) c->spmm_lanes16 = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_PROJ_DFMA")) c->proj_dfma = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_HALO_OVERLAP")) c->halo_ovl = (e[0] == '1');
