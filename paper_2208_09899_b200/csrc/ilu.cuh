@@ -3,8 +3,8 @@
 //
 //   k_ilu0_level   one level of the IKJ factorisation, a warp per row (setup, once per matrix)
 //   k_ilu_trsv_poll  (default) sync-free sparse triangular solve Z = L^{-1} X or U^{-1} X, one
-//                  thread per row (all s columns), rows in level order claimed chunk by chunk
-//                  by a persistent grid, dependencies detected by polling the data itself
+//                  thread per row (all s columns), rows in level order claimed 32 at a time by
+//                  the warps of a persistent grid, dependencies detected by polling the data itself
 //                  (sentinel-filled output); measured 4.3 / 11 / 12 us per level on configs
 //                  2 / 3 / 5 vs 6.9 / 25 / 56 with per-row ready flags and 17 / 46 / 72 with
 //                  one CTA per chunk (round-1 variants, removed; profiles/r01_ilu_apply.txt)
@@ -72,49 +72,94 @@ __device__ __forceinline__ double ld_volatile_d(const double* p) {
   asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ double2 ld_volatile_d2(const double* p) {
+  double2 v;
+  asm volatile("ld.volatile.global.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool not_sentinel(double v) {
+  return (unsigned long long)__double_as_longlong(v) != kIluSentinel;
+}
 __global__ void k_fill_sentinel(long count, double* __restrict__ z) {
   const double v = __longlong_as_double((long long)kIluSentinel);
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < count; e += (long)gridDim.x * blockDim.x)
     z[e] = v;
 }
+// Persistent solve: each WARP claims the next chunk of 32 rows (level order) from a global
+// counter — no CTA barrier, so a warp never waits for the slowest row of a 256-row chunk — and
+// a row's dependencies are polled in batches of up to 4 at once (every S value of every
+// dependency in the batch loaded together, retried until none is the sentinel), so a ready
+// row costs one L2 round trip per batch instead of one per dependency.  Warps only wait on rows
+// of earlier chunks, claimed by warps that are already running: no deadlock.  The arithmetic
+// (CSR order over the dependencies, then the diagonal) is the round-1 kernel's.
 template <int S, bool LOWER>
 __global__ void __launch_bounds__(256)
 k_ilu_trsv_poll(int nrows, const int* __restrict__ order, const int* __restrict__ rp,
                 const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
                 int n_local, const double* __restrict__ X, double* Z, unsigned* ctr,
-                const int* __restrict__ active) {
-  __shared__ int chunk;
+                const int* __restrict__ active, int backoff_ns) {
   const bool live = !(active && *active == 0);
-  const int nchunks = (nrows + blockDim.x - 1) / blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int nchunks = (nrows + 31) / 32;
+  constexpr int DB = 4;                       // dependencies polled per batch
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) chunk = live ? (int)atomicAdd(ctr, 1u) : nchunks;
-    __syncthreads();
+    int chunk = 0;
+    if (lane == 0) chunk = live ? (int)atomicAdd(ctr, 1u) : nchunks;
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
     if (chunk >= nchunks) break;
-    const int t = chunk * blockDim.x + threadIdx.x;
+    const int t = chunk * 32 + lane;
     if (t < nrows) {
       const int i = order[t];
       const int p0 = rp[i], p1 = rp[i + 1];
       double acc[S];
 #pragma unroll
       for (int c = 0; c < S; ++c) acc[c] = 0.0;
-      for (int p = p0; p < p1; ++p) {
-        const int k = ci[p];
-        if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
-        const double a = lu[p];
-        const double* zk = Z + (size_t)k * S;
-        double y[S];
-        for (;;) {
+      int p = p0;
+      while (p < p1) {
+        // next batch: up to DB dependency entries of this row (CSR order)
+        int ent[DB], nb = 0;
+        for (; p < p1 && nb < DB; ++p) {
+          const int k = ci[p];
+          if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
+          ent[nb++] = p;
+        }
+        double y[DB][S];
+        // (a failed poll backs off: thousands of spinning rows would otherwise saturate L2
+        // with requests and slow the rows they wait for)
+        for (int sleep_ns = backoff_ns;; sleep_ns = min(2 * sleep_ns, 1024)) {
           bool ok = true;
 #pragma unroll
-          for (int c = 0; c < S; ++c) {
-            y[c] = ld_volatile_d(zk + c);
-            ok = ok && ((unsigned long long)__double_as_longlong(y[c]) != kIluSentinel);
+          for (int d = 0; d < DB; ++d) {
+            if (d < nb) {
+              const double* zk = Z + (size_t)ci[ent[d]] * S;
+              if constexpr (S % 2 == 0) {
+#pragma unroll
+                for (int c = 0; c < S; c += 2) {
+                  const double2 v = ld_volatile_d2(zk + c);
+                  y[d][c] = v.x;
+                  y[d][c + 1] = v.y;
+                  ok = ok && not_sentinel(v.x) && not_sentinel(v.y);
+                }
+              } else {
+#pragma unroll
+                for (int c = 0; c < S; ++c) {
+                  y[d][c] = ld_volatile_d(zk + c);
+                  ok = ok && not_sentinel(y[d][c]);
+                }
+              }
+            }
           }
           if (ok) break;
+          if (sleep_ns > 0) __nanosleep(sleep_ns);
         }
 #pragma unroll
-        for (int c = 0; c < S; ++c) acc[c] = fma(a, y[c], acc[c]);
+        for (int d = 0; d < DB; ++d) {
+          if (d < nb) {
+            const double a = lu[ent[d]];
+#pragma unroll
+            for (int c = 0; c < S; ++c) acc[c] = fma(a, y[d][c], acc[c]);
+          }
+        }
       }
       const double dinv = LOWER ? 1.0 : lu[diag[i]];
       double* zi = Z + (size_t)i * S;
@@ -125,6 +170,7 @@ k_ilu_trsv_poll(int nrows, const int* __restrict__ order, const int* __restrict_
       }
     }
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned e = atomicAdd(ctr + 1, 1u);
     if (e == gridDim.x - 1) {

@@ -128,6 +128,7 @@ struct lsba_ctx_ {
   double* d_ilu_tmp = nullptr;   // n x s intermediate of the data-polling variant
   unsigned* d_ticket = nullptr;  // CTA start tickets (2: L and U solves)
   int ilu_levels[2] = {0, 0};
+  int ilu_backoff = 0;           // ns of the first back-off after a failed dependency poll (LSBA_ILU_BACKOFF)
   int ilu_ctas = 1;              // persistent CTAs per SM (LSBA_ILU_CTAS)
   cudaEvent_t ev_status = nullptr;
   cudaStream_t cstream = nullptr;  // P > 1: halo exchange stream (overlaps the interior SpMM)
@@ -359,14 +360,14 @@ static lsba_status ilu_apply_t(lsba_ctx c, double* Y, const int* active) {
     LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
     k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, c->d_ilu_tmp);
     k_ilu_trsv_poll<S, true><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordL, c->d_rp, c->d_ci,
-        c->d_lu, c->d_diag, c->n, Y, c->d_ilu_tmp, c->d_ticket, active);
+        c->d_lu, c->d_diag, c->n, Y, c->d_ilu_tmp, c->d_ticket, active, c->ilu_backoff);
     CKL();
   }
   {
     LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
     k_fill_sentinel<<<fgrid, kThreads, 0, c->stream>>>(cnt, Y);
     k_ilu_trsv_poll<S, false><<<grid, kThreads, 0, c->stream>>>(c->n, c->d_ordU, c->d_rp, c->d_ci,
-        c->d_lu, c->d_diag, c->n, c->d_ilu_tmp, Y, c->d_ticket + 2, active);
+        c->d_lu, c->d_diag, c->n, c->d_ilu_tmp, Y, c->d_ticket + 2, active, c->ilu_backoff);
     CKL();
   }
   return LSBA_OK;
@@ -1943,6 +1944,7 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_SPMM_LANES16")) c->spmm_lanes16 = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_PROJ_DFMA")) c->proj_dfma = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("LSBA_ILU_BACKOFF")) c->ilu_backoff = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_HALO_OVERLAP")) c->halo_ovl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_DEVAR")) c->devar_req = (e[0] == '1');
