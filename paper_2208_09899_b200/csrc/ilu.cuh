@@ -102,15 +102,31 @@ k_ilu_trsv_poll(int nrows, const int* __restrict__ order, const int* __restrict_
   const int lane = threadIdx.x & 31;
   const int nchunks = (nrows + 31) / 32;
   constexpr int DB = 4;                       // dependencies polled per batch
+  // one chunk ahead: the next chunk is claimed, and its row index and row pointers loaded,
+  // before this chunk's dependencies are polled (the claim -> order -> row pointer chain leaves
+  // the critical path; a warp only ever waits inside its current, smaller chunk: no deadlock)
+  auto claim = [&]() {
+    int ch = 0;
+    if (lane == 0) ch = live ? (int)atomicAdd(ctr, 1u) : nchunks;
+    return __shfl_sync(0xffffffffu, ch, 0);
+  };
+  int nx = claim(), nx_i = 0, nx_p0 = 0, nx_p1 = 0;
+  auto meta = [&](int ch, int& i, int& q0, int& q1) {
+    const int t = ch * 32 + lane;
+    if (ch < nchunks && t < nrows) {
+      i = order[t];
+      q0 = rp[i];
+      q1 = rp[i + 1];
+    }
+  };
+  meta(nx, nx_i, nx_p0, nx_p1);
   for (;;) {
-    int chunk = 0;
-    if (lane == 0) chunk = live ? (int)atomicAdd(ctr, 1u) : nchunks;
-    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    const int chunk = nx, i = nx_i, p0 = nx_p0, p1 = nx_p1;
     if (chunk >= nchunks) break;
+    nx = claim();
+    meta(nx, nx_i, nx_p0, nx_p1);
     const int t = chunk * 32 + lane;
     if (t < nrows) {
-      const int i = order[t];
-      const int p0 = rp[i], p1 = rp[i + 1];
       double acc[S];
 #pragma unroll
       for (int c = 0; c < S; ++c) acc[c] = 0.0;
@@ -124,8 +140,7 @@ k_ilu_trsv_poll(int nrows, const int* __restrict__ order, const int* __restrict_
           ent[nb++] = p;
         }
         double y[DB][S];
-        // (a failed poll backs off: thousands of spinning rows would otherwise saturate L2
-        // with requests and slow the rows they wait for)
+        // (a failed poll may back off: LSBA_ILU_BACKOFF; measured neutral, default 0)
         for (int sleep_ns = backoff_ns;; sleep_ns = min(2 * sleep_ns, 1024)) {
           bool ok = true;
 #pragma unroll
