@@ -9,7 +9,7 @@
 // So: no shared-memory tiles and no barriers in the main loop; each warp keeps U 4-row steps
 // of loads in flight (issued together, then consumed), register budget sized for MINB CTAs of
 // 256 threads per SM; the CTA partial is reduced through shared memory in one ordered pass
-// and the cross-CTA reduction is the deterministic two-level tree of k_gram_v6.
+// and the cross-CTA reduction is a deterministic two-level ticketed tree.
 //
 // Fragment mapping (as v5/v6): lane (r4 = lane & 3, c8 = lane >> 2) loads a 16-byte column
 // pair (2cp, 2cp+1) of row r4 of a block and feeds two DMMAs (M tile "even" columns, M tile
