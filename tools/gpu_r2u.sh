@@ -1,0 +1,7 @@
+#!/bin/bash
+# sustained config-5 region: does the SpMM's instruction count move the power-capped clock?
+for env in "LSBA_SPMM_LANES16=0" "LSBA_SPMM_LANES16=1" "LSBA_SPMM_LANES16=0"; do
+  r=$(env $env timeout 400 python bench.py --steps 20 --warmup 5 --repeats 2 --no-cpu-baseline --no-e2e --no-sweep --no-tts 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), d['kernel_gbs'], d['repeats']['GBps'], d['clocks']['sm_mhz'])")
+  echo "config 5 [$env]: $r"
+done
+nvidia-smi --query-gpu=power.limit,power.draw,clocks.sm,clocks.mem --format=csv
