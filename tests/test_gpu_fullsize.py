@@ -79,11 +79,12 @@ def sub_csr(A, rows):
     return out_rp, ci[idx], va[idx]
 
 
-def run_steps(L, p, ip, K):
+def run_steps(L, p, ip, K, skel="pip"):
     """K GPU steps through the C ABI; returns (H, beta, [V_1..V_{K+1}] as device tensors)."""
     import torch
     b = p.s if ip == "cl" else 1
     with L.Context(p.n, p.s, p.m, p.row_ptr, p.col_idx, p.vals) as ctx:
+        L.lsba_set_skeleton(ctx.ctx, skel)
         B = torch.from_numpy(p.B).cuda()
         assert ctx.begin(B, ip) == 0
         infos = [ctx.step() for _ in range(K)]
@@ -94,18 +95,22 @@ def run_steps(L, p, ip, K):
     return H, beta, Vs
 
 
-STEP_CASES = [(2, "cl"), (3, "cl"), (4, "cl"), (4, "gl"), (5, "cl")]
+# (cfg, ip, skeleton): BCGS-PIP on every config; the NEXT skeletons (SURVEY.md 8(f) f1, f3:
+# BMGS-CWY / ICWY, Alg 6; BCGS-IRO-LS, Alg 7) on configs 3, 4 (gl) and 5
+STEP_CASES = [(2, "cl", "pip"), (3, "cl", "pip"), (4, "cl", "pip"), (4, "gl", "pip"), (5, "cl", "pip"),
+              (5, "cl", "cwy"), (3, "cl", "icwy"), (3, "cl", "irols"), (4, "gl", "cwy")]
 
 
-@pytest.mark.parametrize("cfg,ip", STEP_CASES, ids=lambda x: str(x))
-def test_fullsize_steps_vs_oracle(L, cfg, ip):
+@pytest.mark.parametrize("cfg,ip,skel", STEP_CASES, ids=lambda x: str(x))
+def test_fullsize_steps_vs_oracle(L, cfg, ip, skel):
     """5 free-running steps at full size vs the oracle's (goldens), normwise 1e-10."""
     import torch
-    g, meta = golden(f"c{cfg}_{ip}_steps")
+    g, meta = golden(f"c{cfg}_{ip}_steps" if skel == "pip" else f"c{cfg}_{ip}_{skel}_steps")
     p = problem(cfg)
     assert (meta["n"], meta["s"], meta["nnz"]) == (p.n, p.s, int(p.row_ptr[-1]))
+    assert meta.get("skel", "pip") == skel
     b = p.s if ip == "cl" else 1
-    H, beta, Vs = run_steps(L, p, ip, K)
+    H, beta, Vs = run_steps(L, p, ip, K, skel)
     tol = 1e-10
     assert np.linalg.norm(beta - g["beta"]) <= tol * np.linalg.norm(g["beta"])
     for k in range(K):

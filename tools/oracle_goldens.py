@@ -43,7 +43,23 @@ CASES = {
     "c5_cl_steps": (5, "cl", "steps"),
     "c4_cl_solve": (4, "cl", "solve"),
     "c4_gl_solve": (4, "gl", "solve"),
+    # the NEXT skeletons at full size: 5 free-running steps
+    "c5_cl_cwy_steps": (5, "cl", "steps", "cwy"),
+    "c3_cl_icwy_steps": (3, "cl", "steps", "icwy"),
+    "c3_cl_irols_steps": (3, "cl", "steps", "irols"),
+    "c4_gl_cwy_steps": (4, "gl", "steps", "cwy"),
 }
+
+
+def arnoldi(skel, A, ip, K, s):
+    """The oracle's skeleton objects (same begin/step/V/Hbar/beta interface)."""
+    if skel == "pip":
+        return O.PipArnoldi(A, ip, K, s)
+    if skel in ("cwy", "icwy"):
+        return O.CwyArnoldi(A, ip, K, s, inverse=(skel == "icwy"))
+    if skel == "irols":
+        return O.IrolsArnoldi(A, ip, K, s)
+    raise ValueError(skel)
 
 
 def sketch(V):
@@ -55,17 +71,18 @@ def sketch(V):
 
 
 def run_case(name):
-    cfg, ip, kind = CASES[name]
+    cfg, ip, kind = CASES[name][:3]
+    skel = CASES[name][3] if len(CASES[name]) > 3 else "pip"
     t0 = time.time()
     p = make_config(cfg)
     A = (p.row_ptr, p.col_idx, p.vals)
     n, s = p.B.shape
     b = s if ip == "cl" else 1
     rows = sample_rows(n)
-    meta = {"case": name, "config": cfg, "workload": p.name, "ip": ip, "n": n, "s": s, "m": p.m,
+    meta = {"case": name, "config": cfg, "workload": p.name, "ip": ip, "skel": skel, "n": n, "s": s, "m": p.m,
             "nnz": int(p.row_ptr[-1]), "written_by": "tools/oracle_goldens.py (oracle/ only)"}
     if kind == "steps":
-        arn = O.PipArnoldi(A, ip, K, s)
+        arn = arnoldi(skel, A, ip, K, s)
         assert not arn.begin(p.B)
         for k in range(K):
             assert not arn.step().flag, k
@@ -73,7 +90,9 @@ def run_case(name):
         out = dict(beta=np.asarray(arn.beta, dtype=np.float64), Hbar=arn.Hbar[:(K + 1) * b, :K * b].copy(),
                    vnorm=np.array([np.linalg.norm(v) for v in Vs]), rows=rows,
                    Vrows=np.stack([v[rows] for v in Vs]), sketch=np.stack([sketch(v) for v in Vs]))
-        meta.update(K=K, cite="Alg 3 PAPER.md:262-275; north star 5-step parity (BASELINE.json)")
+        meta.update(K=K, cite={"pip": "Alg 3 PAPER.md:262-275", "cwy": "Alg 6 PAPER.md:316-348",
+                               "icwy": "Alg 6 PAPER.md:316-348", "irols": "Alg 7 PAPER.md:350-379"}[skel]
+                    + "; north star 5-step parity (BASELINE.json)")
     else:
         X, info = O.solve(A, p.B, m=p.m, tol=p.tol, max_restarts=p.max_restarts, ip=ip, mod="gmres",
                           cond_threshold=p.cond_threshold)
