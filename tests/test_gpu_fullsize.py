@@ -96,9 +96,10 @@ def run_steps(L, p, ip, K, skel="pip"):
 
 
 # (cfg, ip, skeleton): BCGS-PIP on every config; the NEXT skeletons (SURVEY.md 8(f) f1, f3:
-# BMGS-CWY / ICWY, Alg 6; BCGS-IRO-LS, Alg 7) on configs 3, 4 (gl) and 5
+# BMGS-CWY / ICWY, Alg 6; BCGS-IRO-LS, Alg 7; BCGS-PIO, Alg 4; BMGS, Alg 2) on configs 3, 4 (gl), 5
 STEP_CASES = [(2, "cl", "pip"), (3, "cl", "pip"), (4, "cl", "pip"), (4, "gl", "pip"), (5, "cl", "pip"),
-              (5, "cl", "cwy"), (3, "cl", "icwy"), (3, "cl", "irols"), (4, "gl", "cwy")]
+              (5, "cl", "cwy"), (3, "cl", "icwy"), (3, "cl", "irols"), (4, "gl", "cwy"), (3, "cl", "pio"),
+              (3, "cl", "bmgs")]
 
 
 @pytest.mark.parametrize("cfg,ip,skel", STEP_CASES, ids=lambda x: str(x))

@@ -48,6 +48,8 @@ CASES = {
     "c3_cl_icwy_steps": (3, "cl", "steps", "icwy"),
     "c3_cl_irols_steps": (3, "cl", "steps", "irols"),
     "c4_gl_cwy_steps": (4, "gl", "steps", "cwy"),
+    "c3_cl_pio_steps": (3, "cl", "steps", "pio"),
+    "c3_cl_bmgs_steps": (3, "cl", "steps", "bmgs"),
 }
 
 
@@ -59,6 +61,10 @@ def arnoldi(skel, A, ip, K, s):
         return O.CwyArnoldi(A, ip, K, s, inverse=(skel == "icwy"))
     if skel == "irols":
         return O.IrolsArnoldi(A, ip, K, s)
+    if skel == "pio":
+        return O.PioArnoldi(A, ip, K, s)
+    if skel == "bmgs":
+        return O.BmgsArnoldi(A, ip, K, s)
     raise ValueError(skel)
 
 
@@ -91,7 +97,8 @@ def run_case(name):
                    vnorm=np.array([np.linalg.norm(v) for v in Vs]), rows=rows,
                    Vrows=np.stack([v[rows] for v in Vs]), sketch=np.stack([sketch(v) for v in Vs]))
         meta.update(K=K, cite={"pip": "Alg 3 PAPER.md:262-275", "cwy": "Alg 6 PAPER.md:316-348",
-                               "icwy": "Alg 6 PAPER.md:316-348", "irols": "Alg 7 PAPER.md:350-379"}[skel]
+                               "icwy": "Alg 6 PAPER.md:316-348", "irols": "Alg 7 PAPER.md:350-379",
+                               "pio": "Alg 4 PAPER.md:277-290", "bmgs": "Alg 2 PAPER.md:164-178"}[skel]
                     + "; north star 5-step parity (BASELINE.json)")
     else:
         X, info = O.solve(A, p.B, m=p.m, tol=p.tol, max_restarts=p.max_restarts, ip=ip, mod="gmres",
