@@ -148,7 +148,7 @@ lsba_status lsba_create_with_allocator(lsba_ctx* out, int64_t n, int32_t s, int3
 
 /* Distributed code path on ONE rank: with LSBA_FORCE_COMM=1 in the environment, lsba_create on
  * nranks == 1 builds a one-rank NCCL communicator and runs exactly the P > 1 code path (every
- * Gram through ncclAllReduce, the small step as its own launch, no speculative cycle end);
+ * Gram through ncclAllReduce, the small step as its own launch);
  * results match the default path to rounding. */
 
 /* Loopback group (testing the multi-rank path on one device): P contexts, each driven by its

@@ -1269,7 +1269,9 @@ static lsba_status solve_impl(lsba_ctx c, const double* B, double* X, int m, dou
     // status read, so the GPU solves the projected problem and combines while the host wakes
     // up; it no-ops on the device for any other ending, which the host then handles below
     const int par = cycle & 1;
-    const bool spec = c->spec_end && !c->comm && m_cur >= 1;
+    // (also on P > 1: the cycle end and the combine are row-local, no collective, and the
+    // device guard is a replicated decision, so every rank runs or skips them alike)
+    const bool spec = c->spec_end && m_cur >= 1;
     if (spec) {
       // the status is copied (and waited for) BEFORE the speculative kernels, so the host
       // decides while the GPU solves and combines, and enqueues the next cycle behind them
