@@ -54,15 +54,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 
 // Ordered sum over c < cnt of p[c * stride] (c ascending, the same rounding as a plain loop);
-// the loads are issued 16 at a time so the sum costs a few L2 round trips, not cnt of them.
+// the loads are issued BATCH at a time so the sum costs a few L2 round trips, not cnt of them
+// (the final level's 37 group partials: 2 round trips with batches of 20 instead of 3 with 16).
+template <int BATCH = 16>
 __device__ __forceinline__ double ordered_partial_sum(const double* p, size_t stride, int cnt) {
   double s = 0.0;
-  for (int c0 = 0; c0 < cnt; c0 += 16) {
-    double v[16];
+  for (int c0 = 0; c0 < cnt; c0 += BATCH) {
+    double v[BATCH];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) v[c] = (c0 + c < cnt) ? __ldcg(p + (size_t)(c0 + c) * stride) : 0.0;
+    for (int c = 0; c < BATCH; ++c) v[c] = (c0 + c < cnt) ? __ldcg(p + (size_t)(c0 + c) * stride) : 0.0;
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
+    for (int c = 0; c < BATCH; ++c)
       if (c0 + c < cnt) s += v[c];
   }
   return s;
@@ -342,7 +344,7 @@ k_gram_v7(GramArgs g, GramFuse f) {
   // where the small step reads G (no global round trip)
   const bool g_smem = f.on && passes == 1 && NY == 1;
   for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
-    const double s2 = ordered_partial_sum(g.gpart + e, E, ngroups);
+    const double s2 = ordered_partial_sum<20>(g.gpart + e, E, ngroups);
     g.G[e] = s2;
     if (g_smem) sm7[e] = s2;
   }
@@ -464,7 +466,7 @@ k_gram_gl2(GramArgs g, GramFuse f) {
   __syncthreads();
   if (ticket != (unsigned)(ngroups - 1)) return;
   for (int e = tid; e < E; e += blockDim.x)
-    g.G[e] = ordered_partial_sum(g.gpart + e, E, ngroups) * (1.0 / S);   // Table 1: (1/s) tr(X^T Y)
+    g.G[e] = ordered_partial_sum<20>(g.gpart + e, E, ngroups) * (1.0 / S);   // Table 1: (1/s) tr(X^T Y)
   if (tid == 0) g.tickets[ngroups] = 0u;
   (void)gsm;
   if (NY != 1 || !f.on) return;
