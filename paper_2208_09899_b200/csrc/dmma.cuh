@@ -40,6 +40,8 @@ struct GramArgs {
   double* G;               // result, E = J S S doubles, row-major [(j S + a) S + b]
   const int* active;       // nullable: skip when *active == 0
   const double* Y2 = nullptr;  // k_gram_v7<.., NY = 2>: second B-operand block, G = X^T [Y Y2]
+  int pf_batches = 0;          // k_gram_v7: row batches of the basis blocks prefetched into L2
+                               // before waiting on the SpMM (gram7.cuh)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -69,13 +71,19 @@ template <int S>
 __global__ void __launch_bounds__(256)
 k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
                const double* base0, double* out0, int J1, const double* __restrict__ C1, double* out1,
-               const int* __restrict__ flag_ptr) {
+               const int* __restrict__ flag_ptr, int pf_ctas = 0) {
   static_assert(S == 4 || S == 8 || S == 16, "DMMA projection for s in {4,8,16}");
-  pdl_begin();
-  if (flag_ptr && *flag_ptr) return;
   constexpr int KC = S / 4;                 // K chunks
   constexpr int NT = S >= 8 ? S / 8 : 1;    // N tiles
   constexpr int RB = S >= 16 ? 2 : 4;       // 8-row blocks per warp iteration
+  pdl_launch();
+  {  // the CTA's first grid-stride iteration: its 8 warps' super-blocks are contiguous rows
+    const long r0 = (long)blockIdx.x * (blockDim.x >> 5) * RB * 8;
+    prefetch_blocks_l2(pf_ctas, X, xstride, max(J0, J1), r0 * S,
+                       8L * S * (min((long)n, r0 + (long)(blockDim.x >> 5) * RB * 8) - r0));
+  }
+  pdl_wait();
+  if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   double* c0 = sm;
   double* c1 = sm + (size_t)J0 * S * S;

@@ -156,20 +156,9 @@ __global__ void __launch_bounds__(256, MINB)
 k_gram_v7(GramArgs g, GramFuse f) {
   using C = G7Cfg<S, GMAX, U, MINB, NY>;
   static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v7 Gram: s in {2,4,8,16}");
-  pdl_begin();
-  if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
-    if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
-    return;
-  }
-  // the fused small step's fault-injection state, read now (off the tail's critical path)
-  const int pre_force = (f.on && f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
+  pdl_launch();
   extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-#ifdef LSBA_TAIL_TRACE
-  unsigned long long tt[8] = {};
-  if (tid == 0) atomicMin(&g7_t0, gtimer());
-#endif
-  const uint64_t xpol = l2pol(c_l2hint & 2, false);
   const int J = g.J, E = J * S * C::NCOL;
   const int NG = g7_groups<S>(J);
   const int passes = g7_passes(NG, C::GMAX);
@@ -181,6 +170,37 @@ k_gram_v7(GramArgs g, GramFuse f) {
   const int gA = gp0 + ((gp1 - gp0) * qs) / QW, gB = gp0 + ((gp1 - gp0) * (qs + 1)) / QW;
   const int ng = gB - gA;
   const int jlo = gp0 * C::PB, jhi = min(J, gp1 * C::PB);   // blocks (entries) of this pass
+  const long NS = ((long)g.n + 3) / 4;                 // 4-row steps (rows padded)
+  if (g.pf_batches > 0 && tid == 0) {
+    // Pre-wait prefetch: a CTA becomes resident as the SpMM drains; before waiting on it, the
+    // rows of the basis blocks (constant during the step; not W, which the SpMM is writing)
+    // that this CTA streams in its first pf_batches batches go to L2, so the stream starts at
+    // once instead of after the SpMM's last CTA.  L2 only: never stale (kernels.cuh).
+    const long bsteps = (long)C::U * RW;
+    for (int i = 0; i < g.pf_batches; ++i) {
+      const long st0 = WIN ? ((long)i * nchunks + chunk) * bsteps
+                           : NS * chunk / nchunks + (long)i * bsteps;
+      const long st1 = min(NS, min(st0 + bsteps, WIN ? NS : NS * (chunk + 1) / nchunks));
+      if (st1 <= st0) break;
+      for (int j = jlo; j < jhi; ++j) {
+        const double* xj = g.X + (size_t)j * g.xstride;
+        if (xj == g.Y) continue;
+        bulk_prefetch_l2(xj + (size_t)st0 * 4 * S, 32L * S * (st1 - st0));
+      }
+    }
+  }
+  pdl_wait();
+  if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
+    if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
+    return;
+  }
+  // the fused small step's fault-injection state, read now (off the tail's critical path)
+  const int pre_force = (f.on && f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
+#ifdef LSBA_TAIL_TRACE
+  unsigned long long tt[8] = {};
+  if (tid == 0) atomicMin(&g7_t0, gtimer());
+#endif
+  const uint64_t xpol = l2pol(c_l2hint & 2, false);
   const int e0 = jlo * S * C::NCOL, EP = (jhi - jlo) * S * C::NCOL;
   const int r4 = lane & 3, c8 = lane >> 2;
   constexpr int LPB = S >= 16 ? 8 : S / 2;
@@ -208,7 +228,6 @@ k_gram_v7(GramArgs g, GramFuse f) {
 #pragma unroll
       for (int tn = 0; tn < C::NT; ++tn) acc[a][e][tn][0] = acc[a][e][tn][1] = 0.0;
 
-  const long NS = ((long)g.n + 3) / 4;                 // 4-row steps (rows padded)
   // Row order ("windowed"): warp slice rs of chunk c takes the U consecutive steps starting at
   // ((i nchunks + c) RW + rs) U in its i-th batch, so the whole grid sweeps one moving window
   // of rows (few open DRAM pages, 16-row contiguous runs per block and warp).  Measured 3-8%

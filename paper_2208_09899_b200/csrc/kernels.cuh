@@ -44,6 +44,8 @@ __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ uint64_t l2pol(bool hint, bool last) {
   uint64_t p;
   if (!hint) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -163,6 +165,18 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, long bytes) {
     const unsigned sz = (unsigned)((e - q) < 65536 ? (e - q) : 65536);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(q), "r"(sz) : "memory");
   }
+}
+
+// Projection pre-wait prefetch: a projection CTA launched early (PDL) sits on an SM the Gram
+// has left while the Gram's serial tail (the last CTAs' reductions and the fused small step,
+// ~7 us) runs and HBM idles.  Before waiting on the Gram, thread 0 of each of the first
+// pf_ctas CTAs bulk-prefetches into L2 the rows of every input block that the CTA reads first,
+// so that tail overlaps the projection's stream.  Only L2 is touched (the point of coherence):
+// the data cannot be stale whatever the predecessor still writes.
+__device__ __forceinline__ void prefetch_blocks_l2(int pf_ctas, const double* X, size_t xstride, int J,
+                                                   long off, long bytes) {
+  if ((int)blockIdx.x >= pf_ctas || threadIdx.x != 0 || bytes <= 0) return;
+  for (int j = 0; j < J; ++j) bulk_prefetch_l2(X + (size_t)j * xstride + off, bytes);
 }
 
 // 32-byte vector access (sm_100a LDG.E.256 / STG.E.256)
@@ -526,8 +540,14 @@ __device__ __forceinline__ double2 ldh2_co(const double* p, uint64_t pol) {   //
 static __global__ void __launch_bounds__(kThreads)
 k_project_flat(long cnt2, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
                const double* base0, double* out0, int J1, const double* __restrict__ C1, double* out1,
-               const int* __restrict__ flag_ptr) {
-  pdl_begin();
+               const int* __restrict__ flag_ptr, int pf_ctas = 0) {
+  pdl_launch();
+  {
+    const long e0 = (long)blockIdx.x * blockDim.x;
+    prefetch_blocks_l2(pf_ctas, X, xstride, max(J0, J1), 2 * e0,
+                       16L * (min(cnt2, e0 + (long)blockDim.x) - e0));
+  }
+  pdl_wait();
   if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   double* c0 = sm;
@@ -569,8 +589,14 @@ template <int S, bool GLOBAL>
 __global__ void __launch_bounds__(kThreads)
 k_project(int n, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
           const double* base0, double* out0, int J1, const double* __restrict__ C1,
-          double* out1, const int* __restrict__ flag_ptr) {
-  pdl_begin();
+          double* out1, const int* __restrict__ flag_ptr, int pf_ctas = 0) {
+  pdl_launch();
+  {
+    const long r0 = (long)blockIdx.x * blockDim.x;
+    prefetch_blocks_l2(pf_ctas, X, xstride, max(J0, J1), r0 * S,
+                       8L * S * (min((long)n, r0 + (long)blockDim.x) - r0));
+  }
+  pdl_wait();
   if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   constexpr int CB = GLOBAL ? 1 : S * S;   // coefficients per block

@@ -146,6 +146,8 @@ struct lsba_ctx_ {
   int spmm_pfv = 1;              // ... and of the CTA's V rows (LSBA_SPMM_PFV)
   bool spmm_lanes16 = false;     // diagnostics: LSBA_SPMM_LANES16=1 forces 16-byte SpMM lanes
   bool proj_dfma = false;        // diagnostics: LSBA_PROJ_DFMA=1 uses the DFMA projection at s = 8, 16
+  long proj_pf = 12L << 20;      // projection pre-wait L2 prefetch budget in bytes (LSBA_PROJ_PF_MB)
+  long gram_pf = 8L << 20;       // Gram pre-wait L2 prefetch budget in bytes (LSBA_GRAM_PF_MB)
   bool force_comm = false;       // LSBA_FORCE_COMM=1: one rank through the distributed code path
   int force_sing_cycle = 0;      // test hook: the cycle end of this cycle reports singular
   int cur_cycle = 0;
@@ -498,7 +500,12 @@ static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse&
   if ((size_t)geo.grid * a.J * S * S * NY > c->part_cap || geo.passes > kMaxGramPasses)
     return fail(c, LSBA_E_STATE, "v7 Gram workspace too small (J=%d)", a.J);
   if (geo.smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
-  CK(launch_k(c, fn, dim3(geo.grid), dim3(256), geo.smem, a, f));
+  GramArgs ap = a;
+  {  // pre-wait L2 prefetch: whole batches of every basis block within the budget c->gram_pf
+    const long per_batch = 8L * U * 4 * S * 8 * a.J * geo.grid;   // (upper bound: 8 row slices)
+    ap.pf_batches = (c->pdl && c->gram_pf > 0) ? (int)std::min<long>(4, c->gram_pf / per_batch) : 0;
+  }
+  CK(launch_k(c, fn, dim3(geo.grid), dim3(256), geo.smem, ap, f));
   return LSBA_OK;
 }
 
@@ -680,6 +687,12 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
 }
 
 // ---------------------------------------------------------------- a4/a6: projection
+// CTAs of a projection launch that prefetch their first rows into L2 before waiting on the
+// Gram (kernels.cuh prefetch_blocks_l2): as many as the budget c->proj_pf covers.
+static int proj_pf_ctas(lsba_ctx c, long bytes_per_cta, int grid) {
+  if (!c->pdl || c->proj_pf <= 0 || bytes_per_cta <= 0) return 0;
+  return (int)std::min<long>(grid, c->proj_pf / bytes_per_cta);
+}
 template <int S>
 static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0,
                              const double* C0, const double* base0, double* out0, int J1,
@@ -708,7 +721,7 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
       const int rows_per_warp = (S >= 16 ? 16 : 32);
       const int grid = std::max(1, std::min(cdiv(cdiv(n, rows_per_warp), 8), occ * c->n_sms));
       CK(launch_k(c, fn, dim3(grid), dim3(256), smem, n, X, xstride, J0, C0, base0, out0, J1, C1,
-                  out1, flag_ptr));
+                  out1, flag_ptr, proj_pf_ctas(c, 8L * rows_per_warp * S * 8 * Jmax, grid)));
       return LSBA_OK;
     }
   }
@@ -716,19 +729,20 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
     const long cnt2 = (long)n * S / 2;
     const int grid = std::max(1, std::min(cdiv(cnt2, kThreads), 8 * c->n_sms));
     CK(launch_k(c, k_project_flat, dim3(grid), dim3(kThreads), smem, cnt2, X, xstride, J0, C0, base0,
-                out0, J1, C1, out1, flag_ptr));
+                out0, J1, C1, out1, flag_ptr, proj_pf_ctas(c, 16L * kThreads * Jmax, grid)));
     return LSBA_OK;
   }
   if (gl) {
     auto fn = k_project<S, true>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<cdiv(n, kThreads), kThreads, smem, c->stream>>>(n, X, xstride, J0, C0, base0, out0,
-                                                             J1, C1, out1, flag_ptr);
+                                                             J1, C1, out1, flag_ptr, 0);
   } else {
     auto fn = k_project<S, false>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(launch_k(c, fn, dim3(cdiv(n, kThreads)), dim3(kThreads), smem, n, X, xstride, J0, C0,
-                base0, out0, J1, C1, out1, flag_ptr));
+                base0, out0, J1, C1, out1, flag_ptr,
+                proj_pf_ctas(c, 8L * kThreads * S * Jmax, cdiv(n, kThreads))));
   }
   CKL();
   return LSBA_OK;
@@ -1945,6 +1959,8 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_SPMM_PFV")) c->spmm_pfv = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPMM_LANES16")) c->spmm_lanes16 = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_PROJ_DFMA")) c->proj_dfma = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_PROJ_PF_MB")) c->proj_pf = std::atol(e) << 20;
+  if (const char* e = std::getenv("LSBA_GRAM_PF_MB")) c->gram_pf = std::atol(e) << 20;
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("LSBA_ILU_BACKOFF")) c->ilu_backoff = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
