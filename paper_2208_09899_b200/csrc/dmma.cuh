@@ -76,6 +76,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
   constexpr int KC = S / 4;                 // K chunks
   constexpr int NT = S >= 8 ? S / 8 : 1;    // N tiles
   constexpr int RB = S >= 16 ? 2 : 4;       // 8-row blocks per warp iteration
+  PDL_TRACE_ENTRY
   pdl_launch();
   {  // the CTA's first grid-stride iteration: its 8 warps' super-blocks are contiguous rows
     const long r0 = (long)blockIdx.x * (blockDim.x >> 5) * RB * 8;
@@ -83,6 +84,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
                        8L * S * (min((long)n, r0 + (long)(blockDim.x >> 5) * RB * 8) - r0));
   }
   pdl_wait();
+  PDL_TRACE_WAITED(kTrProj, max(J0, J1));
   if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   double* c0 = sm;
@@ -173,6 +175,7 @@ k_project_dmma(int n, const double* X, size_t xstride, int J0, const double* __r
       }
     }
   }
+  TRACE_EXIT(1);
 }
 
 }  // namespace lsba

@@ -40,15 +40,8 @@ __device__ __noinline__ void step_coef_noinline(const SmallState2& st, const dou
 }
 
 #ifdef LSBA_TAIL_TRACE
-// diagnostics build only (LSBA_NVCC_EXTRA=-DLSBA_TAIL_TRACE): globaltimer stamps of the Gram's
-// tail, printed by the CTA that runs the fused small step
-__device__ unsigned long long g7_t0 = ~0ull;
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define G7T(i) do { if (tid == 0) tt[i] = gtimer(); } while (0)
+// diagnostics build only: stamps of the Gram's tail, recorded by the CTA that runs the small step
+#define G7T(i) do { if (tid == 0) tt[i] = gtime(); } while (0)
 #else
 #define G7T(i) do { } while (0)
 #endif
@@ -156,6 +149,7 @@ __global__ void __launch_bounds__(256, MINB)
 k_gram_v7(GramArgs g, GramFuse f) {
   using C = G7Cfg<S, GMAX, U, MINB, NY>;
   static_assert(S == 2 || S == 4 || S == 8 || S == 16, "v7 Gram: s in {2,4,8,16}");
+  PDL_TRACE_ENTRY
   pdl_launch();
   extern __shared__ __align__(16) double sm7[];     // [RW][pass entries] row-slice partials
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -190,6 +184,8 @@ k_gram_v7(GramArgs g, GramFuse f) {
     }
   }
   pdl_wait();
+  PDL_TRACE_WAITED(kTrGram, J);
+  TRACE_PREV_EXIT(0, 8);
   if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
     if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
     return;
@@ -198,7 +194,6 @@ k_gram_v7(GramArgs g, GramFuse f) {
   const int pre_force = (f.on && f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
 #ifdef LSBA_TAIL_TRACE
   unsigned long long tt[8] = {};
-  if (tid == 0) atomicMin(&g7_t0, gtimer());
 #endif
   const uint64_t xpol = l2pol(c_l2hint & 2, false);
   const int e0 = jlo * S * C::NCOL, EP = (jhi - jlo) * S * C::NCOL;
@@ -390,11 +385,9 @@ k_gram_v7(GramArgs g, GramFuse f) {
 #ifdef LSBA_TAIL_TRACE
   __syncthreads();
   if (tid == 0) {
-    const unsigned long long t4 = gtimer(), t0 = g7_t0;
-    printf("G7TAIL S=%d J=%d k=%d passes=%d grid=%d ngroups=%d | loop_end %llu grp_last %llu final %llu "
-           "small_start %llu end %llu (ns from first CTA start)\n", S, J, f.k, passes, (int)gridDim.x, ngroups,
-           tt[0] - t0, tt[1] - t0, tt[2] - t0, tt[3] - t0, t4 - t0);
-    g7_t0 = ~0ull;
+    const unsigned long long t4 = gtime();
+    for (int i = 0; i < 4; ++i) trace_rec(kTrTail + i, (unsigned)J, tt[i]);
+    trace_rec(kTrTail + 4, (unsigned)J, t4);
   }
 #endif
 }

@@ -46,6 +46,44 @@ __device__ __forceinline__ void pdl_begin() {
 }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#ifdef LSBA_TAIL_TRACE
+// Diagnostics build only (LSBA_NVCC_EXTRA=-DLSBA_TAIL_TRACE): globaltimer stamps appended to a
+// device buffer (two words per record: time, tag << 32 | J), read back by lsba_trace_dump.
+// (Device printf costs ~40 us per call and would distort the timeline it measures.)
+constexpr unsigned kTraceWords = 1u << 18;
+static __device__ unsigned long long g_trace[kTraceWords];
+static __device__ unsigned g_trace_n;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_rec(unsigned tag, unsigned J, unsigned long long t) {
+  const unsigned i = atomicAdd(&g_trace_n, 2u);
+  if (i + 1 < kTraceWords) {
+    g_trace[i] = t;
+    g_trace[i + 1] = ((unsigned long long)tag << 32) | J;
+  }
+}
+// block 0 of a kernel: its time at entry (before the PDL wait) and after the wait
+#define PDL_TRACE_ENTRY const unsigned long long pdl_t_entry = (blockIdx.x == 0 && threadIdx.x == 0) ? gtime() : 0ull;
+#define PDL_TRACE_WAITED(tag, J) do { if (blockIdx.x == 0 && threadIdx.x == 0) { \
+  trace_rec(tag, (unsigned)(J), pdl_t_entry); trace_rec((tag) + 1, (unsigned)(J), gtime()); } } while (0)
+// the latest CTA exit of the SpMM (slot 0) / projection (slot 1) as thread 0 of each CTA saw it,
+// recorded by block 0 of the next kernel once its wait returned (tags 8: SpMM, 9: projection)
+static __device__ unsigned long long g_trace_exit[2];
+#define TRACE_EXIT(slot) do { if (threadIdx.x == 0) atomicMax(&g_trace_exit[slot], gtime()); } while (0)
+#define TRACE_PREV_EXIT(slot, tag) do { if (blockIdx.x == 0 && threadIdx.x == 0) \
+  trace_rec(tag, 0, *(volatile unsigned long long*)&g_trace_exit[slot]); } while (0)
+#else
+#define PDL_TRACE_ENTRY
+#define PDL_TRACE_WAITED(tag, J) do { } while (0)
+#define TRACE_EXIT(slot) do { } while (0)
+#define TRACE_PREV_EXIT(slot, tag) do { } while (0)
+#endif
+// trace tags: 2/3 SpMM entry/waited, 4/5 Gram, 6/7 projection; 10..14 the Gram tail (gram7.cuh)
+enum { kTrSpmm = 2, kTrGram = 4, kTrProj = 6, kTrTail = 10 };
 __device__ __forceinline__ uint64_t l2pol(bool hint, bool last) {
   uint64_t p;
   if (!hint) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
@@ -213,7 +251,10 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
        const double* __restrict__ Vghost, const double* __restrict__ Bm,
        double* __restrict__ W, double* __restrict__ sq_part, const int* __restrict__ active = nullptr,
        int pf_dist = 0, int pf_v = 0, int row0 = 0, int row1 = -1) {
+  PDL_TRACE_ENTRY
   pdl_begin();
+  PDL_TRACE_WAITED(kTrSpmm, 0);
+  TRACE_PREV_EXIT(1, 9);
   if (active && *active == 0) return;
   constexpr int C = CW;                // columns per lane
   constexpr int L = S / CW;            // lanes per row
@@ -301,6 +342,7 @@ k_spmm(int n, const int* __restrict__ rp, const int* __restrict__ ci,
       sq_part[blockIdx.x] = t;
     }
   }
+  TRACE_EXIT(0);
 }
 
 // P > 1 without a contiguous interior block (config 4's random columns): the SpMM runs on the
@@ -541,6 +583,7 @@ static __global__ void __launch_bounds__(kThreads)
 k_project_flat(long cnt2, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
                const double* base0, double* out0, int J1, const double* __restrict__ C1, double* out1,
                const int* __restrict__ flag_ptr, int pf_ctas = 0) {
+  PDL_TRACE_ENTRY
   pdl_launch();
   {
     const long e0 = (long)blockIdx.x * blockDim.x;
@@ -548,6 +591,7 @@ k_project_flat(long cnt2, const double* X, size_t xstride, int J0, const double*
                        16L * (min(cnt2, e0 + (long)blockDim.x) - e0));
   }
   pdl_wait();
+  PDL_TRACE_WAITED(kTrProj, max(J0, J1));
   if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   double* c0 = sm;
@@ -590,6 +634,7 @@ __global__ void __launch_bounds__(kThreads)
 k_project(int n, const double* X, size_t xstride, int J0, const double* __restrict__ C0,
           const double* base0, double* out0, int J1, const double* __restrict__ C1,
           double* out1, const int* __restrict__ flag_ptr, int pf_ctas = 0) {
+  PDL_TRACE_ENTRY
   pdl_launch();
   {
     const long r0 = (long)blockIdx.x * blockDim.x;
@@ -597,6 +642,7 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
                        8L * S * (min((long)n, r0 + (long)blockDim.x) - r0));
   }
   pdl_wait();
+  PDL_TRACE_WAITED(kTrProj, max(J0, J1));
   if (flag_ptr && *flag_ptr) return;
   extern __shared__ double sm[];
   constexpr int CB = GLOBAL ? 1 : S * S;   // coefficients per block
@@ -605,8 +651,10 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
   for (int e = threadIdx.x; e < J0 * CB; e += blockDim.x) c0[e] = C0[e];
   for (int e = threadIdx.x; e < J1 * CB; e += blockDim.x) c1[e] = C1[e];
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  // grid-stride over rows on a resident grid: the coefficients are staged once per CTA, and the
+  // CTAs the next kernel's early launch waits on all start together (config 2 +3% in situ,
+  // profiles/r02_coef_flag_raw.txt)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
   double o0[S], o1[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) { o0[c] = 0.0; o1[c] = 0.0; }
@@ -657,7 +705,7 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
     } else {
       store_row<S>(out0 + (size_t)i * S, o0);
     }
-    return;
+    continue;
   }
   const int Jmax = max(J0, J1);
   for (int j = 0; j < Jmax; ++j) {
@@ -698,6 +746,8 @@ k_project(int n, const double* X, size_t xstride, int J0, const double* __restri
   }
   if (J0 > 0) store_row<S>(out0 + (size_t)i * S, o0);
   if (J1 > 0) store_row<S>(out1 + (size_t)i * S, o1);
+  }
+  TRACE_EXIT(1);
 }
 
 // ------------------------------------------------------------------------------------------

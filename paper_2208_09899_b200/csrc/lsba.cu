@@ -732,17 +732,23 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
                 out0, J1, C1, out1, flag_ptr, proj_pf_ctas(c, 16L * kThreads * Jmax, grid)));
     return LSBA_OK;
   }
+  // one-row-per-thread kernel on a resident (grid-stride) grid
+  auto resident_grid = [&](auto fn) -> int {
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+    return std::max(1, std::min(cdiv(n, kThreads), occ * c->n_sms));
+  };
   if (gl) {
     auto fn = k_project<S, true>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<cdiv(n, kThreads), kThreads, smem, c->stream>>>(n, X, xstride, J0, C0, base0, out0,
-                                                             J1, C1, out1, flag_ptr, 0);
+    fn<<<resident_grid(fn), kThreads, smem, c->stream>>>(n, X, xstride, J0, C0, base0, out0,
+                                                          J1, C1, out1, flag_ptr, 0);
   } else {
     auto fn = k_project<S, false>;
     if (smem > 32 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(launch_k(c, fn, dim3(cdiv(n, kThreads)), dim3(kThreads), smem, n, X, xstride, J0, C0,
-                base0, out0, J1, C1, out1, flag_ptr,
-                proj_pf_ctas(c, 8L * kThreads * S * Jmax, cdiv(n, kThreads))));
+    const int grid = resident_grid(fn);
+    CK(launch_k(c, fn, dim3(grid), dim3(kThreads), smem, n, X, xstride, J0, C0,
+                base0, out0, J1, C1, out1, flag_ptr, proj_pf_ctas(c, 8L * kThreads * S * Jmax, grid)));
   }
   CKL();
   return LSBA_OK;
@@ -2454,3 +2460,19 @@ extern "C" lsba_status lsba_workspace_bytes(lsba_ctx c, int64_t* bytes) {
   *bytes = c->ws_bytes;
   return LSBA_OK;
 }
+
+#ifdef LSBA_TAIL_TRACE
+// Diagnostics build only: copy the trace records (kernels.cuh trace_rec) to `out` (2 words per
+// record), reset the buffer, return the number of words copied.  Not declared in lsba.h.
+extern "C" int lsba_trace_dump(unsigned long long* out, int max_words) {
+  unsigned n = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  cudaMemcpyFromSymbol(&n, lsba::g_trace_n, sizeof(unsigned));
+  if (n > lsba::kTraceWords) n = lsba::kTraceWords;
+  if ((int)n > max_words) n = (unsigned)max_words & ~1u;
+  if (out && n) cudaMemcpyFromSymbol(out, lsba::g_trace, sizeof(unsigned long long) * n);
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(lsba::g_trace_n, &z, sizeof(unsigned));
+  return (int)n;
+}
+#endif

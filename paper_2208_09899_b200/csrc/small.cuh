@@ -367,9 +367,8 @@ __device__ __forceinline__ void step_coef_body(const SmallState2& st, const doub
 #ifdef LSBA_TAIL_TRACE
   __syncthreads();
   SCT(4);
-  if (threadIdx.x == 0 && (k == 5 || k == 15))
-    printf("STEPCOEF B=%d k=%d | entry->G %llu S %llu chol+Rinv %llu coef+stores %llu ns\n", B, k,
-           tq[1] - tq[0], tq[2] - tq[1], tq[3] - tq[2], tq[4] - tq[3]);
+  if (threadIdx.x == 0)   // tags 20..24: entry, G -> smem done, S done, chol + R^-1 done, end
+    for (int i = 0; i < 5; ++i) trace_rec(20 + i, (unsigned)k, tq[i]);
 #endif
 #undef SCT
 }
