@@ -492,7 +492,7 @@ static lsba_status wait_update(lsba_ctx c) {
 
 // ---------------------------------------------------------------- a2: v7 streaming Gram
 // Tuned (GMAX groups per warp, U steps per batch, MINB CTAs per SM) per s and J from the
-// standalone sweep in tools/gram_bench.cu (profiles/r01_gram_sweep.md).
+// standalone sweep in tools/gram_bench.cu (profiles/r01_gram_sweep*_raw.txt).
 template <int S, int GMAX, int U, int MINB, bool WIN = true, int NY = 1>
 static lsba_status gram_v7_launch(lsba_ctx c, const GramArgs& a, const GramFuse& f) {
   auto fn = k_gram_v7<S, GMAX, U, MINB, WIN, NY>;
@@ -711,7 +711,7 @@ static lsba_status project_t(lsba_ctx c, const double* X, size_t xstride, int J0
   LaunchScope Ls(c, kid, bytes);
   if (n == 0) return LSBA_OK;
   // s = 4: the DFMA kernel streams faster than the DMMA one (5.8 vs 5.0 TB/s on config 2,
-  // profiles/r01_variants.md); s = 8, 16: DMMA (6.65 TB/s on configs 3 and 5)
+  // tools/gpu_variants.sh); s = 8, 16: DMMA (6.65 TB/s on configs 3 and 5)
   if constexpr (S == 8 || S == 16) {
     if (!gl && c->variant == 0 && !c->proj_dfma) {
       auto fn = k_project_dmma<S>;
