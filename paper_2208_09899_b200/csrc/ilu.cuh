@@ -2,7 +2,9 @@
 // incomplete LU (ILU) preconditioner with no fill"; left side, IKJ variant).
 //
 //   k_ilu0_level   one level of the IKJ factorisation, a warp per row (setup, once per matrix)
-//   k_ilu_trsv_poll  (default) sync-free sparse triangular solve Z = L^{-1} X or U^{-1} X, one
+//   k_ilu_pack     level-ordered packed rows of each factor half (setup)
+//   k_ilu_trsv_level (default, round 2) level-synchronous solve on the packs, grid barriers
+//   k_ilu_trsv_poll  (LSBA_ILU_SOLVE=0) sync-free sparse triangular solve Z = L^{-1} X or U^{-1} X, one
 //                  thread per row (all s columns), rows in level order claimed 32 at a time by
 //                  the warps of a persistent grid, dependencies detected by polling the data itself
 //                  (sentinel-filled output); measured 4.3 / 11 / 12 us per level on configs
@@ -191,6 +193,223 @@ k_ilu_trsv_poll(int nrows, const int* __restrict__ order, const int* __restrict_
     if (e == gridDim.x - 1) {
       ctr[0] = 0u;
       ctr[1] = 0u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Level-synchronous solve on level-ordered packed rows (round 2; for matrices whose levels
+// are wide, e.g. 3D stencils: 5-22 K rows per level).  Setup packs, for every position t of
+// the level order, the row index, its first kIluW dependencies (columns and factor values, in
+// CSR order), the CSR position after them (the rest, rare, is read from the CSR), and the
+// pivot: structure-of-arrays, so a level's threads read them coalesced, in one round trip,
+// independent of the solve's data.  A resident grid walks the levels with one grid barrier
+// between them; thread g holds row r0 + g of the level.  Software-pipelined: the packed data
+// of level l+1 is loaded before the barrier that ends level l-1 and used after the one ending
+// level l, so a level costs the barrier plus one round trip for its dependency values and the
+// store.  Dependencies summed in CSR order, then the diagonal: the same arithmetic as
+// k_ilu_trsv_poll, bitwise.
+// ---------------------------------------------------------------------------------------
+constexpr int kIluW = 4;          // packed dependencies per row
+constexpr int kThreadsIluLvl = 256;
+struct IluPack {                  // level-ordered, n entries each ([q * n + t] for k, v)
+  int* row;                       // row index
+  int* rest;                      // CSR position after the kIluW-th dependency (p1 if fewer)
+  int* k;                         // dependency columns (-1: none)
+  double* v;                      // factor values of those entries
+  double* piv;                    // U: the pivot (L: unused)
+};
+// build the pack of one factor half: thread per level-order position
+template <bool LOWER>
+__global__ void k_ilu_pack(int n, const int* __restrict__ order, const int* __restrict__ rp,
+                           const int* __restrict__ ci, const double* __restrict__ lu, const int* __restrict__ diag,
+                           int n_local, IluPack pk) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int i = order[t];
+  const int p0 = rp[i], p1 = rp[i + 1];
+  int nd = 0, p = p0;
+  for (; p < p1 && nd < kIluW; ++p) {
+    const int k = ci[p];
+    if (k >= n_local || (LOWER ? k >= i : k <= i)) continue;
+    pk.k[(size_t)nd * n + t] = k;
+    pk.v[(size_t)nd * n + t] = lu[p];
+    ++nd;
+  }
+  for (int q = nd; q < kIluW; ++q) {
+    pk.k[(size_t)q * n + t] = -1;
+    pk.v[(size_t)q * n + t] = 0.0;
+  }
+  pk.row[t] = i;
+  pk.rest[t] = p;
+  if (!LOWER) pk.piv[t] = lu[diag[i]];
+}
+#ifndef LSBA_BAR_NS
+#define LSBA_BAR_NS 0
+#endif
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(bar) : "memory");
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(LSBA_BAR_NS);
+    }
+  }
+  __syncthreads();
+}
+// 32-byte L2 (coherent) access: rows written by other CTAs during the solve never come from L1
+__device__ __forceinline__ double4 ldcg4(const double* p) {
+  double4 v;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void stcg4(double* p, double4 v) {
+  asm volatile("st.global.cg.v4.f64 [%0], {%1,%2,%3,%4};" :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+struct IluLvlRow {
+  int i, rest, p1;
+  int k[kIluW];
+  double v[kIluW];
+  double piv;
+};
+template <bool LOWER>
+__device__ __forceinline__ void ilu_pack_load(long t, int n, const IluPack& pk, const int* __restrict__ rp,
+                                              IluLvlRow& r) {
+  r.i = __ldcg(pk.row + t);
+  r.rest = __ldcg(pk.rest + t);
+#pragma unroll
+  for (int q = 0; q < kIluW; ++q) {
+    r.k[q] = __ldcg(pk.k + (size_t)q * n + t);
+    r.v[q] = __ldcg(pk.v + (size_t)q * n + t);
+  }
+  r.piv = LOWER ? 1.0 : __ldcg(pk.piv + t);
+  r.p1 = -1;            // (row end: loaded only when a row has more than kIluW dependencies)
+}
+template <int S, bool LOWER>
+__device__ __forceinline__ void ilu_pack_finish(const IluLvlRow& r, const int* __restrict__ rp,
+                                                const int* __restrict__ ci, const double* __restrict__ lu,
+                                                int n_local, const double* __restrict__ X, double* Z) {
+  double y[kIluW][S];
+#pragma unroll
+  for (int q = 0; q < kIluW; ++q)
+    if (r.k[q] >= 0) {
+      if constexpr (S % 4 == 0) {
+#pragma unroll
+        for (int c = 0; c < S; c += 4) {
+          const double4 w = ldcg4(Z + (size_t)r.k[q] * S + c);
+          y[q][c] = w.x;
+          y[q][c + 1] = w.y;
+          y[q][c + 2] = w.z;
+          y[q][c + 3] = w.w;
+        }
+      } else if constexpr (S % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < S; c += 2) {
+          const double2 w = __ldcg(reinterpret_cast<const double2*>(Z + (size_t)r.k[q] * S + c));
+          y[q][c] = w.x;
+          y[q][c + 1] = w.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < S; ++c) y[q][c] = __ldcg(Z + (size_t)r.k[q] * S + c);
+      }
+    }
+  double acc[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) acc[c] = 0.0;
+#pragma unroll
+  for (int q = 0; q < kIluW; ++q)
+    if (r.k[q] >= 0)
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc[c] = fma(r.v[q], y[q][c], acc[c]);
+  if (r.k[kIluW - 1] >= 0) {                      // (more dependencies than packed: CSR)
+    const int p1 = rp[r.i + 1];
+    for (int p = r.rest; p < p1; ++p) {
+      const int k = ci[p];
+      if (k >= n_local || (LOWER ? k >= r.i : k <= r.i)) continue;
+      const double a = lu[p];
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc[c] = fma(a, __ldcg(Z + (size_t)k * S + c), acc[c]);
+    }
+  }
+  double* zi = Z + (size_t)r.i * S;
+  if constexpr (S % 4 == 0) {
+#pragma unroll
+    for (int c = 0; c < S; c += 4) {
+      const double4 xv = ldcg4(X + (size_t)r.i * S + c);
+      double4 o;
+      o.x = LOWER ? xv.x - acc[c] : (xv.x - acc[c]) / r.piv;
+      o.y = LOWER ? xv.y - acc[c + 1] : (xv.y - acc[c + 1]) / r.piv;
+      o.z = LOWER ? xv.z - acc[c + 2] : (xv.z - acc[c + 2]) / r.piv;
+      o.w = LOWER ? xv.w - acc[c + 3] : (xv.w - acc[c + 3]) / r.piv;
+      stcg4(zi + c, o);
+    }
+  } else if constexpr (S % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < S; c += 2) {
+      const double2 xv = __ldcg(reinterpret_cast<const double2*>(X + (size_t)r.i * S + c));
+      double2 o;
+      o.x = LOWER ? xv.x - acc[c] : (xv.x - acc[c]) / r.piv;
+      o.y = LOWER ? xv.y - acc[c + 1] : (xv.y - acc[c + 1]) / r.piv;
+      __stcg(reinterpret_cast<double2*>(zi + c), o);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < S; ++c) {
+      const double v = __ldcg(X + (size_t)r.i * S + c) - acc[c];
+      __stcg(zi + c, LOWER ? v : v / r.piv);
+    }
+  }
+}
+// bar[0]: CTA arrivals (monotonic within a launch), bar[1]: CTA exits (the last resets both);
+// *go: block 0's reading of the cycle control, published by barrier 0 (a uniform no-op).
+template <int S, bool LOWER>
+__global__ void __launch_bounds__(kThreadsIluLvl, 1)
+k_ilu_trsv_level(int n, int nlev, const int* __restrict__ lvl, IluPack pk, const int* __restrict__ rp,
+                 const int* __restrict__ ci, const double* __restrict__ lu, int n_local,
+                 const double* __restrict__ X, double* Z, unsigned* bar, int* go, const int* __restrict__ active) {
+  const long T = (long)gridDim.x * blockDim.x;
+  const long g = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned nbar = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *(volatile int*)go = (active && *active == 0) ? 0 : 1;
+  IluLvlRow cur, nxt;
+  long c0 = 0, ccnt = 0;
+  if (nlev > 0) {
+    c0 = lvl[0];
+    ccnt = lvl[1] - c0;
+    if (g < ccnt) ilu_pack_load<LOWER>(c0 + g, n, pk, rp, cur);
+  }
+  grid_barrier(bar, (++nbar) * gridDim.x);
+  if (*(volatile int*)go != 0) {
+    for (int l = 0; l < nlev; ++l) {
+      // the next level's packed rows: loaded now, used after the next barrier
+      long n0 = 0, ncnt = 0;
+      if (l + 1 < nlev) {
+        n0 = lvl[l + 1];
+        ncnt = lvl[l + 2] - n0;
+        if (g < ncnt) ilu_pack_load<LOWER>(n0 + g, n, pk, rp, nxt);
+      }
+      if (g < ccnt) ilu_pack_finish<S, LOWER>(cur, rp, ci, lu, n_local, X, Z);
+      for (long t = g + T; t < ccnt; t += T) {            // (levels wider than the grid)
+        IluLvlRow r2;
+        ilu_pack_load<LOWER>(c0 + t, n, pk, rp, r2);
+        ilu_pack_finish<S, LOWER>(r2, rp, ci, lu, n_local, X, Z);
+      }
+      if (l + 1 < nlev) grid_barrier(bar, (++nbar) * gridDim.x);   // level l complete
+      cur = nxt;
+      c0 = n0;
+      ccnt = ncnt;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned e = atomicAdd(bar + 1, 1u);
+    if (e == gridDim.x - 1) {
+      bar[0] = 0u;
+      bar[1] = 0u;
     }
   }
 }

@@ -125,6 +125,10 @@ struct lsba_ctx_ {
   int* d_diag = nullptr;         // CSR position of a_ii
   int* d_ordL = nullptr;         // rows by level of L (ascending dependencies)
   int* d_ordU = nullptr;         // rows by level of U
+  int* d_lvlL = nullptr;         // level pointers into d_ordL (nlL + 1) and d_ordU (nlU + 1)
+  int* d_lvlU = nullptr;
+  IluPack packL{}, packU{};      // level-ordered packed rows (ilu.cuh k_ilu_trsv_level)
+  int ilu_solve = 1;             // 1 level-synchronous on packed rows, 0 sync-free polling (LSBA_ILU_SOLVE)
   double* d_ilu_tmp = nullptr;   // n x s intermediate of the data-polling variant
   unsigned* d_ticket = nullptr;  // CTA start tickets (2: L and U solves)
   int ilu_levels[2] = {0, 0};
@@ -354,6 +358,40 @@ static lsba_status ilu_apply_t(lsba_ctx c, double* Y, const int* active) {
   // algorithmic bytes per solve: the factor half (~12 B per stored entry + row pointers and
   // the row order) and Y read + written once
   const double by = 6.0 * c->nnz + 8.0 * (c->n + 1) + 16.0 * c->n * S;
+  // level-synchronous on packed rows (default; LSBA_ILU_SOLVE=0: sync-free data polling)
+  if (c->ilu_solve != 0) {
+    auto fl = k_ilu_trsv_level<S, true>;
+    auto fu = k_ilu_trsv_level<S, false>;
+    int occ = 1, occ2 = 1;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fl, kThreadsIluLvl, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fu, kThreadsIluLvl, 0));
+    // every CTA resident (grid barriers): occupancy x SMs, less two slots for the 1-CTA kernels
+    // of stream 2 that may hold part of an SM meanwhile
+    const int lgrid = std::max(1, std::min(std::min(occ, occ2) * c->n_sms - 2, cdiv(c->n, kThreadsIluLvl)));
+    unsigned* bar = c->d_ticket + 4;
+    int* go = reinterpret_cast<int*>(c->d_ticket + 6);
+    // cooperative launches: the runtime refuses a grid that cannot be co-resident (the grid
+    // barriers would otherwise wait forever)
+    auto coop = [&](auto fn, int nlev_h, const int* lvl, const IluPack& pk, const double* Xin, double* Zout) -> cudaError_t {
+      int n_ = c->n, nl_ = nlev_h, nloc = c->n;
+      const int* rp_ = c->d_rp;
+      const int* ci_ = c->d_ci;
+      const double* lu_ = c->d_lu;
+      IluPack pk_ = pk;
+      void* args[] = {&n_, &nl_, (void*)&lvl, &pk_, (void*)&rp_, (void*)&ci_, (void*)&lu_, &nloc, (void*)&Xin, (void*)&Zout,
+                      (void*)&bar, (void*)&go, (void*)&active};
+      return cudaLaunchCooperativeKernel((const void*)fn, dim3(lgrid), dim3(kThreadsIluLvl), args, 0, c->stream);
+    };
+    {
+      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+      CK(coop(fl, c->ilu_levels[0], c->d_lvlL, c->packL, Y, c->d_ilu_tmp));
+    }
+    {
+      LaunchScope Ls(c, LSBA_K_ILU_SOLVE, by);
+      CK(coop(fu, c->ilu_levels[1], c->d_lvlU, c->packU, c->d_ilu_tmp, Y));
+    }
+    return LSBA_OK;
+  }
   // data polling, out of place: Y -> T (L), T -> Y (U)
   const int grid = std::min(nblk, c->n_sms * c->ilu_ctas);
   const long cnt = (long)c->n * S;
@@ -1574,7 +1612,9 @@ static void release(lsba_ctx c) {
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
                   c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
-                  c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL,
+                  c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL, c->d_lvlL, c->d_lvlU,
+                  c->packL.row, c->packL.rest, c->packL.k, c->packL.v, c->packL.piv, c->packU.row,
+                  c->packU.rest, c->packU.k, c->packU.v, c->packU.piv,
                   c->d_ordU, c->d_ticket, c->d_ilu_tmp, c->d_rpL, c->d_ciL, c->d_vaL, c->d_rowsG,
                   c->d_rpG, c->d_ciG, c->d_vaG};
   // (the caller's allocator may hand the memory to other work at once: drain our streams first)
@@ -1969,6 +2009,7 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_GRAM_PF_MB")) c->gram_pf = std::atol(e) << 20;
   if (const char* e = std::getenv("LSBA_ILU_CTAS")) c->ilu_ctas = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("LSBA_ILU_BACKOFF")) c->ilu_backoff = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("LSBA_ILU_SOLVE")) c->ilu_solve = std::atoi(e);
   if (const char* e = std::getenv("LSBA_FORCE_COMM")) c->force_comm = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_HALO_OVERLAP")) c->halo_ovl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_DEVAR")) c->devar_req = (e[0] == '1');
@@ -2255,12 +2296,23 @@ static lsba_status ilu0_factor(lsba_ctx c) {
     TRY(dalloc(c, &c->d_diag, n));
     TRY(dalloc(c, &c->d_ordL, n));
     TRY(dalloc(c, &c->d_ordU, n));
+    TRY(dalloc(c, &c->d_lvlL, (size_t)nlL + 1));
+    TRY(dalloc(c, &c->d_lvlU, (size_t)nlU + 1));
+    for (IluPack* pk : {&c->packL, &c->packU}) {
+      TRY(dalloc(c, &pk->row, n));
+      TRY(dalloc(c, &pk->rest, n));
+      TRY(dalloc(c, &pk->k, (size_t)kIluW * n));
+      TRY(dalloc(c, &pk->v, (size_t)kIluW * n));
+      TRY(dalloc(c, &pk->piv, n));
+    }
     TRY(dalloc(c, &c->d_ticket, 8));
     TRY(dalloc(c, &c->d_ilu_tmp, (size_t)n * c->s));
   }
   CK(cudaMemcpy(c->d_diag, diag.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ordL, ordL.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_ordU, ordU.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_lvlL, ptrL.data(), sizeof(int32_t) * (nlL + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_lvlU, ptrU.data(), sizeof(int32_t) * (nlU + 1), cudaMemcpyHostToDevice));
   CK(cudaMemset(c->d_ticket, 0, sizeof(unsigned) * 8));
   if (c->nnz) CK(cudaMemcpy(c->d_lu, c->d_va, sizeof(double) * c->nnz, cudaMemcpyDeviceToDevice));
   CK(cudaMemsetAsync(c->d_info, 0, sizeof(int), c->stream));
@@ -2274,6 +2326,13 @@ static lsba_status ilu0_factor(lsba_ctx c) {
   CK(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (c->h_info[0]) return fail(c, LSBA_E_NUMERIC, "ILU(0): zero pivot");
+  // level-ordered packs for the level-synchronous solve (factor values final now)
+  k_ilu_pack<true><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(n, c->d_ordL, c->d_rp, c->d_ci, c->d_lu,
+                                                                   c->d_diag, n, c->packL);
+  k_ilu_pack<false><<<cdiv(n, kThreads), kThreads, 0, c->stream>>>(n, c->d_ordU, c->d_rp, c->d_ci, c->d_lu,
+                                                                    c->d_diag, n, c->packU);
+  CKL();
+  CK(cudaStreamSynchronize(c->stream));
   c->ilu_levels[0] = nlL;
   c->ilu_levels[1] = nlU;
   c->ilu_ready = true;

@@ -211,3 +211,19 @@ def test_fullsize_config2_properties(L):
     assert np.abs(d).max() <= 1e-12 * np.abs(p.vals).max()
     R = Lf @ (Uf @ Y) - X
     assert np.linalg.norm(R) <= 1e-12 * np.linalg.norm(X)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_level_and_polling_solves_bitwise_equal(L, cfg, monkeypatch):
+    """The level-synchronous solve on packed rows (default, LSBA_ILU_SOLVE=1) and the sync-free
+    polling solve (LSBA_ILU_SOLVE=0) sum every row's dependencies in CSR order, then divide by
+    the pivot: the same arithmetic, so the same bits (and both match the oracle, above)."""
+    p = twin(cfg)
+    X = np.random.default_rng(100 + cfg).standard_normal((p.n, p.s))
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("LSBA_ILU_SOLVE", mode)
+        with L.Context(p.n, p.s, 4, p.row_ptr, p.col_idx, p.vals) as ctx:
+            L.lsba_ilu0_setup(ctx.ctx, True)
+            out[mode] = ctx.ilu0_apply(dev(X)).cpu().numpy()
+    assert np.array_equal(out["1"], out["0"])
