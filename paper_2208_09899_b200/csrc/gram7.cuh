@@ -85,7 +85,35 @@ struct GramFuse {
   ncclWindow_t win;
   const ncclDevComm* dcomm;   // device copy (a pointer: the kernel parameter block stays small
                               // and is never addressed, which would copy it to local memory)
+  // Device-side join of the previous step's update kernel (stream 2; one rank, v7 only): the
+  // main stream does not wait on its event, so this Gram launches programmatically behind the
+  // SpMM; the CTA that runs the small step acquires *upd_done >= upd_seq first.  Until then
+  // the cycle control may still change, so CTAs that see the cycle ended skip their rows but
+  // keep the ticket protocol, and the tail re-reads the control after the join.
+  int upd_wait;
+  unsigned upd_seq;
+  const unsigned* upd_done;
 };
+
+// Spin (one thread) until the update kernel carrying sequence `seq` has exited.  The update
+// kernel was made ready before this Gram's SpMM and runs on a high-priority stream, so it
+// holds an SM long before this tail; the bound only turns a broken invariant into a fault
+// instead of a hang.
+__device__ __noinline__ void wait_update_seq(const unsigned* done, unsigned seq) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+  if ((int)(v - seq) >= 0) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    __nanosleep(64);
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if ((int)(v - seq) >= 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) __trap();
+  }
+}
 
 // f2: the step's single sync folded into the Gram's tail
 // through the NCCL device API.  The CTA that holds this rank's final G publishes it in its slot
@@ -186,12 +214,16 @@ k_gram_v7(GramArgs g, GramFuse f) {
   pdl_wait();
   PDL_TRACE_WAITED(kTrGram, J);
   TRACE_PREV_EXIT(0, 8);
+  bool skip = false;                    // (device join: this CTA's rows are not needed)
   if (g.active && *g.active == 0) {     // speculative launch after the cycle ended: no-op
-    if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
-    return;
+    if (!f.upd_wait) {
+      if (f.on && blockIdx.x == 0 && threadIdx.x == 0) *f.st.flag_dev = 1;   // (projection no-ops)
+      return;
+    }
+    skip = true;
   }
   // the fused small step's fault-injection state, read now (off the tail's critical path)
-  const int pre_force = (f.on && f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
+  int pre_force = (f.on && f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
 #ifdef LSBA_TAIL_TRACE
   unsigned long long tt[8] = {};
 #endif
@@ -242,7 +274,8 @@ k_gram_v7(GramArgs g, GramFuse f) {
       }
     }
   };
-  if constexpr (WIN) {
+  if (skip) {
+  } else if constexpr (WIN) {
     // windowed order (above): U consecutive steps per batch, the grid sweeping one window
     for (long st = ((long)chunk * RW + rs) * C::U; st < NS; st += GS) {
       double2 av[C::U][C::GMAX];
@@ -372,6 +405,16 @@ k_gram_v7(GramArgs g, GramFuse f) {
     __syncthreads();
     if (ticket7 != (unsigned)(passes - 1)) return;
     if (tid == 0) *tpass = 0u;
+  }
+  if (f.upd_wait) {
+    __syncthreads();
+    if (tid == 0) wait_update_seq(f.upd_done, f.upd_seq);
+    __syncthreads();
+    if (*(volatile const int*)g.active == 0) {   // the update ended the cycle meanwhile
+      if (tid == 0) *f.st.flag_dev = 1;
+      return;
+    }
+    pre_force = (f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
   }
   G7T(3);
   if (f.ar) {

@@ -145,6 +145,8 @@ struct lsba_ctx_ {
   int* d_rowsG = nullptr; int* d_rpG = nullptr; int* d_ciG = nullptr; double* d_vaG = nullptr;
   bool halo_ovl = true;            // LSBA_HALO_OVERLAP
   bool upd_main = false;         // diagnostics: LSBA_UPD_MAIN=1
+  int devjoin = 1;               // Gram joins the update on the device: 0 never (stream event),
+                                 // 1 for basis blocks <= 64 MB, 2 always (LSBA_DEVJOIN)
   bool spec_end = true;          // speculative cycle end before the status read (LSBA_SPEC_END)
   int spmm_pf = -1;              // SpMM L2 prefetch distance in CTAs (-1: 4 x SMs; LSBA_SPMM_PF)
   int spmm_pfv = 1;              // ... and of the CTA's V rows (LSBA_SPMM_PFV)
@@ -651,10 +653,23 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
   const size_t E = gl ? (size_t)J : (size_t)J * S * S;
   if (coef_fused) *coef_fused = false;
   if (Vk) TRY(spmm_t<S>(c, Vk, Y, active));
-  TRY(wait_update(c));
   const bool y_is_block = (X + (size_t)(J - 1) * xstride == Y);
   const bool slots = c->variant == 0 && in_basis(c, X) && in_basis(c, Y) && c->d_tickets;
   constexpr bool v7_s = (S == 2 || S == 4 || S == 8 || S == 16);
+  // one rank, a v7 Gram with the small step fused into its tail: the tail joins the previous
+  // step's update kernel on the device (GramFuse::upd_wait) instead of the main stream
+  // waiting on its event, which would keep this Gram from launching behind the SpMM (PDL)
+  // Cost model: it saves ~2-4 us per step (the event join keeps the Gram from launching behind
+  // the SpMM), but a Gram enqueued speculatively past a mid-cycle ending (convergence, kappa,
+  // flag) may now stream before it sees the ending — a whole wasted Gram.  So by default only
+  // for basis blocks <= 64 MB, where a step is short and a Gram cheap (config 2: +1.4%; config
+  // 4's 537 MB blocks: -2%; configs 3 and 5 neutral; profiles/r02_devjoin_ab_raw.txt).
+  const bool devjoin = (c->devjoin == 2 || (c->devjoin == 1 && 8.0 * c->n * S <= 64.0 * (1 << 20))) &&
+                       c->pending_upd && !c->comm && !gl && v7_s && slots && c->n > 0 &&
+                       coef_k > 0 && coef_fused && !c->no_fuse && E * sizeof(double) <= 64 * 1024 &&
+                       !c->upd_main;
+  if (devjoin) c->pending_upd = false;
+  TRY(wait_update(c));
   bool ar_in_kernel = false;       // f2: the kernel's tail did the allreduce
   if (slots && ((!gl && v7_s) || (gl && S % 2 == 0))) {
     LaunchScope Ls(c, LSBA_K_GRAM, 8.0 * c->n * S * (J - (y_is_block ? 1 : 0)) + 8.0 * c->n * S);
@@ -677,6 +692,11 @@ static lsba_status gram_t(lsba_ctx c, const double* X, size_t xstride, int J, do
         f.k = coef_k;
         f.prm = prm ? *prm : CycleParams{};
         *coef_fused = true;
+        if (devjoin) {
+          f.upd_wait = 1;
+          f.upd_seq = c->st.upd_seq;
+          f.upd_done = c->st.upd_done;
+        }
         if (devar) {
           f.ar = 1;
           f.woff = (size_t)(c->ar_seq++ & 1) * c->ar_slot;
@@ -901,6 +921,7 @@ static lsba_status step_update_t(lsba_ctx c, int k, const double* G) {
   cudaStream_t st = c->upd_main ? c->stream : c->stream2;
   LaunchScope Ls(c, LSBA_K_STEP_UPDATE, 0.0, st);
   const double rfac = (c->ip == LSBA_IP_GLOBAL) ? std::sqrt((double)c->s) : 1.0;
+  ++c->st.upd_seq;   // released to st.upd_done when this launch exits (device-side join)
   CK(launch_step_update<B>(c->st, G, k, rfac, st));
   return LSBA_OK;
 }
@@ -985,7 +1006,9 @@ static lsba_status pip_step_async(lsba_ctx c, int k) {
   const CycleParams none{};   // (k > 0 launches read their parameters from the device control)
   // The SpMM of step k runs while the update kernel of step k-1 (stream 2) is still taking
   // the continue/restart decision: it only writes slot k, scratch if the cycle ended at step
-  // k-1.  The Gram (and the small step fused into its tail) waits for the update (wait_update).
+  // k-1.  The Gram (and the small step fused into its tail) waits for the update: its tail
+  // acquires the update's exit on the device when fused (GramFuse::upd_wait), else the main
+  // stream joins the update's event (wait_update).
   c->d_G = c->d_Gbase + (size_t)(k & 1) * c->g_half;
   c->pending_upd = (k > 1);
   bool fused = false;
@@ -1611,7 +1634,7 @@ static void release(lsba_ctx c) {
   void* ptrs[] = {c->d_rp, c->d_ci, c->d_V, c->d_ghost, c->d_send_idx, c->d_sendbuf,
                   c->d_part, c->d_Gbase, c->d_small, c->d_Y, c->d_Z, c->d_info, c->d_Xc,
                   c->d_sq, c->d_scalar, c->d_Bh, c->d_Xh, c->st.status, c->st.flag_dev,
-                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr,
+                  c->d_gpart, c->d_tickets, c->d_ctl, c->d_zeros, c->st.rscr, c->st.iscr, c->st.upd_done,
                   c->st.Tm, c->st.TmT, c->st.gpip, c->st.Jb, c->d_lu, c->d_diag, c->d_ordL, c->d_lvlL, c->d_lvlU,
                   c->packL.row, c->packL.rest, c->packL.k, c->packL.v, c->packL.piv, c->packU.row,
                   c->packU.rest, c->packU.k, c->packU.v, c->packU.piv,
@@ -1958,6 +1981,9 @@ static lsba_status create_impl(lsba_ctx c, int64_t n, int32_t s, int32_t m_max, 
   }
   TRY(dalloc(c, &c->st.rscr, 2 * (size_t)s * s));
   TRY(dalloc(c, &c->st.iscr, 4));
+  TRY(dalloc(c, &c->st.upd_done, 1));
+  CK(cudaMemset(c->st.upd_done, 0, sizeof(unsigned)));
+  c->st.upd_seq = 0;
   {  // the update kernel's single CTA should get an SM as soon as one frees up
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1998,6 +2024,7 @@ static lsba_status create_any(lsba_ctx* out, int64_t n, int32_t s, int32_t m_max
   if (const char* e = std::getenv("LSBA_PDL")) c->pdl = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_G7")) c->g7force = std::atoi(e);
   if (const char* e = std::getenv("LSBA_UPD_MAIN")) c->upd_main = (e[0] == '1');
+  if (const char* e = std::getenv("LSBA_DEVJOIN")) c->devjoin = std::atoi(e);
   if (const char* e = std::getenv("LSBA_PDL_PROJ")) c->pdl_proj = (e[0] == '1');
   if (const char* e = std::getenv("LSBA_L2PERSIST")) c->l2persist = std::atoi(e);
   if (const char* e = std::getenv("LSBA_SPEC_END")) c->spec_end = (e[0] == '1');

@@ -45,6 +45,11 @@ struct SmallState2 {
   double* TmT;          // and its transpose (T row-major), for row-wise dot products
   double* gpip;         // BMGS-(I)CWY: H_{1:k,k} in the Gram layout the update kernel reads
   double* Jb;           // BCGS-IRO-LS: the tentative next Hessenberg column J ((k+1)b x b, row-major)
+  // Device-side join of the update kernel (one rank, fused small step): every k_step_update
+  // launch carries the next value of a per-context sequence and releases it to *upd_done at
+  // its exit; the Gram tail acquires it instead of the main stream waiting on an event.
+  unsigned* upd_done;
+  unsigned upd_seq;
 };
 
 // publish the step just decided to the host (mapped pinned memory; the host bounds how far
@@ -383,8 +388,8 @@ k_step_coef(SmallState2 st, const double* __restrict__ G, int k, CycleParams prm
 
 // k_step_update (k >= 1): blockDim 32 * (B + 2); dyn smem (k+1) B B + (k-1)(2 B B + B).
 template <int B>
-__global__ void __launch_bounds__(32 * (B + 2))
-k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) {
+__device__ __forceinline__ void step_update_body(const SmallState2& st, const double* __restrict__ G, int k,
+                                                 double rfac) {
   extern __shared__ double Gs[];         // (k+1) B B copy of G, then (k-1) reflector sets
   __shared__ double Rs[B * B], Ris[B * B], Ht[B * B], Gh[B * B];
   __shared__ double red[32];
@@ -602,6 +607,20 @@ k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) 
       else if (k >= ctl->m_cur) { ctl->active = 0; ctl->why = 4; }
     }
     publish_progress(st, k, ctl->active);
+  }
+}
+
+// Every exit of the body is block-uniform, so the CTA meets here once whatever the ending; the
+// sequence release orders all of the CTA's writes (barrier cumulativity) before the Gram tail
+// that acquires it (gram7.cuh, GramFuse::upd_wait).
+template <int B>
+__global__ void __launch_bounds__(32 * (B + 2))
+k_step_update(SmallState2 st, const double* __restrict__ G, int k, double rfac) {
+  step_update_body<B>(st, G, k, rfac);
+  if (st.upd_done) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(st.upd_done), "r"(st.upd_seq) : "memory");
   }
 }
 

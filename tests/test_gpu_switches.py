@@ -18,6 +18,8 @@ SWITCHES = [
     {"LSBA_UPD_MAIN": "1"},
     {"LSBA_G7": "2"},
     {"LSBA_SPEC_END": "0"},
+    {"LSBA_DEVJOIN": "0"},
+    {"LSBA_DEVJOIN": "2"},
 ]
 
 
