@@ -390,6 +390,16 @@ k_gram_v7(GramArgs g, GramFuse f) {
   // one pass (and a fused small step): the final sums also go straight into shared memory,
   // where the small step reads G (no global round trip)
   const bool g_smem = f.on && passes == 1 && NY == 1;
+  // device join (one pass): the CTA's last thread (idle in the final level when E < 256) waits
+  // for the update and reads the control the small step needs while the others sum
+  __shared__ int join7[2];
+  const int jt = C::NTHR - 1;
+  auto join_update = [&]() {
+    wait_update_seq(f.upd_done, f.upd_seq);
+    join7[0] = *(volatile const int*)g.active;
+    join7[1] = (f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
+  };
+  if (f.upd_wait && passes == 1 && tid == jt) join_update();
   for (int e = e0 + tid; e < e0 + EP; e += C::NTHR) {
     const double s2 = ordered_partial_sum<20>(g.gpart + e, E, ngroups);
     g.G[e] = s2;
@@ -407,14 +417,13 @@ k_gram_v7(GramArgs g, GramFuse f) {
     if (tid == 0) *tpass = 0u;
   }
   if (f.upd_wait) {
+    if (passes > 1 && tid == jt) join_update();
     __syncthreads();
-    if (tid == 0) wait_update_seq(f.upd_done, f.upd_seq);
-    __syncthreads();
-    if (*(volatile const int*)g.active == 0) {   // the update ended the cycle meanwhile
+    if (join7[0] == 0) {                 // the update ended the cycle meanwhile
       if (tid == 0) *f.st.flag_dev = 1;
       return;
     }
-    pre_force = (f.k > 0) ? ((f.k == f.st.ctl->force_k && !f.st.ctl->forced_done) ? 1 : 0) : 0;
+    pre_force = join7[1];
   }
   G7T(3);
   if (f.ar) {
