@@ -174,13 +174,29 @@ def partition(n_global, world, rank, unit=1):
     return u0 * unit, u1 * unit
 
 
-def build_workload(config, rank, world, need_sha=True):
+def build_workload(config, rank, world, need_sha=True, rank_proxy=0):
     """The GLOBAL problem of BASELINE config `config` (strong scaling: the same A and B at
-    every N), and this rank's rows of it."""
+    every N), and this rank's rows of it.
+
+    rank_proxy = P > 1 (one GPU, stencils only; tools/gpu_rank_proxy.sh): NOT a BASELINE
+    workload -- the stencil on one rank's slab of a P-rank run (N^(d-1) x N/P grid, the same
+    rows, nonzeros per row and block sizes as that rank's share; the neighbours' planes are
+    cut off instead of exchanged), run as a one-rank problem so that one GPU can time the
+    per-rank kernels at the P-rank size."""
     from lsba_inputs import CONFIGS, csr_sha256, random_sparse, rhs, stencil
     spec = dict(CONFIGS[config])
     s, m = spec["s"], spec["m"]
     sha = None
+    if rank_proxy > 1:
+        assert world == 1 and spec["kind"] == "stencil" and spec["N"] % rank_proxy == 0
+        dims, N = spec["dims"], spec["N"]
+        shape = (N,) * (dims - 1) + (N // rank_proxy,)
+        A = stencil(dims, N, spec["v"], shape=shape)
+        n = int(np.prod(shape))
+        spec["name"] = f"{spec['name']}_slab_1of{rank_proxy}_proxy"
+        return dict(name=spec["name"], n_global=n, row_begin=0, row_end=n, A=A,
+                    B=np.ascontiguousarray(rhs(n, s)), s=s, m=m, tol=spec["tol"], tau=spec["tau"],
+                    nnz=int(A[0][-1]), spec=spec, sha=csr_sha256(*A) if need_sha else None)
     if spec["kind"] == "stencil":
         dims, N = spec["dims"], spec["N"]
         n = N ** dims
@@ -329,6 +345,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the fixed-k step sweep")
     ap.add_argument("--no-tts", action="store_true", help="skip the full time-to-solution run")
+    ap.add_argument("--rank-proxy", type=int, default=0,
+                    help="one-GPU diagnostic, not a BASELINE workload: time one rank's slab of a P-rank "
+                         "stencil run as a one-rank problem (see build_workload)")
     ap.add_argument("--ip", default="cl", choices=["cl", "gl"], help="block inner product (Table 1)")
     ap.add_argument("--prec", default="none", choices=["none", "ilu0"],
                     help="left ILU(0) preconditioning (SURVEY 8(f) f4); factored before the timed region")
@@ -351,7 +370,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = build_workload(args.config, rank, world)
+    wl = build_workload(args.config, rank, world, rank_proxy=args.rank_proxy)
     nccl_id = None
     if world > 1:
         idt = torch.zeros(128, dtype=torch.uint8, device="cuda")

@@ -49,6 +49,32 @@ def test_strong_scaling_slices_of_one_problem(world, monkeypatch):
     assert seen == 12 ** 3
 
 
+def test_rank_proxy_slab_has_a_rank_s_share(monkeypatch):
+    """--rank-proxy P (one-GPU diagnostic): the slab problem has exactly the rows of one rank of
+    the P-rank partition, and each row keeps that rank's in-slab entries (the entries reaching
+    into the neighbours' planes are cut off)."""
+    import bench
+    import lsba_inputs
+    from lsba_inputs import CONFIGS
+    small = dict(CONFIGS[5], N=12)
+    monkeypatch.setitem(lsba_inputs.CONFIGS, 5, small)
+    monkeypatch.setattr(lsba_inputs.generators, "CONFIGS", lsba_inputs.CONFIGS)
+    P = 3
+    wl = bench.build_workload(5, 0, 1, rank_proxy=P)
+    mid = bench.build_workload(5, 1, P, need_sha=False)          # an interior rank of the real run
+    r0, r1 = mid["row_begin"], mid["row_end"]
+    assert wl["n_global"] == r1 - r0 == 12 * 12 * 4 and wl["B"].shape == (r1 - r0, 8)
+    assert wl["name"].endswith("_slab_1of3_proxy")
+    prp, pci, pva = wl["A"]
+    rp, ci, va = mid["A"]
+    assert wl["nnz"] == prp[-1] == rp[-1] - 2 * 144             # two cut-off planes of ghost entries
+    for i in (0, 5, 143, 144, 300, 12 * 12 * 4 - 1):
+        cols = ci[rp[i]:rp[i + 1]]
+        keep = (cols >= r0) & (cols < r1)
+        assert np.array_equal(pci[prp[i]:prp[i + 1]], cols[keep] - r0)
+        assert np.array_equal(pva[prp[i]:prp[i + 1]], va[rp[i]:rp[i + 1]][keep])
+
+
 def test_algorithmic_bytes_is_sum_of_roof():
     import bench
     nnz, n, s, m = 1000, 100, 4, 7
