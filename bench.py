@@ -217,6 +217,21 @@ def build_workload(config, rank, world, need_sha=True, rank_proxy=0):
                 tol=spec["tol"], tau=spec["tau"], nnz=nnz, spec=spec, sha=sha)
 
 
+def workload_config(wl, n_gpus, ip="cl", skel="pip", prec="none"):
+    """`config` of the JSON line: what identifies the workload and the method, identical in
+    both arms (ours and --impl reference); what is specific to an arm goes under `run`."""
+    n, s, m = wl["n_global"], wl["s"], wl["m"]
+    return {"workload": wl["name"], "n": n, "nnz": int(wl["nnz"]), "s": s, "m": m, "tol": wl["tol"],
+            "tau": wl["tau"] if np.isfinite(wl["tau"]) else None,     # None = no kappa_F trigger
+            "method": f"{ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY",
+                                          "irols": "BCGS-IRO-LS", "bmgs": "BMGS", "pio": "BCGS-PIO"}[skel]
+                      + " skeleton, " + ("CholQR IO" if ip == "cl" else "global IO")
+                      + (", left ILU(0)" if prec == "ilu0" else ""),
+            "parallelism": f"rows-dp{n_gpus} (strong scaling: the same global problem, "
+                           f"{'z-plane slabs' if wl['spec']['kind'] == 'stencil' else 'row blocks'})",
+            "l2": f"inputs larger than L2 (the workload's basis: {8 * n * s * (m + 1) / 1e9:.2f} GB)"}
+
+
 # --------------------------------------------------------------------------- oracle timing
 def oracle_sample_problem(wl):
     """The bounded CPU sample: the leading principal submatrix of A on the first SAMPLE_ROWS
@@ -318,9 +333,9 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "block_steps_per_s": tot_steps / tot_s,
-        "config": {"workload": wl["name"], "n": wl["n_global"], "s": wl["s"], "m": wl["m"],
-                   "method": "cl-BCGS-PIP block Arnoldi (oracle, NumPy fp64, accurate Gram)",
-                   "timed_unit": f"bounded sample: IO + the first block steps of one cycle on the {desc}"},
+        "config": workload_config(wl, args.gpus),
+        "run": {"implementation": "cl-BCGS-PIP block Arnoldi (oracle, NumPy fp64, accurate Gram)",
+                "timed_unit": f"bounded sample: IO + the first block steps of one cycle on the {desc}"},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": host_cores(), "kind": "oracle",
                          "cpu_model": cpu_model(),
                          "sample": f"{tot_steps} block steps over {args.steps} samples of config {args.config} "
@@ -579,23 +594,17 @@ def main():
             "repeats": {"n": len(reps), "GBps": [round(x, 1) for x in reps], "mean": statistics.mean(reps),
                         "min": min(reps), "max": max(reps),
                         "ms_per_step": [round(x / args.steps, 3) for x in reps_ms]},
-            "config": {"workload": wl["name"], "n": n_glob, "nnz": wl["nnz"], "s": s, "m": m, "tol": tol,
-                       "tau": tau, "csr_sha256": wl["sha"] if world == 1 else None,
-                       "csr_sha256_rank0_rows": wl["sha"] if world > 1 else None,
-                       "method": f"{args.ip}-BGMRES, " + {"pip": "BCGS-PIP", "cwy": "BMGS-CWY", "icwy": "BMGS-ICWY",
-                                                          "irols": "BCGS-IRO-LS", "bmgs": "BMGS",
-                                                          "pio": "BCGS-PIO"}[args.skel]
-                                 + " skeleton, " + ("CholQR IO" if args.ip == "cl" else "global IO")
-                                 + (", left ILU(0)" if args.prec == "ilu0" else ""),
-                       "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
-                                      f"{iters / args.steps:.1f} block steps)") if full_solve
-                                     else f"restart cycle = IO + {m} block steps + cycle end (K cycles from X0 = 0)",
-                       "parallelism": f"rows-dp{world} (strong scaling: the same global problem, "
-                                      f"{'z-plane slabs' if wl['spec']['kind'] == 'stencil' else 'row blocks'})",
-                       "rows_rank0": [wl["row_begin"], wl["row_end"]],
-                       "l2": f"inputs larger than L2 (basis {8 * n_loc * s * (m + 1) / 1e9:.2f} GB per rank)"
-                             + (f"; the CSR ({12 * wl['nnz'] / 1e6:.0f} MB) is kept in the persisting L2 set-aside"
-                                if l2_resident_csr(wl["nnz"], world) else "")},
+            "config": workload_config(wl, world, args.ip, args.skel, args.prec),
+            "run": {"implementation": "liblsba.so (sm_100a CUDA) through the C ABI",
+                    "csr_sha256": wl["sha"] if world == 1 else None,
+                    "csr_sha256_rank0_rows": wl["sha"] if world > 1 else None,
+                    "timed_unit": (f"full solve to tol {tol} from X0 = 0 ({cycles / args.steps:.1f} cycles, "
+                                   f"{iters / args.steps:.1f} block steps)") if full_solve
+                                  else f"restart cycle = IO + {m} block steps + cycle end (K cycles from X0 = 0)",
+                    "rows_rank0": [wl["row_begin"], wl["row_end"]],
+                    "l2": f"inputs larger than L2 (basis {8 * n_loc * s * (m + 1) / 1e9:.2f} GB per rank)"
+                          + (f"; the CSR ({12 * wl['nnz'] / 1e6:.0f} MB) is kept in the persisting L2 set-aside"
+                             if l2_resident_csr(wl["nnz"], world) else "")},
             "roofline": {"bound": "hbm", "kernel": dom,
                          **({"note": "level-scheduled triangular solves: latency-bound (one dependency "
                                      "level after another), reported against the HBM roof"}
