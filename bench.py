@@ -228,7 +228,7 @@ def workload_config(wl, n_gpus, ip="cl", skel="pip", prec="none"):
                       + " skeleton, " + ("CholQR IO" if ip == "cl" else "global IO")
                       + (", left ILU(0)" if prec == "ilu0" else ""),
             "parallelism": f"rows-dp{n_gpus} (strong scaling: the same global problem, "
-                           f"{'z-plane slabs' if wl['spec']['kind'] == 'stencil' else 'row blocks'})",
+                           f"{'slabs of whole slowest-dimension planes' if wl['spec']['kind'] == 'stencil' else 'row blocks'})",
             "l2": f"inputs larger than L2 (the workload's basis: {8 * n * s * (m + 1) / 1e9:.2f} GB)"}
 
 
