@@ -159,8 +159,15 @@ class ClockSampler:
         mx = [float(p[1]) for p in self.samples if p[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for p in self.samples for i in range(4) if p[2 + i].lower().startswith("active")})
+        pw = []
+        for p in self.samples:
+            try:
+                pw.append(float(p[6]))
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # --------------------------------------------------------------------------- workload
