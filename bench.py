@@ -622,6 +622,9 @@ def main():
                                      "level after another), reported against the HBM roof"}
                             if dom == "ilu_solve" else {}), "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "peak_note": "peak = the measured COPY bandwidth (read + write); a read-mostly "
+                                      "stream can exceed it (pure-read ceiling measured at 7.3 TB/s, "
+                                      "profiles/r01_microbench.txt), so frac may pass 1",
                          "launches": dn, "kernel_share_of_step": dms / tot_ms if tot_ms else None,
                          "measured_in": "instrumented re-run of the same K cycles (per-launch CUDA events "
                                         f"on the launching streams; {ms_prof / args.steps:.3f} ms per cycle)"},
