@@ -224,6 +224,20 @@ def build_workload(config, rank, world, need_sha=True, rank_proxy=0):
                 tol=spec["tol"], tau=spec["tau"], nnz=nnz, spec=spec, sha=sha)
 
 
+def strict_json(o):
+    """The line must be strict JSON: non-finite floats (a residual that was never computed, an
+    infinite threshold) become null."""
+    if isinstance(o, float):
+        return o if np.isfinite(o) else None
+    if isinstance(o, dict):
+        return {k: strict_json(v) for k, v in o.items()}
+    if isinstance(o, (list, tuple)):
+        return [strict_json(v) for v in o]
+    if isinstance(o, np.generic):
+        return strict_json(o.item())
+    return o
+
+
 def workload_config(wl, n_gpus, ip="cl", skel="pip", prec="none"):
     """`config` of the JSON line: what identifies the workload and the method, identical in
     both arms (ours and --impl reference); what is specific to an arm goes under `run`."""
@@ -349,7 +363,7 @@ def run_reference(args, rank, world):
                                    f"({desc})"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(strict_json(line), allow_nan=False), flush=True)
     return 0
 
 
@@ -639,7 +653,7 @@ def main():
             "solver": {"cycles": cycles, "iterations": iters, "nan_flags": info.nan_flags,
                        "res_est_rel": info.res_est, "true_relres": info.true_relres},
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(strict_json(line), allow_nan=False), flush=True)
     ctx.close()
     if dist is not None:
         dist.barrier()

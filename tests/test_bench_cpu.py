@@ -82,3 +82,25 @@ def test_algorithmic_bytes_is_sum_of_roof():
     gram_blocks = 2 * sum(k + 1 for k in range(1, m + 1))
     expect = 2 * (sum(bench.roof_step(nnz, n, s, k) for k in range(1, m + 1)) + bench.roof_cycle_extra(n, s, m))
     assert bench.algorithmic_bytes(nnz, n, s, iters, cycles, gram_blocks) == pytest.approx(expect, rel=1e-14)
+
+
+def test_reference_arm_line_contract():
+    """`bench.py --impl reference` (the oracle timed on the host cores) prints ONE JSON line with
+    the contract's keys; its `config` is what the GPU arm prints for the same workload."""
+    import json
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 1 and d["warmup"] == 0 and d["n_gpus"] == 1
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["value"] == d["value"] == d["e2e"]["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    import bench
+    wl = bench.build_workload(1, 0, 1, need_sha=False)
+    assert d["config"] == json.loads(json.dumps(bench.workload_config(wl, 1)))
+    assert "Infinity" not in lines[0] and "NaN" not in lines[0]          # strict JSON
